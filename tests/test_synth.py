@@ -28,7 +28,7 @@ def test_distributions():
     lim = 0.02 * (1 + 2.0**-10)   # fp16 rounding of the bound
     assert u.min() >= -lim and u.max() <= lim and abs(u.std() - 0.02 / np.sqrt(3)) < 2e-4
     g = synth.draw(1, 1, 0, synth.KIND_GAMMA, 0.1, 0, n)
-    assert g.min() >= 0.9 and g.max() <= 1.1
+    assert g.min() >= 0.9 - 1e-3 and g.max() <= 1.1 + 1e-3   # fp16 grid near 1 is 2^-11
 
 
 def test_prompts_range():
