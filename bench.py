@@ -1,0 +1,319 @@
+"""bench.py — decode tokens/s of the streamed-weight PIPO pipeline (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--wfmt int4|fp16]
+    python bench.py --impl reference ...     # the CPU oracle arm (reads oracle/)
+
+A "step" is one decode_step: all n_layers decoder layers (weights streamed from
+pinned host memory over PCIe, chunk by chunk, consumed as they land) plus the LM
+head and greedy argmax, for a batch of b sequences per GPU.  Default workload is
+configs[4] (c5): OPT-30B shapes, int4-g64 weights, b = 64 per GPU, prompt 512,
+gen 32 (31 decode steps fit; more are allowed, positions keep growing).
+Multi-GPU: one process per GPU (torchrun), batch-sharded, no collective on the
+hot path; timing = max over ranks (device events), barrier on both sides.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import pipo_synth as synth  # noqa: E402
+
+CONFIGS = {
+    "c1": dict(shape=synth.OPTShape(768, 1, 12, 3072), b=4, P=32, G=8, weight_tier=1, kv_tier=0,
+               desc="configs[0]: one OPT-125M-shaped decoder layer, int4 g64, b=4, P=32, gen 8"),
+    "c2": dict(shape=synth.OPT_1_3B, b=16, P=256, G=32, weight_tier=1, kv_tier=0,
+               desc="configs[1]: OPT-1.3B, weights in pinned host memory, b=16, P=256, gen 32"),
+    "c3": dict(shape=synth.OPT_6_7B, b=32, P=512, G=32, weight_tier=1, kv_tier=1,
+               desc="configs[2]: OPT-6.7B streamed weights + host-resident KV, b=32, P=512, gen 32"),
+    "c4": dict(shape=synth.OPT_13B, b=64, P=512, G=32, weight_tier=2, kv_tier=0,
+               desc="configs[3]: OPT-13B streamed weights from disk -> pinned host ring, b=64, P=512, gen 32"),
+    "c5": dict(shape=synth.OPT_30B, b=64, P=512, G=32, weight_tier=1, kv_tier=0,
+               desc="configs[4]: OPT-30B streamed weights, b=64/GPU, P=512, gen 32 (batch-sharded)"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="pipo", choices=["pipo", "reference"])
+    ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
+    ap.add_argument("--wfmt", default="int4", choices=["int4", "fp16"])
+    ap.add_argument("--ring", type=int, default=2)
+    ap.add_argument("--chunk-mb", type=float, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--disk-dir", default="/tmp/pipo_disk")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = max(mx, float(p[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        return {}
+
+
+# ---------------------------------------------------------------------------
+def oracle_sample(cfg_name: str, wfmt: str, reps: int = 1):
+    """The CPU oracle as it stands (oracle/opt.py), on a bounded sample of the
+    workload: one decode step through ONE decoder layer at full batch b and
+    L = P + G/2 cached positions, plus the LM head; extrapolated to a full step as
+    n_layers * t_layer + t_head.  Returns (tokens/s, sample description, cores)."""
+    from oracle import opt
+    c = CONFIGS[cfg_name]
+    s, b, P, G = c["shape"], c["b"], c["P"], c["G"]
+    cores = len(os.sched_getaffinity(0))
+    for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ.setdefault(v, str(cores))
+    lw = opt.layer_from_masters(synth.layer_masters(s, 0), wfmt)
+    emb = synth.embed_masters(s)
+    tok = emb["tok"].astype(np.float64)
+    past = P + G // 2 - 1
+    rng = np.random.default_rng(0)
+    kc = rng.standard_normal((b, past + 1, s.d_model)) * 0.5
+    vc = rng.standard_normal((b, past + 1, s.d_model)) * 0.5
+    h = rng.standard_normal((b, 1, s.d_model))
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        h2 = opt.decoder_layer(h, lw, kc, vc, past, s.n_heads)
+        t1 = time.perf_counter()
+        opt.layer_norm(h2[:, 0], emb["lnf_g"], emb["lnf_b"]) @ tok.T
+        t2 = time.perf_counter()
+        times.append((t1 - t0) * s.n_layers + (t2 - t1))
+    step = min(times)
+    desc = (f"oracle/opt.py fp64: 1 of {s.n_layers} decoder layers + LM head at b={b}, L={past + 1}, "
+            f"extrapolated x{s.n_layers} layers")
+    return b / step, desc, cores, step
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    c = CONFIGS[args.config]
+    t_all = []
+    tps = None
+    for i in range(args.warmup + args.steps):
+        tps, desc, cores, step = oracle_sample(args.config, args.wfmt)
+        if i >= args.warmup:
+            t_all.append(step)
+    ms = statistics.mean(t_all) * 1e3
+    value = c["b"] / (ms / 1e3)
+    line = {"impl": "reference", "metric": f"decode tokens/s, {c['desc']}", "value": value, "unit": "tokens/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": args.config, "wfmt": args.wfmt},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": desc},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+def run_pipo(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2504_03664_b200 import pipo
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    torch.cuda.set_device(local)
+    c = CONFIGS[args.config]
+    s, b, P, G = c["shape"], c["b"], c["P"], c["G"]
+    steps_needed = args.warmup + args.steps * (1 if args.no_e2e else 2)
+    max_seq = P + max(G, steps_needed + 1)
+    disk_dir = f"{args.disk_dir}/rank{rank}" if c["weight_tier"] == 2 else None
+    if disk_dir:
+        os.makedirs(disk_dir, exist_ok=True)
+    cfg = pipo.make_config(s, device=local, max_batch=b, max_seq=max_seq,
+                           wfmt=pipo.PIPO_W_INT4_G64 if args.wfmt == "int4" else pipo.PIPO_W_FP16,
+                           weight_tier=c["weight_tier"], kv_tier=c["kv_tier"], ring_layers=args.ring,
+                           chunk_bytes=int(args.chunk_mb * (1 << 20)), disk_dir=disk_dir,
+                           flags=pipo.PIPO_F_TIMELINE)
+    t_setup = time.perf_counter()
+    pl = pipo.Pipeline(cfg)
+    pl.load_synthetic(pipo.PIPO_LAYER_EMBED, synth.WEIGHT_SEED)
+    for j in range(s.n_layers):
+        pl.load_synthetic(j, synth.WEIGHT_SEED)
+    t_load = time.perf_counter() - t_setup
+    link_probe = pipo.pipo_probe_h2d(pl.ctx, 256 << 20, 5)
+    # batch shard: rank r owns sequences [r*b, (r+1)*b) of the global prompt batch
+    prompt = synth.prompts(b * world, P, s.vocab)[rank * b:(rank + 1) * b]
+    t0 = time.perf_counter()
+    nxt, _ = pl.prefill(prompt)
+    t_prefill = time.perf_counter() - t0
+    for _ in range(args.warmup):
+        nxt, _ = pl.decode_step(nxt)
+
+    comp = torch.cuda.ExternalStream(pipo.pipo_stream(pl.ctx, 0), device=local)
+    tok_dev = torch.from_numpy(nxt.astype(np.int32)).cuda(local)
+
+    def barrier():
+        torch.cuda.synchronize(local)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(local)
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- value: inputs resident in HBM (device token ids, no host round trip) ----
+    pl.stats_reset()
+    barrier()
+    with ClockSampler(local) as clk:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(comp)
+        for _ in range(args.steps):
+            pipo.decode_step_dev(pl.ctx, tok_dev.data_ptr(), tok_dev.data_ptr())
+        e1.record(comp)
+        torch.cuda.synchronize(local)
+    barrier()
+    t_dev = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+    st = pl.stats()
+    clocks = clk.summary()
+
+    # ---- e2e: the public C-ABI call with HOST buffers, H2D ids + D2H ids every step ----
+    e2e = None
+    if not args.no_e2e:
+        nxt = tok_dev.cpu().numpy()
+        barrier()
+        e0.record(comp)
+        for _ in range(args.steps):
+            nxt, _ = pl.decode_step(nxt)
+        e1.record(comp)
+        torch.cuda.synchronize(local)
+        barrier()
+        t_e2e = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+        per_step_h2d = st["h2d_bytes"] / max(1, st["decode_steps"]) + b * 4
+        e2e = {"value": world * b * args.steps / t_e2e, "unit": "tokens/s",
+               "h2d_bytes_per_step": int(per_step_h2d), "d2h_bytes_per_step": int(b * 4),
+               "note": "decode_step(host tokens) -> host next ids; h2d counts the streamed weights too"}
+
+    value = world * b * args.steps / t_dev
+    ms = t_dev / args.steps * 1e3
+    peaks = measured_peaks()
+    layer_bytes = st["h2d_bytes"] / max(1, st["decode_steps"])
+    link_floor_s = layer_bytes / (link_probe * 1e9)
+    line = None
+    if rank == 0:
+        line = {
+            "metric": "decode tokens/s, OPT-30B streamed weights (int4-g64), b=64/GPU, P=512" if args.config == "c5"
+            else f"decode tokens/s, {c['desc']}",
+            "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f16", "weights": args.wfmt + ("-g64" if args.wfmt == "int4" else ""),
+            "data": "synthetic (seeded counter-based OPT weights + prompts, pipo_synth)",
+            "config": {"workload": f"{args.config}: {c['desc']}", "global_batch": b * world, "seq_len": P,
+                       "gen": G, "n_layers": s.n_layers, "d_model": s.d_model,
+                       "parallelism": f"batch-shard x{world} (no hot-path collective)",
+                       "weight_tier": ["device", "host", "disk"][c["weight_tier"]],
+                       "kv_tier": ["device", "host"][c["kv_tier"]], "ring_layers": args.ring,
+                       "l2": "inputs larger than L2 (every step streams all layer weights through HBM)"},
+            "clocks": clocks,
+            "e2e": e2e,
+            "gpu_launches": int(st["kernel_launches"]),
+            "link_roofline": {"bound": "host-link", "bytes_per_step": int(layer_bytes),
+                              "probe_gbs": link_probe, "achieved_gbs": layer_bytes / (ms / 1e3) / 1e9,
+                              "frac": link_floor_s / (ms / 1e3), "copy_engine_gbs": st["h2d_gbs"]},
+            "busy": {"union": st["union_busy"], "copy": st["copy_busy"], "kernel": st["kernel_busy"]},
+            "setup": {"load_s": t_load, "prefill_s": t_prefill, "hbm_bytes": st["hbm_bytes"],
+                      "pinned_host_bytes": st["pinned_host_bytes"]},
+            "peaks": {"hbm_gbs": peaks.get("hbm_gbs"), "bf16_tflops": peaks.get("bf16_tflops")},
+        }
+    pl.close()
+    if rank == 0 and not args.no_cpu_baseline and world == 1:
+        tps, desc, cores, _ = oracle_sample(args.config, args.wfmt)
+        line["cpu_baseline"] = {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": desc}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_pipo(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,218 @@
+/*
+ * pipo.h — C-ABI of the B200-native PIPO hot path (arXiv 2504.03664).
+ *
+ * PIPO = "pipelined offloading" (§3).  This library implements
+ * its data-parallel hot path for OPT decoders: weights (and optionally the KV
+ * cache) live off-GPU — pinned host memory (§3.1.1) or files on disk
+ * read through a pinned host ring (§3.3) — and are streamed to
+ * HBM chunk by chunk on a copy stream while the GPU computes the previous layer
+ * (Alg. 1; "weight loading ... overlapping with the computation
+ * of the previous layer").  Linear layers run as fused int4-g64
+ * unpack+scale GEMV/GEMM kernels (§3.4) or fp16 GEMMs
+ * (PAPER.md:396), attention as a decode kernel over the KV cache.
+ *
+ * The call sequence follows the paper's workflow (Alg. 2):
+ *   pipeline_init              ~ Configure + InitModel + InitTransferSuitAndOperators
+ *   load_layer_weights (xl+1)  ~ InitModel (host store: quantize, merge, pin)
+ *   prefill / decode_step      ~ PipelineScheduling (Alg. 1) for one token step
+ *   pipeline_stats             ~ the paper's throughput / GPU-utilisation metrics
+ *   pipeline_destroy
+ *
+ * Conventions (all functions):
+ *  - Every pointer argument is a HOST pointer unless its name ends in `_dev`.
+ *  - The caller owns every pointer it passes; the library copies what it keeps
+ *    before returning.  The context owns all device memory, streams, events and
+ *    pinned/disk storage it allocates, and frees them in pipeline_destroy().
+ *  - Calls on one context must come from one host thread at a time.  Different
+ *    contexts (one per GPU / process) share no state.
+ *  - Return value: PIPO_OK or an error status; pipo_last_error() gives a
+ *    thread-local human-readable message for the last failing call.
+ *  - After any CUDA error the context is poisoned: every later call on it returns
+ *    PIPO_E_STATE (pipeline_destroy still frees it).
+ *  - No CPU fallback exists: when no sm_100 device is present pipeline_init
+ *    returns PIPO_E_CUDA.
+ */
+#ifndef PIPO_H_
+#define PIPO_H_
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PIPO_ABI_VERSION 1
+
+typedef enum {
+  PIPO_OK = 0,
+  PIPO_E_INVALID_ARG = 1, /* bad shape/size/pointer; SPEC.md:469 ShapeError, :226 LayoutError */
+  PIPO_E_STATE = 2,       /* wrong call order (decode before prefill), poisoned context */
+  PIPO_E_OOM = 3,         /* device/pinned allocation failed; SPEC.md:236 OutOfMemory */
+  PIPO_E_IO = 4,          /* disk-tier read/write failure; SPEC.md:167 IoError */
+  PIPO_E_FORMAT = 5,      /* disk-tier blob header/size mismatch; SPEC.md:246 FormatError */
+  PIPO_E_INFEASIBLE = 6,  /* configuration cannot fit (Eq. 1) */
+  PIPO_E_CUDA = 7         /* CUDA runtime error / no usable device */
+} pipo_status;
+
+typedef enum { PIPO_W_FP16 = 0, PIPO_W_INT4_G64 = 1 } pipo_wfmt;
+
+/* Storage tiers of Eq. (1).  DEVICE = all layer weights
+ * resident in HBM (no streaming; the tier-invariance reference).  HOST = pinned
+ * host memory, streamed per layer.  DISK = one blob file per layer under
+ * cfg.disk_dir, read by a reader-thread pool into a pinned ring, then streamed. */
+typedef enum { PIPO_TIER_DEVICE = 0, PIPO_TIER_HOST = 1, PIPO_TIER_DISK = 2 } pipo_tier;
+
+/* flags */
+#define PIPO_F_TIMELINE 1u  /* record per-segment CUDA events for busy fractions (default on) */
+
+typedef struct {
+  int32_t device;        /* CUDA ordinal */
+  /* model shape (OPT): d_model % 64 == 0, ffn_dim % 64 == 0, n_heads | d_model,
+   * head_dim = d_model / n_heads in {64, 128}                                  */
+  int32_t d_model, n_layers, n_heads, ffn_dim, vocab, max_pos;  /* OPT: max_pos 2048 */
+  /* workload capacity: KV cache holds max_batch x max_seq positions
+   * (s = prompt + generated)                                     */
+  int32_t max_batch, max_seq;
+  int32_t wfmt;          /* pipo_wfmt for the four decoder linear weights            */
+  int32_t weight_tier;   /* pipo_tier: where decoder-layer weights live              */
+  int32_t kv_tier;       /* PIPO_TIER_DEVICE or PIPO_TIER_HOST         */
+  int32_t ring_layers;   /* HBM weight ring depth in layers: >= 2 = performance-optimized
+                            pipeline (preload next layer); 1 = memory-
+                            efficient (one layer resident). 0 -> 2    */
+  int64_t chunk_bytes;   /* blockwise-transfer chunk; 0 -> whole segment */
+  int32_t gemv_max_m;    /* rows M <= this use the CUDA-core int4 GEMV (PAPER.md:360
+                            "batch sizes less than 16"); larger M the tensor-core GEMM.
+                            0 -> 15                                                  */
+  int32_t disk_threads;  /* DISK tier reader threads; 0 -> 4        */
+  const char* disk_dir;  /* DISK tier directory (copied at init)                      */
+  uint32_t flags;        /* PIPO_F_*                                                   */
+} pipo_config;
+
+/* fp32 masters (values must be finite; fp16-representable for exact parity).
+ * Row-major.  w_qkv rows are q | k | v ([3d][d]); w_out [d][d]; w_fc1 [F][d];
+ * w_fc2 [d][F]; vectors have the obvious lengths. */
+typedef struct {
+  const float *ln1_g, *ln1_b, *w_qkv, *b_qkv, *w_out, *b_out;
+  const float *ln2_g, *ln2_b, *w_fc1, *b_fc1, *w_fc2, *b_fc2;
+} pipo_layer_weights;
+
+/* tok [vocab][d], pos [max_pos + 2][d] (OPT learned positions, offset 2), final LN. */
+typedef struct {
+  const float *tok, *pos, *lnf_g, *lnf_b;
+} pipo_embed_weights;
+
+#define PIPO_LAYER_EMBED (-1)
+
+typedef struct {
+  int64_t prefill_calls, decode_steps, tokens_generated;
+  double prefill_s, decode_s;     /* wall seconds inside prefill / decode_step calls */
+  double ttft_s;                  /* last prefill call's wall time (first token)      */
+  double decode_tokens_per_s;     /* b * decode_steps / decode_s                       */
+  int64_t h2d_bytes, d2h_bytes;   /* streamed weight + KV bytes, token ids              */
+  double h2d_gbs;                 /* h2d_bytes / copy-busy seconds (decode window)     */
+  double copy_busy, kernel_busy, union_busy;  /* fractions of the decode window (Q9)   */
+  double window_s;                /* decode window measured by device events           */
+  int64_t kernel_launches;        /* library kernels launched since the last reset     */
+  int64_t hbm_bytes;              /* device bytes allocated by the context             */
+  int64_t pinned_host_bytes;      /* pinned host bytes allocated by the context        */
+} pipo_stats;
+
+/* ---- lifecycle ---------------------------------------------------------- */
+
+/* Validate cfg, select the device, allocate the HBM ring, KV cache, activation
+ * workspace and resident embeddings, create streams/events.
+ * Errors: INVALID_ARG (shape rules above), OOM, CUDA.  *out is NULL on error. */
+typedef struct pipo_ctx pipo_ctx;
+pipo_status pipeline_init(const pipo_config* cfg, pipo_ctx** out);
+void pipeline_destroy(pipo_ctx* ctx);
+const char* pipo_last_error(void);
+int32_t pipo_abi_version(void);
+
+/* ---- host store (InitModel) --------------------------------------------- */
+
+/* Decoder layer `layer` in [0, n_layers), or PIPO_LAYER_EMBED with a
+ * pipo_embed_weights*.  Decoder weights are quantized (wfmt INT4: SURVEY.md
+ * §8(c) step 1) or rounded to fp16, merged in consumption order into one blob
+ * (data merging) and placed in the layer's tier.  Embeddings
+ * are always resident in HBM (reading Q20).  Synchronous; the caller may free w
+ * on return.  Errors: INVALID_ARG (range, non-finite / fp16-overflowing input),
+ * OOM, IO (disk tier). */
+pipo_status load_layer_weights(pipo_ctx* ctx, int32_t layer, const void* w);
+
+/* Same tensors drawn on the GPU by the library's own implementation of the
+ * pipo_synth counter-based generator — used for the
+ * large configurations where fp32 masters would not fit a test host.  The
+ * quantizer is the same definition (bit-exact with the host path). */
+pipo_status pipo_load_synthetic(pipo_ctx* ctx, int32_t layer, uint64_t seed);
+
+/* ---- PipelineScheduling (Alg. 1) ---------------------------------------- */
+
+/* Start a new batch: b sequences of P prompt tokens (tokens: [b][P] int32, ids
+ * in [0, vocab)).  Runs every layer with M = b*P rows, writes P KV positions,
+ * returns the greedy next token per sequence (next: [b]) and optionally the
+ * last-position logits (logits: [b][vocab] fp32, may be NULL).
+ * Errors: INVALID_ARG (b > max_batch, P >= max_seq, P + 2 > max_pos + 2),
+ * STATE (missing weights). */
+pipo_status prefill(pipo_ctx* ctx, const int32_t* tokens, int32_t b, int32_t P,
+                    int32_t* next, float* logits);
+
+/* One decode step for the current batch: feeds tokens[b] at position past,
+ * attends over past+1 positions.  Returns next[b] and optional logits[b][vocab].
+ * Errors: STATE (no prefill yet), INVALID_ARG (KV capacity max_seq exceeded). */
+pipo_status decode_step(pipo_ctx* ctx, const int32_t* tokens, int32_t* next, float* logits);
+
+/* Device-resident variant of decode_step (inputs already in HBM): tokens_dev and
+ * next_dev are device int32[b] buffers (may alias: next overwrites tokens). */
+pipo_status decode_step_dev(pipo_ctx* ctx, const int32_t* tokens_dev, int32_t* next_dev);
+
+pipo_status pipeline_stats(pipo_ctx* ctx, pipo_stats* out);
+pipo_status pipeline_stats_reset(pipo_ctx* ctx);
+
+/* cudaStream_t of the compute stream (which=0) or weight-copy stream (which=1),
+ * as an opaque handle for external CUDA-event timing. */
+void* pipo_stream(pipo_ctx* ctx, int32_t which);
+
+/* ---- test / measurement hooks (parity contract SURVEY.md §8(c)) ----------- */
+
+/* Host quantizer (no GPU): w [rows][cols] fp32, cols % 64 == 0 ->
+ * codes [rows][cols/2] packed (low nibble = even k), scales [rows][cols/64]
+ * fp16 bits.  Errors: INVALID_ARG (non-finite, fp16-overflowing scale). */
+pipo_status pipo_quantize_int4_g64(const float* w, int64_t rows, int64_t cols,
+                                   uint8_t* codes, uint16_t* scales);
+
+/* GPU quantizer (same definition), device-side; all host buffers as above. */
+pipo_status pipo_quantize_int4_g64_gpu(pipo_ctx* ctx, const float* w, int64_t rows,
+                                       int64_t cols, uint8_t* codes, uint16_t* scales);
+
+/* Kernel K8: unpack + scale on the GPU: out[r][k] = fp16_rne(q * s), fp16 bits. */
+pipo_status pipo_unpack_int4_g64(pipo_ctx* ctx, const uint8_t* codes, const uint16_t* scales,
+                                 int64_t rows, int64_t cols, uint16_t* out);
+
+/* One fused linear layer on the GPU through the production kernels:
+ * y[M][N] = x[M][K] . W^T + bias (bias may be NULL).  x fp16 bits [M][K];
+ * W given as fp32 masters [N][K] (quantized per wfmt inside); y fp32 [M][N].
+ * path: 0 = automatic (as the pipeline chooses), 1 = int4 GEMV, 2 = GEMM. */
+pipo_status pipo_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, const uint16_t* x,
+                        const float* w, const float* bias, int32_t M, int32_t N, int32_t K,
+                        float* y);
+
+/* Decode attention kernel: q [b][d] fp16 bits (pre-scaled), k/v [L][b][d] fp16
+ * bits (position-major) -> o [b][d] fp32.  n_heads | d. */
+pipo_status pipo_attention_decode(pipo_ctx* ctx, const uint16_t* q, const uint16_t* k,
+                                  const uint16_t* v, int32_t b, int32_t L, int32_t d,
+                                  int32_t n_heads, float* o);
+
+/* Capture per-layer hidden states of the next prefill/decode call:
+ * on != 0 -> after that call, out receives [n_layers][b][n][d] fp32 (n = P for
+ * prefill, 1 for decode).  out must stay valid until that call returns. */
+pipo_status pipo_debug_capture(pipo_ctx* ctx, int32_t on, float* out);
+
+/* H2D probe: best-of-`reps` pinned->device cudaMemcpyAsync bandwidth (GB/s) for
+ * `bytes`-sized copies on the weight-copy stream (App. A sweep). */
+pipo_status pipo_probe_h2d(pipo_ctx* ctx, int64_t bytes, int32_t reps, double* gbs);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PIPO_H_ */

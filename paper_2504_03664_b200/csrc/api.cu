@@ -1,0 +1,998 @@
+// api.cu — the C-ABI (include/pipo.h) and the pipeline scheduler.
+//
+// Algorithm 1 as a CUDA stream/event DAG instead of a thread
+// pool:
+//   CallLoadData(i, j)        -> enqueue_copy(): cudaMemcpyAsync of the layer's merged
+//                                blob, segment by segment, on the weight-copy stream
+//                                into an HBM ring slot; one event per landed segment.
+//                                Prefetch runs R-1 layers ahead (performance-optimized
+//                                pipeline) and across token steps.
+//   PrepareInput(i, j)        -> embedding gather for j = 0; otherwise the hidden state
+//                                already lives in HBM.
+//   SynchronizeLoadTask(i, j) -> cudaStreamWaitEvent(compute, segment-ready) right
+//                                before the first kernel that reads the segment: the
+//                                GPU consumes each segment as soon as it lands; the
+//                                host never blocks.
+//   Compute(i, j)             -> LN1+QKV, attention, out-proj, LN2+FC1, FC2 kernels.
+//   CallStoreCache(i, j)      -> (host-resident KV) D2H of the new KV positions on a
+//                                save stream after attention; its completion event is
+//                                waited for only by the copy stream before the SAME
+//                                layer's KV load in the next step (PAPER.md:162-165,
+//                                243-245).
+// The ring slot of layer G is released by an event recorded after its last kernel;
+// the copy stream waits on it before overwriting the slot (WAR).  Weight loads are
+// gated only by ring capacity: with ring_layers = 2 the next layer loads while the
+// current one computes; ring_layers = 1 is the memory-efficient
+// pipeline, which serialises copy and compute.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "ctx.h"
+#include "disk.h"
+
+using namespace pipo;
+
+namespace {
+
+thread_local std::string g_err;
+
+pipo_status set_err(pipo_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+pipo_status cuda_fail(pipo_ctx* c, cudaError_t e, const char* what, int line) {
+  if (c) c->poisoned = true;
+  char buf[512];
+  snprintf(buf, sizeof buf, "CUDA error %s (%s) at api.cu:%d: %s", cudaGetErrorName(e), cudaGetErrorString(e),
+           line, what);
+  return set_err(PIPO_E_CUDA, buf);
+}
+
+#define CK(x)                                                 \
+  do {                                                        \
+    cudaError_t e_ = (x);                                     \
+    if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #x, __LINE__); \
+  } while (0)
+
+// account a launcher's result: n kernels launched, n < 0 = unsupported config
+#define LAUNCH(expr)                                                           \
+  do {                                                                         \
+    int n_ = (expr);                                                           \
+    if (n_ < 0) return set_err(PIPO_E_INVALID_ARG, "unsupported kernel configuration: " #expr); \
+    ctx->launches += n_;                                                       \
+    CK(cudaGetLastError());                                                    \
+  } while (0)
+
+#define CHECK_CTX()                                                                  \
+  do {                                                                               \
+    if (!ctx) return set_err(PIPO_E_INVALID_ARG, "null context");                    \
+    if (ctx->poisoned) return set_err(PIPO_E_STATE, "context poisoned by an earlier CUDA error"); \
+  } while (0)
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+template <typename T>
+pipo_status dev_alloc(pipo_ctx* ctx, T** p, int64_t bytes) {
+  if (bytes <= 0) { *p = nullptr; return PIPO_OK; }
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), (size_t)bytes);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    return set_err(PIPO_E_OOM, "cudaMalloc of " + std::to_string(bytes) + " bytes failed");
+  }
+  CK(e);
+  ctx->hbm_bytes += bytes;
+  return PIPO_OK;
+}
+
+template <typename T>
+pipo_status host_alloc(pipo_ctx* ctx, T** p, int64_t bytes) {
+  if (bytes <= 0) { *p = nullptr; return PIPO_OK; }
+  cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(p), (size_t)bytes, cudaHostAllocDefault);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    return set_err(PIPO_E_OOM, "cudaHostAlloc of " + std::to_string(bytes) + " bytes failed");
+  }
+  CK(e);
+  ctx->pinned_bytes += bytes;
+  return PIPO_OK;
+}
+
+#define TRY(x)                         \
+  do {                                 \
+    pipo_status s_ = (x);              \
+    if (s_ != PIPO_OK) return s_;      \
+  } while (0)
+
+// ---- timeline ---------------------------------------------------------------
+pipo_status ev_get(pipo_ctx* ctx, cudaEvent_t* ev) {
+  if (ctx->ev_used == ctx->ev_pool.size()) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    ctx->ev_pool.push_back(e);
+  }
+  *ev = ctx->ev_pool[ctx->ev_used++];
+  return PIPO_OK;
+}
+
+pipo_status span_begin(pipo_ctx* ctx, cudaStream_t st, cudaEvent_t* a) {
+  if (!ctx->timeline) return PIPO_OK;
+  TRY(ev_get(ctx, a));
+  CK(cudaEventRecord(*a, st));
+  return PIPO_OK;
+}
+
+pipo_status span_end(pipo_ctx* ctx, cudaStream_t st, cudaEvent_t a, int lane, int64_t bytes) {
+  if (!ctx->timeline) return PIPO_OK;
+  cudaEvent_t b;
+  TRY(ev_get(ctx, &b));
+  CK(cudaEventRecord(b, st));
+  ctx->spans.push_back(Span{a, b, lane, bytes});
+  return PIPO_OK;
+}
+
+// ---- pointers into a layer blob -----------------------------------------------
+const __half* vec_ptr(const pipo_ctx* c, const uint8_t* blob, int v) {
+  return reinterpret_cast<const __half*>(blob + c->lay.vec_off[v]);
+}
+
+bool streamed(const pipo_ctx* c) { return c->weight_tier != PIPO_TIER_DEVICE; }
+bool host_kv(const pipo_ctx* c) { return c->kv_tier == PIPO_TIER_HOST; }
+
+__half* kv_ptr(pipo_ctx* c, int layer, int which, int64_t G) {
+  if (host_kv(c)) return c->kv_slot + ((G % c->R) * 2 + which) * c->kv_elems;
+  return c->kv_dev + ((int64_t)layer * 2 + which) * c->kv_elems;
+}
+
+// H2D copy of one contiguous byte range in chunks (blockwise transfer)
+pipo_status copy_chunks(pipo_ctx* ctx, void* dst, const void* src, int64_t bytes) {
+  const int64_t ch = ctx->chunk > 0 ? ctx->chunk : bytes;
+  for (int64_t off = 0; off < bytes; off += ch) {
+    const int64_t n = std::min(ch, bytes - off);
+    CK(cudaMemcpyAsync(static_cast<uint8_t*>(dst) + off, static_cast<const uint8_t*>(src) + off, (size_t)n,
+                       cudaMemcpyHostToDevice, ctx->s_copy));
+  }
+  return PIPO_OK;
+}
+
+// CallLoadData for global layer G: weights (+ KV positions [0, kv_pos) if host KV).
+pipo_status enqueue_copy(pipo_ctx* ctx, int64_t G, int64_t kv_pos) {
+  const int j = (int)(G % ctx->l), slot = (int)(G % ctx->R);
+  if (G >= ctx->R) CK(cudaStreamWaitEvent(ctx->s_copy, ctx->ev_free[slot], 0));
+  cudaEvent_t t0 = nullptr;
+  TRY(span_begin(ctx, ctx->s_copy, &t0));
+  uint8_t* dst = ctx->ring + (int64_t)slot * ctx->layer_bytes;
+  int64_t bytes = 0;
+  for (int s = 0; s < 4; ++s) {
+    if (ctx->disk) {
+      TRY(disk_enqueue_segment(ctx, j, s, dst + ctx->lay.seg_off[s]));
+    } else {
+      const uint8_t* src = ctx->host_store + (int64_t)j * ctx->layer_bytes;
+      TRY(copy_chunks(ctx, dst + ctx->lay.seg_off[s], src + ctx->lay.seg_off[s], ctx->lay.seg_bytes[s]));
+    }
+    bytes += ctx->lay.seg_bytes[s];
+    CK(cudaEventRecord(ctx->ev_ready[slot][s], ctx->s_copy));
+    if (s == 0 && host_kv(ctx)) {
+      // KV load advanced with the layer's MHA weights (reading Q6)
+      if (G >= ctx->R) CK(cudaStreamWaitEvent(ctx->s_copy, ctx->ev_kv_free[slot], 0));
+      CK(cudaStreamWaitEvent(ctx->s_copy, ctx->ev_saved[j], 0));   // A6 fence
+      const int64_t n = kv_pos * ctx->b_cur * ctx->d;
+      if (n > 0) {
+        for (int w = 0; w < 2; ++w) {
+          const __half* src = ctx->kv_host + ((int64_t)j * 2 + w) * ctx->kv_elems;
+          TRY(copy_chunks(ctx, kv_ptr(ctx, j, w, G), src, n * 2));
+        }
+        bytes += 2 * n * 2;
+      }
+      ctx->kv_load_past[slot] = kv_pos;
+      CK(cudaEventRecord(ctx->ev_ready[slot][4], ctx->s_copy));
+    }
+  }
+  ctx->h2d_bytes += bytes;
+  TRY(span_end(ctx, ctx->s_copy, t0, 0, bytes));
+  return PIPO_OK;
+}
+
+pipo_status enqueue_kv_only(pipo_ctx* ctx, int64_t G, int64_t kv_pos) {
+  // DEVICE weights + HOST KV: only the KV loading task runs on the copy stream
+  const int j = (int)(G % ctx->l), slot = (int)(G % ctx->R);
+  if (G >= ctx->R) CK(cudaStreamWaitEvent(ctx->s_copy, ctx->ev_kv_free[slot], 0));
+  CK(cudaStreamWaitEvent(ctx->s_copy, ctx->ev_saved[j], 0));
+  cudaEvent_t t0 = nullptr;
+  TRY(span_begin(ctx, ctx->s_copy, &t0));
+  const int64_t n = kv_pos * ctx->b_cur * ctx->d;
+  for (int w = 0; w < 2 && n > 0; ++w) {
+    const __half* src = ctx->kv_host + ((int64_t)j * 2 + w) * ctx->kv_elems;
+    TRY(copy_chunks(ctx, kv_ptr(ctx, j, w, G), src, n * 2));
+  }
+  ctx->kv_load_past[slot] = kv_pos;
+  CK(cudaEventRecord(ctx->ev_ready[slot][4], ctx->s_copy));
+  ctx->h2d_bytes += n > 0 ? 2 * n * 2 : 0;
+  TRY(span_end(ctx, ctx->s_copy, t0, 0, n > 0 ? 4 * n : 0));
+  return PIPO_OK;
+}
+
+// one forward pass over all layers: rows M = b * n at positions past .. past+n-1
+pipo_status forward(pipo_ctx* ctx, int b, int n, int past, bool want_logits) {
+  const int M = b * n, d = ctx->d;
+  cudaStream_t cs = ctx->s_comp;
+  const int64_t next_pass_kv = past + n;   // KV positions the next (decode) pass loads
+  LAUNCH(launch_embed(ctx->ids, b, n, past, ctx->tok, ctx->tok_lay.n_kb, ctx->pos, d, ctx->h, cs));
+  LinearArgs la;
+  la.ws = ctx->ws; la.ws_floats = ctx->ws_floats; la.counters = ctx->counters; la.n_counters = ctx->n_counters;
+  la.num_sms = ctx->num_sms; la.M = M;
+  AttnArgs aa;
+  aa.b = b; aa.n = n; aa.past = past; aa.d = d; aa.n_heads = ctx->H; aa.kv_b = b;
+  aa.ws = ctx->ws; aa.ws_floats = ctx->ws_floats; aa.num_sms = ctx->num_sms;
+  const int64_t pass_base = ctx->g_comp;
+
+  for (int j = 0; j < ctx->l; ++j) {
+    const int64_t G = ctx->g_comp++;
+    const int slot = (int)(G % ctx->R);
+    if (streamed(ctx) || host_kv(ctx)) {
+      while (ctx->g_copy <= G + ctx->R - 1) {
+        const int64_t Gc = ctx->g_copy;
+        const bool this_pass = Gc < pass_base + ctx->l;
+        const int64_t kv = this_pass ? (n == 1 ? past : 0) : next_pass_kv;
+        if (streamed(ctx)) {
+          TRY(enqueue_copy(ctx, Gc, kv));
+        } else {
+          TRY(enqueue_kv_only(ctx, Gc, kv));
+        }
+        ctx->g_copy++;
+      }
+    }
+    const uint8_t* blob = streamed(ctx) ? ctx->ring + (int64_t)slot * ctx->layer_bytes
+                                        : ctx->dev_store + (int64_t)j * ctx->layer_bytes;
+    __half* kc = kv_ptr(ctx, j, 0, G);
+    __half* vc = kv_ptr(ctx, j, 1, G);
+    if (host_kv(ctx) && n == 1 && ctx->kv_load_past[slot] != past)
+      return set_err(PIPO_E_STATE, "internal: KV prefetch range mismatch");
+    cudaEvent_t t0;
+    // ---- MHA: LN1 + QKV + attention (seg 0) ----
+    if (streamed(ctx)) CK(cudaStreamWaitEvent(cs, ctx->ev_ready[slot][0], 0));
+    if (host_kv(ctx)) CK(cudaStreamWaitEvent(cs, ctx->ev_ready[slot][4], 0));
+    TRY(span_begin(ctx, cs, &t0));
+    LAUNCH(launch_layernorm(ctx->h, d, M, d, vec_ptr(ctx, blob, V_LN1_G), vec_ptr(ctx, blob, V_LN1_B), ctx->xa, cs));
+    la.x = ctx->xa; la.w = blob + ctx->lay.mat_off[M_QKV]; la.wfmt = ctx->wfmt; la.N = 3 * d; la.K = d;
+    la.epi = EpiParams{};
+    la.epi.kind = EPI_QKV; la.epi.bias = vec_ptr(ctx, blob, V_B_QKV); la.epi.M = M; la.epi.N = 3 * d;
+    la.epi.q = ctx->q; la.epi.kc = kc; la.epi.vc = vc; la.epi.d = d; la.epi.n_tok = n; la.epi.past = past;
+    la.epi.kv_b = b; la.epi.qscale = 1.0f / sqrtf((float)ctx->hd);
+    LAUNCH(launch_linear(la, PATH_AUTO, ctx->gemv_max_m, cs));
+    aa.q = ctx->q; aa.kc = kc; aa.vc = vc; aa.o = ctx->xa;
+    if (n == 1) LAUNCH(launch_attention_decode(aa, cs));
+    else LAUNCH(launch_attention_prefill(aa, cs));
+    TRY(span_end(ctx, cs, t0, 1, 0));
+    if (host_kv(ctx)) {
+      // CallStoreCache: save the new positions after MHA on the save stream
+      CK(cudaEventRecord(ctx->ev_attn[slot], cs));
+      CK(cudaStreamWaitEvent(ctx->s_save, ctx->ev_attn[slot], 0));
+      cudaEvent_t s0;
+      TRY(span_begin(ctx, ctx->s_save, &s0));
+      const int64_t off = (int64_t)past * b * d, cnt = (int64_t)n * b * d;
+      for (int w = 0; w < 2; ++w) {
+        __half* dst = ctx->kv_host + ((int64_t)j * 2 + w) * ctx->kv_elems + off;
+        CK(cudaMemcpyAsync(dst, kv_ptr(ctx, j, w, G) + off, (size_t)cnt * 2, cudaMemcpyDeviceToHost, ctx->s_save));
+      }
+      ctx->d2h_bytes += 2 * cnt * 2;
+      CK(cudaEventRecord(ctx->ev_saved[j], ctx->s_save));
+      CK(cudaEventRecord(ctx->ev_kv_free[slot], ctx->s_save));
+      TRY(span_end(ctx, ctx->s_save, s0, 2, 2 * cnt * 2));
+    }
+    // ---- MHA out-proj + residual (seg 1) ----
+    if (streamed(ctx)) CK(cudaStreamWaitEvent(cs, ctx->ev_ready[slot][1], 0));
+    TRY(span_begin(ctx, cs, &t0));
+    la.x = ctx->xa; la.w = blob + ctx->lay.mat_off[M_OUT]; la.N = d; la.K = d;
+    la.epi = EpiParams{};
+    la.epi.kind = EPI_RESID; la.epi.bias = vec_ptr(ctx, blob, V_B_OUT); la.epi.M = M; la.epi.N = d; la.epi.h = ctx->h;
+    LAUNCH(launch_linear(la, PATH_AUTO, ctx->gemv_max_m, cs));
+    TRY(span_end(ctx, cs, t0, 1, 0));
+    // ---- MLP: LN2 + FC1 + ReLU (seg 2) ----
+    if (streamed(ctx)) CK(cudaStreamWaitEvent(cs, ctx->ev_ready[slot][2], 0));
+    TRY(span_begin(ctx, cs, &t0));
+    LAUNCH(launch_layernorm(ctx->h, d, M, d, vec_ptr(ctx, blob, V_LN2_G), vec_ptr(ctx, blob, V_LN2_B), ctx->xa, cs));
+    la.x = ctx->xa; la.w = blob + ctx->lay.mat_off[M_FC1]; la.N = ctx->F; la.K = d;
+    la.epi = EpiParams{};
+    la.epi.kind = EPI_RELU; la.epi.bias = vec_ptr(ctx, blob, V_B_FC1); la.epi.M = M; la.epi.N = ctx->F; la.epi.u = ctx->u;
+    LAUNCH(launch_linear(la, PATH_AUTO, ctx->gemv_max_m, cs));
+    TRY(span_end(ctx, cs, t0, 1, 0));
+    // ---- MLP: FC2 + residual (seg 3) ----
+    if (streamed(ctx)) CK(cudaStreamWaitEvent(cs, ctx->ev_ready[slot][3], 0));
+    TRY(span_begin(ctx, cs, &t0));
+    la.x = ctx->u; la.w = blob + ctx->lay.mat_off[M_FC2]; la.N = d; la.K = ctx->F;
+    la.epi = EpiParams{};
+    la.epi.kind = EPI_RESID; la.epi.bias = vec_ptr(ctx, blob, V_B_FC2); la.epi.M = M; la.epi.N = d; la.epi.h = ctx->h;
+    LAUNCH(launch_linear(la, PATH_AUTO, ctx->gemv_max_m, cs));
+    TRY(span_end(ctx, cs, t0, 1, 0));
+    if (streamed(ctx)) CK(cudaEventRecord(ctx->ev_free[slot], cs));   // ring slot release (a12)
+    if (ctx->cap_on)
+      CK(cudaMemcpyAsync(ctx->cap_dev + (int64_t)j * M * d, ctx->h, (size_t)M * d * 4, cudaMemcpyDeviceToDevice, cs));
+  }
+  // ---- output embedding: final LN (last position of each sequence), LM head, argmax (a13) ----
+  cudaEvent_t t0;
+  TRY(span_begin(ctx, cs, &t0));
+  LAUNCH(launch_layernorm(ctx->h + (int64_t)(n - 1) * d, (int64_t)n * d, b, d, ctx->lnf_g, ctx->lnf_b, ctx->xa, cs));
+  la.x = ctx->xa; la.w = reinterpret_cast<const uint8_t*>(ctx->tok); la.wfmt = 0; la.M = b; la.N = ctx->V; la.K = d;
+  la.epi = EpiParams{};
+  la.epi.kind = EPI_F32; la.epi.M = b; la.epi.N = ctx->V; la.epi.y = ctx->logits; la.epi.ldy = ctx->V;
+  LAUNCH(launch_linear(la, PATH_GEMM, ctx->gemv_max_m, cs));
+  LAUNCH(launch_argmax(ctx->logits, b, ctx->V, ctx->V, ctx->next, cs));
+  TRY(span_end(ctx, cs, t0, 1, 0));
+  (void)want_logits;
+  return PIPO_OK;
+}
+
+pipo_status finish_call(pipo_ctx* ctx, int b, int n, int32_t* next, float* logits) {
+  CK(cudaMemcpyAsync(ctx->pin_next, ctx->next, (size_t)b * 4, cudaMemcpyDeviceToHost, ctx->s_comp));
+  ctx->d2h_bytes += (int64_t)b * 4;
+  if (logits) {
+    CK(cudaMemcpyAsync(logits, ctx->logits, (size_t)b * ctx->V * 4, cudaMemcpyDeviceToHost, ctx->s_comp));
+    ctx->d2h_bytes += (int64_t)b * ctx->V * 4;
+  }
+  if (ctx->cap_on) {
+    CK(cudaMemcpyAsync(ctx->cap_host, ctx->cap_dev, (size_t)ctx->l * b * n * ctx->d * 4, cudaMemcpyDeviceToHost,
+                       ctx->s_comp));
+  }
+  CK(cudaStreamSynchronize(ctx->s_comp));
+  if (ctx->disk && disk_io_error(ctx)) {
+    ctx->poisoned = true;
+    return set_err(PIPO_E_IO, "disk tier read failed");
+  }
+  if (next) std::memcpy(next, ctx->pin_next, (size_t)b * 4);
+  ctx->cap_on = false;
+  return PIPO_OK;
+}
+
+pipo_status check_ready(pipo_ctx* ctx) {
+  if (!ctx->embed_loaded) return set_err(PIPO_E_STATE, "embedding weights not loaded");
+  for (int j = 0; j < ctx->l; ++j)
+    if (!ctx->layer_loaded[j]) return set_err(PIPO_E_STATE, "decoder layer " + std::to_string(j) + " not loaded");
+  return PIPO_OK;
+}
+
+pipo_status stage_ids(pipo_ctx* ctx, const int32_t* tokens, int64_t count) {
+  for (int64_t i = 0; i < count; ++i)
+    if (tokens[i] < 0 || tokens[i] >= ctx->V) return set_err(PIPO_E_INVALID_ARG, "token id out of range");
+  std::memcpy(ctx->pin_ids, tokens, (size_t)count * 4);
+  CK(cudaMemcpyAsync(ctx->ids, ctx->pin_ids, (size_t)count * 4, cudaMemcpyHostToDevice, ctx->s_comp));
+  ctx->h2d_bytes += count * 4;
+  return PIPO_OK;
+}
+
+pipo_status window_mark(pipo_ctx* ctx, bool start) {
+  if (start && !ctx->win_open) {
+    TRY(ev_get(ctx, &ctx->win_start));
+    CK(cudaEventRecord(ctx->win_start, ctx->s_comp));
+    ctx->win_open = true;
+  }
+  if (!start) {
+    TRY(ev_get(ctx, &ctx->win_end));
+    CK(cudaEventRecord(ctx->win_end, ctx->s_comp));
+  }
+  return PIPO_OK;
+}
+
+double union_len(std::vector<std::pair<double, double>>& v) {
+  std::sort(v.begin(), v.end());
+  double tot = 0, cs = -1, ce = -1;
+  for (auto& p : v) {
+    if (p.first > ce) {
+      if (ce > cs) tot += ce - cs;
+      cs = p.first;
+      ce = p.second;
+    } else {
+      ce = std::max(ce, p.second);
+    }
+  }
+  if (ce > cs) tot += ce - cs;
+  return tot;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pipo_last_error(void) { return g_err.c_str(); }
+int32_t pipo_abi_version(void) { return PIPO_ABI_VERSION; }
+
+pipo_status pipeline_init(const pipo_config* cfg, pipo_ctx** out) {
+  if (!out) return set_err(PIPO_E_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (!cfg) return set_err(PIPO_E_INVALID_ARG, "cfg is NULL");
+  const pipo_config& c = *cfg;
+  if (c.d_model <= 0 || c.d_model % 64 || c.n_layers <= 0 || c.n_heads <= 0 || c.d_model % c.n_heads ||
+      c.ffn_dim <= 0 || c.ffn_dim % 64 || c.vocab <= 0 || c.max_pos <= 0 || c.max_batch <= 0 || c.max_seq <= 1)
+    return set_err(PIPO_E_INVALID_ARG, "invalid model/workload shape");
+  const int hd = c.d_model / c.n_heads;
+  if (hd != 64 && hd != 128) return set_err(PIPO_E_INVALID_ARG, "head_dim must be 64 or 128");
+  if (c.d_model > 8192) return set_err(PIPO_E_INVALID_ARG, "d_model > 8192 unsupported");
+  if (c.max_seq > c.max_pos) return set_err(PIPO_E_INVALID_ARG, "max_seq exceeds max_pos");
+  if (c.wfmt != PIPO_W_FP16 && c.wfmt != PIPO_W_INT4_G64) return set_err(PIPO_E_INVALID_ARG, "bad wfmt");
+  if (c.weight_tier < 0 || c.weight_tier > 2) return set_err(PIPO_E_INVALID_ARG, "bad weight_tier");
+  if (c.kv_tier != PIPO_TIER_DEVICE && c.kv_tier != PIPO_TIER_HOST) return set_err(PIPO_E_INVALID_ARG, "bad kv_tier");
+  if (c.weight_tier == PIPO_TIER_DISK && (!c.disk_dir || !c.disk_dir[0]))
+    return set_err(PIPO_E_INVALID_ARG, "disk tier needs disk_dir");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return set_err(PIPO_E_CUDA, "no CUDA device (the library has no CPU fallback)");
+  }
+  if (c.device < 0 || c.device >= ndev) return set_err(PIPO_E_INVALID_ARG, "device ordinal out of range");
+
+  pipo_ctx* ctx = new pipo_ctx();
+  ctx->cfg = c;
+  ctx->disk_dir = c.disk_dir ? c.disk_dir : "";
+  ctx->cfg.disk_dir = nullptr;
+  ctx->d = c.d_model; ctx->l = c.n_layers; ctx->H = c.n_heads; ctx->F = c.ffn_dim; ctx->V = c.vocab;
+  ctx->hd = hd; ctx->max_b = c.max_batch; ctx->max_s = c.max_seq; ctx->wfmt = c.wfmt;
+  ctx->weight_tier = c.weight_tier; ctx->kv_tier = c.kv_tier;
+  ctx->R = c.ring_layers > 0 ? c.ring_layers : 2;
+  ctx->R = std::min({ctx->R, kMaxRing, ctx->l});
+  if (host_kv(ctx) && ctx->R < 2 && ctx->l >= 2) ctx->R = 2;
+  ctx->chunk = c.chunk_bytes;
+  ctx->gemv_max_m = c.gemv_max_m > 0 ? std::min(c.gemv_max_m, 16) : 15;
+  ctx->timeline = (c.flags & PIPO_F_TIMELINE) != 0;
+  ctx->lay = layer_layout(ctx->d, ctx->F, ctx->wfmt);
+  ctx->layer_bytes = ctx->lay.total;
+  ctx->layer_loaded.assign(ctx->l, 0);
+  ctx->ev_saved.assign(ctx->l, nullptr);
+  ctx->kv_load_past.assign(kMaxRing, -1);
+
+  auto fail = [&](pipo_status s) {
+    std::string m = g_err;
+    pipeline_destroy(ctx);
+    g_err = m;
+    return s;
+  };
+#define TRYI(x)                        \
+  do {                                 \
+    pipo_status s_ = (x);              \
+    if (s_ != PIPO_OK) return fail(s_); \
+  } while (0)
+#define CKI(x)                                                            \
+  do {                                                                    \
+    cudaError_t e_ = (x);                                                 \
+    if (e_ != cudaSuccess) return fail(cuda_fail(ctx, e_, #x, __LINE__)); \
+  } while (0)
+
+  CKI(cudaSetDevice(c.device));
+  cudaDeviceProp prop;
+  CKI(cudaGetDeviceProperties(&prop, c.device));
+  if (prop.major < 10) return fail(set_err(PIPO_E_CUDA, "device is not sm_100-class (built for sm_100a only)"));
+  ctx->num_sms = prop.multiProcessorCount;
+  CKI(cudaStreamCreateWithFlags(&ctx->s_comp, cudaStreamNonBlocking));
+  CKI(cudaStreamCreateWithFlags(&ctx->s_copy, cudaStreamNonBlocking));
+  CKI(cudaStreamCreateWithFlags(&ctx->s_save, cudaStreamNonBlocking));
+  for (int i = 0; i < kMaxRing; ++i) {
+    for (int s = 0; s < 5; ++s) CKI(cudaEventCreateWithFlags(&ctx->ev_ready[i][s], cudaEventDisableTiming));
+    CKI(cudaEventCreateWithFlags(&ctx->ev_free[i], cudaEventDisableTiming));
+    CKI(cudaEventCreateWithFlags(&ctx->ev_kv_free[i], cudaEventDisableTiming));
+    CKI(cudaEventCreateWithFlags(&ctx->ev_attn[i], cudaEventDisableTiming));
+  }
+  for (int j = 0; j < ctx->l; ++j) CKI(cudaEventCreateWithFlags(&ctx->ev_saved[j], cudaEventDisableTiming));
+
+  // resident embeddings
+  ctx->tok_lay = mat_layout(ctx->V, ctx->d, 0);
+  TRYI(dev_alloc(ctx, &ctx->tok, ctx->tok_lay.bytes));
+  TRYI(dev_alloc(ctx, &ctx->pos, (int64_t)(c.max_pos + 2) * ctx->d * 2));
+  TRYI(dev_alloc(ctx, &ctx->lnf_g, ctx->d * 2));
+  TRYI(dev_alloc(ctx, &ctx->lnf_b, ctx->d * 2));
+  // weights
+  if (ctx->weight_tier == PIPO_TIER_DEVICE) {
+    TRYI(dev_alloc(ctx, &ctx->dev_store, (int64_t)ctx->l * ctx->layer_bytes));
+  } else {
+    TRYI(dev_alloc(ctx, &ctx->ring, (int64_t)ctx->R * ctx->layer_bytes));
+    if (ctx->weight_tier == PIPO_TIER_HOST) {
+      TRYI(host_alloc(ctx, &ctx->host_store, (int64_t)ctx->l * ctx->layer_bytes));
+    } else {
+      TRYI(disk_open(ctx, c.disk_threads > 0 ? c.disk_threads : 4));
+    }
+  }
+  // KV cache
+  ctx->kv_elems = (int64_t)ctx->max_s * ctx->max_b * ctx->d;
+  if (host_kv(ctx)) {
+    TRYI(host_alloc(ctx, &ctx->kv_host, (int64_t)ctx->l * 2 * ctx->kv_elems * 2));
+    TRYI(dev_alloc(ctx, &ctx->kv_slot, (int64_t)ctx->R * 2 * ctx->kv_elems * 2));
+  } else {
+    TRYI(dev_alloc(ctx, &ctx->kv_dev, (int64_t)ctx->l * 2 * ctx->kv_elems * 2));
+  }
+  // activations
+  ctx->rows_cap = (int64_t)ctx->max_b * ctx->max_s;
+  TRYI(dev_alloc(ctx, &ctx->h, ctx->rows_cap * ctx->d * 4));
+  TRYI(dev_alloc(ctx, &ctx->xa, ctx->rows_cap * ctx->d * 2));
+  TRYI(dev_alloc(ctx, &ctx->q, ctx->rows_cap * ctx->d * 2));
+  TRYI(dev_alloc(ctx, &ctx->u, ctx->rows_cap * ctx->F * 2));
+  TRYI(dev_alloc(ctx, &ctx->logits, (int64_t)ctx->max_b * ctx->V * 4));
+  TRYI(dev_alloc(ctx, &ctx->ids, ctx->rows_cap * 4));
+  TRYI(dev_alloc(ctx, &ctx->next, (int64_t)ctx->max_b * 4));
+  TRYI(host_alloc(ctx, &ctx->pin_ids, ctx->rows_cap * 4));
+  TRYI(host_alloc(ctx, &ctx->pin_next, (int64_t)ctx->max_b * 4));
+  ctx->ws_floats = 16ll << 20;
+  TRYI(dev_alloc(ctx, &ctx->ws, ctx->ws_floats * 4));
+  ctx->n_counters = 1 << 16;
+  TRYI(dev_alloc(ctx, &ctx->counters, (int64_t)ctx->n_counters * 4));
+  CKI(cudaMemset(ctx->counters, 0, (size_t)ctx->n_counters * 4));
+  TRYI(dev_alloc(ctx, &ctx->quant_bad, 4));
+  CKI(cudaMemset(ctx->kv_dev ? (void*)ctx->kv_dev : (void*)ctx->kv_slot, 0,
+                 (size_t)(host_kv(ctx) ? ctx->R : ctx->l) * 2 * ctx->kv_elems * 2));
+  CKI(cudaDeviceSynchronize());
+  *out = ctx;
+  return PIPO_OK;
+#undef TRYI
+#undef CKI
+}
+
+void pipeline_destroy(pipo_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->cfg.device);
+  cudaDeviceSynchronize();
+  cudaGetLastError();
+  if (ctx->disk) disk_close(ctx);
+  void* dev[] = {ctx->tok, ctx->pos, ctx->lnf_g, ctx->lnf_b, ctx->dev_store, ctx->ring, ctx->kv_dev, ctx->kv_slot,
+                 ctx->h, ctx->xa, ctx->q, ctx->u, ctx->logits, ctx->ids, ctx->next, ctx->ws, ctx->counters,
+                 ctx->quant_bad, ctx->cap_dev};
+  for (void* p : dev)
+    if (p) cudaFree(p);
+  void* hst[] = {ctx->host_store, ctx->kv_host, ctx->pin_ids, ctx->pin_next};
+  for (void* p : hst)
+    if (p) cudaFreeHost(p);
+  for (int i = 0; i < kMaxRing; ++i) {
+    for (int s = 0; s < 5; ++s)
+      if (ctx->ev_ready[i][s]) cudaEventDestroy(ctx->ev_ready[i][s]);
+    if (ctx->ev_free[i]) cudaEventDestroy(ctx->ev_free[i]);
+    if (ctx->ev_kv_free[i]) cudaEventDestroy(ctx->ev_kv_free[i]);
+    if (ctx->ev_attn[i]) cudaEventDestroy(ctx->ev_attn[i]);
+  }
+  for (auto e : ctx->ev_saved)
+    if (e) cudaEventDestroy(e);
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  if (ctx->s_comp) cudaStreamDestroy(ctx->s_comp);
+  if (ctx->s_copy) cudaStreamDestroy(ctx->s_copy);
+  if (ctx->s_save) cudaStreamDestroy(ctx->s_save);
+  cudaGetLastError();
+  delete ctx;
+}
+
+pipo_status load_layer_weights(pipo_ctx* ctx, int32_t layer, const void* w) {
+  CHECK_CTX();
+  if (!w) return set_err(PIPO_E_INVALID_ARG, "weights pointer is NULL");
+  CK(cudaSetDevice(ctx->cfg.device));
+  if (layer == PIPO_LAYER_EMBED) {
+    const pipo_embed_weights* e = static_cast<const pipo_embed_weights*>(w);
+    if (!e->tok || !e->pos || !e->lnf_g || !e->lnf_b) return set_err(PIPO_E_INVALID_ARG, "NULL embedding tensor");
+    std::vector<uint8_t> tiled((size_t)ctx->tok_lay.bytes);
+    tile_fp16(e->tok, ctx->V, ctx->d, tiled.data());
+    CK(cudaMemcpy(ctx->tok, tiled.data(), tiled.size(), cudaMemcpyHostToDevice));
+    const int64_t npos = (int64_t)(ctx->cfg.max_pos + 2) * ctx->d;
+    std::vector<uint16_t> tmp((size_t)npos);
+    for (int64_t i = 0; i < npos; ++i) tmp[i] = f32_to_f16_rne(e->pos[i]);
+    CK(cudaMemcpy(ctx->pos, tmp.data(), (size_t)npos * 2, cudaMemcpyHostToDevice));
+    for (int64_t i = 0; i < ctx->d; ++i) tmp[i] = f32_to_f16_rne(e->lnf_g[i]);
+    CK(cudaMemcpy(ctx->lnf_g, tmp.data(), (size_t)ctx->d * 2, cudaMemcpyHostToDevice));
+    for (int64_t i = 0; i < ctx->d; ++i) tmp[i] = f32_to_f16_rne(e->lnf_b[i]);
+    CK(cudaMemcpy(ctx->lnf_b, tmp.data(), (size_t)ctx->d * 2, cudaMemcpyHostToDevice));
+    ctx->embed_loaded = true;
+    return PIPO_OK;
+  }
+  if (layer < 0 || layer >= ctx->l) return set_err(PIPO_E_INVALID_ARG, "layer index out of range");
+  const pipo_layer_weights* lw = static_cast<const pipo_layer_weights*>(w);
+  uint8_t* dst = nullptr;
+  std::vector<uint8_t> tmp;
+  if (ctx->weight_tier == PIPO_TIER_HOST) {
+    dst = ctx->host_store + (int64_t)layer * ctx->layer_bytes;
+  } else {
+    tmp.resize((size_t)ctx->layer_bytes);
+    dst = tmp.data();
+  }
+  if (!build_layer_blob(lw, ctx->lay, ctx->d, ctx->F, ctx->wfmt, dst))
+    return set_err(PIPO_E_INVALID_ARG, "non-finite weight, NULL tensor or fp16-overflowing group scale");
+  if (ctx->weight_tier == PIPO_TIER_DEVICE)
+    CK(cudaMemcpy(ctx->dev_store + (int64_t)layer * ctx->layer_bytes, dst, (size_t)ctx->layer_bytes,
+                  cudaMemcpyHostToDevice));
+  else if (ctx->weight_tier == PIPO_TIER_DISK)
+    TRY(disk_write_layer(ctx, layer, dst));
+  ctx->layer_loaded[layer] = 1;
+  return PIPO_OK;
+}
+
+pipo_status pipo_load_synthetic(pipo_ctx* ctx, int32_t layer, uint64_t seed) {
+  CHECK_CTX();
+  CK(cudaSetDevice(ctx->cfg.device));
+  cudaStream_t st = ctx->s_comp;
+  const int64_t d = ctx->d, F = ctx->F;
+  auto draw = [&](float* dst, uint32_t slot, uint32_t tid, int kind, double param, int64_t count) -> pipo_status {
+    LAUNCH(launch_synth(dst, 0, count, synth_key(seed, slot, tid), kind, synth_scale(kind, param), st));
+    return PIPO_OK;
+  };
+  if (layer == PIPO_LAYER_EMBED) {
+    const int64_t ntok = (int64_t)ctx->V * d, npos = (int64_t)(ctx->cfg.max_pos + 2) * d;
+    float* buf = nullptr;
+    TRY(dev_alloc(ctx, &buf, std::max(ntok, npos) * 4));
+    pipo_status s = PIPO_OK;
+    do {
+      if ((s = draw(buf, 0, 0, 0, 0.02, ntok)) != PIPO_OK) break;
+      LAUNCH(launch_tile_fp16(buf, ctx->V, d, reinterpret_cast<uint8_t*>(ctx->tok), st));
+      if ((s = draw(buf, 0, 1, 0, 0.02, npos)) != PIPO_OK) break;
+      LAUNCH(launch_f32_to_f16(buf, ctx->pos, npos, st));
+      if ((s = draw(buf, 0, 2, 2, 0.1, d)) != PIPO_OK) break;
+      LAUNCH(launch_f32_to_f16(buf, ctx->lnf_g, d, st));
+      if ((s = draw(buf, 0, 3, 1, 0.1, d)) != PIPO_OK) break;
+      LAUNCH(launch_f32_to_f16(buf, ctx->lnf_b, d, st));
+    } while (0);
+    CK(cudaStreamSynchronize(st));
+    cudaFree(buf);
+    ctx->hbm_bytes -= std::max(ntok, npos) * 4;
+    if (s == PIPO_OK) ctx->embed_loaded = true;
+    return s;
+  }
+  if (layer < 0 || layer >= ctx->l) return set_err(PIPO_E_INVALID_ARG, "layer index out of range");
+  // draw + quantize/tile into a device blob, then place it in its tier
+  uint8_t* blob = nullptr;
+  const bool direct = ctx->weight_tier == PIPO_TIER_DEVICE;
+  if (direct) {
+    blob = ctx->dev_store + (int64_t)layer * ctx->layer_bytes;
+  } else {
+    TRY(dev_alloc(ctx, &blob, ctx->layer_bytes));
+  }
+  const int64_t big = std::max(3 * d * d, F * d);
+  float* buf = nullptr;
+  pipo_status s = dev_alloc(ctx, &buf, big * 4);
+  const uint32_t slot = (uint32_t)layer + 1;
+  const int vkinds[V_COUNT] = {2, 1, 1, 1, 2, 1, 1, 1};
+  const double vparams[V_COUNT] = {0.1, 0.1, 0.02, 0.02, 0.1, 0.1, 0.02, 0.02};
+  const uint32_t vtids[V_COUNT] = {0, 1, 3, 5, 6, 7, 9, 11};
+  const uint32_t mtids[M_COUNT] = {2, 4, 8, 10};
+  const int64_t mrows[M_COUNT] = {3 * d, d, F, d}, mcols[M_COUNT] = {d, d, d, F};
+  if (s == PIPO_OK) {
+    CK(cudaMemsetAsync(blob, 0, (size_t)ctx->layer_bytes, st));
+    CK(cudaMemsetAsync(ctx->quant_bad, 0, 4, st));
+    for (int v = 0; v < V_COUNT && s == PIPO_OK; ++v) {
+      s = draw(buf, slot, vtids[v], vkinds[v], vparams[v], ctx->lay.vec_len[v]);
+      if (s == PIPO_OK)
+        LAUNCH(launch_f32_to_f16(buf, reinterpret_cast<__half*>(blob + ctx->lay.vec_off[v]), ctx->lay.vec_len[v], st));
+    }
+    for (int m = 0; m < M_COUNT && s == PIPO_OK; ++m) {
+      s = draw(buf, slot, mtids[m], 0, 0.02, mrows[m] * mcols[m]);
+      if (s != PIPO_OK) break;
+      if (ctx->wfmt == PIPO_W_INT4_G64)
+        LAUNCH(launch_quantize(buf, mrows[m], mcols[m], nullptr, nullptr, blob + ctx->lay.mat_off[m], ctx->quant_bad, st));
+      else
+        LAUNCH(launch_tile_fp16(buf, mrows[m], mcols[m], blob + ctx->lay.mat_off[m], st));
+    }
+  }
+  if (s == PIPO_OK && !direct) {
+    if (ctx->weight_tier == PIPO_TIER_HOST) {
+      CK(cudaMemcpyAsync(ctx->host_store + (int64_t)layer * ctx->layer_bytes, blob, (size_t)ctx->layer_bytes,
+                         cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    } else {
+      std::vector<uint8_t> tmp((size_t)ctx->layer_bytes);
+      CK(cudaMemcpyAsync(tmp.data(), blob, tmp.size(), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      s = disk_write_layer(ctx, layer, tmp.data());
+    }
+  }
+  CK(cudaStreamSynchronize(st));
+  if (buf) { cudaFree(buf); ctx->hbm_bytes -= big * 4; }
+  if (!direct && blob) { cudaFree(blob); ctx->hbm_bytes -= ctx->layer_bytes; }
+  if (s == PIPO_OK) ctx->layer_loaded[layer] = 1;
+  return s;
+}
+
+pipo_status prefill(pipo_ctx* ctx, const int32_t* tokens, int32_t b, int32_t P, int32_t* next, float* logits) {
+  CHECK_CTX();
+  if (!tokens || !next) return set_err(PIPO_E_INVALID_ARG, "NULL tokens/next");
+  if (b <= 0 || b > ctx->max_b) return set_err(PIPO_E_INVALID_ARG, "batch exceeds max_batch");
+  if (P <= 0 || P >= ctx->max_s) return set_err(PIPO_E_INVALID_ARG, "prompt length must be in [1, max_seq)");
+  TRY(check_ready(ctx));
+  CK(cudaSetDevice(ctx->cfg.device));
+  const double t0 = now_s();
+  // a new batch: wait until every in-flight KV save of the previous batch is done
+  CK(cudaStreamSynchronize(ctx->s_save));
+  ctx->b_cur = b;
+  ctx->past = 0;
+  ctx->have_batch = false;
+  TRY(stage_ids(ctx, tokens, (int64_t)b * P));
+  TRY(forward(ctx, b, P, 0, logits != nullptr));
+  TRY(finish_call(ctx, b, P, next, logits));
+  ctx->past = P;
+  ctx->have_batch = true;
+  ctx->prefill_calls++;
+  ctx->tokens += b;
+  ctx->prefill_s += now_s() - t0;
+  ctx->ttft_s = now_s() - t0;
+  return PIPO_OK;
+}
+
+static pipo_status decode_common(pipo_ctx* ctx) {
+  if (!ctx->have_batch) return set_err(PIPO_E_STATE, "decode_step before prefill");
+  if (ctx->past + 1 > ctx->max_s) return set_err(PIPO_E_INVALID_ARG, "KV capacity max_seq exceeded");
+  return PIPO_OK;
+}
+
+pipo_status decode_step(pipo_ctx* ctx, const int32_t* tokens, int32_t* next, float* logits) {
+  CHECK_CTX();
+  if (!tokens || !next) return set_err(PIPO_E_INVALID_ARG, "NULL tokens/next");
+  TRY(decode_common(ctx));
+  CK(cudaSetDevice(ctx->cfg.device));
+  const double t0 = now_s();
+  TRY(window_mark(ctx, true));
+  TRY(stage_ids(ctx, tokens, ctx->b_cur));
+  TRY(forward(ctx, ctx->b_cur, 1, ctx->past, logits != nullptr));
+  TRY(window_mark(ctx, false));
+  TRY(finish_call(ctx, ctx->b_cur, 1, next, logits));
+  ctx->past += 1;
+  ctx->decode_steps++;
+  ctx->tokens += ctx->b_cur;
+  ctx->decode_s += now_s() - t0;
+  return PIPO_OK;
+}
+
+pipo_status decode_step_dev(pipo_ctx* ctx, const int32_t* tokens_dev, int32_t* next_dev) {
+  CHECK_CTX();
+  if (!tokens_dev || !next_dev) return set_err(PIPO_E_INVALID_ARG, "NULL device buffers");
+  TRY(decode_common(ctx));
+  CK(cudaSetDevice(ctx->cfg.device));
+  const double t0 = now_s();
+  TRY(window_mark(ctx, true));
+  CK(cudaMemcpyAsync(ctx->ids, tokens_dev, (size_t)ctx->b_cur * 4, cudaMemcpyDeviceToDevice, ctx->s_comp));
+  TRY(forward(ctx, ctx->b_cur, 1, ctx->past, false));
+  CK(cudaMemcpyAsync(next_dev, ctx->next, (size_t)ctx->b_cur * 4, cudaMemcpyDeviceToDevice, ctx->s_comp));
+  TRY(window_mark(ctx, false));
+  ctx->past += 1;
+  ctx->decode_steps++;
+  ctx->tokens += ctx->b_cur;
+  ctx->decode_s += now_s() - t0;   // enqueue time only; device time is in stats.window_s
+  return PIPO_OK;
+}
+
+pipo_status pipeline_stats(pipo_ctx* ctx, pipo_stats* out) {
+  CHECK_CTX();
+  if (!out) return set_err(PIPO_E_INVALID_ARG, "out is NULL");
+  CK(cudaSetDevice(ctx->cfg.device));
+  CK(cudaDeviceSynchronize());
+  pipo_stats s{};
+  s.prefill_calls = ctx->prefill_calls;
+  s.decode_steps = ctx->decode_steps;
+  s.tokens_generated = ctx->tokens;
+  s.prefill_s = ctx->prefill_s;
+  s.decode_s = ctx->decode_s;
+  s.ttft_s = ctx->ttft_s;
+  s.h2d_bytes = ctx->h2d_bytes;
+  s.d2h_bytes = ctx->d2h_bytes;
+  s.kernel_launches = ctx->launches;
+  s.hbm_bytes = ctx->hbm_bytes;
+  s.pinned_host_bytes = ctx->pinned_bytes;
+  if (ctx->win_open && ctx->win_end) {
+    float w = 0;
+    CK(cudaEventElapsedTime(&w, ctx->win_start, ctx->win_end));
+    s.window_s = w * 1e-3;
+    std::vector<std::pair<double, double>> lanes[3], all;
+    double copy_bytes = 0;
+    for (const Span& sp : ctx->spans) {
+      float a = 0, b = 0;
+      CK(cudaEventElapsedTime(&a, ctx->win_start, sp.a));
+      CK(cudaEventElapsedTime(&b, ctx->win_start, sp.b));
+      double lo = std::max(0.0, (double)a), hi = std::min((double)w, (double)b);
+      if (hi <= lo) continue;
+      lanes[sp.lane].push_back({lo, hi});
+      if (sp.lane != 2) all.push_back({lo, hi});
+      if (sp.lane == 0 && b > a) copy_bytes += sp.bytes * (hi - lo) / (b - a);
+    }
+    const double copy_t = union_len(lanes[0]);
+    if (w > 0) {
+      s.copy_busy = copy_t / w;
+      s.kernel_busy = union_len(lanes[1]) / w;
+      s.union_busy = union_len(all) / w;
+    }
+    s.h2d_gbs = copy_t > 0 ? copy_bytes / (copy_t * 1e-3) / 1e9 : 0;
+    if (s.window_s > 0 && ctx->b_cur > 0) s.decode_tokens_per_s = (double)ctx->b_cur * ctx->decode_steps / s.window_s;
+  } else if (ctx->decode_s > 0) {
+    s.decode_tokens_per_s = (double)ctx->b_cur * ctx->decode_steps / ctx->decode_s;
+  }
+  *out = s;
+  return PIPO_OK;
+}
+
+pipo_status pipeline_stats_reset(pipo_ctx* ctx) {
+  CHECK_CTX();
+  CK(cudaSetDevice(ctx->cfg.device));
+  CK(cudaDeviceSynchronize());
+  ctx->spans.clear();
+  ctx->ev_used = 0;
+  ctx->win_open = false;
+  ctx->win_start = ctx->win_end = nullptr;
+  ctx->launches = 0;
+  ctx->prefill_calls = ctx->decode_steps = ctx->tokens = 0;
+  ctx->prefill_s = ctx->decode_s = 0;
+  ctx->h2d_bytes = ctx->d2h_bytes = 0;
+  return PIPO_OK;
+}
+
+void* pipo_stream(pipo_ctx* ctx, int32_t which) {
+  if (!ctx) return nullptr;
+  return which == 0 ? (void*)ctx->s_comp : which == 1 ? (void*)ctx->s_copy : (void*)ctx->s_save;
+}
+
+// ---- hooks ---------------------------------------------------------------------
+pipo_status pipo_quantize_int4_g64(const float* w, int64_t rows, int64_t cols, uint8_t* codes, uint16_t* scales) {
+  if (!w || !codes || !scales || rows <= 0 || cols <= 0 || cols % 64)
+    return set_err(PIPO_E_INVALID_ARG, "bad quantize arguments");
+  if (!quantize_canonical(w, rows, cols, codes, scales))
+    return set_err(PIPO_E_INVALID_ARG, "non-finite weight or fp16-overflowing group scale");
+  return PIPO_OK;
+}
+
+pipo_status pipo_quantize_int4_g64_gpu(pipo_ctx* ctx, const float* w, int64_t rows, int64_t cols, uint8_t* codes,
+                                       uint16_t* scales) {
+  CHECK_CTX();
+  if (!w || !codes || !scales || rows <= 0 || cols <= 0 || cols % 64)
+    return set_err(PIPO_E_INVALID_ARG, "bad quantize arguments");
+  CK(cudaSetDevice(ctx->cfg.device));
+  float* dw = nullptr; uint8_t* dc = nullptr; uint16_t* ds = nullptr;
+  TRY(dev_alloc(ctx, &dw, rows * cols * 4));
+  TRY(dev_alloc(ctx, &dc, rows * cols / 2));
+  TRY(dev_alloc(ctx, &ds, rows * cols / 64 * 2));
+  cudaStream_t st = ctx->s_comp;
+  CK(cudaMemcpyAsync(dw, w, (size_t)(rows * cols * 4), cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(ctx->quant_bad, 0, 4, st));
+  LAUNCH(launch_quantize(dw, rows, cols, dc, ds, nullptr, ctx->quant_bad, st));
+  int bad = 0;
+  CK(cudaMemcpyAsync(codes, dc, (size_t)(rows * cols / 2), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(scales, ds, (size_t)(rows * cols / 64 * 2), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&bad, ctx->quant_bad, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  cudaFree(dw); cudaFree(dc); cudaFree(ds);
+  ctx->hbm_bytes -= rows * cols * 4 + rows * cols / 2 + rows * cols / 64 * 2;
+  if (bad) return set_err(PIPO_E_INVALID_ARG, "non-finite weight or fp16-overflowing group scale");
+  return PIPO_OK;
+}
+
+pipo_status pipo_unpack_int4_g64(pipo_ctx* ctx, const uint8_t* codes, const uint16_t* scales, int64_t rows,
+                                 int64_t cols, uint16_t* out) {
+  CHECK_CTX();
+  if (!codes || !scales || !out || rows <= 0 || cols <= 0 || cols % 64)
+    return set_err(PIPO_E_INVALID_ARG, "bad unpack arguments");
+  CK(cudaSetDevice(ctx->cfg.device));
+  uint8_t* dc = nullptr; uint16_t* ds = nullptr; __half* dout = nullptr;
+  TRY(dev_alloc(ctx, &dc, rows * cols / 2));
+  TRY(dev_alloc(ctx, &ds, rows * cols / 64 * 2));
+  TRY(dev_alloc(ctx, &dout, rows * cols * 2));
+  cudaStream_t st = ctx->s_comp;
+  CK(cudaMemcpyAsync(dc, codes, (size_t)(rows * cols / 2), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ds, scales, (size_t)(rows * cols / 64 * 2), cudaMemcpyHostToDevice, st));
+  LAUNCH(launch_unpack_int4(dc, ds, rows, cols, dout, st));
+  CK(cudaMemcpyAsync(out, dout, (size_t)(rows * cols * 2), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  cudaFree(dc); cudaFree(ds); cudaFree(dout);
+  ctx->hbm_bytes -= rows * cols / 2 + rows * cols / 64 * 2 + rows * cols * 2;
+  return PIPO_OK;
+}
+
+pipo_status pipo_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, const uint16_t* x, const float* w,
+                        const float* bias, int32_t M, int32_t N, int32_t K, float* y) {
+  CHECK_CTX();
+  if (!x || !w || !y || M <= 0 || N <= 0 || K <= 0 || K % 64 || (wfmt != 0 && wfmt != 1) || path < 0 || path > 2)
+    return set_err(PIPO_E_INVALID_ARG, "bad linear arguments");
+  CK(cudaSetDevice(ctx->cfg.device));
+  const MatLayout ml = mat_layout(N, K, wfmt);
+  std::vector<uint8_t> tiled((size_t)ml.bytes);
+  if (wfmt == 1) {
+    if (!quantize_tiled(w, N, K, tiled.data())) return set_err(PIPO_E_INVALID_ARG, "non-finite weight");
+  } else {
+    tile_fp16(w, N, K, tiled.data());
+  }
+  std::vector<uint16_t> bh;
+  if (bias) {
+    bh.resize(N);
+    for (int i = 0; i < N; ++i) bh[i] = f32_to_f16_rne(bias[i]);
+  }
+  uint8_t* dw = nullptr; __half* dx = nullptr; __half* db = nullptr; float* dy = nullptr;
+  TRY(dev_alloc(ctx, &dw, ml.bytes));
+  TRY(dev_alloc(ctx, &dx, (int64_t)M * K * 2));
+  TRY(dev_alloc(ctx, &dy, (int64_t)M * N * 4));
+  if (bias) TRY(dev_alloc(ctx, &db, (int64_t)N * 2));
+  cudaStream_t st = ctx->s_comp;
+  CK(cudaMemcpyAsync(dw, tiled.data(), tiled.size(), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dx, x, (size_t)M * K * 2, cudaMemcpyHostToDevice, st));
+  if (bias) CK(cudaMemcpyAsync(db, bh.data(), (size_t)N * 2, cudaMemcpyHostToDevice, st));
+  LinearArgs la;
+  la.x = dx; la.w = dw; la.wfmt = wfmt; la.M = M; la.N = N; la.K = K;
+  la.ws = ctx->ws; la.ws_floats = ctx->ws_floats; la.counters = ctx->counters; la.n_counters = ctx->n_counters;
+  la.num_sms = ctx->num_sms;
+  la.epi.kind = EPI_F32; la.epi.bias = db; la.epi.M = M; la.epi.N = N; la.epi.y = dy; la.epi.ldy = N;
+  LAUNCH(launch_linear(la, path, ctx->gemv_max_m, st));
+  CK(cudaMemcpyAsync(y, dy, (size_t)M * N * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  cudaFree(dw); cudaFree(dx); cudaFree(dy);
+  if (db) cudaFree(db);
+  ctx->hbm_bytes -= ml.bytes + (int64_t)M * K * 2 + (int64_t)M * N * 4 + (bias ? N * 2 : 0);
+  return PIPO_OK;
+}
+
+pipo_status pipo_attention_decode(pipo_ctx* ctx, const uint16_t* q, const uint16_t* k, const uint16_t* v, int32_t b,
+                                  int32_t L, int32_t d, int32_t n_heads, float* o) {
+  CHECK_CTX();
+  if (!q || !k || !v || !o || b <= 0 || L <= 0 || d <= 0 || n_heads <= 0 || d % n_heads)
+    return set_err(PIPO_E_INVALID_ARG, "bad attention arguments");
+  CK(cudaSetDevice(ctx->cfg.device));
+  __half *dq = nullptr, *dk = nullptr, *dv = nullptr, *dout = nullptr;
+  float* df = nullptr;
+  const int64_t nq = (int64_t)b * d, nkv = (int64_t)L * b * d;
+  TRY(dev_alloc(ctx, &dq, nq * 2));
+  TRY(dev_alloc(ctx, &dk, nkv * 2));
+  TRY(dev_alloc(ctx, &dv, nkv * 2));
+  TRY(dev_alloc(ctx, &dout, nq * 2));
+  TRY(dev_alloc(ctx, &df, nq * 4));
+  cudaStream_t st = ctx->s_comp;
+  CK(cudaMemcpyAsync(dq, q, (size_t)nq * 2, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dk, k, (size_t)nkv * 2, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dv, v, (size_t)nkv * 2, cudaMemcpyHostToDevice, st));
+  AttnArgs aa;
+  aa.q = dq; aa.kc = dk; aa.vc = dv; aa.o = dout; aa.b = b; aa.n = 1; aa.past = L - 1; aa.d = d;
+  aa.n_heads = n_heads; aa.kv_b = b; aa.ws = ctx->ws; aa.ws_floats = ctx->ws_floats; aa.num_sms = ctx->num_sms;
+  LAUNCH(launch_attention_decode(aa, st));
+  LAUNCH(launch_f16_to_f32(dout, df, nq, st));
+  CK(cudaMemcpyAsync(o, df, (size_t)nq * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  cudaFree(dq); cudaFree(dk); cudaFree(dv); cudaFree(dout); cudaFree(df);
+  ctx->hbm_bytes -= nq * 2 * 2 + nkv * 2 * 2 + nq * 4;
+  return PIPO_OK;
+}
+
+pipo_status pipo_debug_capture(pipo_ctx* ctx, int32_t on, float* out) {
+  CHECK_CTX();
+  if (!on) { ctx->cap_on = false; return PIPO_OK; }
+  if (!out) return set_err(PIPO_E_INVALID_ARG, "capture buffer is NULL");
+  CK(cudaSetDevice(ctx->cfg.device));
+  const int64_t need = (int64_t)ctx->l * ctx->rows_cap * ctx->d * 4;
+  if (ctx->cap_dev_bytes < need) {
+    if (ctx->cap_dev) { cudaFree(ctx->cap_dev); ctx->hbm_bytes -= ctx->cap_dev_bytes; }
+    ctx->cap_dev = nullptr;
+    ctx->cap_dev_bytes = 0;
+    TRY(dev_alloc(ctx, &ctx->cap_dev, need));
+    ctx->cap_dev_bytes = need;
+  }
+  ctx->cap_on = true;
+  ctx->cap_host = out;
+  return PIPO_OK;
+}
+
+pipo_status pipo_probe_h2d(pipo_ctx* ctx, int64_t bytes, int32_t reps, double* gbs) {
+  CHECK_CTX();
+  if (bytes <= 0 || reps <= 0 || !gbs) return set_err(PIPO_E_INVALID_ARG, "bad probe arguments");
+  CK(cudaSetDevice(ctx->cfg.device));
+  uint8_t *hsrc = nullptr, *ddst = nullptr;
+  TRY(host_alloc(ctx, &hsrc, bytes));
+  TRY(dev_alloc(ctx, &ddst, bytes));
+  std::memset(hsrc, 1, (size_t)bytes);
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  double best = 0;
+  for (int r = 0; r < reps + 1; ++r) {
+    CK(cudaEventRecord(a, ctx->s_copy));
+    CK(cudaMemcpyAsync(ddst, hsrc, (size_t)bytes, cudaMemcpyHostToDevice, ctx->s_copy));
+    CK(cudaEventRecord(b, ctx->s_copy));
+    CK(cudaEventSynchronize(b));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    if (r > 0) best = std::max(best, bytes / (ms * 1e-3) / 1e9);
+  }
+  cudaEventDestroy(a); cudaEventDestroy(b);
+  cudaFreeHost(hsrc); cudaFree(ddst);
+  ctx->pinned_bytes -= bytes;
+  ctx->hbm_bytes -= bytes;
+  *gbs = best;
+  return PIPO_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,110 @@
+// ctx.h — the pipeline context (internal).
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <string>
+#include <vector>
+
+#include "../../include/pipo.h"
+#include "host.h"
+#include "kernels.h"
+#include "layout.h"
+
+namespace pipo {
+
+constexpr int kMaxRing = 8;
+
+struct Span {            // one interval on a device lane, between two timed events
+  cudaEvent_t a, b;
+  int lane;              // 0 = H2D copy, 1 = kernels, 2 = D2H save
+  int64_t bytes;
+};
+
+struct DiskTier;         // disk.cpp
+
+}  // namespace pipo
+
+struct pipo_ctx {
+  pipo_config cfg{};
+  std::string disk_dir;
+  int d = 0, l = 0, H = 0, F = 0, V = 0, hd = 0, max_b = 0, max_s = 0, wfmt = 1;
+  int weight_tier = 1, kv_tier = 0, R = 2, gemv_max_m = 15;
+  int64_t chunk = 0;
+  pipo::LayerLayout lay;
+  int64_t layer_bytes = 0;
+  int num_sms = 148;
+  bool poisoned = false;
+
+  cudaStream_t s_comp = nullptr, s_copy = nullptr, s_save = nullptr;
+
+  // resident embeddings (Q20)
+  pipo::MatLayout tok_lay;
+  __half* tok = nullptr;      // tiled [V_pad x d]
+  __half* pos = nullptr;      // [max_pos + 2][d]
+  __half* lnf_g = nullptr;
+  __half* lnf_b = nullptr;
+  bool embed_loaded = false;
+  std::vector<char> layer_loaded;
+
+  // weights
+  uint8_t* host_store = nullptr;   // pinned, l * layer_bytes (HOST tier)
+  uint8_t* dev_store = nullptr;    // HBM, l * layer_bytes (DEVICE tier)
+  uint8_t* ring = nullptr;         // HBM, R * layer_bytes (HOST / DISK tiers)
+  pipo::DiskTier* disk = nullptr;
+
+  // KV cache: position-major [pos][b][d] per (layer, K/V)
+  int64_t kv_elems = 0;            // max_s * max_b * d per tensor
+  __half* kv_dev = nullptr;        // DEVICE kv tier: [l][2][kv_elems]
+  __half* kv_host = nullptr;       // HOST kv tier (pinned): [l][2][kv_elems]
+  __half* kv_slot = nullptr;       // HOST kv tier: [R][2][kv_elems] staging in HBM
+
+  // activations
+  int64_t rows_cap = 0;
+  float* h = nullptr;              // [rows][d] fp32 residual stream
+  __half* xa = nullptr;            // [rows][d] LN output / attention output
+  __half* q = nullptr;             // [rows][d]
+  __half* u = nullptr;             // [rows][F]
+  float* logits = nullptr;         // [max_b][V]
+  int32_t* ids = nullptr;          // [rows]
+  int32_t* next = nullptr;         // [max_b]
+  int32_t* pin_ids = nullptr;      // pinned staging
+  int32_t* pin_next = nullptr;
+  float* ws = nullptr;
+  int64_t ws_floats = 0;
+  int* counters = nullptr;
+  int n_counters = 0;
+  int* quant_bad = nullptr;        // device flag for the GPU quantizer
+
+  // pipeline state (Alg. 1 as a stream/event DAG)
+  int64_t g_copy = 0;              // next global layer index whose copy is enqueued
+  int64_t g_comp = 0;              // next global layer index to compute
+  cudaEvent_t ev_ready[pipo::kMaxRing][5] = {};   // seg 0..3 landed, [4] = KV landed
+  cudaEvent_t ev_free[pipo::kMaxRing] = {};       // compute done with the slot
+  cudaEvent_t ev_kv_free[pipo::kMaxRing] = {};    // KV slot free (after save)
+  cudaEvent_t ev_attn[pipo::kMaxRing] = {};       // attention done (save may start)
+  std::vector<cudaEvent_t> ev_saved;              // per layer: last KV save done (A6 fence)
+  std::vector<int64_t> kv_load_past;              // per ring slot: positions its KV load covers
+  int b_cur = 0, past = 0;
+  bool have_batch = false;
+
+  // capture (pipo_debug_capture)
+  bool cap_on = false;
+  float* cap_host = nullptr;
+  float* cap_dev = nullptr;
+  int64_t cap_dev_bytes = 0;
+
+  // stats / timeline
+  bool timeline = true;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<pipo::Span> spans;
+  cudaEvent_t win_start = nullptr, win_end = nullptr;
+  bool win_open = false;
+  int64_t launches = 0;
+  int64_t prefill_calls = 0, decode_steps = 0, tokens = 0;
+  double prefill_s = 0, decode_s = 0, ttft_s = 0;
+  int64_t h2d_bytes = 0, d2h_bytes = 0;
+  int64_t hbm_bytes = 0, pinned_bytes = 0;
+};

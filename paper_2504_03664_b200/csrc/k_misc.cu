@@ -1,0 +1,240 @@
+// k_misc.cu — embedding gather (a4 PrepareInput), LayerNorm, greedy argmax (a13),
+// int4 unpack+scale (kernel K8), GPU quantizer (a0 for synthetic loads) and fp16
+// tiling.
+#include <float.h>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "layout.h"
+
+namespace pipo {
+
+// a4: h[m][:] = E_tok[id] + E_pos[past + t + 2]   ([ext] OPT learned positions, offset 2)
+// tok is the fp16 tiled LM-head matrix (layout.h), pos row-major fp16.
+__global__ void embed_kernel(const int32_t* ids, int n, int past, const __half* tok, int64_t n_kb,
+                             const __half* pos, int d, float* h) {
+  const int m = blockIdx.x;
+  const int t = m % n;
+  const int64_t id = ids[m];
+  const __half* prow = pos + (int64_t)(past + t + 2) * d;
+  for (int k = threadIdx.x; k < d; k += blockDim.x) {
+    const float a = __half2float(tok[fp16_tiled_index(id, k, n_kb)]);
+    h[(int64_t)m * d + k] = a + __half2float(prow[k]);
+  }
+}
+
+int launch_embed(const int32_t* ids, int b, int n, int past, const __half* tok_tiled, int64_t tok_n_kb,
+                 const __half* pos, int d, float* h, cudaStream_t st) {
+  embed_kernel<<<b * n, 256, 0, st>>>(ids, n, past, tok_tiled, tok_n_kb, pos, d, h);
+  return 1;
+}
+
+// LayerNorm (biased variance, eps 1e-5, [ext] nn.LayerNorm) of the fp32 residual
+// stream, fp16 output for the next GEMM.  One CTA per row; two-pass statistics
+// from registers; fixed-order block reduction (deterministic).
+constexpr int LN_THREADS = 256;
+constexpr int LN_MAX_PER_THREAD = 32;   // d <= 8192
+
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  float t = 0.f;
+  for (int i = 0; i < LN_THREADS / 32; ++i) t += red[i];
+  return t;
+}
+
+__global__ void __launch_bounds__(LN_THREADS) layernorm_kernel(const float* h, int64_t row_stride, int d,
+                                                                 const __half* g, const __half* beta,
+                                                                 __half* x) {
+  __shared__ float red[LN_THREADS / 32];
+  const float* row = h + blockIdx.x * row_stride;
+  float v[LN_MAX_PER_THREAD];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < LN_MAX_PER_THREAD; ++i) {
+    const int k = threadIdx.x + i * LN_THREADS;
+    v[i] = k < d ? row[k] : 0.f;
+    s += v[i];
+  }
+  const float mean = block_sum(s, red) / d;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < LN_MAX_PER_THREAD; ++i) {
+    const int k = threadIdx.x + i * LN_THREADS;
+    const float c = k < d ? v[i] - mean : 0.f;
+    q = fmaf(c, c, q);
+  }
+  const float var = block_sum(q, red) / d;
+  const float rstd = rsqrtf(var + 1e-5f);
+  __half* out = x + (int64_t)blockIdx.x * d;
+#pragma unroll
+  for (int i = 0; i < LN_MAX_PER_THREAD; ++i) {
+    const int k = threadIdx.x + i * LN_THREADS;
+    if (k < d) out[k] = __float2half_rn((v[i] - mean) * rstd * __half2float(g[k]) + __half2float(beta[k]));
+  }
+}
+
+int launch_layernorm(const float* h, int64_t row_stride, int rows, int d, const __half* g,
+                     const __half* beta, __half* x, cudaStream_t st) {
+  if (d > LN_THREADS * LN_MAX_PER_THREAD) return -1;
+  layernorm_kernel<<<rows, LN_THREADS, 0, st>>>(h, row_stride, d, g, beta, x);
+  return 1;
+}
+
+// a13: greedy next token = argmax over the vocabulary, lowest index on exact ties;
+// NaN never wins.
+__global__ void __launch_bounds__(1024) argmax_kernel(const float* logits, int V, int ldl, int32_t* out) {
+  __shared__ float sv[32];
+  __shared__ int si[32];
+  const float* row = logits + (int64_t)blockIdx.x * ldl;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) {
+    const float v = row[i];
+    if (v > best || (v == best && i < bi)) { best = v; bi = i; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) { sv[w] = best; si[w] = bi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i)
+      if (sv[i] > best || (sv[i] == best && si[i] < bi)) { best = sv[i]; bi = si[i]; }
+    out[blockIdx.x] = bi == 0x7fffffff ? 0 : bi;
+  }
+}
+
+int launch_argmax(const float* logits, int rows, int V, int ldl, int32_t* out, cudaStream_t st) {
+  argmax_kernel<<<rows, 1024, 0, st>>>(logits, V, ldl, out);
+  return 1;
+}
+
+// K8: unpack + scale: out[r][k] = fp16_rne(q * s) (HMUL2 of exact q and s).
+__global__ void unpack_int4_kernel(const uint8_t* codes, const uint16_t* scales, int64_t rows, int64_t cols,
+                                   __half* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // one byte = 2 codes
+  const int64_t nbytes = rows * cols / 2;
+  if (i >= nbytes) return;
+  const int64_t r = i / (cols / 2), kb = i - r * (cols / 2);
+  const uint32_t b = codes[i];
+  const __half s = __ushort_as_half(scales[r * (cols / 64) + (2 * kb) / 64]);
+  const __half2 v = __hmul2(codes_to_half2((b & 0xFu) | ((b >> 4) << 16)), __half2half2(s));
+  reinterpret_cast<__half2*>(out)[i] = v;
+}
+
+int launch_unpack_int4(const uint8_t* codes, const uint16_t* scales, int64_t rows, int64_t cols, __half* out,
+                       cudaStream_t st) {
+  const int64_t n = rows * cols / 2;
+  unpack_int4_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(codes, scales, rows, cols, out);
+  return 1;
+}
+
+// a0 on the GPU (same definition as the host packer):
+// one thread per (row, group): a = max|g|; s = fp16_rne(a / 7.0f); q = clamp(rint(g/s)).
+// IEEE division and RNE conversions are spelled out (no fast-math contraction).
+// Output: canonical packed codes [rows][cols/2] + scales, and/or the tiled block.
+__global__ void quantize_kernel(const float* w, int64_t rows, int64_t cols, uint8_t* codes, uint16_t* scales,
+                                uint8_t* tiled, int* bad) {
+  const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t ng = cols / 64;
+  const int64_t rows_pad = (rows + 127) / 128 * 128;
+  if (gi >= rows_pad * ng) return;
+  const int64_t r = gi / ng, c = gi - r * ng;
+  float g[64];
+  float a = 0.f;
+  bool finite = true;
+  if (r < rows) {
+    const float4* src = reinterpret_cast<const float4*>(w + r * cols + c * 64);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float4 v = src[i];
+      g[4 * i] = v.x; g[4 * i + 1] = v.y; g[4 * i + 2] = v.z; g[4 * i + 3] = v.w;
+    }
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+      finite = finite && isfinite(g[i]);
+      a = fmaxf(a, fabsf(g[i]));
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 64; ++i) g[i] = 0.f;
+  }
+  const __half s16 = __float2half_rn(__fdiv_rn(a, 7.0f));
+  const float s = __half2float(s16);
+  if (!finite || isinf(s)) atomicExch(bad, 1);
+  uint32_t pw[8];
+#pragma unroll
+  for (int wi = 0; wi < 8; ++wi) {
+    uint32_t word = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      int q = 0;
+      if (s != 0.f) q = (int)fminf(fmaxf(rintf(__fdiv_rn(g[wi * 8 + j], s)), -8.f), 7.f);
+      word |= (uint32_t)(q & 0xF) << (4 * j);
+    }
+    pw[wi] = word;
+  }
+  if (codes && r < rows) {
+    uint32_t* cdst = reinterpret_cast<uint32_t*>(codes + r * (cols / 2) + c * 32);
+#pragma unroll
+    for (int wi = 0; wi < 8; ++wi) cdst[wi] = pw[wi];
+    scales[r * ng + c] = __half_as_ushort(s16);
+  }
+  if (tiled) {
+    uint8_t* blk = tiled + ((r >> 7) * ng + c) * kInt4BlockBytes;
+    const int rr = (int)(r & 127);
+    *reinterpret_cast<uint4*>(blk + (0 * 128 + rr) * 16) = make_uint4(pw[0], pw[1], pw[2], pw[3]);
+    *reinterpret_cast<uint4*>(blk + (1 * 128 + rr) * 16) = make_uint4(pw[4], pw[5], pw[6], pw[7]);
+    *reinterpret_cast<__half*>(blk + 4096 + rr * 2) = s16;
+  }
+}
+
+int launch_quantize(const float* w, int64_t rows, int64_t cols, uint8_t* codes, uint16_t* scales,
+                    uint8_t* tiled, int* bad_flag, cudaStream_t st) {
+  const int64_t rows_pad = tiled ? (rows + 127) / 128 * 128 : rows;
+  const int64_t n = rows_pad * (cols / 64);
+  quantize_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(w, rows, cols, codes, scales, tiled, bad_flag);
+  return 1;
+}
+
+// fp16 tiling of fp32 masters: element (r, k) -> block (r/128, k/64), row-major inside.
+__global__ void tile_fp16_kernel(const float* w, int64_t rows, int64_t cols, __half* out) {
+  const int64_t rows_pad = (rows + 127) / 128 * 128;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows_pad * cols) return;
+  const int64_t r = i / cols, k = i - r * cols;
+  out[fp16_tiled_index(r, k, cols / 64)] = __float2half_rn(r < rows ? w[r * cols + k] : 0.f);
+}
+
+int launch_tile_fp16(const float* w, int64_t rows, int64_t cols, uint8_t* tiled, cudaStream_t st) {
+  const int64_t n = (rows + 127) / 128 * 128 * cols;
+  tile_fp16_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(w, rows, cols, reinterpret_cast<__half*>(tiled));
+  return 1;
+}
+
+__global__ void f32_to_f16_kernel(const float* s, __half* d, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) d[i] = __float2half_rn(s[i]);
+}
+__global__ void f16_to_f32_kernel(const __half* s, float* d, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) d[i] = __half2float(s[i]);
+}
+int launch_f32_to_f16(const float* src, __half* dst, int64_t n, cudaStream_t st) {
+  f32_to_f16_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src, dst, n);
+  return 1;
+}
+int launch_f16_to_f32(const __half* src, float* dst, int64_t n, cudaStream_t st) {
+  f16_to_f32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src, dst, n);
+  return 1;
+}
+
+}  // namespace pipo

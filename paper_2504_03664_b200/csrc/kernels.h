@@ -1,0 +1,87 @@
+// kernels.h — host-side launchers of the sm_100a kernels (internal, C++).
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pipo {
+
+enum EpiKind { EPI_QKV = 0, EPI_RESID = 1, EPI_RELU = 2, EPI_F32 = 3 };
+
+// Fused epilogue of a linear layer (acc = x . W^T for output row m, feature n):
+//  EPI_QKV  : v = acc + b; n < d -> q[m][n] = fp16(v * qscale);  d <= n < 2d -> K cache;
+//             2d <= n -> V cache.  Row m = bi * n_tok + t is written at position past + t
+//             of the position-major cache [pos][kv_b][d] (a6).
+//  EPI_RESID: h[m][n] += acc + b          (out-proj, FC2: residual add, fp32 stream)
+//  EPI_RELU : u[m][n] = fp16(relu(acc + b))  (FC1)
+//  EPI_F32  : y[m][n] = acc               (LM head logits; pipo_linear hook)
+struct EpiParams {
+  int kind = EPI_F32;
+  const __half* bias = nullptr;
+  int M = 0, N = 0;
+  __half* q = nullptr;
+  __half* kc = nullptr;
+  __half* vc = nullptr;
+  int d = 0, n_tok = 1, past = 0, kv_b = 1;
+  float qscale = 1.f;
+  float* h = nullptr;
+  __half* u = nullptr;
+  float* y = nullptr;
+  int ldy = 0;
+};
+
+struct LinearArgs {
+  const __half* x = nullptr;  // [M][K] fp16, row stride K
+  const uint8_t* w = nullptr; // tiled matrix (layout.h)
+  int wfmt = 1;               // 1 int4-g64, 0 fp16
+  int M = 0, N = 0, K = 0;
+  EpiParams epi;
+  float* ws = nullptr;        // split-K partials
+  int64_t ws_floats = 0;
+  int* counters = nullptr;    // split-K arrival counters (zeroed, self-resetting)
+  int n_counters = 0;
+  int num_sms = 148;
+};
+
+enum LinearPath { PATH_AUTO = 0, PATH_GEMV = 1, PATH_GEMM = 2 };
+
+// returns the number of kernels launched (0 on a launch error -> check cudaGetLastError)
+int launch_linear(const LinearArgs& a, int path, int gemv_max_m, cudaStream_t st);
+
+// attention: q [b][d] (pre-scaled), K/V position-major [pos][kv_b][d]
+struct AttnArgs {
+  const __half* q = nullptr;  // decode: [b][d]; prefill: [b][n][d]
+  const __half* kc = nullptr;
+  const __half* vc = nullptr;
+  __half* o = nullptr;        // same shape as q
+  int b = 0, n = 1, past = 0, d = 0, n_heads = 0, kv_b = 0;
+  float* ws = nullptr;
+  int64_t ws_floats = 0;
+  int num_sms = 148;
+};
+int launch_attention_decode(const AttnArgs& a, cudaStream_t st);
+int launch_attention_prefill(const AttnArgs& a, cudaStream_t st);
+
+// misc
+int launch_embed(const int32_t* ids, int b, int n, int past, const __half* tok_tiled, int64_t tok_n_kb,
+                 const __half* pos, int d, float* h, cudaStream_t st);
+int launch_layernorm(const float* h, int64_t row_stride, int rows, int d, const __half* g,
+                     const __half* beta, __half* x, cudaStream_t st);
+int launch_argmax(const float* logits, int rows, int V, int ldl, int32_t* out, cudaStream_t st);
+int launch_unpack_int4(const uint8_t* codes, const uint16_t* scales, int64_t rows, int64_t cols,
+                       __half* out, cudaStream_t st);
+// quantize fp32 masters [rows][cols] (device) -> canonical codes/scales and/or tiled blob
+int launch_quantize(const float* w, int64_t rows, int64_t cols, uint8_t* codes, uint16_t* scales,
+                    uint8_t* tiled, int* bad_flag, cudaStream_t st);
+// fp16 tiling of fp32 masters (exact for fp16-representable input)
+int launch_tile_fp16(const float* w, int64_t rows, int64_t cols, uint8_t* tiled, cudaStream_t st);
+int launch_f32_to_f16(const float* src, __half* dst, int64_t n, cudaStream_t st);
+int launch_f16_to_f32(const __half* src, float* dst, int64_t n, cudaStream_t st);
+
+// synthetic generator (pipo_synth mirror; input generation, not the method)
+int launch_synth(float* out, int64_t start, int64_t count, uint64_t key, int kind, float scale,
+                 cudaStream_t st);
+uint64_t synth_key(uint64_t seed, uint32_t slot, uint32_t tid);
+float synth_scale(int kind, double param);
+
+}  // namespace pipo

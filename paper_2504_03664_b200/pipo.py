@@ -1,0 +1,307 @@
+"""Thin ctypes binding of include/pipo.h — argument marshalling only.
+
+Every function keeps the C-ABI name; all compute happens in libpipo.so (CUDA,
+sm_100a).  There is no CPU fallback: importing this module without the built
+library raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libpipo.so")
+if not os.path.exists(_LIB_PATH):
+    raise ImportError(f"PIPO CUDA library not built: {_LIB_PATH} missing "
+                      "(run __graft_entry__.build() or python -m paper_2504_03664_b200.build)")
+_lib = C.CDLL(_LIB_PATH)
+
+PIPO_OK, PIPO_E_INVALID_ARG, PIPO_E_STATE, PIPO_E_OOM, PIPO_E_IO, PIPO_E_FORMAT, PIPO_E_INFEASIBLE, PIPO_E_CUDA = range(8)
+STATUS_NAMES = ["OK", "INVALID_ARG", "STATE", "OOM", "IO", "FORMAT", "INFEASIBLE", "CUDA"]
+PIPO_W_FP16, PIPO_W_INT4_G64 = 0, 1
+PIPO_TIER_DEVICE, PIPO_TIER_HOST, PIPO_TIER_DISK = 0, 1, 2
+PIPO_F_TIMELINE = 1
+PIPO_LAYER_EMBED = -1
+PATH_AUTO, PATH_GEMV, PATH_GEMM = 0, 1, 2
+
+_f = C.POINTER(C.c_float)
+_u8 = C.POINTER(C.c_uint8)
+_u16 = C.POINTER(C.c_uint16)
+_i32 = C.POINTER(C.c_int32)
+
+
+class pipo_config(C.Structure):
+    _fields_ = [("device", C.c_int32), ("d_model", C.c_int32), ("n_layers", C.c_int32), ("n_heads", C.c_int32),
+                ("ffn_dim", C.c_int32), ("vocab", C.c_int32), ("max_pos", C.c_int32),
+                ("max_batch", C.c_int32), ("max_seq", C.c_int32), ("wfmt", C.c_int32),
+                ("weight_tier", C.c_int32), ("kv_tier", C.c_int32), ("ring_layers", C.c_int32),
+                ("chunk_bytes", C.c_int64), ("gemv_max_m", C.c_int32), ("disk_threads", C.c_int32),
+                ("disk_dir", C.c_char_p), ("flags", C.c_uint32)]
+
+
+class pipo_layer_weights(C.Structure):
+    _fields_ = [(n, _f) for n in ("ln1_g", "ln1_b", "w_qkv", "b_qkv", "w_out", "b_out",
+                                  "ln2_g", "ln2_b", "w_fc1", "b_fc1", "w_fc2", "b_fc2")]
+
+
+class pipo_embed_weights(C.Structure):
+    _fields_ = [(n, _f) for n in ("tok", "pos", "lnf_g", "lnf_b")]
+
+
+class pipo_stats(C.Structure):
+    _fields_ = [("prefill_calls", C.c_int64), ("decode_steps", C.c_int64), ("tokens_generated", C.c_int64),
+                ("prefill_s", C.c_double), ("decode_s", C.c_double), ("ttft_s", C.c_double),
+                ("decode_tokens_per_s", C.c_double), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
+                ("h2d_gbs", C.c_double), ("copy_busy", C.c_double), ("kernel_busy", C.c_double),
+                ("union_busy", C.c_double), ("window_s", C.c_double), ("kernel_launches", C.c_int64),
+                ("hbm_bytes", C.c_int64), ("pinned_host_bytes", C.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+def _sig(name, restype, *args):
+    fn = getattr(_lib, name)
+    fn.restype = restype
+    fn.argtypes = list(args)
+    return fn
+
+
+_P = C.c_void_p
+_sig("pipo_last_error", C.c_char_p)
+_sig("pipo_abi_version", C.c_int32)
+_sig("pipeline_init", C.c_int, C.POINTER(pipo_config), C.POINTER(_P))
+_sig("pipeline_destroy", None, _P)
+_sig("load_layer_weights", C.c_int, _P, C.c_int32, _P)
+_sig("pipo_load_synthetic", C.c_int, _P, C.c_int32, C.c_uint64)
+_sig("prefill", C.c_int, _P, _i32, C.c_int32, C.c_int32, _i32, _f)
+_sig("decode_step", C.c_int, _P, _i32, _i32, _f)
+_sig("decode_step_dev", C.c_int, _P, _P, _P)
+_sig("pipeline_stats", C.c_int, _P, C.POINTER(pipo_stats))
+_sig("pipeline_stats_reset", C.c_int, _P)
+_sig("pipo_stream", _P, _P, C.c_int32)
+_sig("pipo_quantize_int4_g64", C.c_int, _f, C.c_int64, C.c_int64, _u8, _u16)
+_sig("pipo_quantize_int4_g64_gpu", C.c_int, _P, _f, C.c_int64, C.c_int64, _u8, _u16)
+_sig("pipo_unpack_int4_g64", C.c_int, _P, _u8, _u16, C.c_int64, C.c_int64, _u16)
+_sig("pipo_linear", C.c_int, _P, C.c_int32, C.c_int32, _u16, _f, _f, C.c_int32, C.c_int32, C.c_int32, _f)
+_sig("pipo_attention_decode", C.c_int, _P, _u16, _u16, _u16, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _f)
+_sig("pipo_debug_capture", C.c_int, _P, C.c_int32, _f)
+_sig("pipo_probe_h2d", C.c_int, _P, C.c_int64, C.c_int32, C.POINTER(C.c_double))
+
+EXPORTED = ["pipo_last_error", "pipo_abi_version", "pipeline_init", "pipeline_destroy", "load_layer_weights",
+            "pipo_load_synthetic", "prefill", "decode_step", "decode_step_dev", "pipeline_stats",
+            "pipeline_stats_reset", "pipo_stream", "pipo_quantize_int4_g64", "pipo_quantize_int4_g64_gpu",
+            "pipo_unpack_int4_g64", "pipo_linear", "pipo_attention_decode", "pipo_debug_capture", "pipo_probe_h2d"]
+
+
+class PipoError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES[status] if 0 <= status < 8 else status}: {msg}")
+        self.status = status
+
+
+def _check(st):
+    if st != PIPO_OK:
+        raise PipoError(st, _lib.pipo_last_error().decode(errors="replace"))
+
+
+def _ptr(a, ct):
+    return a.ctypes.data_as(C.POINTER(ct))
+
+
+def _c(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+def lib_path():
+    return _LIB_PATH
+
+
+def pipo_abi_version():
+    return _lib.pipo_abi_version()
+
+
+def pipeline_init(cfg: pipo_config):
+    h = _P()
+    _check(_lib.pipeline_init(C.byref(cfg), C.byref(h)))
+    return h
+
+
+def pipeline_destroy(ctx):
+    _lib.pipeline_destroy(ctx)
+
+
+def load_layer_weights(ctx, layer: int, w: dict):
+    if layer == PIPO_LAYER_EMBED:
+        keep = {k: _c(w[k], np.float32) for k in ("tok", "pos", "lnf_g", "lnf_b")}
+        st = pipo_embed_weights(**{k: _ptr(v, C.c_float) for k, v in keep.items()})
+    else:
+        names = [n for n, _ in pipo_layer_weights._fields_]
+        keep = {k: _c(w[k], np.float32) for k in names}
+        st = pipo_layer_weights(**{k: _ptr(v, C.c_float) for k, v in keep.items()})
+    _check(_lib.load_layer_weights(ctx, layer, C.byref(st)))
+
+
+def pipo_load_synthetic(ctx, layer: int, seed: int):
+    _check(_lib.pipo_load_synthetic(ctx, layer, seed))
+
+
+def prefill(ctx, tokens, want_logits=False, vocab=None):
+    t = _c(tokens, np.int32)
+    b, p = t.shape
+    nxt = np.empty(b, dtype=np.int32)
+    lg = np.empty((b, vocab), dtype=np.float32) if want_logits else None
+    _check(_lib.prefill(ctx, _ptr(t, C.c_int32), b, p, _ptr(nxt, C.c_int32),
+                        _ptr(lg, C.c_float) if lg is not None else None))
+    return nxt, lg
+
+
+def decode_step(ctx, tokens, want_logits=False, vocab=None):
+    t = _c(tokens, np.int32)
+    nxt = np.empty(t.shape[0], dtype=np.int32)
+    lg = np.empty((t.shape[0], vocab), dtype=np.float32) if want_logits else None
+    _check(_lib.decode_step(ctx, _ptr(t, C.c_int32), _ptr(nxt, C.c_int32),
+                            _ptr(lg, C.c_float) if lg is not None else None))
+    return nxt, lg
+
+
+def decode_step_dev(ctx, tokens_dev_ptr: int, next_dev_ptr: int):
+    _check(_lib.decode_step_dev(ctx, C.c_void_p(tokens_dev_ptr), C.c_void_p(next_dev_ptr)))
+
+
+def pipeline_stats(ctx) -> dict:
+    s = pipo_stats()
+    _check(_lib.pipeline_stats(ctx, C.byref(s)))
+    return s.as_dict()
+
+
+def pipeline_stats_reset(ctx):
+    _check(_lib.pipeline_stats_reset(ctx))
+
+
+def pipo_stream(ctx, which=0) -> int:
+    return _lib.pipo_stream(ctx, which) or 0
+
+
+def pipo_quantize_int4_g64(w):
+    w = _c(w, np.float32)
+    rows, cols = w.shape
+    codes = np.empty((rows, cols // 2), dtype=np.uint8)
+    scales = np.empty((rows, cols // 64), dtype=np.uint16)
+    _check(_lib.pipo_quantize_int4_g64(_ptr(w, C.c_float), rows, cols, _ptr(codes, C.c_uint8),
+                                       _ptr(scales, C.c_uint16)))
+    return codes, scales
+
+
+def pipo_quantize_int4_g64_gpu(ctx, w):
+    w = _c(w, np.float32)
+    rows, cols = w.shape
+    codes = np.empty((rows, cols // 2), dtype=np.uint8)
+    scales = np.empty((rows, cols // 64), dtype=np.uint16)
+    _check(_lib.pipo_quantize_int4_g64_gpu(ctx, _ptr(w, C.c_float), rows, cols, _ptr(codes, C.c_uint8),
+                                           _ptr(scales, C.c_uint16)))
+    return codes, scales
+
+
+def pipo_unpack_int4_g64(ctx, codes, scales):
+    codes = _c(codes, np.uint8)
+    scales = _c(scales, np.uint16)
+    rows, half = codes.shape
+    out = np.empty((rows, half * 2), dtype=np.uint16)
+    _check(_lib.pipo_unpack_int4_g64(ctx, _ptr(codes, C.c_uint8), _ptr(scales, C.c_uint16), rows, half * 2,
+                                     _ptr(out, C.c_uint16)))
+    return out.view(np.float16)
+
+
+def pipo_linear(ctx, wfmt, path, x, w, bias=None):
+    x = _c(np.asarray(x, dtype=np.float16).view(np.uint16), np.uint16)
+    w = _c(w, np.float32)
+    M, K = x.shape
+    N = w.shape[0]
+    b = _c(bias, np.float32) if bias is not None else None
+    y = np.empty((M, N), dtype=np.float32)
+    _check(_lib.pipo_linear(ctx, wfmt, path, _ptr(x, C.c_uint16), _ptr(w, C.c_float),
+                            _ptr(b, C.c_float) if b is not None else None, M, N, K, _ptr(y, C.c_float)))
+    return y
+
+
+def pipo_attention_decode(ctx, q, k, v, n_heads):
+    q = _c(np.asarray(q, dtype=np.float16).view(np.uint16), np.uint16)
+    k = _c(np.asarray(k, dtype=np.float16).view(np.uint16), np.uint16)
+    v = _c(np.asarray(v, dtype=np.float16).view(np.uint16), np.uint16)
+    b, d = q.shape
+    L = k.shape[0]
+    o = np.empty((b, d), dtype=np.float32)
+    _check(_lib.pipo_attention_decode(ctx, _ptr(q, C.c_uint16), _ptr(k, C.c_uint16), _ptr(v, C.c_uint16),
+                                      b, L, d, n_heads, _ptr(o, C.c_float)))
+    return o
+
+
+def pipo_debug_capture(ctx, out: np.ndarray | None):
+    if out is None:
+        _check(_lib.pipo_debug_capture(ctx, 0, None))
+    else:
+        assert out.dtype == np.float32 and out.flags.c_contiguous
+        _check(_lib.pipo_debug_capture(ctx, 1, _ptr(out, C.c_float)))
+
+
+def pipo_probe_h2d(ctx, nbytes: int, reps: int = 5) -> float:
+    g = C.c_double()
+    _check(_lib.pipo_probe_h2d(ctx, nbytes, reps, C.byref(g)))
+    return g.value
+
+
+def make_config(shape, *, device=0, max_batch, max_seq, wfmt=PIPO_W_INT4_G64, weight_tier=PIPO_TIER_HOST,
+                kv_tier=PIPO_TIER_DEVICE, ring_layers=2, chunk_bytes=0, gemv_max_m=15, disk_threads=4,
+                disk_dir=None, flags=PIPO_F_TIMELINE, n_layers=None) -> pipo_config:
+    """pipo_config from a pipo_synth.OPTShape-like object (d_model, n_layers, n_heads, ffn_dim, vocab, max_pos)."""
+    return pipo_config(device=device, d_model=shape.d_model, n_layers=n_layers or shape.n_layers,
+                       n_heads=shape.n_heads, ffn_dim=shape.ffn_dim, vocab=shape.vocab, max_pos=shape.max_pos,
+                       max_batch=max_batch, max_seq=max_seq, wfmt=wfmt, weight_tier=weight_tier, kv_tier=kv_tier,
+                       ring_layers=ring_layers, chunk_bytes=chunk_bytes, gemv_max_m=gemv_max_m,
+                       disk_threads=disk_threads, disk_dir=(disk_dir.encode() if disk_dir else None), flags=flags)
+
+
+class Pipeline:
+    """Owns one pipo_ctx (one GPU).  Marshalling only."""
+
+    def __init__(self, cfg: pipo_config):
+        self.cfg = cfg
+        self.vocab = cfg.vocab
+        self.ctx = pipeline_init(cfg)
+
+    def close(self):
+        if self.ctx:
+            pipeline_destroy(self.ctx)
+            self.ctx = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def load_layer_weights(self, layer, w):
+        load_layer_weights(self.ctx, layer, w)
+
+    def load_synthetic(self, layer, seed):
+        pipo_load_synthetic(self.ctx, layer, seed)
+
+    def prefill(self, tokens, want_logits=False):
+        return prefill(self.ctx, tokens, want_logits, self.vocab)
+
+    def decode_step(self, tokens, want_logits=False):
+        return decode_step(self.ctx, tokens, want_logits, self.vocab)
+
+    def stats(self):
+        return pipeline_stats(self.ctx)
+
+    def stats_reset(self):
+        pipeline_stats_reset(self.ctx)

@@ -1,0 +1,143 @@
+"""GPU parity of the individual kernels through the C-ABI, against the oracle.
+
+Bars (BASELINE.json north_star): bit-exact for the 4-bit pack/unpack (K8) and the
+GPU quantizer; max relative error <= 2e-2 for the fp16/int4 linear layers and the
+decode attention, with the special cases that pin layouts exactly.
+"""
+import numpy as np
+import pytest
+
+from oracle import opt, quant
+from tests.gpu_util import pipo_mod, rel_inf
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    pipo = pipo_mod()
+    import pipo_synth as synth
+    shape = synth.OPTShape(d_model=256, n_layers=1, n_heads=4, ffn_dim=512, vocab=512, max_pos=64)
+    pl = pipo.Pipeline(pipo.make_config(shape, max_batch=4, max_seq=16, weight_tier=pipo.PIPO_TIER_DEVICE))
+    yield pipo, pl
+    pl.close()
+
+
+def test_unpack_exhaustive_bit_exact(env):
+    pipo, pl = env
+    scales = np.array([0.0999755859375, 2.0**-24, 3 * 2.0**-20, 6.103515625e-05, 1.0, 8188.0, 0.0, -0.5],
+                      dtype=np.float16)
+    packed = np.tile(np.arange(256, dtype=np.uint8), (len(scales), 1))          # K = 512
+    s16 = np.repeat(scales[:, None], 8, axis=1)
+    got = pipo.pipo_unpack_int4_g64(pl.ctx, packed, s16.view(np.uint16))
+    ref = quant.unpack_scale_fp16(packed, s16)
+    assert np.array_equal(got.view(np.uint16), ref.view(np.uint16))
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_gpu_quantizer_bit_exact(env, seed):
+    pipo, pl = env
+    rng = np.random.default_rng(seed)
+    w = (rng.standard_normal((200, 384)) * 0.02).astype(np.float16).astype(np.float32)
+    w[0, :64] = 0
+    w[1, :64] = 0.875
+    w[2, :64] = 2.5e-7 * rng.standard_normal(64).astype(np.float32)
+    w[3, 64:128] = rng.choice([-1, 1], 64) * 4095 * 2.0**-14
+    codes, scales = pipo.pipo_quantize_int4_g64_gpu(pl.ctx, w)
+    q, s = quant.quantize_int4_g64(w)
+    assert np.array_equal(codes, quant.pack_int4(q))
+    assert np.array_equal(scales, quant.scales_to_bits(s))
+    with pytest.raises(pipo.PipoError):
+        pipo.pipo_quantize_int4_g64_gpu(pl.ctx, np.full((1, 64), np.inf, dtype=np.float32))
+
+
+def _ref_linear(x16, w, bias, wfmt):
+    wh = quant.quant_dequant(w) if wfmt == 1 else w.astype(np.float16).astype(np.float32)
+    y = x16.astype(np.float64) @ wh.astype(np.float64).T
+    if bias is not None:
+        y = y + bias.astype(np.float16).astype(np.float64)
+    return y
+
+
+SHAPES = [(1, 128, 64), (3, 200, 256), (4, 384, 1024), (13, 130, 512), (16, 256, 256), (17, 384, 320),
+          (40, 200, 1024), (64, 512, 2048), (100, 256, 192), (130, 384, 512)]
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+@pytest.mark.parametrize("wfmt", [1, 0])
+def test_linear_vs_oracle(env, M, N, K, wfmt):
+    pipo, pl = env
+    rng = np.random.default_rng(M * 7 + N + K)
+    x = rng.standard_normal((M, K)).astype(np.float16)
+    w = (rng.standard_normal((N, K)) * 0.02).astype(np.float16).astype(np.float32)
+    bias = (rng.uniform(-0.02, 0.02, N)).astype(np.float32)
+    ref = _ref_linear(x, w, bias, wfmt)
+    paths = [pipo.PATH_GEMM] + ([pipo.PATH_GEMV] if wfmt == 1 and M <= 16 else [])
+    for path in paths:
+        y = pipo.pipo_linear(pl.ctx, wfmt, path, x, w, bias)
+        err = rel_inf(y, ref)
+        assert err < 2e-2, (path, err)
+        # fp16-rounded dequantized weights (GEMM) / exact codes (GEMV): far inside the bar
+        assert err < (2e-3 if wfmt == 1 else 1e-4), (path, err)
+
+
+@pytest.mark.parametrize("path", ["gemv", "gemm"])
+def test_linear_special_cases_exact(env, path):
+    pipo, pl = env
+    p = pipo.PATH_GEMV if path == "gemv" else pipo.PATH_GEMM
+    rng = np.random.default_rng(5)
+    N, K = 200, 256
+    w = (rng.standard_normal((N, K)) * 0.02).astype(np.float16).astype(np.float32)
+    bias = rng.uniform(-0.02, 0.02, N).astype(np.float16).astype(np.float32)
+    # x = 0 -> bias exactly
+    y0 = pipo.pipo_linear(pl.ctx, 1, p, np.zeros((3, K), np.float16), w, bias)
+    assert np.array_equal(y0, np.broadcast_to(bias, (3, N)))
+    # one-hot x_k -> column k of the dequantized weight (+ bias, one fp32 rounding):
+    # GEMV multiplies exact codes: q*s exact; GEMM multiplies fp16_rne(q*s) (kernel K8)
+    q, s = quant.quantize_int4_g64(w)
+    col_exact = quant.dequantize(q, s)
+    col_fp16 = col_exact.astype(np.float16).astype(np.float32)
+    for k in (0, 63, 64, 255):
+        x = np.zeros((2, K), np.float16)
+        x[:, k] = 1
+        y = pipo.pipo_linear(pl.ctx, 1, p, x, w, bias)
+        col = col_exact[:, k] if path == "gemv" else col_fp16[:, k]
+        assert np.array_equal(y[0], (col + bias).astype(np.float32)), k
+    # power-of-two linearity, bit-exact
+    x = rng.standard_normal((4, K)).astype(np.float16)
+    y1 = pipo.pipo_linear(pl.ctx, 1, p, x, w, None)
+    y2 = pipo.pipo_linear(pl.ctx, 1, p, (x.astype(np.float32) * 4).astype(np.float16), w, None)
+    assert np.array_equal(y2, y1 * 4)
+
+
+@pytest.mark.parametrize("b,L,d,H", [(1, 1, 128, 2), (2, 7, 256, 4), (3, 65, 256, 2), (4, 300, 512, 4),
+                                     (2, 544, 1024, 8), (64, 40, 512, 8)])
+def test_attention_decode_vs_oracle(env, b, L, d, H):
+    pipo, pl = env
+    rng = np.random.default_rng(b * 1000 + L)
+    q = (rng.standard_normal((b, d)) * (d // H) ** -0.5).astype(np.float16)
+    k = rng.standard_normal((L, b, d)).astype(np.float16)
+    v = rng.standard_normal((L, b, d)).astype(np.float16)
+    o = pipo.pipo_attention_decode(pl.ctx, q, k, v, H)
+    ref = opt.attention(q.astype(np.float64)[:, None], k.astype(np.float64).transpose(1, 0, 2),
+                        v.astype(np.float64).transpose(1, 0, 2), L - 1, H)[:, 0]
+    assert rel_inf(o, ref) < 2e-2
+    assert rel_inf(o, ref) < 5e-3
+
+
+def test_attention_special_cases_exact(env):
+    pipo, pl = env
+    rng = np.random.default_rng(9)
+    b, d, H = 2, 256, 2
+    q = rng.standard_normal((b, d)).astype(np.float16)
+    k = rng.standard_normal((1, b, d)).astype(np.float16)
+    v = rng.standard_normal((1, b, d)).astype(np.float16)
+    # one cached position: softmax of one logit is 1 -> output is the V row, exactly
+    o = pipo.pipo_attention_decode(pl.ctx, q, k, v, H)
+    assert np.array_equal(o, v[0].astype(np.float32))
+    # all-equal keys -> mean of V (within fp16 output rounding)
+    L = 33
+    k2 = np.repeat(k, L, axis=0)
+    v2 = rng.standard_normal((L, b, d)).astype(np.float16)
+    o2 = pipo.pipo_attention_decode(pl.ctx, q, k2, v2, H)
+    assert np.abs(o2 - v2.astype(np.float64).mean(0)).max() < 2e-3
