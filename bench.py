@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--disk-dir", default="/tmp/pipo_disk")
+    ap.add_argument("--profile", action="store_true",
+                    help="cudaProfilerStart/Stop around the timed region (ncu --profile-from-start off)")
     return ap.parse_args()
 
 
@@ -121,37 +123,39 @@ def measured_peaks():
 
 
 # ---------------------------------------------------------------------------
-def oracle_sample(cfg_name: str, wfmt: str, reps: int = 1):
+class OracleSample:
     """The CPU oracle as it stands (oracle/opt.py), on a bounded sample of the
     workload: one decode step through ONE decoder layer at full batch b and
-    L = P + G/2 cached positions, plus the LM head; extrapolated to a full step as
-    n_layers * t_layer + t_head.  Returns (tokens/s, sample description, cores)."""
-    from oracle import opt
-    c = CONFIGS[cfg_name]
-    s, b, P, G = c["shape"], c["b"], c["P"], c["G"]
-    cores = len(os.sched_getaffinity(0))
-    for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
-        os.environ.setdefault(v, str(cores))
-    lw = opt.layer_from_masters(synth.layer_masters(s, 0), wfmt)
-    emb = synth.embed_masters(s)
-    tok = emb["tok"].astype(np.float64)
-    past = P + G // 2 - 1
-    rng = np.random.default_rng(0)
-    kc = rng.standard_normal((b, past + 1, s.d_model)) * 0.5
-    vc = rng.standard_normal((b, past + 1, s.d_model)) * 0.5
-    h = rng.standard_normal((b, 1, s.d_model))
-    times = []
-    for _ in range(reps):
+    L = P + G/2 cached positions, plus the LM head; a full step is extrapolated as
+    n_layers * t_layer + t_head.  Weights are drawn once (setup, untimed)."""
+
+    def __init__(self, cfg_name: str, wfmt: str):
+        from oracle import opt
+        self.opt = opt
+        c = CONFIGS[cfg_name]
+        self.s, self.b, P, G = c["shape"], c["b"], c["P"], c["G"]
+        self.cores = len(os.sched_getaffinity(0))
+        self.lw = opt.layer_from_masters(synth.layer_masters(self.s, 0), wfmt)
+        emb = synth.embed_masters(self.s)
+        self.lnf = (emb["lnf_g"].astype(np.float64), emb["lnf_b"].astype(np.float64))
+        self.tok = emb["tok"].astype(np.float64)
+        self.past = P + G // 2 - 1
+        rng = np.random.default_rng(0)
+        d = self.s.d_model
+        self.kc = rng.standard_normal((self.b, self.past + 1, d)) * 0.5
+        self.vc = rng.standard_normal((self.b, self.past + 1, d)) * 0.5
+        self.h = rng.standard_normal((self.b, 1, d))
+        self.desc = (f"oracle/opt.py fp64: 1 of {self.s.n_layers} decoder layers + LM head at b={self.b}, "
+                     f"L={self.past + 1}, extrapolated x{self.s.n_layers} layers")
+
+    def step(self) -> float:
+        opt = self.opt
         t0 = time.perf_counter()
-        h2 = opt.decoder_layer(h, lw, kc, vc, past, s.n_heads)
+        h2 = opt.decoder_layer(self.h, self.lw, self.kc, self.vc, self.past, self.s.n_heads)
         t1 = time.perf_counter()
-        opt.layer_norm(h2[:, 0], emb["lnf_g"], emb["lnf_b"]) @ tok.T
+        opt.greedy(opt.layer_norm(h2[:, 0], *self.lnf) @ self.tok.T)
         t2 = time.perf_counter()
-        times.append((t1 - t0) * s.n_layers + (t2 - t1))
-    step = min(times)
-    desc = (f"oracle/opt.py fp64: 1 of {s.n_layers} decoder layers + LM head at b={b}, L={past + 1}, "
-            f"extrapolated x{s.n_layers} layers")
-    return b / step, desc, cores, step
+        return (t1 - t0) * self.s.n_layers + (t2 - t1)
 
 
 def run_reference(args):
@@ -159,10 +163,10 @@ def run_reference(args):
     if rank != 0:
         return 0
     c = CONFIGS[args.config]
+    sample = OracleSample(args.config, args.wfmt)
     t_all = []
-    tps = None
     for i in range(args.warmup + args.steps):
-        tps, desc, cores, step = oracle_sample(args.config, args.wfmt)
+        step = sample.step()
         if i >= args.warmup:
             t_all.append(step)
     ms = statistics.mean(t_all) * 1e3
@@ -171,7 +175,8 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": args.config, "wfmt": args.wfmt},
-            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": desc},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": sample.cores, "kind": "oracle",
+                             "sample": sample.desc},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -183,6 +188,7 @@ def run_pipo(args):
     import torch.distributed as dist
 
     from paper_2504_03664_b200 import pipo
+    from paper_2504_03664_b200.shard import aggregate_throughput, max_over_ranks, shard_range
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -201,7 +207,7 @@ def run_pipo(args):
                            wfmt=pipo.PIPO_W_INT4_G64 if args.wfmt == "int4" else pipo.PIPO_W_FP16,
                            weight_tier=c["weight_tier"], kv_tier=c["kv_tier"], ring_layers=args.ring,
                            chunk_bytes=int(args.chunk_mb * (1 << 20)), disk_dir=disk_dir,
-                           flags=pipo.PIPO_F_TIMELINE)
+                           flags=pipo.PIPO_F_TIMELINE | pipo.PIPO_F_KPROF)
     t_setup = time.perf_counter()
     pl = pipo.Pipeline(cfg)
     pl.load_synthetic(pipo.PIPO_LAYER_EMBED, synth.WEIGHT_SEED)
@@ -210,7 +216,8 @@ def run_pipo(args):
     t_load = time.perf_counter() - t_setup
     link_probe = pipo.pipo_probe_h2d(pl.ctx, 256 << 20, 5)
     # batch shard: rank r owns sequences [r*b, (r+1)*b) of the global prompt batch
-    prompt = synth.prompts(b * world, P, s.vocab)[rank * b:(rank + 1) * b]
+    lo, hi = shard_range(b * world, world, rank)
+    prompt = synth.prompts(b * world, P, s.vocab)[lo:hi]
     t0 = time.perf_counter()
     nxt, _ = pl.prefill(prompt)
     t_prefill = time.perf_counter() - t0
@@ -226,27 +233,25 @@ def run_pipo(args):
             dist.barrier()
         torch.cuda.synchronize(local)
 
-    def max_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
     # ---- value: inputs resident in HBM (device token ids, no host round trip) ----
     pl.stats_reset()
     barrier()
     with ClockSampler(local) as clk:
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        if args.profile:
+            torch.cuda.cudart().cudaProfilerStart()
         e0.record(comp)
         for _ in range(args.steps):
             pipo.decode_step_dev(pl.ctx, tok_dev.data_ptr(), tok_dev.data_ptr())
         e1.record(comp)
         torch.cuda.synchronize(local)
+        if args.profile:
+            torch.cuda.cudart().cudaProfilerStop()
     barrier()
     t_dev = max_over_ranks(e0.elapsed_time(e1) / 1e3)
     st = pl.stats()
+    kst = pipo.pipo_kernel_stats(pl.ctx)
     clocks = clk.summary()
 
     # ---- e2e: the public C-ABI call with HOST buffers, H2D ids + D2H ids every step ----
@@ -262,15 +267,36 @@ def run_pipo(args):
         barrier()
         t_e2e = max_over_ranks(e0.elapsed_time(e1) / 1e3)
         per_step_h2d = st["h2d_bytes"] / max(1, st["decode_steps"]) + b * 4
-        e2e = {"value": world * b * args.steps / t_e2e, "unit": "tokens/s",
+        e2e = {"value": aggregate_throughput(b, world, args.steps, t_e2e), "unit": "tokens/s",
                "h2d_bytes_per_step": int(per_step_h2d), "d2h_bytes_per_step": int(b * 4),
                "note": "decode_step(host tokens) -> host next ids; h2d counts the streamed weights too"}
 
-    value = world * b * args.steps / t_dev
+    value = aggregate_throughput(b, world, args.steps, t_dev)
     ms = t_dev / args.steps * 1e3
     peaks = measured_peaks()
     layer_bytes = st["h2d_bytes"] / max(1, st["decode_steps"])
     link_floor_s = layer_bytes / (link_probe * 1e9)
+    kernels = {}
+    for name, k in kst.items():
+        if k["units"] and k["ms"] > 0:
+            kernels[name] = {"units": k["units"], "ms_per_step": k["ms"] / args.steps,
+                             "share_of_step": k["ms"] / args.steps / ms,
+                             "gbs": k["bytes"] / (k["ms"] / 1e3) / 1e9, "tflops": k["flops"] / (k["ms"] / 1e3) / 1e12}
+    dom = max(kernels, key=lambda n: kernels[n]["ms_per_step"]) if kernels else None
+    roofline = None
+    if dom:
+        kd = kst[dom]
+        per_unit_bytes = kd["bytes"] / kd["units"]
+        per_unit_s = kd["ms"] / kd["units"] / 1e3
+        hbm = peaks.get("hbm_gbs") or 6650.0
+        tc = peaks.get("bf16_tflops_sustained") or 1400.0
+        ach = per_unit_bytes / per_unit_s / 1e9
+        roofline = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                    "frac": ach / hbm, "traffic": None,
+                    "bytes_per_unit": per_unit_bytes, "us_per_unit": per_unit_s * 1e6,
+                    "tflops": kd["flops"] / kd["units"] / per_unit_s / 1e12,
+                    "tflops_frac_of_fp16_peak": kd["flops"] / kd["units"] / per_unit_s / 1e12 / tc,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy), bf16_tflops_sustained (fp16 same rate)"}
     line = None
     if rank == 0:
         line = {
@@ -289,6 +315,8 @@ def run_pipo(args):
             "clocks": clocks,
             "e2e": e2e,
             "gpu_launches": int(st["kernel_launches"]),
+            "roofline": roofline,
+            "kernels": kernels,
             "link_roofline": {"bound": "host-link", "bytes_per_step": int(layer_bytes),
                               "probe_gbs": link_probe, "achieved_gbs": layer_bytes / (ms / 1e3) / 1e9,
                               "frac": link_floor_s / (ms / 1e3), "copy_engine_gbs": st["h2d_gbs"]},
@@ -299,8 +327,10 @@ def run_pipo(args):
         }
     pl.close()
     if rank == 0 and not args.no_cpu_baseline and world == 1:
-        tps, desc, cores, _ = oracle_sample(args.config, args.wfmt)
-        line["cpu_baseline"] = {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": desc}
+        sample = OracleSample(args.config, args.wfmt)
+        t = min(sample.step() for _ in range(2))
+        line["cpu_baseline"] = {"value": b / t, "unit": "tokens/s", "cores": sample.cores, "kind": "oracle",
+                                "sample": sample.desc + "; best of 2"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -65,6 +65,7 @@ typedef enum { PIPO_TIER_DEVICE = 0, PIPO_TIER_HOST = 1, PIPO_TIER_DISK = 2 } pi
 
 /* flags */
 #define PIPO_F_TIMELINE 1u  /* record per-segment CUDA events for busy fractions (default on) */
+#define PIPO_F_KPROF 2u     /* time every kernel unit with CUDA events (pipo_kernel_stats) */
 
 typedef struct {
   int32_t device;        /* CUDA ordinal */
@@ -169,6 +170,16 @@ pipo_status decode_step_dev(pipo_ctx* ctx, const int32_t* tokens_dev, int32_t* n
 pipo_status pipeline_stats(pipo_ctx* ctx, pipo_stats* out);
 pipo_status pipeline_stats_reset(pipo_ctx* ctx);
 
+/* Per-kernel-class timing (needs PIPO_F_KPROF): one unit = one linear layer / one
+ * attention layer / one LM head; ms from CUDA events on the compute stream around
+ * each unit; bytes / flops are the ALGORITHMIC counts. */
+typedef enum {
+  PIPO_K_LINEAR_DECODE = 0, PIPO_K_ATTN_DECODE = 1, PIPO_K_HEAD = 2,
+  PIPO_K_LINEAR_PREFILL = 3, PIPO_K_ATTN_PREFILL = 4, PIPO_K_MISC = 5, PIPO_K_COUNT = 6
+} pipo_kclass;
+typedef struct { int64_t units; double ms, bytes, flops; } pipo_kstats;
+pipo_status pipo_kernel_stats(pipo_ctx* ctx, int32_t cls, pipo_kstats* out);
+
 /* cudaStream_t of the compute stream (which=0) or weight-copy stream (which=1),
  * as an opaque handle for external CUDA-event timing. */
 void* pipo_stream(pipo_ctx* ctx, int32_t which);
@@ -192,7 +203,8 @@ pipo_status pipo_unpack_int4_g64(pipo_ctx* ctx, const uint8_t* codes, const uint
 /* One fused linear layer on the GPU through the production kernels:
  * y[M][N] = x[M][K] . W^T + bias (bias may be NULL).  x fp16 bits [M][K];
  * W given as fp32 masters [N][K] (quantized per wfmt inside); y fp32 [M][N].
- * path: 0 = automatic (as the pipeline chooses), 1 = int4 GEMV, 2 = GEMM. */
+ * path: 0 = automatic (as the pipeline chooses), 1 = int4 GEMV (CUDA cores),
+ * 2 = mma.sync GEMM (legacy baseline), 3 = tcgen05/TMEM GEMM. */
 pipo_status pipo_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, const uint16_t* x,
                         const float* w, const float* bias, int32_t M, int32_t N, int32_t K,
                         float* y);

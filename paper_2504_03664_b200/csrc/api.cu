@@ -138,6 +138,44 @@ pipo_status span_end(pipo_ctx* ctx, cudaStream_t st, cudaEvent_t a, int lane, in
   return PIPO_OK;
 }
 
+pipo_status kbegin(pipo_ctx* ctx, cudaEvent_t* a) {
+  if (!ctx->kprof) return PIPO_OK;
+  TRY(ev_get(ctx, a));
+  CK(cudaEventRecord(*a, ctx->s_comp));
+  return PIPO_OK;
+}
+
+pipo_status kend(pipo_ctx* ctx, cudaEvent_t a, int cls, double bytes, double flops) {
+  if (!ctx->kprof) return PIPO_OK;
+  cudaEvent_t b;
+  TRY(ev_get(ctx, &b));
+  CK(cudaEventRecord(b, ctx->s_comp));
+  ctx->krecs.push_back(KRec{a, b, cls, bytes, flops});
+  return PIPO_OK;
+}
+
+// algorithmic bytes of one linear layer (weights + x + output traffic)
+double linear_bytes(const LinearArgs& la) {
+  const double nk = (double)la.N * la.K;
+  const double w = la.wfmt == 1 ? nk / 2 + nk / 64 * 2 : nk * 2;
+  double out = 0;
+  switch (la.epi.kind) {
+    case EPI_QKV: out = (double)la.M * la.N * 2; break;
+    case EPI_RESID: out = (double)la.M * la.N * 8; break;
+    case EPI_RELU: out = (double)la.M * la.N * 2; break;
+    default: out = (double)la.M * la.N * 4; break;
+  }
+  return w + (double)la.M * la.K * 2 + out + (la.epi.bias ? la.N * 2.0 : 0.0);
+}
+
+pipo_status run_linear(pipo_ctx* ctx, const LinearArgs& la, int path, int cls) {
+  cudaEvent_t a = nullptr;
+  TRY(kbegin(ctx, &a));
+  LAUNCH(launch_linear(la, path, ctx->gemv_max_m, ctx->s_comp));
+  TRY(kend(ctx, a, cls, linear_bytes(la), 2.0 * la.M * la.N * la.K));
+  return PIPO_OK;
+}
+
 // ---- pointers into a layer blob -----------------------------------------------
 const __half* vec_ptr(const pipo_ctx* c, const uint8_t* blob, int v) {
   return reinterpret_cast<const __half*>(blob + c->lay.vec_off[v]);
@@ -232,6 +270,7 @@ pipo_status forward(pipo_ctx* ctx, int b, int n, int past, bool want_logits) {
   aa.b = b; aa.n = n; aa.past = past; aa.d = d; aa.n_heads = ctx->H; aa.kv_b = b;
   aa.ws = ctx->ws; aa.ws_floats = ctx->ws_floats; aa.num_sms = ctx->num_sms;
   const int64_t pass_base = ctx->g_comp;
+  const int lin_cls = n == 1 ? PIPO_K_LINEAR_DECODE : PIPO_K_LINEAR_PREFILL;
 
   for (int j = 0; j < ctx->l; ++j) {
     const int64_t G = ctx->g_comp++;
@@ -266,10 +305,18 @@ pipo_status forward(pipo_ctx* ctx, int b, int n, int past, bool want_logits) {
     la.epi.kind = EPI_QKV; la.epi.bias = vec_ptr(ctx, blob, V_B_QKV); la.epi.M = M; la.epi.N = 3 * d;
     la.epi.q = ctx->q; la.epi.kc = kc; la.epi.vc = vc; la.epi.d = d; la.epi.n_tok = n; la.epi.past = past;
     la.epi.kv_b = b; la.epi.qscale = 1.0f / sqrtf((float)ctx->hd);
-    LAUNCH(launch_linear(la, PATH_AUTO, ctx->gemv_max_m, cs));
+    TRY(run_linear(ctx, la, PATH_AUTO, lin_cls));
     aa.q = ctx->q; aa.kc = kc; aa.vc = vc; aa.o = ctx->xa;
-    if (n == 1) LAUNCH(launch_attention_decode(aa, cs));
-    else LAUNCH(launch_attention_prefill(aa, cs));
+    {
+      cudaEvent_t ka = nullptr;
+      TRY(kbegin(ctx, &ka));
+      if (n == 1) LAUNCH(launch_attention_decode(aa, cs));
+      else LAUNCH(launch_attention_prefill(aa, cs));
+      const double L = past + n;
+      const double kvb = n == 1 ? 2.0 * L * b * d * 2 : 2.0 * L * b * d * 2;
+      const double fl = n == 1 ? 4.0 * b * d * L : 2.0 * b * d * (double)n * (past + (n + 1) / 2.0);
+      TRY(kend(ctx, ka, n == 1 ? PIPO_K_ATTN_DECODE : PIPO_K_ATTN_PREFILL, kvb + 4.0 * M * d, fl));
+    }
     TRY(span_end(ctx, cs, t0, 1, 0));
     if (host_kv(ctx)) {
       // CallStoreCache: save the new positions after MHA on the save stream
@@ -293,7 +340,7 @@ pipo_status forward(pipo_ctx* ctx, int b, int n, int past, bool want_logits) {
     la.x = ctx->xa; la.w = blob + ctx->lay.mat_off[M_OUT]; la.N = d; la.K = d;
     la.epi = EpiParams{};
     la.epi.kind = EPI_RESID; la.epi.bias = vec_ptr(ctx, blob, V_B_OUT); la.epi.M = M; la.epi.N = d; la.epi.h = ctx->h;
-    LAUNCH(launch_linear(la, PATH_AUTO, ctx->gemv_max_m, cs));
+    TRY(run_linear(ctx, la, PATH_AUTO, lin_cls));
     TRY(span_end(ctx, cs, t0, 1, 0));
     // ---- MLP: LN2 + FC1 + ReLU (seg 2) ----
     if (streamed(ctx)) CK(cudaStreamWaitEvent(cs, ctx->ev_ready[slot][2], 0));
@@ -302,7 +349,7 @@ pipo_status forward(pipo_ctx* ctx, int b, int n, int past, bool want_logits) {
     la.x = ctx->xa; la.w = blob + ctx->lay.mat_off[M_FC1]; la.N = ctx->F; la.K = d;
     la.epi = EpiParams{};
     la.epi.kind = EPI_RELU; la.epi.bias = vec_ptr(ctx, blob, V_B_FC1); la.epi.M = M; la.epi.N = ctx->F; la.epi.u = ctx->u;
-    LAUNCH(launch_linear(la, PATH_AUTO, ctx->gemv_max_m, cs));
+    TRY(run_linear(ctx, la, PATH_AUTO, lin_cls));
     TRY(span_end(ctx, cs, t0, 1, 0));
     // ---- MLP: FC2 + residual (seg 3) ----
     if (streamed(ctx)) CK(cudaStreamWaitEvent(cs, ctx->ev_ready[slot][3], 0));
@@ -310,7 +357,7 @@ pipo_status forward(pipo_ctx* ctx, int b, int n, int past, bool want_logits) {
     la.x = ctx->u; la.w = blob + ctx->lay.mat_off[M_FC2]; la.N = d; la.K = ctx->F;
     la.epi = EpiParams{};
     la.epi.kind = EPI_RESID; la.epi.bias = vec_ptr(ctx, blob, V_B_FC2); la.epi.M = M; la.epi.N = d; la.epi.h = ctx->h;
-    LAUNCH(launch_linear(la, PATH_AUTO, ctx->gemv_max_m, cs));
+    TRY(run_linear(ctx, la, PATH_AUTO, lin_cls));
     TRY(span_end(ctx, cs, t0, 1, 0));
     if (streamed(ctx)) CK(cudaEventRecord(ctx->ev_free[slot], cs));   // ring slot release (a12)
     if (ctx->cap_on)
@@ -323,7 +370,7 @@ pipo_status forward(pipo_ctx* ctx, int b, int n, int past, bool want_logits) {
   la.x = ctx->xa; la.w = reinterpret_cast<const uint8_t*>(ctx->tok); la.wfmt = 0; la.M = b; la.N = ctx->V; la.K = d;
   la.epi = EpiParams{};
   la.epi.kind = EPI_F32; la.epi.M = b; la.epi.N = ctx->V; la.epi.y = ctx->logits; la.epi.ldy = ctx->V;
-  LAUNCH(launch_linear(la, PATH_GEMM, ctx->gemv_max_m, cs));
+  TRY(run_linear(ctx, la, PATH_GEMM, PIPO_K_HEAD));
   LAUNCH(launch_argmax(ctx->logits, b, ctx->V, ctx->V, ctx->next, cs));
   TRY(span_end(ctx, cs, t0, 1, 0));
   (void)want_logits;
@@ -440,6 +487,7 @@ pipo_status pipeline_init(const pipo_config* cfg, pipo_ctx** out) {
   ctx->chunk = c.chunk_bytes;
   ctx->gemv_max_m = c.gemv_max_m > 0 ? std::min(c.gemv_max_m, 16) : 15;
   ctx->timeline = (c.flags & PIPO_F_TIMELINE) != 0;
+  ctx->kprof = (c.flags & PIPO_F_KPROF) != 0;
   ctx->lay = layer_layout(ctx->d, ctx->F, ctx->wfmt);
   ctx->layer_bytes = ctx->lay.total;
   ctx->layer_loaded.assign(ctx->l, 0);
@@ -807,6 +855,7 @@ pipo_status pipeline_stats_reset(pipo_ctx* ctx) {
   CK(cudaSetDevice(ctx->cfg.device));
   CK(cudaDeviceSynchronize());
   ctx->spans.clear();
+  ctx->krecs.clear();
   ctx->ev_used = 0;
   ctx->win_open = false;
   ctx->win_start = ctx->win_end = nullptr;
@@ -814,6 +863,25 @@ pipo_status pipeline_stats_reset(pipo_ctx* ctx) {
   ctx->prefill_calls = ctx->decode_steps = ctx->tokens = 0;
   ctx->prefill_s = ctx->decode_s = 0;
   ctx->h2d_bytes = ctx->d2h_bytes = 0;
+  return PIPO_OK;
+}
+
+pipo_status pipo_kernel_stats(pipo_ctx* ctx, int32_t cls, pipo_kstats* out) {
+  CHECK_CTX();
+  if (!out || cls < 0 || cls >= PIPO_K_COUNT) return set_err(PIPO_E_INVALID_ARG, "bad kernel class");
+  CK(cudaSetDevice(ctx->cfg.device));
+  CK(cudaDeviceSynchronize());
+  pipo_kstats k{};
+  for (const KRec& r : ctx->krecs) {
+    if (r.cls != cls) continue;
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, r.a, r.b));
+    k.units++;
+    k.ms += ms;
+    k.bytes += r.bytes;
+    k.flops += r.flops;
+  }
+  *out = k;
   return PIPO_OK;
 }
 
@@ -880,7 +948,7 @@ pipo_status pipo_unpack_int4_g64(pipo_ctx* ctx, const uint8_t* codes, const uint
 pipo_status pipo_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, const uint16_t* x, const float* w,
                         const float* bias, int32_t M, int32_t N, int32_t K, float* y) {
   CHECK_CTX();
-  if (!x || !w || !y || M <= 0 || N <= 0 || K <= 0 || K % 64 || (wfmt != 0 && wfmt != 1) || path < 0 || path > 2)
+  if (!x || !w || !y || M <= 0 || N <= 0 || K <= 0 || K % 64 || (wfmt != 0 && wfmt != 1) || path < 0 || path > 3)
     return set_err(PIPO_E_INVALID_ARG, "bad linear arguments");
   CK(cudaSetDevice(ctx->cfg.device));
   const MatLayout ml = mat_layout(N, K, wfmt);

@@ -22,6 +22,12 @@ struct Span {            // one interval on a device lane, between two timed eve
   int64_t bytes;
 };
 
+struct KRec {            // one timed kernel unit (PIPO_F_KPROF)
+  cudaEvent_t a, b;
+  int cls;
+  double bytes, flops;
+};
+
 struct DiskTier;         // disk.cpp
 
 }  // namespace pipo
@@ -100,6 +106,8 @@ struct pipo_ctx {
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   std::vector<pipo::Span> spans;
+  bool kprof = false;
+  std::vector<pipo::KRec> krecs;
   cudaEvent_t win_start = nullptr, win_end = nullptr;
   bool win_open = false;
   int64_t launches = 0;

@@ -19,29 +19,9 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "layout.h"
+#include "epilogue.cuh"
 
 namespace pipo {
-
-__device__ __forceinline__ void epi_store(const EpiParams& e, int m, int n, float acc) {
-  if (m >= e.M || n >= e.N) return;
-  const float v = acc + (e.bias ? __half2float(e.bias[n]) : 0.f);
-  switch (e.kind) {
-    case EPI_QKV: {
-      const int bi = m / e.n_tok, t = m - bi * e.n_tok;
-      if (n < e.d) {
-        e.q[(int64_t)m * e.d + n] = __float2half_rn(v * e.qscale);
-      } else {
-        const int64_t off = ((int64_t)(e.past + t) * e.kv_b + bi) * e.d;
-        if (n < 2 * e.d) e.kc[off + n - e.d] = __float2half_rn(v);
-        else e.vc[off + n - 2 * e.d] = __float2half_rn(v);
-      }
-      break;
-    }
-    case EPI_RESID: e.h[(int64_t)m * e.N + n] += v; break;
-    case EPI_RELU: e.u[(int64_t)m * e.N + n] = __float2half_rn(fmaxf(v, 0.f)); break;
-    default: e.y[(int64_t)m * e.ldy + n] = v; break;
-  }
-}
 
 // ---------------------------------------------------------------------------
 // split-K fixup: returns true in the CTA that must run the epilogue; `acc` then
@@ -348,6 +328,7 @@ int launch_linear(const LinearArgs& a, int path, int gemv_max_m, cudaStream_t st
   bool gemv = false;
   if (path == PATH_GEMV) gemv = true;
   else if (path == PATH_AUTO) gemv = (a.wfmt == 1 && a.M <= gemv_max_m);
+  if (path == PATH_TC || (path == PATH_AUTO && !gemv)) return launch_linear_tc(a, st);
   if (gemv) {
     if (a.wfmt != 1 || a.M > 16) return -1;
     if (a.M <= 4) return run_gemv<4>(a, st);

@@ -43,7 +43,10 @@ struct LinearArgs {
   int num_sms = 148;
 };
 
-enum LinearPath { PATH_AUTO = 0, PATH_GEMV = 1, PATH_GEMM = 2 };
+enum LinearPath { PATH_AUTO = 0, PATH_GEMV = 1, PATH_GEMM = 2, PATH_TC = 3 };
+
+// tcgen05 / TMEM fused dequant GEMM (k_gemm_tc.cu)
+int launch_linear_tc(const LinearArgs& a, cudaStream_t st);
 
 // returns the number of kernels launched (0 on a launch error -> check cudaGetLastError)
 int launch_linear(const LinearArgs& a, int path, int gemv_max_m, cudaStream_t st);

@@ -22,8 +22,10 @@ STATUS_NAMES = ["OK", "INVALID_ARG", "STATE", "OOM", "IO", "FORMAT", "INFEASIBLE
 PIPO_W_FP16, PIPO_W_INT4_G64 = 0, 1
 PIPO_TIER_DEVICE, PIPO_TIER_HOST, PIPO_TIER_DISK = 0, 1, 2
 PIPO_F_TIMELINE = 1
+PIPO_F_KPROF = 2
+K_CLASSES = ["linear_decode", "attn_decode", "lm_head", "linear_prefill", "attn_prefill", "misc"]
 PIPO_LAYER_EMBED = -1
-PATH_AUTO, PATH_GEMV, PATH_GEMM = 0, 1, 2
+PATH_AUTO, PATH_GEMV, PATH_GEMM, PATH_TC = 0, 1, 2, 3
 
 _f = C.POINTER(C.c_float)
 _u8 = C.POINTER(C.c_uint8)
@@ -47,6 +49,10 @@ class pipo_layer_weights(C.Structure):
 
 class pipo_embed_weights(C.Structure):
     _fields_ = [(n, _f) for n in ("tok", "pos", "lnf_g", "lnf_b")]
+
+
+class pipo_kstats(C.Structure):
+    _fields_ = [("units", C.c_int64), ("ms", C.c_double), ("bytes", C.c_double), ("flops", C.c_double)]
 
 
 class pipo_stats(C.Structure):
@@ -81,6 +87,7 @@ _sig("decode_step_dev", C.c_int, _P, _P, _P)
 _sig("pipeline_stats", C.c_int, _P, C.POINTER(pipo_stats))
 _sig("pipeline_stats_reset", C.c_int, _P)
 _sig("pipo_stream", _P, _P, C.c_int32)
+_sig("pipo_kernel_stats", C.c_int, _P, C.c_int32, C.POINTER(pipo_kstats))
 _sig("pipo_quantize_int4_g64", C.c_int, _f, C.c_int64, C.c_int64, _u8, _u16)
 _sig("pipo_quantize_int4_g64_gpu", C.c_int, _P, _f, C.c_int64, C.c_int64, _u8, _u16)
 _sig("pipo_unpack_int4_g64", C.c_int, _P, _u8, _u16, C.c_int64, C.c_int64, _u16)
@@ -91,7 +98,7 @@ _sig("pipo_probe_h2d", C.c_int, _P, C.c_int64, C.c_int32, C.POINTER(C.c_double))
 
 EXPORTED = ["pipo_last_error", "pipo_abi_version", "pipeline_init", "pipeline_destroy", "load_layer_weights",
             "pipo_load_synthetic", "prefill", "decode_step", "decode_step_dev", "pipeline_stats",
-            "pipeline_stats_reset", "pipo_stream", "pipo_quantize_int4_g64", "pipo_quantize_int4_g64_gpu",
+            "pipeline_stats_reset", "pipo_stream", "pipo_kernel_stats", "pipo_quantize_int4_g64", "pipo_quantize_int4_g64_gpu",
             "pipo_unpack_int4_g64", "pipo_linear", "pipo_attention_decode", "pipo_debug_capture", "pipo_probe_h2d"]
 
 
@@ -178,6 +185,15 @@ def pipeline_stats(ctx) -> dict:
 
 def pipeline_stats_reset(ctx):
     _check(_lib.pipeline_stats_reset(ctx))
+
+
+def pipo_kernel_stats(ctx) -> dict:
+    out = {}
+    for i, name in enumerate(K_CLASSES):
+        k = pipo_kstats()
+        _check(_lib.pipo_kernel_stats(ctx, i, C.byref(k)))
+        out[name] = {"units": k.units, "ms": k.ms, "bytes": k.bytes, "flops": k.flops}
+    return out
 
 
 def pipo_stream(ctx, which=0) -> int:

@@ -60,7 +60,7 @@ def _ref_linear(x16, w, bias, wfmt):
 
 
 SHAPES = [(1, 128, 64), (3, 200, 256), (4, 384, 1024), (13, 130, 512), (16, 256, 256), (17, 384, 320),
-          (40, 200, 1024), (64, 512, 2048), (100, 256, 192), (130, 384, 512)]
+          (40, 200, 1024), (64, 512, 2048), (100, 256, 192), (130, 384, 512), (300, 256, 320), (64, 7168, 7168)]
 
 
 @pytest.mark.parametrize("M,N,K", SHAPES)
@@ -72,7 +72,7 @@ def test_linear_vs_oracle(env, M, N, K, wfmt):
     w = (rng.standard_normal((N, K)) * 0.02).astype(np.float16).astype(np.float32)
     bias = (rng.uniform(-0.02, 0.02, N)).astype(np.float32)
     ref = _ref_linear(x, w, bias, wfmt)
-    paths = [pipo.PATH_GEMM] + ([pipo.PATH_GEMV] if wfmt == 1 and M <= 16 else [])
+    paths = [pipo.PATH_TC, pipo.PATH_GEMM] + ([pipo.PATH_GEMV] if wfmt == 1 and M <= 16 else [])
     for path in paths:
         y = pipo.pipo_linear(pl.ctx, wfmt, path, x, w, bias)
         err = rel_inf(y, ref)
@@ -81,10 +81,10 @@ def test_linear_vs_oracle(env, M, N, K, wfmt):
         assert err < (2e-3 if wfmt == 1 else 1e-4), (path, err)
 
 
-@pytest.mark.parametrize("path", ["gemv", "gemm"])
+@pytest.mark.parametrize("path", ["gemv", "gemm", "tc"])
 def test_linear_special_cases_exact(env, path):
     pipo, pl = env
-    p = pipo.PATH_GEMV if path == "gemv" else pipo.PATH_GEMM
+    p = {"gemv": pipo.PATH_GEMV, "gemm": pipo.PATH_GEMM, "tc": pipo.PATH_TC}[path]
     rng = np.random.default_rng(5)
     N, K = 200, 256
     w = (rng.standard_normal((N, K)) * 0.02).astype(np.float16).astype(np.float32)
