@@ -208,14 +208,11 @@ pipo_status enqueue_copy(pipo_ctx* ctx, int64_t G, int64_t kv_pos) {
   TRY(span_begin(ctx, ctx->s_copy, &t0));
   uint8_t* dst = ctx->ring + (int64_t)slot * ctx->layer_bytes;
   int64_t bytes = 0;
-  for (int s = 0; s < 4; ++s) {
-    if (ctx->disk) {
-      TRY(disk_enqueue_segment(ctx, j, s, dst + ctx->lay.seg_off[s]));
-    } else {
-      const uint8_t* src = ctx->host_store + (int64_t)j * ctx->layer_bytes;
-      TRY(copy_chunks(ctx, dst + ctx->lay.seg_off[s], src + ctx->lay.seg_off[s], ctx->lay.seg_bytes[s]));
-    }
-    bytes += ctx->lay.seg_bytes[s];
+  // The merged blob is loaded as ONE request (data merging), split
+  // into chunk_bytes blocks (blockwise transfer; 0 = one block).
+  // A segment's ready event is recorded right after the block holding its last byte,
+  // so the compute stream consumes each segment as soon as it has landed.
+  auto after_segment = [&](int s) -> pipo_status {
     CK(cudaEventRecord(ctx->ev_ready[slot][s], ctx->s_copy));
     if (s == 0 && host_kv(ctx)) {
       // KV load advanced with the layer's MHA weights (reading Q6)
@@ -231,6 +228,31 @@ pipo_status enqueue_copy(pipo_ctx* ctx, int64_t G, int64_t kv_pos) {
       }
       ctx->kv_load_past[slot] = kv_pos;
       CK(cudaEventRecord(ctx->ev_ready[slot][4], ctx->s_copy));
+    }
+    return PIPO_OK;
+  };
+  if (ctx->disk) {
+    for (int s = 0; s < 4; ++s) {
+      const pipo_status ds = disk_enqueue_segment(ctx, j, s, dst + ctx->lay.seg_off[s]);
+      if (ds != PIPO_OK) {
+        ctx->poisoned = true;
+        return set_err(ds, ds == PIPO_E_IO ? "disk tier read failed" : ds == PIPO_E_FORMAT ? "disk blob header mismatch"
+                                                                                          : "disk tier transfer setup failed");
+      }
+      bytes += ctx->lay.seg_bytes[s];
+      TRY(after_segment(s));
+    }
+  } else {
+    const uint8_t* src = ctx->host_store + (int64_t)j * ctx->layer_bytes;
+    const int64_t total = ctx->lay.seg_off[3] + ctx->lay.seg_bytes[3];
+    const int64_t ch = ctx->chunk > 0 ? ctx->chunk : total;
+    int next_seg = 0;
+    for (int64_t off = 0; off < total; off += ch) {
+      const int64_t n = std::min(ch, total - off);
+      CK(cudaMemcpyAsync(dst + off, src + off, (size_t)n, cudaMemcpyHostToDevice, ctx->s_copy));
+      bytes += n;
+      while (next_seg < 4 && ctx->lay.seg_off[next_seg] + ctx->lay.seg_bytes[next_seg] <= off + n)
+        TRY(after_segment(next_seg++));
     }
   }
   ctx->h2d_bytes += bytes;
@@ -541,7 +563,8 @@ pipo_status pipeline_init(const pipo_config* cfg, pipo_ctx** out) {
     if (ctx->weight_tier == PIPO_TIER_HOST) {
       TRYI(host_alloc(ctx, &ctx->host_store, (int64_t)ctx->l * ctx->layer_bytes));
     } else {
-      TRYI(disk_open(ctx, c.disk_threads > 0 ? c.disk_threads : 4));
+      const pipo_status ds = disk_open(ctx, c.disk_threads > 0 ? c.disk_threads : 4);
+      if (ds != PIPO_OK) return fail(set_err(ds, "disk tier init failed (stream memory operations / pinned ring)"));
     }
   }
   // KV cache
@@ -645,8 +668,10 @@ pipo_status load_layer_weights(pipo_ctx* ctx, int32_t layer, const void* w) {
   if (ctx->weight_tier == PIPO_TIER_DEVICE)
     CK(cudaMemcpy(ctx->dev_store + (int64_t)layer * ctx->layer_bytes, dst, (size_t)ctx->layer_bytes,
                   cudaMemcpyHostToDevice));
-  else if (ctx->weight_tier == PIPO_TIER_DISK)
-    TRY(disk_write_layer(ctx, layer, dst));
+  else if (ctx->weight_tier == PIPO_TIER_DISK) {
+    const pipo_status ds = disk_write_layer(ctx, layer, dst);
+    if (ds != PIPO_OK) return set_err(ds, "writing the layer blob file failed");
+  }
   ctx->layer_loaded[layer] = 1;
   return PIPO_OK;
 }
@@ -726,6 +751,7 @@ pipo_status pipo_load_synthetic(pipo_ctx* ctx, int32_t layer, uint64_t seed) {
       CK(cudaMemcpyAsync(tmp.data(), blob, tmp.size(), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
       s = disk_write_layer(ctx, layer, tmp.data());
+      if (s != PIPO_OK) set_err(s, "writing the layer blob file failed");
     }
   }
   CK(cudaStreamSynchronize(st));

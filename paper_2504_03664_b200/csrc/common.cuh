@@ -47,27 +47,49 @@ __device__ __forceinline__ void mma_16816(float* c, const uint32_t* a, uint32_t 
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-// Two int4 codes (bits 0-3 -> low half, bits 16-19 -> high half of `t`) to the
-// exact fp16 pair (q_lo, q_hi): 0x6400|(c^8) is fp16 1024+(q+8); minus 1032 is q.
+__device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;   // (a & b) | c
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;\n" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+// One tiled-layout word (8 offset-binary codes, nibble order e0 e2 e4 e6 e1 e3 e5 e7,
+// layout.h) -> 4 half2 = fp16_rne(q * s) in natural order (e0,e1) (e2,e3) (e4,e5) (e6,e7).
+// 0x6400 | u is fp16 1024 + u; (1024 + u) - 1032 = q exactly; the high-nibble lanes hold
+// 1024 + 16u, and (1024 + 16u) * 1/16 - 72 = q exactly (one HFMA2).  Then one HMUL2 by
+// the group scale: the K8 unpack+scale arithmetic, bit for bit.
+__device__ __forceinline__ void dequant8(uint32_t w, __half2 s2, __half2* out) {
+  const uint32_t kMagic = 0x64006400u;
+  const __half2 k1032 = __half2half2(__ushort_as_half(0x6408));      // 1032
+  const __half2 k1_16 = __half2half2(__ushort_as_half(0x2C00));      // 1/16
+  const __half2 km72 = __half2half2(__ushort_as_half(0xD480));       // -72
+  const uint32_t w2 = w >> 8;
+  uint32_t t0 = lop3_and_or(w, 0x000F000Fu, kMagic);
+  uint32_t t1 = lop3_and_or(w, 0x00F000F0u, kMagic);
+  uint32_t t2 = lop3_and_or(w2, 0x000F000Fu, kMagic);
+  uint32_t t3 = lop3_and_or(w2, 0x00F000F0u, kMagic);
+  const __half2 q01 = __hsub2(*reinterpret_cast<__half2*>(&t0), k1032);
+  const __half2 q23 = __hfma2(*reinterpret_cast<__half2*>(&t1), k1_16, km72);
+  const __half2 q45 = __hsub2(*reinterpret_cast<__half2*>(&t2), k1032);
+  const __half2 q67 = __hfma2(*reinterpret_cast<__half2*>(&t3), k1_16, km72);
+  out[0] = __hmul2(q01, s2);
+  out[1] = __hmul2(q23, s2);
+  out[2] = __hmul2(q45, s2);
+  out[3] = __hmul2(q67, s2);
+}
+
+// signed code of element e (0..7, natural order) of a tiled-layout word
+__device__ __forceinline__ int code_at(uint32_t w, int e) {
+  const int pos = (e >> 1) + ((e & 1) << 2);            // e0->0 e1->4 e2->1 e3->5 ...
+  return (int)((w >> (4 * pos)) & 0xFu) - 8;
+}
+
+// Two canonical (two's complement) codes, bits 0-3 -> low half, bits 16-19 -> high
+// half, to the exact fp16 pair (q_lo, q_hi) (K8 unpack of the canonical format).
 __device__ __forceinline__ __half2 codes_to_half2(uint32_t t) {
   t = (t ^ 0x00080008u) | 0x64006400u;
   __half2 h = *reinterpret_cast<__half2*>(&t);
   return __hsub2(h, __half2half2(__ushort_as_half(0x6408)));  // 1032.0
-}
-
-// 8 codes in one 32-bit word (byte j = codes 2j, 2j+1) -> 4 half2 = fp16_rne(q*s)
-__device__ __forceinline__ void dequant8(uint32_t w, __half2 s2, __half2* out) {
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    uint32_t b = (w >> (8 * j)) & 0xFFu;
-    uint32_t t = (b & 0xFu) | ((b >> 4) << 16);
-    out[j] = __hmul2(codes_to_half2(t), s2);
-  }
-}
-
-// code i (0..7) of a 32-bit word as a signed int (arithmetic shift sign-extends)
-__device__ __forceinline__ int code_at(uint32_t w, int i) {
-  return static_cast<int>(w << (28 - 4 * i)) >> 28;
 }
 
 __device__ __forceinline__ float warp_sum(float v) {

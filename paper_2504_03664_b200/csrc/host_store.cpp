@@ -72,8 +72,8 @@ void parallel_for(int64_t n, const std::function<void(int64_t, int64_t)>& fn, in
   for (auto& t : th) t.join();
 }
 
-// one group: returns false on a domain error; writes 32 packed bytes + scale bits
-static inline bool quant_group(const float* g, uint8_t* packed, uint16_t* scale_bits) {
+// one group: returns false on a domain error; writes 64 signed codes + scale bits
+static inline bool quant_codes(const float* g, int* q, uint16_t* scale_bits) {
   float a = 0.f;
   bool ok = true;
   for (int i = 0; i < 64; ++i) {
@@ -84,19 +84,22 @@ static inline bool quant_group(const float* g, uint8_t* packed, uint16_t* scale_
   const uint16_t sb = f32_to_f16_rne(a7);
   const float s = f16_to_f32(sb);
   if (!std::isfinite(s)) ok = false;
-  for (int i = 0; i < 32; ++i) {
-    int q[2] = {0, 0};
+  for (int i = 0; i < 64; ++i) {
+    q[i] = 0;
     if (s != 0.f) {
-      for (int j = 0; j < 2; ++j) {
-        const volatile float r = g[2 * i + j] / s;    // IEEE fp32 division
-        float qf = std::nearbyintf(r);                // RNE (default rounding mode)
-        qf = std::min(7.f, std::max(-8.f, qf));
-        q[j] = (int)qf;
-      }
+      const volatile float r = g[i] / s;             // IEEE fp32 division
+      q[i] = (int)std::min(7.f, std::max(-8.f, std::nearbyintf(r)));   // RNE
     }
-    packed[i] = (uint8_t)((q[0] & 0xF) | ((q[1] & 0xF) << 4));
   }
   *scale_bits = sb;
+  return ok;
+}
+
+// one group in the canonical packing: 32 bytes (low nibble = even k, two's complement)
+static inline bool quant_group(const float* g, uint8_t* packed, uint16_t* scale_bits) {
+  int q[64];
+  const bool ok = quant_codes(g, q, scale_bits);
+  for (int i = 0; i < 32; ++i) packed[i] = (uint8_t)((q[2 * i] & 0xF) | ((q[2 * i + 1] & 0xF) << 4));
   return ok;
 }
 
@@ -120,7 +123,6 @@ bool quantize_tiled(const float* w, int64_t rows, int64_t cols, uint8_t* tiled) 
   std::atomic<bool> ok{true};
   parallel_for(m.n_rt, [&](int64_t t0, int64_t t1) {
     bool good = true;
-    uint8_t packed[32];
     const float zeros[64] = {0};
     for (int64_t rt = t0; rt < t1; ++rt)
       for (int64_t kb = 0; kb < m.n_kb; ++kb) {
@@ -128,9 +130,12 @@ bool quantize_tiled(const float* w, int64_t rows, int64_t cols, uint8_t* tiled) 
         for (int rr = 0; rr < 128; ++rr) {
           const int64_t r = rt * 128 + rr;
           uint16_t sb;
-          good &= quant_group(r < rows ? w + r * cols + kb * 64 : zeros, packed, &sb);
-          std::memcpy(blk + (0 * 128 + rr) * 16, packed, 16);
-          std::memcpy(blk + (1 * 128 + rr) * 16, packed + 16, 16);
+          int q[64];
+          good &= quant_codes(r < rows ? w + r * cols + kb * 64 : zeros, q, &sb);
+          uint32_t words[8];
+          for (int wi = 0; wi < 8; ++wi) words[wi] = pack_tiled_word(q + wi * 8);
+          std::memcpy(blk + (0 * 128 + rr) * 16, words, 16);
+          std::memcpy(blk + (1 * 128 + rr) * 16, words + 4, 16);
           std::memcpy(blk + 4096 + rr * 2, &sb, 2);
         }
       }

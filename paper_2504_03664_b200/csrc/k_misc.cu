@@ -170,25 +170,25 @@ __global__ void quantize_kernel(const float* w, int64_t rows, int64_t cols, uint
   const __half s16 = __float2half_rn(__fdiv_rn(a, 7.0f));
   const float s = __half2float(s16);
   if (!finite || isinf(s)) atomicExch(bad, 1);
-  uint32_t pw[8];
+  int q[64];
 #pragma unroll
-  for (int wi = 0; wi < 8; ++wi) {
-    uint32_t word = 0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      int q = 0;
-      if (s != 0.f) q = (int)fminf(fmaxf(rintf(__fdiv_rn(g[wi * 8 + j], s)), -8.f), 7.f);
-      word |= (uint32_t)(q & 0xF) << (4 * j);
-    }
-    pw[wi] = word;
-  }
+  for (int i = 0; i < 64; ++i)
+    q[i] = s != 0.f ? (int)fminf(fmaxf(rintf(__fdiv_rn(g[i], s)), -8.f), 7.f) : 0;
   if (codes && r < rows) {
     uint32_t* cdst = reinterpret_cast<uint32_t*>(codes + r * (cols / 2) + c * 32);
 #pragma unroll
-    for (int wi = 0; wi < 8; ++wi) cdst[wi] = pw[wi];
+    for (int wi = 0; wi < 8; ++wi) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) word |= (uint32_t)(q[wi * 8 + j] & 0xF) << (4 * j);
+      cdst[wi] = word;
+    }
     scales[r * ng + c] = __half_as_ushort(s16);
   }
   if (tiled) {
+    uint32_t pw[8];
+#pragma unroll
+    for (int wi = 0; wi < 8; ++wi) pw[wi] = pack_tiled_word(q + wi * 8);
     uint8_t* blk = tiled + ((r >> 7) * ng + c) * kInt4BlockBytes;
     const int rr = (int)(r & 127);
     *reinterpret_cast<uint4*>(blk + (0 * 128 + rr) * 16) = make_uint4(pw[0], pw[1], pw[2], pw[3]);

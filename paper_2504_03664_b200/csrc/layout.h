@@ -15,8 +15,13 @@
 // (one int4 quantization group wide), N padded to a multiple of 128 with zero rows:
 //   block (rt, kb) at ((rt * (K/64)) + kb) * block_bytes
 //   int4 block (4352 B): codes [h=0..1][r=0..127][16 B] then scales [r] fp16 (256 B)
-//        16-B chunk (h, r) = 32 codes of row r, k = kb*64 + h*32 + 0..31, byte j holds
-//        k = 2j (bits 0-3) and 2j+1 (bits 4-7), two's complement
+//        16-B chunk (h, r) = 32 codes of row r, k = kb*64 + h*32 + 0..31, as four
+//        32-bit words of 8 consecutive k each.  Inside a word the codes are stored
+//        OFFSET-BINARY (u = q + 8, 0..15) in nibble order e0 e2 e4 e6 e1 e3 e5 e7
+//        (nibble i holds element kNibbleElem[i]) so that one shift + four LOP3 yield
+//        the fp16 pairs (e0,e1) (e2,e3) (e4,e5) (e6,e7) (common.cuh dequant8).
+//        (The canonical packing of the hooks/oracle — two's complement, low nibble =
+//        even k — is a different, documented format.)
 //   fp16 block (16384 B): [r=0..127][64] row-major halves
 // so that one 128-row strip of the matrix is contiguous (rows land in order) and a
 // CTA reads each k-block of its strip as one contiguous 4.25 KiB / 16 KiB piece.
@@ -57,6 +62,17 @@ inline MatLayout mat_layout(int64_t N, int64_t K, int wfmt) {
 // element offset (in halves) of (r, k) inside an fp16 tiled matrix
 PIPO_HD inline int64_t fp16_tiled_index(int64_t r, int64_t k, int64_t n_kb) {
   return (((r >> 7) * n_kb + (k >> 6)) << 13) + ((r & 127) << 6) + (k & 63);
+}
+
+// word-internal code order of the tiled int4 block
+constexpr int kNibbleElem[8] = {0, 2, 4, 6, 1, 3, 5, 7};
+
+// pack 8 signed codes (natural k order) into one tiled-layout word
+PIPO_HD inline uint32_t pack_tiled_word(const int* q8) {
+  const int pos_of_elem[8] = {0, 4, 1, 5, 2, 6, 3, 7};
+  uint32_t w = 0;
+  for (int e = 0; e < 8; ++e) w |= (uint32_t)((q8[e] + 8) & 0xF) << (4 * pos_of_elem[e]);
+  return w;
 }
 
 enum Vec { V_LN1_G, V_LN1_B, V_B_QKV, V_B_OUT, V_LN2_G, V_LN2_B, V_B_FC1, V_B_FC2, V_COUNT };

@@ -199,3 +199,40 @@ def test_stats_busy_and_launches():
         assert 0 < st[k] <= 1.0 + 1e-6, (k, st[k])
     assert st["union_busy"] >= max(st["copy_busy"], st["kernel_busy"]) - 1e-9
     assert st["h2d_bytes"] > 0 and st["window_s"] > 0
+
+
+@pytest.mark.parametrize("env_kw", [{}, {"PIPO_DISK_DELAY_US": "300"}])
+def test_disk_tier_bit_identical(tmp_path, monkeypatch, env_kw):
+    """DISK tier (blob files -> reader pool -> pinned ring -> H2D): same
+    logits as the DEVICE tier, also with injected reader delays."""
+    pipo = pipo_mod()
+    for k, v in env_kw.items():
+        monkeypatch.setenv(k, v)
+    prompt = synth.prompts(3, 20, SMALL.vocab)
+    def syn(pl):
+        pl.load_synthetic(pipo.PIPO_LAYER_EMBED, 11)
+        for j in range(SMALL.n_layers):
+            pl.load_synthetic(j, 11)
+    ref, _ = _run(pipo, SMALL, dict(weight_tier=pipo.PIPO_TIER_DEVICE), syn, prompt, 5)
+    got, st = _run(pipo, SMALL, dict(weight_tier=pipo.PIPO_TIER_DISK, disk_dir=str(tmp_path), chunk_bytes=1 << 18,
+                                     disk_threads=3), syn, prompt, 5)
+    assert np.array_equal(got, ref)
+    assert len(list(tmp_path.glob("layer_*.pipo"))) == SMALL.n_layers
+
+
+def test_disk_tier_io_failure_surfaces(tmp_path, monkeypatch):
+    pipo = pipo_mod()
+    monkeypatch.setenv("PIPO_DISK_FAIL_AT", "5")
+    cfg = pipo.make_config(SMALL, max_batch=2, max_seq=16, weight_tier=pipo.PIPO_TIER_DISK, disk_dir=str(tmp_path),
+                           chunk_bytes=1 << 18)
+    with pipo.Pipeline(cfg) as pl:
+        pl.load_synthetic(pipo.PIPO_LAYER_EMBED, 1)
+        for j in range(SMALL.n_layers):
+            pl.load_synthetic(j, 1)
+        with pytest.raises(pipo.PipoError) as e:
+            pl.prefill(np.zeros((2, 4), np.int32))
+        assert e.value.status == pipo.PIPO_E_IO
+        with pytest.raises(pipo.PipoError) as e:       # poisoned afterwards
+            pl.prefill(np.zeros((2, 4), np.int32))
+        assert e.value.status == pipo.PIPO_E_STATE
+
