@@ -115,6 +115,37 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def disk_probe(directory: str, threads: int = 4, chunk: int = 32 << 20) -> float:
+    """Raw O_DIRECT read bandwidth (GB/s) of the layer blob files with `threads`
+    concurrent readers and `chunk`-byte requests — the disk tier's roofline (App. A /
+    Fig. 6 analogue)."""
+    import mmap
+    from concurrent.futures import ThreadPoolExecutor
+    files = sorted(os.path.join(directory, f) for f in os.listdir(directory) if f.endswith(".pipo"))
+    jobs = []
+    for f in files:
+        size = os.path.getsize(f)
+        jobs += [(f, off, min(chunk, size - off)) for off in range(0, size, chunk)]
+    bufs = [mmap.mmap(-1, chunk) for _ in range(threads)]
+    flag = getattr(os, "O_DIRECT", 0)
+
+    def work(t):
+        buf, total = bufs[t], 0
+        for f, off, n in jobs[t::threads]:
+            fd = os.open(f, os.O_RDONLY | flag)
+            try:
+                n4 = (n + 4095) // 4096 * 4096
+                total += os.preadv(fd, [memoryview(buf)[:n4]], off)
+            finally:
+                os.close(fd)
+        return total
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        total = sum(ex.map(work, range(threads)))
+    return total / (time.perf_counter() - t0) / 1e9
+
+
 def measured_peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -224,6 +255,10 @@ def run_pipo(args):
     for _ in range(args.warmup):
         nxt, _ = pl.decode_step(nxt)
 
+    kpre = pipo.pipo_kernel_stats(pl.ctx)
+    prefill_kernels = {n: {"ms": k["ms"], "tflops": k["flops"] / (k["ms"] / 1e3) / 1e12 if k["ms"] else 0.0,
+                           "gbs": k["bytes"] / (k["ms"] / 1e3) / 1e9 if k["ms"] else 0.0}
+                       for n, k in kpre.items() if n.endswith("prefill") and k["units"]}
     comp = torch.cuda.ExternalStream(pipo.pipo_stream(pl.ctx, 0), device=local)
     tok_dev = torch.from_numpy(nxt.astype(np.int32)).cuda(local)
 
@@ -321,11 +356,17 @@ def run_pipo(args):
                               "probe_gbs": link_probe, "achieved_gbs": layer_bytes / (ms / 1e3) / 1e9,
                               "frac": link_floor_s / (ms / 1e3), "copy_engine_gbs": st["h2d_gbs"]},
             "busy": {"union": st["union_busy"], "copy": st["copy_busy"], "kernel": st["kernel_busy"]},
+            "prefill_kernels": prefill_kernels,
             "setup": {"load_s": t_load, "prefill_s": t_prefill, "hbm_bytes": st["hbm_bytes"],
                       "pinned_host_bytes": st["pinned_host_bytes"]},
             "peaks": {"hbm_gbs": peaks.get("hbm_gbs"), "bf16_tflops": peaks.get("bf16_tflops")},
         }
     pl.close()
+    if rank == 0 and disk_dir:
+        dgbs = disk_probe(disk_dir, threads=4)
+        line["disk_roofline"] = {"bound": "disk (O_DIRECT, 4 readers, 32 MiB)", "probe_gbs": dgbs,
+                                 "achieved_gbs": layer_bytes / (ms / 1e3) / 1e9,
+                                 "frac": layer_bytes / (dgbs * 1e9) / (ms / 1e3)}
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         sample = OracleSample(args.config, args.wfmt)
         t = min(sample.step() for _ in range(2))

@@ -204,16 +204,31 @@ pipo_status pipo_unpack_int4_g64(pipo_ctx* ctx, const uint8_t* codes, const uint
  * y[M][N] = x[M][K] . W^T + bias (bias may be NULL).  x fp16 bits [M][K];
  * W given as fp32 masters [N][K] (quantized per wfmt inside); y fp32 [M][N].
  * path: 0 = automatic (as the pipeline chooses), 1 = int4 GEMV (CUDA cores),
- * 2 = mma.sync GEMM (legacy baseline), 3 = tcgen05/TMEM GEMM. */
+ * 2 = mma.sync GEMM (legacy baseline), 3 = tcgen05/TMEM GEMM (synchronous pipeline),
+ * 4 = warp-specialized stream-K tcgen05 GEMM (int4; the pipeline's M >= 16 path). */
 pipo_status pipo_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, const uint16_t* x,
                         const float* w, const float* bias, int32_t M, int32_t N, int32_t K,
                         float* y);
+
+/* Kernel micro-benchmark: one linear layer y[M][N] = x . W^T on device-resident
+ * synthetic data (weights drawn + quantized on the GPU), `iters` back-to-back
+ * launches on the compute stream, average microseconds per launch in *us. */
+pipo_status pipo_bench_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, int32_t M, int32_t N, int32_t K,
+                              int32_t iters, double* us);
 
 /* Decode attention kernel: q [b][d] fp16 bits (pre-scaled), k/v [L][b][d] fp16
  * bits (position-major) -> o [b][d] fp32.  n_heads | d. */
 pipo_status pipo_attention_decode(pipo_ctx* ctx, const uint16_t* q, const uint16_t* k,
                                   const uint16_t* v, int32_t b, int32_t L, int32_t d,
                                   int32_t n_heads, float* o);
+
+/* Prefill (causal) attention kernel: q [b][n][d] (pre-scaled) at positions
+ * past..past+n-1, k/v [past+n][b][d] position-major -> o [b][n][d] fp32.
+ * cuda_cores != 0 selects the CUDA-core reference kernel instead of the
+ * tensor-core (mma.sync) one. */
+pipo_status pipo_attention_prefill(pipo_ctx* ctx, const uint16_t* q, const uint16_t* k, const uint16_t* v,
+                                   int32_t b, int32_t n, int32_t past, int32_t d, int32_t n_heads, int32_t cuda_cores,
+                                   float* o);
 
 /* Capture per-layer hidden states of the next prefill/decode call:
  * on != 0 -> after that call, out receives [n_layers][b][n][d] fp32 (n = P for

@@ -974,7 +974,7 @@ pipo_status pipo_unpack_int4_g64(pipo_ctx* ctx, const uint8_t* codes, const uint
 pipo_status pipo_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, const uint16_t* x, const float* w,
                         const float* bias, int32_t M, int32_t N, int32_t K, float* y) {
   CHECK_CTX();
-  if (!x || !w || !y || M <= 0 || N <= 0 || K <= 0 || K % 64 || (wfmt != 0 && wfmt != 1) || path < 0 || path > 3)
+  if (!x || !w || !y || M <= 0 || N <= 0 || K <= 0 || K % 64 || (wfmt != 0 && wfmt != 1) || path < 0 || path > 4)
     return set_err(PIPO_E_INVALID_ARG, "bad linear arguments");
   CK(cudaSetDevice(ctx->cfg.device));
   const MatLayout ml = mat_layout(N, K, wfmt);
@@ -1012,6 +1012,46 @@ pipo_status pipo_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, const uint16_
   return PIPO_OK;
 }
 
+pipo_status pipo_bench_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, int32_t M, int32_t N, int32_t K,
+                              int32_t iters, double* us) {
+  CHECK_CTX();
+  if (!us || M <= 0 || N <= 0 || K <= 0 || K % 64 || iters <= 0 || (wfmt != 0 && wfmt != 1) || path < 0 || path > 4)
+    return set_err(PIPO_E_INVALID_ARG, "bad bench arguments");
+  CK(cudaSetDevice(ctx->cfg.device));
+  const MatLayout ml = mat_layout(N, K, wfmt);
+  uint8_t* dw = nullptr; __half* dx = nullptr; float* dy = nullptr; float* tmp = nullptr;
+  TRY(dev_alloc(ctx, &dw, ml.bytes));
+  TRY(dev_alloc(ctx, &dx, (int64_t)M * K * 2));
+  TRY(dev_alloc(ctx, &dy, (int64_t)M * N * 4));
+  TRY(dev_alloc(ctx, &tmp, std::max<int64_t>((int64_t)N * K, (int64_t)M * K) * 4));
+  cudaStream_t st = ctx->s_comp;
+  LAUNCH(launch_synth(tmp, 0, (int64_t)N * K, synth_key(7, 1, 2), 0, synth_scale(0, 0.02), st));
+  if (wfmt == 1) LAUNCH(launch_quantize(tmp, N, K, nullptr, nullptr, dw, ctx->quant_bad, st));
+  else LAUNCH(launch_tile_fp16(tmp, N, K, dw, st));
+  LAUNCH(launch_synth(tmp, 0, (int64_t)M * K, synth_key(7, 1, 3), 0, synth_scale(0, 1.0), st));
+  LAUNCH(launch_f32_to_f16(tmp, dx, (int64_t)M * K, st));
+  LinearArgs la;
+  la.x = dx; la.w = dw; la.wfmt = wfmt; la.M = M; la.N = N; la.K = K;
+  la.ws = ctx->ws; la.ws_floats = ctx->ws_floats; la.counters = ctx->counters; la.n_counters = ctx->n_counters;
+  la.num_sms = ctx->num_sms;
+  la.epi.kind = EPI_F32; la.epi.M = M; la.epi.N = N; la.epi.y = dy; la.epi.ldy = N;
+  LAUNCH(launch_linear(la, path, ctx->gemv_max_m, st));   // warm-up
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, st));
+  for (int i = 0; i < iters; ++i) LAUNCH(launch_linear(la, path, ctx->gemv_max_m, st));
+  CK(cudaEventRecord(e1, st));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0); cudaEventDestroy(e1);
+  cudaFree(dw); cudaFree(dx); cudaFree(dy); cudaFree(tmp);
+  ctx->hbm_bytes -= ml.bytes + (int64_t)M * K * 2 + (int64_t)M * N * 4 + std::max<int64_t>((int64_t)N * K, (int64_t)M * K) * 4;
+  *us = ms * 1e3 / iters;
+  return PIPO_OK;
+}
+
 pipo_status pipo_attention_decode(pipo_ctx* ctx, const uint16_t* q, const uint16_t* k, const uint16_t* v, int32_t b,
                                   int32_t L, int32_t d, int32_t n_heads, float* o) {
   CHECK_CTX();
@@ -1034,6 +1074,38 @@ pipo_status pipo_attention_decode(pipo_ctx* ctx, const uint16_t* q, const uint16
   aa.q = dq; aa.kc = dk; aa.vc = dv; aa.o = dout; aa.b = b; aa.n = 1; aa.past = L - 1; aa.d = d;
   aa.n_heads = n_heads; aa.kv_b = b; aa.ws = ctx->ws; aa.ws_floats = ctx->ws_floats; aa.num_sms = ctx->num_sms;
   LAUNCH(launch_attention_decode(aa, st));
+  LAUNCH(launch_f16_to_f32(dout, df, nq, st));
+  CK(cudaMemcpyAsync(o, df, (size_t)nq * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  cudaFree(dq); cudaFree(dk); cudaFree(dv); cudaFree(dout); cudaFree(df);
+  ctx->hbm_bytes -= nq * 2 * 2 + nkv * 2 * 2 + nq * 4;
+  return PIPO_OK;
+}
+
+pipo_status pipo_attention_prefill(pipo_ctx* ctx, const uint16_t* q, const uint16_t* k, const uint16_t* v,
+                                   int32_t b, int32_t n, int32_t past, int32_t d, int32_t n_heads, int32_t cuda_cores,
+                                   float* o) {
+  CHECK_CTX();
+  if (!q || !k || !v || !o || b <= 0 || n <= 0 || past < 0 || d <= 0 || n_heads <= 0 || d % n_heads)
+    return set_err(PIPO_E_INVALID_ARG, "bad attention arguments");
+  CK(cudaSetDevice(ctx->cfg.device));
+  __half *dq = nullptr, *dk = nullptr, *dv = nullptr, *dout = nullptr;
+  float* df = nullptr;
+  const int64_t L = past + n, nq = (int64_t)b * n * d, nkv = L * b * d;
+  TRY(dev_alloc(ctx, &dq, nq * 2));
+  TRY(dev_alloc(ctx, &dk, nkv * 2));
+  TRY(dev_alloc(ctx, &dv, nkv * 2));
+  TRY(dev_alloc(ctx, &dout, nq * 2));
+  TRY(dev_alloc(ctx, &df, nq * 4));
+  cudaStream_t st = ctx->s_comp;
+  CK(cudaMemcpyAsync(dq, q, (size_t)nq * 2, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dk, k, (size_t)nkv * 2, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dv, v, (size_t)nkv * 2, cudaMemcpyHostToDevice, st));
+  AttnArgs aa;
+  aa.q = dq; aa.kc = dk; aa.vc = dv; aa.o = dout; aa.b = b; aa.n = n; aa.past = past; aa.d = d;
+  aa.n_heads = n_heads; aa.kv_b = b; aa.ws = ctx->ws; aa.ws_floats = ctx->ws_floats; aa.num_sms = ctx->num_sms;
+  aa.use_cuda_cores = cuda_cores;
+  LAUNCH(launch_attention_prefill(aa, st));
   LAUNCH(launch_f16_to_f32(dout, df, nq, st));
   CK(cudaMemcpyAsync(o, df, (size_t)nq * 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));

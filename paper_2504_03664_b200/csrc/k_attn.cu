@@ -201,6 +201,170 @@ __global__ void __launch_bounds__(256) attn_prefill_kernel(AttnArgs a) {
   }
 }
 
+
+// Prefill (causal) on tensor cores, flash-attention-2 style (mma.sync m16n8k16,
+// fp16 in / fp32 accumulate): CTA = (head, sequence, 64 query rows), 4 warps x 16
+// rows; K/V tiles of 64 positions double-buffered with cp.async; online softmax on
+// the S fragments in fp32 (exp2 with log2e folded in); P re-packed to fp16 A
+// fragments for P.V; V fragments via ldmatrix.trans from the position-major cache.
+template <int HD>
+__global__ void __launch_bounds__(128) attn_prefill_mma_kernel(AttnArgs a) {
+  constexpr int KP = HD + 8;                 // padded smem row (halves): conflict-free ldmatrix
+  constexpr int NT_O = HD / 8;               // n8 tiles of the output
+  extern __shared__ __align__(16) uint8_t smem_attn[];
+  __half* sQ = reinterpret_cast<__half*>(smem_attn);          // [64][KP]
+  __half* sK = sQ + 64 * KP;                                   // [2][64][KP]
+  __half* sV = sK + 2 * 64 * KP;                               // [2][64][KP]
+  const int head = blockIdx.x, bi = blockIdx.y, qt = blockIdx.z;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int q0 = qt * 64;
+  const int L = a.past + a.n;
+  const int kv_end = min(L, a.past + min(a.n, q0 + 64));     // exclusive, causal bound of this CTA
+  const int n_kv = (kv_end + 63) / 64;
+  const int64_t pstride = (int64_t)a.kv_b * a.d;
+  constexpr int CH = HD / 8;                 // 16-B chunks per row
+
+  for (int c = tid; c < 64 * CH; c += 128) {
+    const int r = c / CH, ch = c % CH, t = q0 + r;
+    const __half* src = a.q + ((int64_t)bi * a.n + min(t, a.n - 1)) * a.d + head * HD + ch * 8;
+    cp_async16(sQ + r * KP + ch * 8, src, t < a.n ? 16 : 0);
+  }
+  auto load_kv = [&](int j, int buf) {
+    for (int c = tid; c < 64 * CH; c += 128) {
+      const int r = c / CH, ch = c % CH, p = j * 64 + r;
+      const int64_t off = (int64_t)min(p, L - 1) * pstride + (int64_t)bi * a.d + head * HD + ch * 8;
+      const int bytes = p < L ? 16 : 0;
+      cp_async16(sK + (buf * 64 + r) * KP + ch * 8, a.kc + off, bytes);
+      cp_async16(sV + (buf * 64 + r) * KP + ch * 8, a.vc + off, bytes);
+    }
+  };
+  load_kv(0, 0);
+  cp_async_commit();
+
+  float o[NT_O][4];
+#pragma unroll
+  for (int i = 0; i < NT_O; ++i)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) o[i][c] = 0.f;
+  float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f};
+  uint32_t qf[HD / 16][4];
+  const int row0 = q0 + warp * 16 + g;          // query rows of this thread: row0, row0 + 8
+
+  for (int j = 0; j < n_kv; ++j) {
+    const int buf = j & 1;
+    if (j + 1 < n_kv) load_kv(j + 1, buf ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    if (j == 0) {
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk)
+        ldmatrix_x4(qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3],
+                    sQ + (warp * 16 + (lane & 15)) * KP + kk * 16 + (lane >> 4) * 8);
+    }
+    // S = Q K^T for 64 positions
+    float sc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) sc[i][c] = 0.f;
+    const __half* kb = sK + buf * 64 * KP;
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk) {
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        uint32_t b0, b1, b2, b3;
+        ldmatrix_x4(b0, b1, b2, b3,
+                    kb + (jj * 16 + (lane & 7) + ((lane >> 4) << 3)) * KP + kk * 16 + ((lane >> 3) & 1) * 8);
+        mma_16816(sc[2 * jj], qf[kk], b0, b1);
+        mma_16816(sc[2 * jj + 1], qf[kk], b2, b3);
+      }
+    }
+    // mask + online softmax (log2 domain)
+    float mx[2] = {m_r[0], m_r[1]};
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int p = j * 64 + i * 8 + 2 * tq + (c & 1);
+        const int t = row0 + (c >> 1) * 8;
+        const bool ok = p < L && p <= a.past + t;
+        sc[i][c] = ok ? sc[i][c] * kLog2e : -INFINITY;
+        mx[c >> 1] = fmaxf(mx[c >> 1], sc[i][c]);
+      }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 1));
+      mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 2));
+    }
+    float corr[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      corr[h] = mx[h] == -INFINITY ? 1.f : exp2f(m_r[h] - mx[h]);
+      m_r[h] = mx[h];
+      l_r[h] *= corr[h];
+    }
+#pragma unroll
+    for (int i = 0; i < NT_O; ++i) {
+      o[i][0] *= corr[0]; o[i][1] *= corr[0];
+      o[i][2] *= corr[1]; o[i][3] *= corr[1];
+    }
+    uint32_t pf[4][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float e[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float mm = m_r[c >> 1];
+        e[c] = mm == -INFINITY ? 0.f : exp2f(sc[i][c] - mm);
+        l_r[c >> 1] += e[c];
+      }
+      const __half2 lo = __floats2half2_rn(e[0], e[1]), hi = __floats2half2_rn(e[2], e[3]);
+      const int kk2 = i >> 1;
+      if ((i & 1) == 0) {
+        pf[kk2][0] = *reinterpret_cast<const uint32_t*>(&lo);
+        pf[kk2][1] = *reinterpret_cast<const uint32_t*>(&hi);
+      } else {
+        pf[kk2][2] = *reinterpret_cast<const uint32_t*>(&lo);
+        pf[kk2][3] = *reinterpret_cast<const uint32_t*>(&hi);
+      }
+    }
+    // O += P V
+    const __half* vb = sV + buf * 64 * KP;
+#pragma unroll
+    for (int kk2 = 0; kk2 < 4; ++kk2) {
+#pragma unroll
+      for (int nt2 = 0; nt2 < HD / 16; ++nt2) {
+        uint32_t b0, b1, b2, b3;
+        const __half* ptr = vb + (kk2 * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * KP + nt2 * 16 + (lane >> 4) * 8;
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                     : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
+                     : "r"(smem_u32(ptr)));
+        mma_16816(o[2 * nt2], pf[kk2], b0, b1);
+        mma_16816(o[2 * nt2 + 1], pf[kk2], b2, b3);
+      }
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    l_r[h] += __shfl_xor_sync(0xffffffffu, l_r[h], 1);
+    l_r[h] += __shfl_xor_sync(0xffffffffu, l_r[h], 2);
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int t = row0 + h * 8;
+    if (t >= a.n) continue;
+    const float inv = 1.f / l_r[h];
+    __half* op = a.o + ((int64_t)bi * a.n + t) * a.d + head * HD;
+#pragma unroll
+    for (int i = 0; i < NT_O; ++i)
+      *reinterpret_cast<__half2*>(op + i * 8 + 2 * tq) = __floats2half2_rn(o[i][2 * h] * inv, o[i][2 * h + 1] * inv);
+  }
+}
+
 int launch_attention_decode(const AttnArgs& a, cudaStream_t st) {
   const int hd = a.d / a.n_heads;
   if (hd != 64 && hd != 128) return -1;
@@ -225,9 +389,24 @@ int launch_attention_decode(const AttnArgs& a, cudaStream_t st) {
 int launch_attention_prefill(const AttnArgs& a, cudaStream_t st) {
   const int hd = a.d / a.n_heads;
   if (hd != 64 && hd != 128) return -1;
-  dim3 grid(a.n_heads, a.b, (a.n + 31) / 32);
-  if (hd == 64) attn_prefill_kernel<64><<<grid, 256, 0, st>>>(a);
-  else attn_prefill_kernel<128><<<grid, 256, 0, st>>>(a);
+  if (a.use_cuda_cores) {   // the v1 CUDA-core kernel, kept as a cross-check
+    dim3 grid(a.n_heads, a.b, (a.n + 31) / 32);
+    if (hd == 64) attn_prefill_kernel<64><<<grid, 256, 0, st>>>(a);
+    else attn_prefill_kernel<128><<<grid, 256, 0, st>>>(a);
+    return 1;
+  }
+  dim3 grid(a.n_heads, a.b, (a.n + 63) / 64);
+  if (hd == 64) {
+    const int smem = 5 * 64 * (64 + 8) * 2;
+    static bool set64 = false;
+    if (!set64) { cudaFuncSetAttribute(attn_prefill_mma_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); set64 = true; }
+    attn_prefill_mma_kernel<64><<<grid, 128, smem, st>>>(a);
+  } else {
+    const int smem = 5 * 64 * (128 + 8) * 2;
+    static bool set128 = false;
+    if (!set128) { cudaFuncSetAttribute(attn_prefill_mma_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); set128 = true; }
+    attn_prefill_mma_kernel<128><<<grid, 128, smem, st>>>(a);
+  }
   return 1;
 }
 

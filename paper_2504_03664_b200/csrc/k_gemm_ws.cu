@@ -1,0 +1,421 @@
+// k_gemm_ws.cu — warp-specialized, persistent stream-K int4-g64 GEMM on tcgen05 for
+// the decode linears (M = b <= 256) and prefill.  This is the kernel that consumes each
+// streamed weight segment as it lands (a6/a8/a10/a11 of SURVEY.md §8(a)).
+//
+// Grid = min(#SMs, units) CTAs; the (weight-row-tile, m-tile, k-block) units are split
+// into equal contiguous ranges (stream-K), so every SM reads the same number of
+// weight bytes — no wave quantization, no per-CTA split-K tail.  A range spans 1..3
+// output tiles; a tile covered by several CTAs is finished by the last CTA to arrive,
+// which sums the partials in k order (deterministic) and runs the fused epilogue.
+//
+// Roles (320 threads):
+//   warp 0      producer: cp.async.bulk of each raw int4 block (4352 B, contiguous in
+//               the blob) and a TMA 2D load of the x tile (SWIZZLE_128B, zero-filled
+//               out of bounds) into NR / NX -stage rings, mbarrier complete_tx;
+//   warp 1      MMA issuer: 4 x tcgen05.mma (128 x BN x 16) per k-block into one of
+//               two TMEM accumulators, tcgen05.commit releases the stages;
+//   warps 2-5   unpack + scale: thread r turns row r's 64 codes into fp16_rne(q*s)
+//               (kernel K8 arithmetic, 1 SHR + 4 LOP3 + 8 HALF2 ops per 8 codes)
+//               written to the swizzled A tile; the dequantized weight never exists
+//               in HBM;
+//   warps 6-9   epilogue: tcgen05.ld the finished accumulator (lanes = weight rows),
+//               bias / residual / ReLU / QKV-scatter, or stream-K partials + fixup.
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "epilogue.cuh"
+#include "kernels.h"
+#include "layout.h"
+
+namespace pipo {
+namespace ws {
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
+
+// stream-K partition of U units over G CTAs
+__device__ __forceinline__ int64_t u_begin(int64_t c, int64_t U, int64_t G) { return c * U / G; }
+__device__ __forceinline__ int cta_of_unit(int64_t u, int64_t U, int64_t G) {
+  int64_t c = u * G / U;
+  while (c + 1 < G && u_begin(c + 1, U, G) <= u) ++c;
+  while (c > 0 && u_begin(c, U, G) > u) --c;
+  return (int)c;
+}
+
+}  // namespace ws
+
+constexpr int WS_THREADS = 448;   // producer, MMA, 8 unpack warps, 4 epilogue warps
+
+// One stream-K unit = TWO 128-row weight tiles (256 output features) x one 64-wide
+// k-block: 8.5 KiB of int4 weights per x tile (halves the x re-reads from L2 and the
+// per-unit synchronisation cost).
+template <int BN>
+struct WsCfg {
+  static constexpr int NS = BN <= 32 ? 8 : (BN <= 64 ? 6 : 4); // raw + x ring stages
+  static constexpr int NA = 3;                                 // fp16 A stages (2 tiles each)
+  static constexpr int RAW = 2 * (int)kInt4BlockBytes;        // 8704
+  static constexpr int X_TILE = BN * 128;
+  static constexpr int A_TILE = 2 * 128 * 128;                 // two 128 x 64 fp16 tiles
+  static constexpr int TMEM_COLS = 4 * BN < 32 ? 32 : 4 * BN;  // 2 accumulators x 2 tiles
+  static constexpr int SMEM = 1024 + NS * X_TILE + NA * A_TILE + NS * RAW + 512;
+  static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
+  static_assert(TMEM_COLS <= 512, "TMEM budget");
+};
+
+template <int BN>
+__global__ void __launch_bounds__(WS_THREADS, 1)
+    gemm_ws_kernel(const __grid_constant__ CUtensorMap xmap, LinearArgs a, int n_rt, int m_tiles, int dbg) {
+  using C = WsCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  uint8_t* base = smem_raw + (base_u32 - smem_u32(smem_raw));
+  uint8_t* xs = base;
+  uint8_t* as = xs + C::NS * C::X_TILE;
+  uint8_t* raw = as + C::NA * C::A_TILE;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(raw + C::NS * C::RAW);
+  uint64_t* raw_full = bar;
+  uint64_t* raw_empty = raw_full + C::NS;
+  uint64_t* x_full = raw_empty + C::NS;
+  uint64_t* x_empty = x_full + C::NS;
+  uint64_t* a_full = x_empty + C::NS;
+  uint64_t* a_empty = a_full + C::NA;
+  uint64_t* acc_full = a_empty + C::NA;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  int* s_flag = reinterpret_cast<int*>(tmem_slot + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n_kb = a.K / 64;
+  const int n_pairs = (n_rt + 1) >> 1;
+  const int64_t U = (int64_t)n_pairs * m_tiles * n_kb, G = gridDim.x;
+  const int64_t u0 = ws::u_begin(blockIdx.x, U, G), u1 = ws::u_begin(blockIdx.x + 1, U, G);
+
+  if (tid == 0) {
+    for (int i = 0; i < C::NS; ++i) {
+      ws::mbar_init(&raw_full[i], 1);
+      ws::mbar_init(&raw_empty[i], 8);
+      ws::mbar_init(&x_full[i], 1);
+      ws::mbar_init(&x_empty[i], 1);
+    }
+    for (int i = 0; i < C::NA; ++i) { ws::mbar_init(&a_full[i], 8); ws::mbar_init(&a_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { ws::mbar_init(&acc_full[i], 1); ws::mbar_init(&acc_empty[i], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&xmap) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"((uint32_t)C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  ws::tc_before();
+  __syncthreads();
+  ws::tc_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------ producer ------------------------------
+    if (lane == 0) {
+      int i = 0;
+      for (int64_t u = u0; u < u1; ++u, ++i) {
+        const int64_t tile = u / n_kb;
+        const int kb = (int)(u - tile * n_kb);
+        const int pr = (int)(tile % n_pairs), mt = (int)(tile / n_pairs);
+        const int s = i % C::NS;
+        const uint32_t ph = ((i / C::NS) & 1) ^ 1;
+        const int rt0 = 2 * pr;
+        const bool two = rt0 + 1 < n_rt;
+        ws::mbar_wait(&raw_empty[s], ph);
+        ws::mbar_expect_tx(&raw_full[s], two ? C::RAW : C::RAW / 2);
+        ws::bulk_g2s(raw + s * C::RAW, a.w + ((int64_t)rt0 * n_kb + kb) * kInt4BlockBytes, kInt4BlockBytes,
+                     &raw_full[s]);
+        if (two)
+          ws::bulk_g2s(raw + s * C::RAW + kInt4BlockBytes, a.w + ((int64_t)(rt0 + 1) * n_kb + kb) * kInt4BlockBytes,
+                       kInt4BlockBytes, &raw_full[s]);
+        ws::mbar_wait(&x_empty[s], ph);
+        if (dbg & 4) {
+          ws::mbar_arrive(&x_full[s]);
+        } else {
+          ws::mbar_expect_tx(&x_full[s], C::X_TILE);
+          ws::tma_2d(xs + s * C::X_TILE, &xmap, kb * 64, mt * BN, &x_full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------ MMA issuer ------------------------------
+    if (lane == 0) {
+      int i = 0, seg = 0;
+      int64_t u = u0;
+      while (u < u1) {
+        const int64_t tile = u / n_kb;
+        const int64_t seg_end = min(u1, (tile + 1) * n_kb);
+        const bool two = 2 * (int)(tile % n_pairs) + 1 < n_rt;
+        const int ab = seg & 1;
+        ws::mbar_wait(&acc_empty[ab], ((seg >> 1) & 1) ^ 1);
+        ws::tc_after();
+        const uint32_t d = tmem + ab * (2 * BN);
+        for (int64_t v = u; v < seg_end; ++v, ++i) {
+          const int sa = i % C::NA, s = i % C::NS;
+          ws::mbar_wait(&a_full[sa], (i / C::NA) & 1);
+          ws::mbar_wait(&x_full[s], (i / C::NS) & 1);
+          ws::tc_after();
+          const uint32_t aa = smem_u32(as + sa * C::A_TILE), xa = smem_u32(xs + s * C::X_TILE);
+#pragma unroll
+          if (!(dbg & 2))
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint32_t acc = (v > u || kk > 0) ? 1u : 0u;
+            const uint64_t db = ws::sw128_desc(xa + kk * 32);
+            ws::mma_f16(d, ws::sw128_desc(aa + kk * 32), db, C::IDESC, acc);
+            if (two) ws::mma_f16(d + BN, ws::sw128_desc(aa + 128 * 128 + kk * 32), db, C::IDESC, acc);
+          }
+          ws::mma_commit(&a_empty[sa]);
+          ws::mma_commit(&x_empty[s]);
+        }
+        ws::mma_commit(&acc_full[ab]);
+        u = seg_end;
+        ++seg;
+      }
+    }
+  } else if (warp < 10) {
+    // ------------------------------ unpack + scale ------------------------------
+    // 8 warps, 2 per SM sub-partition: thread d owns row r of tile t (d = t*128 + r)
+    const int d = tid - 64, t = d >> 7, r = d & 127;
+    const int sw = r & 7;
+    int i = 0;
+    for (int64_t u = u0; u < u1; ++u, ++i) {
+      const int s = i % C::NS, sa = i % C::NA;
+      ws::mbar_wait(&raw_full[s], (i / C::NS) & 1);
+      const uint8_t* rs = raw + s * C::RAW + t * kInt4BlockBytes;
+      const uint4 c0 = *reinterpret_cast<const uint4*>(rs + r * 16);
+      const uint4 c1 = *reinterpret_cast<const uint4*>(rs + (128 + r) * 16);
+      const __half2 s2 = __half2half2(*reinterpret_cast<const __half*>(rs + 4096 + r * 2));
+      __syncwarp();
+      if (lane == 0) ws::mbar_arrive(&raw_empty[s]);
+      ws::mbar_wait(&a_empty[sa], ((i / C::NA) & 1) ^ 1);
+      uint8_t* at = as + sa * C::A_TILE + t * (128 * 128) + r * 128;
+      const uint32_t w[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+      if (!(dbg & 1))
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {
+        __half2 o[4];
+        dequant8(w[ch], s2, o);
+        *reinterpret_cast<uint4*>(at + ((ch ^ sw) << 4)) = *reinterpret_cast<const uint4*>(o);
+      }
+      ws::fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) ws::mbar_arrive(&a_full[sa]);
+    }
+  } else {
+    // ------------------------------ epilogue ------------------------------
+    const int quarter = warp & 3;                      // TMEM lanes 32*quarter .. +31
+    const int row = quarter * 32 + lane;
+    const int et = tid - 320;
+    int seg = 0;
+    int64_t u = u0;
+    const int64_t first_tile_mine = u0 / n_kb;
+    while (u < u1) {
+      const int64_t tile = u / n_kb;
+      const int64_t seg_end = min(u1, (tile + 1) * n_kb);
+      const bool full = (u == tile * n_kb) && (seg_end == (tile + 1) * n_kb);
+      const int pr = (int)(tile % n_pairs), mt = (int)(tile / n_pairs);
+      const int m0 = mt * BN;
+      const int ntile = (2 * pr + 1 < n_rt) ? 2 : 1;
+      const int ab = seg & 1;
+      // long wait: sleep between polls so the waiting warps do not steal issue slots
+      {
+        uint32_t done = 0;
+        const uint32_t addr = smem_u32(&acc_full[ab]), par = (seg >> 1) & 1;
+        while (true) {
+          asm volatile(
+              "{\n.reg .pred P1;\nmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
+              : "=r"(done)
+              : "r"(addr), "r"(par)
+              : "memory");
+          if (done) break;
+          __nanosleep(256);
+        }
+      }
+      ws::tc_after();
+      const int slot = 2 * (int)blockIdx.x + (tile == first_tile_mine ? 0 : 1);
+      float* part = a.ws + (int64_t)slot * (2 * BN * 128);
+      for (int t = 0; t < ntile; ++t) {
+        const uint32_t t_row = tmem + ab * (2 * BN) + t * BN + ((uint32_t)(quarter * 32) << 16);
+        const int n = (2 * pr + t) * 128 + row;
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          float v[16];
+          ws::tmem_ld16(t_row + c0, v);
+          if (full) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) epi_store(a.epi, m0 + c0 + j, n, v[j]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) __stcg(part + (t * BN + c0 + j) * 128 + row, v[j]);
+          }
+        }
+      }
+      ws::tc_before();
+      __syncwarp();
+      if (lane == 0) ws::mbar_arrive(&acc_empty[ab]);
+      if (!full) {
+        // stream-K fixup: the last CTA covering this tile sums partials in k order
+        const int cf = ws::cta_of_unit(tile * n_kb, U, G), cl = ws::cta_of_unit((tile + 1) * n_kb - 1, U, G);
+        __threadfence();
+        ws::named_bar(1, 128);
+        if (et == 0) *s_flag = (atomicAdd(&a.counters[tile], 1) == cl - cf);
+        ws::named_bar(1, 128);
+        if (*s_flag) {
+          __threadfence();
+          for (int t = 0; t < ntile; ++t) {
+            const int n = (2 * pr + t) * 128 + row;
+            for (int c0 = 0; c0 < BN; c0 += 16) {
+              float acc[16];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+              for (int cc = cf; cc <= cl; ++cc) {          // k order: deterministic
+                const int64_t ft = ws::u_begin(cc, U, G) / n_kb;
+                const float* src = a.ws + (int64_t)(2 * cc + (ft == tile ? 0 : 1)) * (2 * BN * 128) +
+                                   (t * BN + c0) * 128 + row;
+                float v[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[j] = __ldcg(src + j * 128);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) acc[j] += v[j];
+              }
+#pragma unroll
+              for (int j = 0; j < 16; ++j) epi_store(a.epi, m0 + c0 + j, n, acc[j]);
+            }
+          }
+          if (et == 0) a.counters[tile] = 0;
+        }
+        ws::named_bar(1, 128);
+      }
+      u = seg_end;
+      ++seg;
+    }
+  }
+  ws::tc_before();
+  __syncthreads();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"((uint32_t)C::TMEM_COLS));
+}
+
+// ---------------------------------------------------------------------------------
+// host side: TMA descriptor for the activation matrix x [rows][K] fp16 (row-major)
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess) fn = (PFN_encodeTiled)p;
+    cudaGetLastError();
+  }
+  return fn;
+}
+
+static bool make_xmap(CUtensorMap* map, const __half* x, int64_t rows, int64_t K, int box_rows) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+  const cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(x), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN>
+static int run_ws(const LinearArgs& a, cudaStream_t st) {
+  using C = WsCfg<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(gemm_ws_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    attr_set = true;
+  }
+  const int n_rt = (a.N + 127) / 128, m_tiles = (a.M + BN - 1) / BN, n_kb = a.K / 64;
+  const int n_pairs = (n_rt + 1) / 2;
+  const int64_t U = (int64_t)n_pairs * m_tiles * n_kb;
+  // at least 8 units per CTA: the per-CTA prologue / epilogue must stay amortized
+  const int G = (int)std::max<int64_t>(1, std::min<int64_t>(a.num_sms, U / 8));
+  const int64_t tiles = (int64_t)n_pairs * m_tiles;
+  if ((int64_t)2 * G * 2 * BN * 128 > a.ws_floats || tiles > a.n_counters) return -1;
+  CUtensorMap map;   // rows >= M are out of bounds: TMA zero-fills them
+  if (!make_xmap(&map, a.x, a.M, a.K, BN)) return -1;
+  static const int dbg = getenv("PIPO_WS_DEBUG") ? atoi(getenv("PIPO_WS_DEBUG")) : 0;
+  gemm_ws_kernel<BN><<<G, WS_THREADS, C::SMEM, st>>>(map, a, n_rt, m_tiles, dbg);
+  return 1;
+}
+
+int launch_linear_ws(const LinearArgs& a, cudaStream_t st) {
+  if (a.wfmt != 1) return -1;
+  if (a.M <= 16) return run_ws<16>(a, st);
+  if (a.M <= 32) return run_ws<32>(a, st);
+  if (a.M <= 64) return run_ws<64>(a, st);
+  if (a.M <= 128) return run_ws<128>(a, st);
+  return -1;   // M > 128: the prefill shapes use the tcgen05 tile kernel (k_gemm_tc.cu)
+}
+
+}  // namespace pipo

@@ -43,7 +43,10 @@ struct LinearArgs {
   int num_sms = 148;
 };
 
-enum LinearPath { PATH_AUTO = 0, PATH_GEMV = 1, PATH_GEMM = 2, PATH_TC = 3 };
+enum LinearPath { PATH_AUTO = 0, PATH_GEMV = 1, PATH_GEMM = 2, PATH_TC = 3, PATH_WS = 4 };
+
+// warp-specialized stream-K tcgen05 GEMM, int4 weights (k_gemm_ws.cu)
+int launch_linear_ws(const LinearArgs& a, cudaStream_t st);
 
 // tcgen05 / TMEM fused dequant GEMM (k_gemm_tc.cu)
 int launch_linear_tc(const LinearArgs& a, cudaStream_t st);
@@ -58,6 +61,7 @@ struct AttnArgs {
   const __half* vc = nullptr;
   __half* o = nullptr;        // same shape as q
   int b = 0, n = 1, past = 0, d = 0, n_heads = 0, kv_b = 0;
+  int use_cuda_cores = 0;     // prefill: 1 = the CUDA-core reference kernel
   float* ws = nullptr;
   int64_t ws_floats = 0;
   int num_sms = 148;

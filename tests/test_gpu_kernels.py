@@ -72,7 +72,8 @@ def test_linear_vs_oracle(env, M, N, K, wfmt):
     w = (rng.standard_normal((N, K)) * 0.02).astype(np.float16).astype(np.float32)
     bias = (rng.uniform(-0.02, 0.02, N)).astype(np.float32)
     ref = _ref_linear(x, w, bias, wfmt)
-    paths = [pipo.PATH_TC, pipo.PATH_GEMM] + ([pipo.PATH_GEMV] if wfmt == 1 and M <= 16 else [])
+    paths = [pipo.PATH_TC, pipo.PATH_GEMM] + ([pipo.PATH_GEMV] if wfmt == 1 and M <= 16 else []) + \
+        ([pipo.PATH_WS] if wfmt == 1 and M <= 128 else [])
     for path in paths:
         y = pipo.pipo_linear(pl.ctx, wfmt, path, x, w, bias)
         err = rel_inf(y, ref)
@@ -81,10 +82,10 @@ def test_linear_vs_oracle(env, M, N, K, wfmt):
         assert err < (2e-3 if wfmt == 1 else 1e-4), (path, err)
 
 
-@pytest.mark.parametrize("path", ["gemv", "gemm", "tc"])
+@pytest.mark.parametrize("path", ["gemv", "gemm", "tc", "ws"])
 def test_linear_special_cases_exact(env, path):
     pipo, pl = env
-    p = {"gemv": pipo.PATH_GEMV, "gemm": pipo.PATH_GEMM, "tc": pipo.PATH_TC}[path]
+    p = {"gemv": pipo.PATH_GEMV, "gemm": pipo.PATH_GEMM, "tc": pipo.PATH_TC, "ws": pipo.PATH_WS}[path]
     rng = np.random.default_rng(5)
     N, K = 200, 256
     w = (rng.standard_normal((N, K)) * 0.02).astype(np.float16).astype(np.float32)
@@ -141,3 +142,21 @@ def test_attention_special_cases_exact(env):
     v2 = rng.standard_normal((L, b, d)).astype(np.float16)
     o2 = pipo.pipo_attention_decode(pl.ctx, q, k2, v2, H)
     assert np.abs(o2 - v2.astype(np.float64).mean(0)).max() < 2e-3
+
+
+@pytest.mark.parametrize("b,n,past,d,H", [(1, 5, 0, 128, 2), (2, 64, 0, 256, 2), (2, 100, 0, 512, 4),
+                                          (3, 33, 7, 256, 4), (1, 130, 70, 1024, 8), (2, 512, 0, 512, 4)])
+@pytest.mark.parametrize("cuda_cores", [False, True])
+def test_attention_prefill_vs_oracle(env, b, n, past, d, H, cuda_cores):
+    pipo, pl = env
+    rng = np.random.default_rng(n * 100 + past + d)
+    q = (rng.standard_normal((b, n, d)) * (d // H) ** -0.5).astype(np.float16)
+    L = past + n
+    k = rng.standard_normal((L, b, d)).astype(np.float16)
+    v = rng.standard_normal((L, b, d)).astype(np.float16)
+    o = pipo.pipo_attention_prefill(pl.ctx, q, k, v, past, H, cuda_cores)
+    ref = opt.attention(q.astype(np.float64), k.astype(np.float64).transpose(1, 0, 2),
+                        v.astype(np.float64).transpose(1, 0, 2), past, H)
+    assert rel_inf(o, ref) < 2e-2
+    # P is rounded to fp16 before P.V on the tensor-core path
+    assert rel_inf(o, ref) < (5e-3 if cuda_cores else 1e-2)

@@ -1,0 +1,30 @@
+"""Isolated kernel timing of the linear-layer paths at the OPT decode/prefill shapes."""
+import json
+import sys
+
+sys.path.insert(0, ".")
+import pipo_synth as synth  # noqa: E402
+from paper_2504_03664_b200 import pipo  # noqa: E402
+
+shape = synth.OPTShape(256, 1, 4, 512, vocab=512, max_pos=64)
+pl = pipo.Pipeline(pipo.make_config(shape, max_batch=4, max_seq=16, weight_tier=pipo.PIPO_TIER_DEVICE))
+paths = {"gemm_mma": pipo.PATH_GEMM, "tc_v1": pipo.PATH_TC, "ws": pipo.PATH_WS}
+cases = [("c5_qkv", 64, 21504, 7168), ("c5_out", 64, 7168, 7168), ("c5_fc1", 64, 28672, 7168),
+         ("c5_fc2", 64, 7168, 28672), ("c2_qkv", 16, 6144, 2048), ("c2_fc2", 16, 2048, 8192),
+         ("c3_qkv", 32, 12288, 4096), ("pre_c2_qkv", 4096, 6144, 2048)]
+if len(sys.argv) > 1:
+    cases = [c for c in cases if c[0] in sys.argv[1:]]
+out = {}
+for name, M, N, K in cases:
+    wbytes = N * K / 2 + N * K / 32
+    res = {}
+    for pn, p in paths.items():
+        try:
+            us = pipo.pipo_bench_linear(pl.ctx, 1, p, M, N, K, 10)
+            res[pn] = {"us": round(us, 2), "GBs": round(wbytes / us / 1e3, 1),
+                       "TFLOPs": round(2 * M * N * K / us / 1e6, 1)}
+        except pipo.PipoError as e:
+            res[pn] = str(e)
+    out[name] = res
+    print(name, json.dumps(res), flush=True)
+json.dump(out, open("gpurun_out/kbench.json", "w"), indent=1)
