@@ -224,8 +224,14 @@ def run_pipo(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    ndev = torch.cuda.device_count()
+    if ndev == 0:
+        raise SystemExit("bench.py needs a CUDA device (the library has no CPU path)")
+    shared_gpu = world > ndev                  # smoke-testing N ranks on fewer GPUs
+    local = local % ndev
     if world > 1:
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        # plumbing only (barrier + max of device times): NCCL when every rank owns a GPU
+        dist.init_process_group("gloo" if shared_gpu else "nccl")
     torch.cuda.set_device(local)
     c = CONFIGS[args.config]
     s, b, P, G = c["shape"], c["b"], c["P"], c["G"]

@@ -205,7 +205,8 @@ pipo_status pipo_unpack_int4_g64(pipo_ctx* ctx, const uint8_t* codes, const uint
  * W given as fp32 masters [N][K] (quantized per wfmt inside); y fp32 [M][N].
  * path: 0 = automatic (as the pipeline chooses), 1 = int4 GEMV (CUDA cores),
  * 2 = mma.sync GEMM (legacy baseline), 3 = tcgen05/TMEM GEMM (synchronous pipeline),
- * 4 = warp-specialized stream-K tcgen05 GEMM (int4; the pipeline's M >= 16 path). */
+ * 4 = warp-specialized stream-K tcgen05 GEMM (int4, A in shared memory),
+ * 5 = same with A in TMEM (int4, M <= 64). */
 pipo_status pipo_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, const uint16_t* x,
                         const float* w, const float* bias, int32_t M, int32_t N, int32_t K,
                         float* y);
@@ -215,6 +216,10 @@ pipo_status pipo_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, const uint16_
  * launches on the compute stream, average microseconds per launch in *us. */
 pipo_status pipo_bench_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, int32_t M, int32_t N, int32_t K,
                               int32_t iters, double* us);
+
+/* Measurement aid: HBM -> shared-memory streaming with cp.async.bulk, one CTA per
+ * SM, `stages`-deep mbarrier ring of `chunk`-byte requests; GB/s in *gbs. */
+pipo_status pipo_probe_bulk(pipo_ctx* ctx, int32_t chunk, int32_t stages, double* gbs);
 
 /* Decode attention kernel: q [b][d] fp16 bits (pre-scaled), k/v [L][b][d] fp16
  * bits (position-major) -> o [b][d] fp32.  n_heads | d. */

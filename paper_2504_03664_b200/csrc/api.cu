@@ -31,6 +31,7 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <cstdlib>
 
 #include "ctx.h"
 #include "disk.h"
@@ -974,7 +975,7 @@ pipo_status pipo_unpack_int4_g64(pipo_ctx* ctx, const uint8_t* codes, const uint
 pipo_status pipo_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, const uint16_t* x, const float* w,
                         const float* bias, int32_t M, int32_t N, int32_t K, float* y) {
   CHECK_CTX();
-  if (!x || !w || !y || M <= 0 || N <= 0 || K <= 0 || K % 64 || (wfmt != 0 && wfmt != 1) || path < 0 || path > 4)
+  if (!x || !w || !y || M <= 0 || N <= 0 || K <= 0 || K % 64 || (wfmt != 0 && wfmt != 1) || path < 0 || path > 5)
     return set_err(PIPO_E_INVALID_ARG, "bad linear arguments");
   CK(cudaSetDevice(ctx->cfg.device));
   const MatLayout ml = mat_layout(N, K, wfmt);
@@ -1015,7 +1016,7 @@ pipo_status pipo_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, const uint16_
 pipo_status pipo_bench_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, int32_t M, int32_t N, int32_t K,
                               int32_t iters, double* us) {
   CHECK_CTX();
-  if (!us || M <= 0 || N <= 0 || K <= 0 || K % 64 || iters <= 0 || (wfmt != 0 && wfmt != 1) || path < 0 || path > 4)
+  if (!us || M <= 0 || N <= 0 || K <= 0 || K % 64 || iters <= 0 || (wfmt != 0 && wfmt != 1) || path < 0 || path > 5)
     return set_err(PIPO_E_INVALID_ARG, "bad bench arguments");
   CK(cudaSetDevice(ctx->cfg.device));
   const MatLayout ml = mat_layout(N, K, wfmt);
@@ -1035,6 +1036,7 @@ pipo_status pipo_bench_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, int32_t
   la.ws = ctx->ws; la.ws_floats = ctx->ws_floats; la.counters = ctx->counters; la.n_counters = ctx->n_counters;
   la.num_sms = ctx->num_sms;
   la.epi.kind = EPI_F32; la.epi.M = M; la.epi.N = N; la.epi.y = dy; la.epi.ldy = N;
+  if (getenv("PIPO_WS_DEBUG")) CK(cudaMemsetAsync(ctx->ws + (15ll << 20), 0, 148 * 8 * 8, st));
   LAUNCH(launch_linear(la, path, ctx->gemv_max_m, st));   // warm-up
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
@@ -1046,9 +1048,58 @@ pipo_status pipo_bench_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, int32_t
   float ms = 0;
   CK(cudaEventElapsedTime(&ms, e0, e1));
   cudaEventDestroy(e0); cudaEventDestroy(e1);
+  if (getenv("PIPO_WS_DEBUG") && (atoi(getenv("PIPO_WS_DEBUG")) & 32) && path == 5) {
+    std::vector<uint64_t> wt(148 * 16);
+    CK(cudaMemcpy(wt.data(), ctx->ws + (15ll << 20), wt.size() * 8, cudaMemcpyDeviceToHost));
+    double avg[9] = {0};
+    for (int c = 0; c < 148; ++c)
+      for (int k = 0; k < 9; ++k) avg[k] += wt[c * 16 + k] / 148.0;
+    fprintf(stderr, "tm-waits(kcycles): prod raw_empty %.1f | mma a_full %.1f x_full %.1f | unpack raw_full %.1f a_empty %.1f | xprod x_empty %.1f | total %.1f\n",
+            avg[0] / 1e3, avg[2] / 1e3, avg[3] / 1e3, avg[4] / 1e3, avg[5] / 1e3, avg[6] / 1e3, avg[8] / 1e3);
+  } else if (getenv("PIPO_WS_DEBUG") && (atoi(getenv("PIPO_WS_DEBUG")) & 32)) {
+    std::vector<uint64_t> ts(148 * 8);
+    CK(cudaMemcpy(ts.data(), ctx->ws + (15ll << 20), ts.size() * 8, cudaMemcpyDeviceToHost));
+    uint64_t t0 = ~0ull;
+    for (int c = 0; c < 148; ++c) if (ts[c * 8]) t0 = std::min(t0, ts[c * 8]);
+    for (int k = 0; k < 8; ++k) {
+      std::vector<double> v;
+      for (int c = 0; c < 148; ++c) if (ts[c * 8 + k] >= t0 && ts[c * 8 + k] - t0 < 10000000ull) v.push_back((ts[c * 8 + k] - t0) * 1e-3);
+      std::sort(v.begin(), v.end());
+      if (!v.empty()) fprintf(stderr, "ws-stamp %d: min %.2f med %.2f max %.2f us (n=%zu)\n", k, v.front(), v[v.size() / 2], v.back(), v.size());
+    }
+  }
   cudaFree(dw); cudaFree(dx); cudaFree(dy); cudaFree(tmp);
   ctx->hbm_bytes -= ml.bytes + (int64_t)M * K * 2 + (int64_t)M * N * 4 + std::max<int64_t>((int64_t)N * K, (int64_t)M * K) * 4;
   *us = ms * 1e3 / iters;
+  return PIPO_OK;
+}
+
+pipo_status pipo_probe_bulk(pipo_ctx* ctx, int32_t chunk, int32_t stages, double* gbs) {
+  CHECK_CTX();
+  if (!gbs || chunk <= 0 || chunk % 16 || stages <= 0) return set_err(PIPO_E_INVALID_ARG, "bad probe arguments");
+  CK(cudaSetDevice(ctx->cfg.device));
+  const int ctas = ctx->num_sms;
+  const int64_t per = (int64_t)(512ll << 20) / ctas / chunk * chunk;
+  uint8_t* buf = nullptr;
+  uint32_t* sink = nullptr;
+  TRY(dev_alloc(ctx, &buf, per * ctas));
+  TRY(dev_alloc(ctx, &sink, 4));
+  cudaStream_t st = ctx->s_comp;
+  CK(cudaMemsetAsync(buf, 1, (size_t)(per * ctas), st));
+  LAUNCH(launch_bulk_probe(buf, per, chunk, stages, ctas, sink, st));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, st));
+  for (int i = 0; i < 5; ++i) LAUNCH(launch_bulk_probe(buf, per, chunk, stages, ctas, sink, st));
+  CK(cudaEventRecord(e1, st));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0); cudaEventDestroy(e1);
+  cudaFree(buf); cudaFree(sink);
+  ctx->hbm_bytes -= per * ctas + 4;
+  *gbs = 5.0 * per * ctas / (ms * 1e-3) / 1e9;
   return PIPO_OK;
 }
 

@@ -370,7 +370,9 @@ int launch_attention_decode(const AttnArgs& a, cudaStream_t st) {
   if (hd != 64 && hd != 128) return -1;
   const int L = a.past + 1;
   const int pairs = a.b * a.n_heads;
-  const int target = a.num_sms * 8;
+  // enough CTAs for ~8 waves of resident blocks (9 per SM): the block scheduler then
+  // balances the tail to within ~1/8 of the kernel; splits merge in a second kernel
+  const int target = a.num_sms * 72;
   int n_splits = pairs >= target ? 1 : (target + pairs - 1) / pairs;
   n_splits = max(1, min(n_splits, (L + 63) / 64));
   const int per = (L + n_splits - 1) / n_splits;

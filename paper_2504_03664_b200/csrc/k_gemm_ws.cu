@@ -90,6 +90,13 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
 
 // stream-K partition of U units over G CTAs
@@ -142,7 +149,6 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
   uint64_t* acc_full = a_empty + C::NA;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
-  int* s_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n_kb = a.K / 64;
@@ -171,6 +177,15 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
   __syncthreads();
   ws::tc_after();
   const uint32_t tmem = *tmem_slot;
+  uint64_t* tsbuf = (dbg & 32) ? reinterpret_cast<uint64_t*>(a.ws + (15ll << 20)) + blockIdx.x * 8 : nullptr;
+  auto stamp = [&](int k) {
+    if (tsbuf) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      tsbuf[k] = t;
+    }
+  };
+  if (tid == 0) stamp(0);
 
   if (warp == 0) {
     // ------------------------------ producer ------------------------------
@@ -199,6 +214,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
           ws::tma_2d(xs + s * C::X_TILE, &xmap, kb * 64, mt * BN, &x_full[s]);
         }
       }
+      stamp(1);
     }
   } else if (warp == 1) {
     // ------------------------------ MMA issuer ------------------------------
@@ -227,8 +243,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
             ws::mma_f16(d, ws::sw128_desc(aa + kk * 32), db, C::IDESC, acc);
             if (two) ws::mma_f16(d + BN, ws::sw128_desc(aa + 128 * 128 + kk * 32), db, C::IDESC, acc);
           }
-          ws::mma_commit(&a_empty[sa]);
-          ws::mma_commit(&x_empty[s]);
+          if (dbg & 8) {
+            ws::mbar_arrive(&a_empty[sa]);
+            ws::mbar_arrive(&x_empty[s]);
+          } else {
+            ws::mma_commit(&a_empty[sa]);
+            ws::mma_commit(&x_empty[s]);
+          }
         }
         ws::mma_commit(&acc_full[ab]);
         u = seg_end;
@@ -295,6 +316,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         }
       }
       ws::tc_after();
+      const bool last_seg = seg_end == u1;
+      if (last_seg && et == 0) stamp(4);
       const int slot = 2 * (int)blockIdx.x + (tile == first_tile_mine ? 0 : 1);
       float* part = a.ws + (int64_t)slot * (2 * BN * 128);
       for (int t = 0; t < ntile; ++t) {
@@ -315,47 +338,361 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
       ws::tc_before();
       __syncwarp();
       if (lane == 0) ws::mbar_arrive(&acc_empty[ab]);
-      if (!full) {
-        // stream-K fixup: the last CTA covering this tile sums partials in k order
-        const int cf = ws::cta_of_unit(tile * n_kb, U, G), cl = ws::cta_of_unit((tile + 1) * n_kb - 1, U, G);
-        __threadfence();
-        ws::named_bar(1, 128);
-        if (et == 0) *s_flag = (atomicAdd(&a.counters[tile], 1) == cl - cf);
-        ws::named_bar(1, 128);
-        if (*s_flag) {
-          __threadfence();
-          for (int t = 0; t < ntile; ++t) {
-            const int n = (2 * pr + t) * 128 + row;
-            for (int c0 = 0; c0 < BN; c0 += 16) {
-              float acc[16];
+      if (last_seg && et == 0) stamp(5);
+      u = seg_end;
+      ++seg;
+    }
+    if (et == 0) stamp(2);
+  }
+  __syncwarp();          // lanes 1-31 of the producer / MMA warps wait for lane 0 (bar.sync is .aligned)
+  ws::tc_before();
+  __syncthreads();
+  if (tid == 0) stamp(3);
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"((uint32_t)C::TMEM_COLS));
+}
+
+
+// Stream-K partial reduction (separate launch, fully parallel): tile `tile` of
+// (pair, m-tile) was split across CTAs cf..cl; their partial accumulators are summed
+// in k order (deterministic) and the fused epilogue runs.  grid = (tiles, BN/16).
+template <int BN>
+__global__ void __launch_bounds__(256) ws_reduce_kernel(LinearArgs a, int n_rt, int m_tiles, int G, int kbu) {
+  // grid = (tiles, BN/4): each thread owns one weight row of one tile and 4 columns;
+  // contributors are loaded 8 at a time (32 loads in flight), summed in k order.
+  const int64_t tile = blockIdx.x;
+  const int n_kb = a.K / 64 / kbu, n_pairs = (n_rt + 1) >> 1;     // n_kb = units per tile
+  const int64_t U = (int64_t)n_pairs * m_tiles * n_kb;
+  const int cf = ws::cta_of_unit(tile * n_kb, U, G), cl = ws::cta_of_unit((tile + 1) * n_kb - 1, U, G);
+  if (cf == cl) return;                                   // fully owned: stored by the GEMM
+  const int pr = (int)(tile % n_pairs), mt = (int)(tile / n_pairs);
+  const int t = threadIdx.x >> 7, row = threadIdx.x & 127;
+  if (2 * pr + t >= n_rt) return;
+  const int n = (2 * pr + t) * 128 + row, m0 = mt * BN, c0 = blockIdx.y * 4;
+  const int64_t first_cf = ws::u_begin(cf, U, G) / n_kb;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int cb = cf; cb <= cl; cb += 8) {
+    float v[8][4];
 #pragma unroll
-              for (int j = 0; j < 16; ++j) acc[j] = 0.f;
-              for (int cc = cf; cc <= cl; ++cc) {          // k order: deterministic
-                const int64_t ft = ws::u_begin(cc, U, G) / n_kb;
-                const float* src = a.ws + (int64_t)(2 * cc + (ft == tile ? 0 : 1)) * (2 * BN * 128) +
-                                   (t * BN + c0) * 128 + row;
-                float v[16];
+    for (int q = 0; q < 8; ++q) {
+      const int cc = cb + q;
+      if (cc <= cl) {
+        // slot: the tile is cc's first tile unless cc == cf and cf started in an earlier tile
+        const int sl = 2 * cc + ((cc == cf && first_cf != tile) ? 1 : 0);
+        const float* src = a.ws + (int64_t)sl * (2 * BN * 128) + (t * BN + c0) * 128 + row;
 #pragma unroll
-                for (int j = 0; j < 16; ++j) v[j] = __ldcg(src + j * 128);
-#pragma unroll
-                for (int j = 0; j < 16; ++j) acc[j] += v[j];
-              }
-#pragma unroll
-              for (int j = 0; j < 16; ++j) epi_store(a.epi, m0 + c0 + j, n, acc[j]);
-            }
-          }
-          if (et == 0) a.counters[tile] = 0;
-        }
-        ws::named_bar(1, 128);
+        for (int j = 0; j < 4; ++j) v[q][j] = __ldcg(src + j * 128);
       }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (cb + q <= cl)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j] += v[q][j];
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) epi_store(a.epi, m0 + c0 + j, n, acc[j]);
+}
+
+// ---------------------------------------------------------------------------------
+// v5: A operand in TMEM.  The unpack warps write each dequantized 128 x 64 tile row
+// straight into tensor memory with tcgen05.st (one 32x32b.x32 store per row: the row's
+// 64 fp16 values = 32 columns), and the MMA reads A from TMEM (tcgen05.mma ... [a_tmem]).
+// No shared-memory A ring, no swizzled STS, no generic->async proxy fence, and the
+// freed shared memory deepens the raw-weight ring (NR stages in flight).
+constexpr int TM_THREADS = 480;   // 0 raw producer, 1 MMA, 2-9 unpack, 10-13 epilogue, 14 x producer
+
+// One unit = 2 weight tiles (256 rows) x KBU k-blocks: the per-unit synchronisation
+// (mbarrier waits, tcgen05.commit, producer bookkeeping) is amortised over 8*KBU MMAs.
+template <int BN, int KBU>
+struct TmCfg {
+  static constexpr int RAW_T = KBU * (int)kInt4BlockBytes;     // one tile's blocks (contiguous)
+  static constexpr int RAW = 2 * RAW_T;
+  static constexpr int NR = (KBU == 1 ? 16 : 8);                // raw unit stages
+  static constexpr int X_KB = BN * 128;                         // x tile of one k-block
+  static constexpr int X_TILE = KBU * X_KB;
+  static constexpr int NX = (KBU == 1 ? 8 : 4);
+  static constexpr int ACC_COLS = 2 * 2 * BN;                   // 2 buffers x 2 tiles
+  static constexpr int A_COLS = 2 * 32 * KBU;                   // per A stage (2 tiles x KBU x 32 cols)
+  static constexpr int NA = (512 - ACC_COLS) / A_COLS < 6 ? (512 - ACC_COLS) / A_COLS : 6;
+  static constexpr int SMEM = 1024 + NX * X_TILE + NR * RAW + 512;
+  static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
+  static_assert(NA >= 2, "TMEM budget");
+};
+
+__device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t clk() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+  return t;
+}
+
+template <int BN, int KBU>
+__global__ void __launch_bounds__(TM_THREADS, 1)
+    gemm_tm_kernel(const __grid_constant__ CUtensorMap xmap, LinearArgs a, int n_rt, int m_tiles, int G, int dbg) {
+  using C = TmCfg<BN, KBU>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  uint8_t* base = smem_raw + (base_u32 - smem_u32(smem_raw));
+  uint8_t* xs = base;
+  uint8_t* raw = xs + C::NX * C::X_TILE;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(raw + C::NR * C::RAW);
+  uint64_t* raw_full = bar;
+  uint64_t* raw_empty = raw_full + C::NR;
+  uint64_t* x_full = raw_empty + C::NR;
+  uint64_t* x_empty = x_full + C::NX;
+  uint64_t* a_full = x_empty + C::NX;
+  uint64_t* a_empty = a_full + C::NA;
+  uint64_t* acc_full = a_empty + C::NA;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n_kb = a.K / 64, n_ku = n_kb / KBU;
+  const int n_pairs = (n_rt + 1) >> 1;
+  const int64_t U = (int64_t)n_pairs * m_tiles * n_ku;
+  const int64_t u0 = ws::u_begin(blockIdx.x, U, G), u1 = ws::u_begin(blockIdx.x + 1, U, G);
+
+  if (tid == 0) {
+    for (int i = 0; i < C::NR; ++i) { ws::mbar_init(&raw_full[i], 1); ws::mbar_init(&raw_empty[i], 8); }
+    for (int i = 0; i < C::NX; ++i) { ws::mbar_init(&x_full[i], 1); ws::mbar_init(&x_empty[i], 1); }
+    for (int i = 0; i < C::NA; ++i) { ws::mbar_init(&a_full[i], 8); ws::mbar_init(&a_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { ws::mbar_init(&acc_full[i], 1); ws::mbar_init(&acc_empty[i], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&xmap) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512u));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  ws::tc_before();
+  __syncthreads();
+  ws::tc_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t a_base = tmem + C::ACC_COLS;           // A ring columns
+  uint64_t* wt = (dbg & 32) ? reinterpret_cast<uint64_t*>(a.ws + (15ll << 20)) + blockIdx.x * 16 : nullptr;
+  uint64_t w_acc[2] = {0, 0};
+  const uint64_t t_begin = clk();
+#define TWAIT(slot, bar, par)                          \
+  do {                                                 \
+    const uint64_t t0_ = wt ? clk() : 0;               \
+    ws::mbar_wait(bar, par);                           \
+    if (wt) w_acc[slot] += clk() - t0_;                \
+  } while (0)
+
+  if (warp == 0) {
+    // ------- raw int4 producer: per unit one bulk copy per tile (KBU blocks, contiguous) -------
+    if (lane == 0) {
+      int64_t tile = u0 / n_ku;
+      int ku = (int)(u0 - tile * n_ku);
+      int pr = (int)(tile % n_pairs);
+      int s = 0;
+      uint32_t ph = 1;
+      const int64_t tile_stride = (int64_t)n_kb * kInt4BlockBytes;
+      const uint8_t* wsrc = a.w + (int64_t)(2 * pr) * tile_stride + (int64_t)ku * C::RAW_T;
+      for (int64_t u = u0; u < u1; ++u) {
+        const bool two = 2 * pr + 1 < n_rt;
+        TWAIT(0, &raw_empty[s], ph);
+        ws::mbar_expect_tx(&raw_full[s], two ? C::RAW : C::RAW_T);
+        ws::bulk_g2s(raw + s * C::RAW, wsrc, C::RAW_T, &raw_full[s]);
+        if (two) ws::bulk_g2s(raw + s * C::RAW + C::RAW_T, wsrc + tile_stride, C::RAW_T, &raw_full[s]);
+        wsrc += C::RAW_T;
+        if (++ku == n_ku) {
+          ku = 0;
+          if (++pr == n_pairs) pr = 0;
+          wsrc = a.w + (int64_t)(2 * pr) * tile_stride;
+        }
+        if (++s == C::NR) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 14) {
+    // ---------------- x producer (TMA 2D, SWIZZLE_128B, KBU boxes per unit) ----------------
+    if (lane == 0) {
+      int64_t tile = u0 / n_ku;
+      int ku = (int)(u0 - tile * n_ku);
+      int pr = (int)(tile % n_pairs), mt = (int)(tile / n_pairs);
+      int s = 0;
+      uint32_t ph = 1;
+      for (int64_t u = u0; u < u1; ++u) {
+        TWAIT(0, &x_empty[s], ph);
+        ws::mbar_expect_tx(&x_full[s], C::X_TILE);
+#pragma unroll
+        for (int k = 0; k < KBU; ++k)
+          ws::tma_2d(xs + s * C::X_TILE + k * C::X_KB, &xmap, (ku * KBU + k) * 64, mt * BN, &x_full[s]);
+        if (++ku == n_ku) {
+          ku = 0;
+          if (++pr == n_pairs) { pr = 0; ++mt; }
+        }
+        if (++s == C::NX) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer: A from TMEM, B (x) from shared memory ----------------
+    // The whole warp runs the loop (warp-uniform descriptors stay in uniform registers);
+    // one elected lane issues the tcgen05.mma / tcgen05.commit instructions.
+    int seg = 0, sa = 0, sx = 0;
+    uint32_t ph_a = 0, ph_x = 0;
+    int64_t u = u0;
+    const uint32_t xs_base = smem_u32(xs);
+    while (u < u1) {
+      const int64_t tile = u / n_ku;
+      const int64_t seg_end = min(u1, (tile + 1) * n_ku);
+      const bool two = 2 * (int)(tile % n_pairs) + 1 < n_rt;
+      const int ab = seg & 1;
+      ws::mbar_wait(&acc_empty[ab], ((seg >> 1) & 1) ^ 1);
+      ws::tc_after();
+      const uint32_t d = tmem + ab * (2 * BN);
+      for (int64_t v = u; v < seg_end; ++v) {
+        TWAIT(0, &a_full[sa], ph_a);
+        TWAIT(1, &x_full[sx], ph_x);
+        ws::tc_after();
+        if (ws::elect_one()) {
+          const uint32_t at = a_base + sa * C::A_COLS;
+          const uint64_t db0 = ws::sw128_desc(xs_base + sx * C::X_TILE);
+#pragma unroll
+          for (int k = 0; k < KBU; ++k)
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint32_t acc = (v > u || k > 0 || kk > 0) ? 1u : 0u;
+              const uint64_t db = db0 + (uint64_t)((k * C::X_KB + kk * 32) >> 4);
+              mma_f16_ts(d, at + k * 64 + kk * 8, db, C::IDESC, acc);
+              if (two) mma_f16_ts(d + BN, at + k * 64 + 32 + kk * 8, db, C::IDESC, acc);
+            }
+          ws::mma_commit(&a_empty[sa]);
+          ws::mma_commit(&x_empty[sx]);
+        }
+        __syncwarp();
+        if (++sa == C::NA) { sa = 0; ph_a ^= 1; }
+        if (++sx == C::NX) { sx = 0; ph_x ^= 1; }
+      }
+      if (ws::elect_one()) ws::mma_commit(&acc_full[ab]);
+      __syncwarp();
+      u = seg_end;
+      ++seg;
+    }
+  } else if (warp < 10) {
+    // ---------------- unpack + scale straight into TMEM ----------------
+    // warp w: tile t = (w-2)/4, TMEM lanes 32*(w%4).. (a warp may only touch its lane quarter)
+    const int t = (warp - 2) >> 2, q = warp & 3;
+    const int r = q * 32 + lane;
+    int s = 0, sa = 0;
+    uint32_t ph_r = 0, ph_a = 1;
+    for (int64_t u = u0; u < u1; ++u) {
+      TWAIT(0, &raw_full[s], ph_r);
+      uint4 cw[KBU][2];
+      __half2 s2[KBU];
+#pragma unroll
+      for (int k = 0; k < KBU; ++k) {
+        const uint8_t* rs = raw + s * C::RAW + t * C::RAW_T + k * kInt4BlockBytes;
+        cw[k][0] = *reinterpret_cast<const uint4*>(rs + r * 16);
+        cw[k][1] = *reinterpret_cast<const uint4*>(rs + (128 + r) * 16);
+        s2[k] = __half2half2(*reinterpret_cast<const __half*>(rs + 4096 + r * 2));
+      }
+      __syncwarp();
+      if (lane == 0) ws::mbar_arrive(&raw_empty[s]);
+      TWAIT(1, &a_empty[sa], ph_a);
+      ws::tc_after();
+#pragma unroll
+      for (int k = 0; k < KBU; ++k) {
+        uint32_t o[32];
+        const uint32_t w[8] = {cw[k][0].x, cw[k][0].y, cw[k][0].z, cw[k][0].w,
+                               cw[k][1].x, cw[k][1].y, cw[k][1].z, cw[k][1].w};
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) dequant8(w[ch], s2[k], reinterpret_cast<__half2*>(o + ch * 4));
+        tmem_st32(a_base + sa * C::A_COLS + k * 64 + t * 32 + ((uint32_t)(q * 32) << 16), o);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+      ws::tc_before();
+      __syncwarp();
+      if (lane == 0) ws::mbar_arrive(&a_full[sa]);
+      if (++s == C::NR) { s = 0; ph_r ^= 1; }
+      if (++sa == C::NA) { sa = 0; ph_a ^= 1; }
+    }
+  } else {
+    // ---------------- epilogue ----------------
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    int seg = 0;
+    int64_t u = u0;
+    const int64_t first_tile_mine = u0 / n_ku;
+    while (u < u1) {
+      const int64_t tile = u / n_ku;
+      const int64_t seg_end = min(u1, (tile + 1) * n_ku);
+      const bool full = (u == tile * n_ku) && (seg_end == (tile + 1) * n_ku);
+      const int pr = (int)(tile % n_pairs), mt = (int)(tile / n_pairs);
+      const int m0 = mt * BN;
+      const int ntile = (2 * pr + 1 < n_rt) ? 2 : 1;
+      const int ab = seg & 1;
+      {
+        uint32_t done = 0;
+        const uint32_t addr = smem_u32(&acc_full[ab]), par = (seg >> 1) & 1;
+        while (true) {
+          asm volatile(
+              "{\n.reg .pred P1;\nmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
+              : "=r"(done)
+              : "r"(addr), "r"(par)
+              : "memory");
+          if (done) break;
+          __nanosleep(128);
+        }
+      }
+      ws::tc_after();
+      const int slot = 2 * (int)blockIdx.x + (tile == first_tile_mine ? 0 : 1);
+      float* part = a.ws + (int64_t)slot * (2 * BN * 128);
+      for (int tt = 0; tt < ntile; ++tt) {
+        const uint32_t t_row = tmem + ab * (2 * BN) + tt * BN + ((uint32_t)(quarter * 32) << 16);
+        const int n = (2 * pr + tt) * 128 + row;
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          float v[16];
+          ws::tmem_ld16(t_row + c0, v);
+          if (full) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) epi_store(a.epi, m0 + c0 + j, n, v[j]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) __stcg(part + (tt * BN + c0 + j) * 128 + row, v[j]);
+          }
+        }
+      }
+      ws::tc_before();
+      __syncwarp();
+      if (lane == 0) ws::mbar_arrive(&acc_empty[ab]);
       u = seg_end;
       ++seg;
     }
   }
+  if (wt && lane == 0) {
+    // slots: 0/1 raw producer, 2/3 MMA (a_full, x_full), 4/5 unpack warp 2 (raw_full, a_empty),
+    // 6/7 x producer, 8 = total cycles of the MMA thread
+    const int role = warp == 0 ? 0 : warp == 1 ? 1 : warp == 2 ? 2 : warp == 14 ? 3 : -1;
+    if (role >= 0) { wt[2 * role] = w_acc[0]; wt[2 * role + 1] = w_acc[1]; }
+    if (warp == 1) wt[8] = clk() - t_begin;
+  }
+#undef TWAIT
+  __syncwarp();
   ws::tc_before();
   __syncthreads();
   if (warp == 1)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"((uint32_t)C::TMEM_COLS));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512u));
 }
 
 // ---------------------------------------------------------------------------------
@@ -406,7 +743,43 @@ static int run_ws(const LinearArgs& a, cudaStream_t st) {
   if (!make_xmap(&map, a.x, a.M, a.K, BN)) return -1;
   static const int dbg = getenv("PIPO_WS_DEBUG") ? atoi(getenv("PIPO_WS_DEBUG")) : 0;
   gemm_ws_kernel<BN><<<G, WS_THREADS, C::SMEM, st>>>(map, a, n_rt, m_tiles, dbg);
-  return 1;
+  if (dbg & 64) return 1;   // debug: main kernel only
+  dim3 rg((unsigned)tiles, BN / 4);
+  ws_reduce_kernel<BN><<<rg, 256, 0, st>>>(a, n_rt, m_tiles, G, 1);
+  return 2;
+}
+
+
+template <int BN, int KBU>
+static int run_tm(const LinearArgs& a, cudaStream_t st) {
+  using C = TmCfg<BN, KBU>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(gemm_tm_kernel<BN, KBU>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    attr_set = true;
+  }
+  const int n_rt = (a.N + 127) / 128, m_tiles = (a.M + BN - 1) / BN, n_kb = a.K / 64;
+  const int n_pairs = (n_rt + 1) / 2, n_ku = n_kb / KBU;
+  const int64_t U = (int64_t)n_pairs * m_tiles * n_ku;
+  const int G = (int)std::max<int64_t>(1, std::min<int64_t>(a.num_sms, U / (8 / KBU)));
+  const int64_t tiles = (int64_t)n_pairs * m_tiles;
+  if ((int64_t)2 * G * 2 * BN * 128 > a.ws_floats) return -1;
+  CUtensorMap map;
+  if (!make_xmap(&map, a.x, a.M, a.K, BN)) return -1;
+  static const int dbg = getenv("PIPO_WS_DEBUG") ? atoi(getenv("PIPO_WS_DEBUG")) : 0;
+  gemm_tm_kernel<BN, KBU><<<G, TM_THREADS, C::SMEM, st>>>(map, a, n_rt, m_tiles, G, dbg);
+  dim3 rg((unsigned)tiles, BN / 4);
+  ws_reduce_kernel<BN><<<rg, 256, 0, st>>>(a, n_rt, m_tiles, G, KBU);
+  return 2;
+}
+
+int launch_linear_tm(const LinearArgs& a, cudaStream_t st) {
+  if (a.wfmt != 1) return -1;
+  const bool even = (a.K / 64) % 2 == 0;
+  if (a.M <= 16) return even ? run_tm<16, 2>(a, st) : run_tm<16, 1>(a, st);
+  if (a.M <= 32) return even ? run_tm<32, 2>(a, st) : run_tm<32, 1>(a, st);
+  if (a.M <= 64) return even ? run_tm<64, 2>(a, st) : run_tm<64, 1>(a, st);
+  return -1;
 }
 
 int launch_linear_ws(const LinearArgs& a, cudaStream_t st) {

@@ -43,7 +43,10 @@ struct LinearArgs {
   int num_sms = 148;
 };
 
-enum LinearPath { PATH_AUTO = 0, PATH_GEMV = 1, PATH_GEMM = 2, PATH_TC = 3, PATH_WS = 4 };
+enum LinearPath { PATH_AUTO = 0, PATH_GEMV = 1, PATH_GEMM = 2, PATH_TC = 3, PATH_WS = 4, PATH_TM = 5 };
+
+// warp-specialized stream-K tcgen05 GEMM with A in TMEM, int4 weights, M <= 64
+int launch_linear_tm(const LinearArgs& a, cudaStream_t st);
 
 // warp-specialized stream-K tcgen05 GEMM, int4 weights (k_gemm_ws.cu)
 int launch_linear_ws(const LinearArgs& a, cudaStream_t st);
@@ -84,6 +87,10 @@ int launch_quantize(const float* w, int64_t rows, int64_t cols, uint8_t* codes, 
 int launch_tile_fp16(const float* w, int64_t rows, int64_t cols, uint8_t* tiled, cudaStream_t st);
 int launch_f32_to_f16(const float* src, __half* dst, int64_t n, cudaStream_t st);
 int launch_f16_to_f32(const __half* src, float* dst, int64_t n, cudaStream_t st);
+
+// measurement aid: bulk-copy streaming probe (k_probe.cu)
+int launch_bulk_probe(const uint8_t* src, int64_t bytes_per_cta, int chunk, int stages, int ctas, uint32_t* sink,
+                      cudaStream_t st);
 
 // synthetic generator (pipo_synth mirror; input generation, not the method)
 int launch_synth(float* out, int64_t start, int64_t count, uint64_t key, int kind, float scale,

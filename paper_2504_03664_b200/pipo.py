@@ -25,7 +25,7 @@ PIPO_F_TIMELINE = 1
 PIPO_F_KPROF = 2
 K_CLASSES = ["linear_decode", "attn_decode", "lm_head", "linear_prefill", "attn_prefill", "misc"]
 PIPO_LAYER_EMBED = -1
-PATH_AUTO, PATH_GEMV, PATH_GEMM, PATH_TC, PATH_WS = 0, 1, 2, 3, 4
+PATH_AUTO, PATH_GEMV, PATH_GEMM, PATH_TC, PATH_WS, PATH_TM = 0, 1, 2, 3, 4, 5
 
 _f = C.POINTER(C.c_float)
 _u8 = C.POINTER(C.c_uint8)
@@ -94,6 +94,7 @@ _sig("pipo_unpack_int4_g64", C.c_int, _P, _u8, _u16, C.c_int64, C.c_int64, _u16)
 _sig("pipo_linear", C.c_int, _P, C.c_int32, C.c_int32, _u16, _f, _f, C.c_int32, C.c_int32, C.c_int32, _f)
 _sig("pipo_bench_linear", C.c_int, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
      C.POINTER(C.c_double))
+_sig("pipo_probe_bulk", C.c_int, _P, C.c_int32, C.c_int32, C.POINTER(C.c_double))
 _sig("pipo_attention_decode", C.c_int, _P, _u16, _u16, _u16, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _f)
 _sig("pipo_attention_prefill", C.c_int, _P, _u16, _u16, _u16, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
      C.c_int32, C.c_int32, _f)
@@ -103,7 +104,7 @@ _sig("pipo_probe_h2d", C.c_int, _P, C.c_int64, C.c_int32, C.POINTER(C.c_double))
 EXPORTED = ["pipo_last_error", "pipo_abi_version", "pipeline_init", "pipeline_destroy", "load_layer_weights",
             "pipo_load_synthetic", "prefill", "decode_step", "decode_step_dev", "pipeline_stats",
             "pipeline_stats_reset", "pipo_stream", "pipo_kernel_stats", "pipo_quantize_int4_g64", "pipo_quantize_int4_g64_gpu",
-            "pipo_unpack_int4_g64", "pipo_linear", "pipo_bench_linear", "pipo_attention_decode", "pipo_attention_prefill", "pipo_debug_capture", "pipo_probe_h2d"]
+            "pipo_unpack_int4_g64", "pipo_linear", "pipo_bench_linear", "pipo_probe_bulk", "pipo_attention_decode", "pipo_attention_prefill", "pipo_debug_capture", "pipo_probe_h2d"]
 
 
 class PipoError(RuntimeError):
@@ -250,6 +251,12 @@ def pipo_bench_linear(ctx, wfmt, path, M, N, K, iters=20) -> float:
     us = C.c_double()
     _check(_lib.pipo_bench_linear(ctx, wfmt, path, M, N, K, iters, C.byref(us)))
     return us.value
+
+
+def pipo_probe_bulk(ctx, chunk: int, stages: int) -> float:
+    g = C.c_double()
+    _check(_lib.pipo_probe_bulk(ctx, chunk, stages, C.byref(g)))
+    return g.value
 
 
 def pipo_attention_decode(ctx, q, k, v, n_heads):

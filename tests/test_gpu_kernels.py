@@ -73,7 +73,7 @@ def test_linear_vs_oracle(env, M, N, K, wfmt):
     bias = (rng.uniform(-0.02, 0.02, N)).astype(np.float32)
     ref = _ref_linear(x, w, bias, wfmt)
     paths = [pipo.PATH_TC, pipo.PATH_GEMM] + ([pipo.PATH_GEMV] if wfmt == 1 and M <= 16 else []) + \
-        ([pipo.PATH_WS] if wfmt == 1 and M <= 128 else [])
+        ([pipo.PATH_WS] if wfmt == 1 and M <= 128 else []) + ([pipo.PATH_TM] if wfmt == 1 and M <= 64 else [])
     for path in paths:
         y = pipo.pipo_linear(pl.ctx, wfmt, path, x, w, bias)
         err = rel_inf(y, ref)
@@ -82,10 +82,10 @@ def test_linear_vs_oracle(env, M, N, K, wfmt):
         assert err < (2e-3 if wfmt == 1 else 1e-4), (path, err)
 
 
-@pytest.mark.parametrize("path", ["gemv", "gemm", "tc", "ws"])
+@pytest.mark.parametrize("path", ["gemv", "gemm", "tc", "ws", "tm"])
 def test_linear_special_cases_exact(env, path):
     pipo, pl = env
-    p = {"gemv": pipo.PATH_GEMV, "gemm": pipo.PATH_GEMM, "tc": pipo.PATH_TC, "ws": pipo.PATH_WS}[path]
+    p = {"gemv": pipo.PATH_GEMV, "gemm": pipo.PATH_GEMM, "tc": pipo.PATH_TC, "ws": pipo.PATH_WS, "tm": pipo.PATH_TM}[path]
     rng = np.random.default_rng(5)
     N, K = 200, 256
     w = (rng.standard_normal((N, K)) * 0.02).astype(np.float16).astype(np.float32)
