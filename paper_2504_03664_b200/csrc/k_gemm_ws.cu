@@ -99,11 +99,13 @@ __device__ __forceinline__ bool elect_one() {
 }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
 
-// stream-K partition of U units over G CTAs
-__device__ __forceinline__ int64_t u_begin(int64_t c, int64_t U, int64_t G) { return c * U / G; }
+// stream-K partition of U units over G CTAs (U * G < 2^32: checked by the launchers)
+__device__ __forceinline__ int64_t u_begin(int64_t c, int64_t U, int64_t G) {
+  return (int64_t)((uint32_t)c * (uint32_t)U / (uint32_t)G);
+}
 __device__ __forceinline__ int cta_of_unit(int64_t u, int64_t U, int64_t G) {
-  int64_t c = u * G / U;
-  while (c + 1 < G && u_begin(c + 1, U, G) <= u) ++c;
+  uint32_t c = (uint32_t)u * (uint32_t)G / (uint32_t)U;
+  while (c + 1 < (uint32_t)G && u_begin(c + 1, U, G) <= u) ++c;
   while (c > 0 && u_begin(c, U, G) > u) --c;
   return (int)c;
 }
@@ -358,40 +360,48 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
 // in k order (deterministic) and the fused epilogue runs.  grid = (tiles, BN/16).
 template <int BN>
 __global__ void __launch_bounds__(256) ws_reduce_kernel(LinearArgs a, int n_rt, int m_tiles, int G, int kbu) {
-  // grid = (tiles, BN/4): each thread owns one weight row of one tile and 4 columns;
-  // contributors are loaded 8 at a time (32 loads in flight), summed in k order.
+  // grid = (tiles, BN/8): each thread owns one weight row of one tile and 8 columns;
+  // contributors are loaded 4 at a time (32 loads in flight), summed in k order.
+  __shared__ int s_cf, s_cl, s_first;
   const int64_t tile = blockIdx.x;
-  const int n_kb = a.K / 64 / kbu, n_pairs = (n_rt + 1) >> 1;     // n_kb = units per tile
-  const int64_t U = (int64_t)n_pairs * m_tiles * n_kb;
-  const int cf = ws::cta_of_unit(tile * n_kb, U, G), cl = ws::cta_of_unit((tile + 1) * n_kb - 1, U, G);
+  const int n_ku = a.K / 64 / kbu, n_pairs = (n_rt + 1) >> 1;
+  const int64_t U = (int64_t)n_pairs * m_tiles * n_ku;
+  if (threadIdx.x == 0) {
+    s_cf = ws::cta_of_unit(tile * n_ku, U, G);
+    s_cl = ws::cta_of_unit((tile + 1) * n_ku - 1, U, G);
+    s_first = (int)(ws::u_begin(s_cf, U, G) / n_ku) == (int)tile;
+  }
+  __syncthreads();
+  const int cf = s_cf, cl = s_cl;
   if (cf == cl) return;                                   // fully owned: stored by the GEMM
   const int pr = (int)(tile % n_pairs), mt = (int)(tile / n_pairs);
   const int t = threadIdx.x >> 7, row = threadIdx.x & 127;
   if (2 * pr + t >= n_rt) return;
-  const int n = (2 * pr + t) * 128 + row, m0 = mt * BN, c0 = blockIdx.y * 4;
-  const int64_t first_cf = ws::u_begin(cf, U, G) / n_kb;
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int cb = cf; cb <= cl; cb += 8) {
-    float v[8][4];
+  const int n = (2 * pr + t) * 128 + row, m0 = mt * BN, c0 = blockIdx.y * 8;
+  float acc[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+  for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+  for (int cb = cf; cb <= cl; cb += 4) {
+    float v[4][8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
       const int cc = cb + q;
       if (cc <= cl) {
         // slot: the tile is cc's first tile unless cc == cf and cf started in an earlier tile
-        const int sl = 2 * cc + ((cc == cf && first_cf != tile) ? 1 : 0);
+        const int sl = 2 * cc + ((cc == cf && !s_first) ? 1 : 0);
         const float* src = a.ws + (int64_t)sl * (2 * BN * 128) + (t * BN + c0) * 128 + row;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) v[q][j] = __ldcg(src + j * 128);
+        for (int j = 0; j < 8; ++j) v[q][j] = __ldcg(src + j * 128);
       }
     }
 #pragma unroll
-    for (int q = 0; q < 8; ++q)
+    for (int q = 0; q < 4; ++q)
       if (cb + q <= cl)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[j] += v[q][j];
+        for (int j = 0; j < 8; ++j) acc[j] += v[q][j];
   }
 #pragma unroll
-  for (int j = 0; j < 4; ++j) epi_store(a.epi, m0 + c0 + j, n, acc[j]);
+  for (int j = 0; j < 8; ++j) epi_store(a.epi, m0 + c0 + j, n, acc[j]);
 }
 
 // ---------------------------------------------------------------------------------
@@ -738,13 +748,13 @@ static int run_ws(const LinearArgs& a, cudaStream_t st) {
   // at least 8 units per CTA: the per-CTA prologue / epilogue must stay amortized
   const int G = (int)std::max<int64_t>(1, std::min<int64_t>(a.num_sms, U / 8));
   const int64_t tiles = (int64_t)n_pairs * m_tiles;
-  if ((int64_t)2 * G * 2 * BN * 128 > a.ws_floats || tiles > a.n_counters) return -1;
+  if ((int64_t)2 * G * 2 * BN * 128 > a.ws_floats || tiles > a.n_counters || U * G >= (1ll << 32)) return -1;
   CUtensorMap map;   // rows >= M are out of bounds: TMA zero-fills them
   if (!make_xmap(&map, a.x, a.M, a.K, BN)) return -1;
   static const int dbg = getenv("PIPO_WS_DEBUG") ? atoi(getenv("PIPO_WS_DEBUG")) : 0;
   gemm_ws_kernel<BN><<<G, WS_THREADS, C::SMEM, st>>>(map, a, n_rt, m_tiles, dbg);
   if (dbg & 64) return 1;   // debug: main kernel only
-  dim3 rg((unsigned)tiles, BN / 4);
+  dim3 rg((unsigned)tiles, BN / 8);
   ws_reduce_kernel<BN><<<rg, 256, 0, st>>>(a, n_rt, m_tiles, G, 1);
   return 2;
 }
@@ -763,12 +773,12 @@ static int run_tm(const LinearArgs& a, cudaStream_t st) {
   const int64_t U = (int64_t)n_pairs * m_tiles * n_ku;
   const int G = (int)std::max<int64_t>(1, std::min<int64_t>(a.num_sms, U / (8 / KBU)));
   const int64_t tiles = (int64_t)n_pairs * m_tiles;
-  if ((int64_t)2 * G * 2 * BN * 128 > a.ws_floats) return -1;
+  if ((int64_t)2 * G * 2 * BN * 128 > a.ws_floats || U * G >= (1ll << 32)) return -1;
   CUtensorMap map;
   if (!make_xmap(&map, a.x, a.M, a.K, BN)) return -1;
   static const int dbg = getenv("PIPO_WS_DEBUG") ? atoi(getenv("PIPO_WS_DEBUG")) : 0;
   gemm_tm_kernel<BN, KBU><<<G, TM_THREADS, C::SMEM, st>>>(map, a, n_rt, m_tiles, G, dbg);
-  dim3 rg((unsigned)tiles, BN / 4);
+  dim3 rg((unsigned)tiles, BN / 8);
   ws_reduce_kernel<BN><<<rg, 256, 0, st>>>(a, n_rt, m_tiles, G, KBU);
   return 2;
 }
