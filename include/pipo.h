@@ -221,11 +221,17 @@ pipo_status pipo_bench_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, int32_t
  * SM, `stages`-deep mbarrier ring of `chunk`-byte requests; GB/s in *gbs. */
 pipo_status pipo_probe_bulk(pipo_ctx* ctx, int32_t chunk, int32_t stages, double* gbs);
 
+/* Kernel micro-benchmark: decode attention over device-resident synthetic q/K/V
+ * (b sequences, L positions, d = n_heads * head_dim), average microseconds per launch. */
+pipo_status pipo_bench_attention(pipo_ctx* ctx, int32_t b, int32_t L, int32_t d, int32_t n_heads, int32_t variant,
+                                 int32_t iters, double* us);
+
 /* Decode attention kernel: q [b][d] fp16 bits (pre-scaled), k/v [L][b][d] fp16
- * bits (position-major) -> o [b][d] fp32.  n_heads | d. */
+ * bits (position-major) -> o [b][d] fp32.  n_heads | d.  variant: 0 = production
+ * kernel (16-B row loads, lane groups), 1 = the v1 one-row-per-warp kernel. */
 pipo_status pipo_attention_decode(pipo_ctx* ctx, const uint16_t* q, const uint16_t* k,
                                   const uint16_t* v, int32_t b, int32_t L, int32_t d,
-                                  int32_t n_heads, float* o);
+                                  int32_t n_heads, int32_t variant, float* o);
 
 /* Prefill (causal) attention kernel: q [b][n][d] (pre-scaled) at positions
  * past..past+n-1, k/v [past+n][b][d] position-major -> o [b][n][d] fp32.

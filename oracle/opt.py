@@ -94,17 +94,40 @@ def layer_from_masters(m: dict, wfmt: str) -> LayerW:
     return LayerW(**kw)
 
 
+def kv_quant_dequant(x: np.ndarray) -> np.ndarray:
+    """INT4 KV cache (PAPER.md:96 "quantizing both weights and KV-cache to INT4";
+    reading Q17/NEXT-2): every cached row is stored with the weights' encoding —
+    groups of 64 consecutive features (inside one head for hd in {64, 128}), fp16
+    scale = absmax/7 — and read back as q * s."""
+    shp = x.shape
+    flat = np.asarray(x, dtype=np.float32).reshape(-1, shp[-1])
+    return quant.quant_dequant(flat).reshape(shp).astype(np.float64)
+
+
 def decoder_layer(h: np.ndarray, w: LayerW, kc: np.ndarray, vc: np.ndarray,
-                  past: int, n_heads: int) -> np.ndarray:
-    """h [b, n, d] float64; kc/vc [b, s_max, d] float64 caches (written at past..)."""
+                  past: int, n_heads: int, kv_int4: bool = False) -> np.ndarray:
+    """h [b, n, d] float64; kc/vc [b, s_max, d] float64 caches (written at past..).
+    kv_int4: the cache holds int4-g64 quantize->dequantize'd rows; a multi-token
+    pass (prefill) attends over its freshly computed K/V, a decode step reads the
+    cache (its own new row included) — reading Q17b in DESIGN.md."""
     b, n, d = h.shape
     hd = d // n_heads
     x = layer_norm(h, w.ln1_g, w.ln1_b)
     qkv = x @ w.w_qkv.T + w.b_qkv
     q = qkv[..., :d] * (hd ** -0.5)
-    kc[:, past:past + n] = qkv[..., d:2 * d]
-    vc[:, past:past + n] = qkv[..., 2 * d:]
-    o = attention(q, kc, vc, past, n_heads)
+    k_new, v_new = qkv[..., d:2 * d], qkv[..., 2 * d:]
+    if kv_int4:
+        kc[:, past:past + n] = kv_quant_dequant(k_new)
+        vc[:, past:past + n] = kv_quant_dequant(v_new)
+    else:
+        kc[:, past:past + n] = k_new
+        vc[:, past:past + n] = v_new
+    if kv_int4 and n > 1:
+        if past != 0:
+            raise ValueError("int4-KV multi-token pass only at past = 0 (prefill)")
+        o = attention(q, k_new, v_new, 0, n_heads)
+    else:
+        o = attention(q, kc, vc, past, n_heads)
     h = h + o @ w.w_out.T + w.b_out
     x = layer_norm(h, w.ln2_g, w.ln2_b)
     u = np.maximum(x @ w.w_fc1.T + w.b_fc1, 0.0)
@@ -122,13 +145,14 @@ class OracleOPT:
     layers: list
     s_max: int
     past: int = 0
+    kv_int4: bool = False
     kc: list = field(default_factory=list)
     vc: list = field(default_factory=list)
     capture: list = field(default_factory=list)   # per-layer outputs of the last call
 
     @classmethod
-    def from_masters(cls, n_heads, embed: dict, layer_masters: list, wfmt: str, s_max: int):
-        return cls(n_heads=n_heads,
+    def from_masters(cls, n_heads, embed: dict, layer_masters: list, wfmt: str, s_max: int, kv_int4: bool = False):
+        return cls(n_heads=n_heads, kv_int4=kv_int4,
                    tok=embed["tok"].astype(np.float64), pos=embed["pos"].astype(np.float64),
                    lnf_g=embed["lnf_g"].astype(np.float64), lnf_b=embed["lnf_b"].astype(np.float64),
                    layers=[layer_from_masters(m, wfmt) for m in layer_masters], s_max=s_max)
@@ -153,7 +177,7 @@ class OracleOPT:
         h = self.embed(ids)
         self.capture = []
         for j, w in enumerate(self.layers):
-            h = decoder_layer(h, w, self.kc[j], self.vc[j], self.past, self.n_heads)
+            h = decoder_layer(h, w, self.kc[j], self.vc[j], self.past, self.n_heads, self.kv_int4)
             self.capture.append(h.copy())
         self.past += n
         return self.head(h) if all_logits else self.head(h[:, -1])

@@ -1103,8 +1103,54 @@ pipo_status pipo_probe_bulk(pipo_ctx* ctx, int32_t chunk, int32_t stages, double
   return PIPO_OK;
 }
 
+pipo_status pipo_bench_attention(pipo_ctx* ctx, int32_t b, int32_t L, int32_t d, int32_t n_heads, int32_t variant,
+                                 int32_t iters, double* us) {
+  CHECK_CTX();
+  if (!us || b <= 0 || L <= 0 || d <= 0 || n_heads <= 0 || d % n_heads || iters <= 0)
+    return set_err(PIPO_E_INVALID_ARG, "bad bench arguments");
+  CK(cudaSetDevice(ctx->cfg.device));
+  const int64_t nq = (int64_t)b * d, nkv = (int64_t)L * b * d;
+  __half *dq = nullptr, *dk = nullptr, *dv = nullptr, *dout = nullptr;
+  float* tmp = nullptr;
+  TRY(dev_alloc(ctx, &dq, nq * 2));
+  TRY(dev_alloc(ctx, &dk, nkv * 2));
+  TRY(dev_alloc(ctx, &dv, nkv * 2));
+  TRY(dev_alloc(ctx, &dout, nq * 2));
+  TRY(dev_alloc(ctx, &tmp, std::min<int64_t>(nkv, 64ll << 20) * 4));
+  cudaStream_t st = ctx->s_comp;
+  const int64_t chunk = std::min<int64_t>(nkv, 64ll << 20);
+  for (int w = 0; w < 3; ++w) {
+    __half* dst = w == 0 ? dq : (w == 1 ? dk : dv);
+    const int64_t n = w == 0 ? nq : nkv;
+    for (int64_t off = 0; off < n; off += chunk) {
+      const int64_t c = std::min(chunk, n - off);
+      LAUNCH(launch_synth(tmp, off, c, synth_key(9, 9, w), 0, synth_scale(0, 1.0), st));
+      LAUNCH(launch_f32_to_f16(tmp, dst + off, c, st));
+    }
+  }
+  AttnArgs aa;
+  aa.q = dq; aa.kc = dk; aa.vc = dv; aa.o = dout; aa.b = b; aa.n = 1; aa.past = L - 1; aa.d = d;
+  aa.n_heads = n_heads; aa.kv_b = b; aa.ws = ctx->ws; aa.ws_floats = ctx->ws_floats; aa.num_sms = ctx->num_sms;
+  aa.use_cuda_cores = variant;
+  LAUNCH(launch_attention_decode(aa, st));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, st));
+  for (int i = 0; i < iters; ++i) LAUNCH(launch_attention_decode(aa, st));
+  CK(cudaEventRecord(e1, st));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0); cudaEventDestroy(e1);
+  cudaFree(dq); cudaFree(dk); cudaFree(dv); cudaFree(dout); cudaFree(tmp);
+  ctx->hbm_bytes -= nq * 4 + nkv * 4 + std::min<int64_t>(nkv, 64ll << 20) * 4;
+  *us = ms * 1e3 / iters;
+  return PIPO_OK;
+}
+
 pipo_status pipo_attention_decode(pipo_ctx* ctx, const uint16_t* q, const uint16_t* k, const uint16_t* v, int32_t b,
-                                  int32_t L, int32_t d, int32_t n_heads, float* o) {
+                                  int32_t L, int32_t d, int32_t n_heads, int32_t variant, float* o) {
   CHECK_CTX();
   if (!q || !k || !v || !o || b <= 0 || L <= 0 || d <= 0 || n_heads <= 0 || d % n_heads)
     return set_err(PIPO_E_INVALID_ARG, "bad attention arguments");
@@ -1124,6 +1170,7 @@ pipo_status pipo_attention_decode(pipo_ctx* ctx, const uint16_t* q, const uint16
   AttnArgs aa;
   aa.q = dq; aa.kc = dk; aa.vc = dv; aa.o = dout; aa.b = b; aa.n = 1; aa.past = L - 1; aa.d = d;
   aa.n_heads = n_heads; aa.kv_b = b; aa.ws = ctx->ws; aa.ws_floats = ctx->ws_floats; aa.num_sms = ctx->num_sms;
+  aa.use_cuda_cores = variant;
   LAUNCH(launch_attention_decode(aa, st));
   LAUNCH(launch_f16_to_f32(dout, df, nq, st));
   CK(cudaMemcpyAsync(o, df, (size_t)nq * 4, cudaMemcpyDeviceToHost, st));

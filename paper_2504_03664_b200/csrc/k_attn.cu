@@ -117,6 +117,116 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnArgs a, int n_spli
   }
 }
 
+
+// Decode v2: LPR = HD/8 lanes per K/V row (16-B loads of 8 halves), so one warp
+// instruction fetches RPW = 32/LPR rows.  Each lane group ("virtual warp" of LPR lanes)
+// runs its own online softmax over an interleaved subset of positions, 4 positions per
+// step (8 x 16-B loads in flight per lane); the NV = 4*RPW virtual warps of the CTA are
+// merged in fixed order, splits in a second kernel (deterministic).
+template <int HD>
+__global__ void __launch_bounds__(128) attn_decode_v2_kernel(AttnArgs a, int n_splits, int pos_per_split) {
+  constexpr int LPR = HD / 8, RPW = 32 / LPR, NV = 4 * RPW;
+  __shared__ float sm_m[NV], sm_l[NV];
+  __shared__ float sm_acc[NV][HD];
+  const int head = blockIdx.x, bi = blockIdx.y, split = blockIdx.z;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sub = lane / LPR, sl = lane % LPR;            // row slot within the warp, lane within row
+  const int vw = warp * RPW + sub;                          // virtual warp id 0..NV-1
+  const int L = a.past + 1;
+  const int lo = split * pos_per_split, hi = min(L, lo + pos_per_split);
+  float q[8];
+  {
+    const uint4 qr = *reinterpret_cast<const uint4*>(a.q + (int64_t)bi * a.d + head * HD + sl * 8);
+    const __half2* qh = reinterpret_cast<const __half2*>(&qr);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __half22float2(qh[e]);
+      q[2 * e] = f.x * kLog2e;
+      q[2 * e + 1] = f.y * kLog2e;
+    }
+  }
+  const int64_t pstride = (int64_t)a.kv_b * a.d;
+  const __half* kbase = a.kc + (int64_t)bi * a.d + head * HD + sl * 8;
+  const __half* vbase = a.vc + (int64_t)bi * a.d + head * HD + sl * 8;
+  float m_run = -INFINITY, l_run = 0.f, acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+  constexpr int U = 4;
+  for (int p0 = lo + vw * U; p0 < hi; p0 += NV * U) {
+    uint4 kr[U], vr[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int p = min(p0 + u, hi - 1);
+      kr[u] = ld_nc_v4(kbase + p * pstride);
+      vr[u] = ld_nc_v4(vbase + p * pstride);
+    }
+    float s[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const __half2* kh = reinterpret_cast<const __half2*>(&kr[u]);
+      float t = 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __half22float2(kh[e]);
+        t = fmaf(q[2 * e], f.x, t);
+        t = fmaf(q[2 * e + 1], f.y, t);
+      }
+      s[u] = t;
+    }
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1)
+#pragma unroll
+      for (int u = 0; u < U; ++u) s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
+    float mx = m_run;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (p0 + u >= hi) s[u] = -INFINITY;
+      mx = fmaxf(mx, s[u]);
+    }
+    const float corr = exp2f(m_run - mx);
+    l_run *= corr;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] *= corr;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const float pu = exp2f(s[u] - mx);
+      l_run += pu;
+      const __half2* vh = reinterpret_cast<const __half2*>(&vr[u]);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __half22float2(vh[e]);
+        acc[2 * e] = fmaf(pu, f.x, acc[2 * e]);
+        acc[2 * e + 1] = fmaf(pu, f.y, acc[2 * e + 1]);
+      }
+    }
+    m_run = mx;
+  }
+  if (sl == 0) { sm_m[vw] = m_run; sm_l[vw] = l_run; }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) sm_acc[vw][sl * 8 + e] = acc[e];
+  __syncthreads();
+  if (threadIdx.x < HD) {
+    const int t = threadIdx.x;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < NV; ++w) M = fmaxf(M, sm_m[w]);
+    float l = 0.f, o = 0.f;
+#pragma unroll
+    for (int w = 0; w < NV; ++w) {
+      const float f = sm_m[w] == -INFINITY ? 0.f : exp2f(sm_m[w] - M);
+      l += sm_l[w] * f;
+      o += sm_acc[w][t] * f;
+    }
+    if (n_splits == 1) {
+      a.o[(int64_t)bi * a.d + head * HD + t] = __float2half_rn(o / l);
+    } else {
+      float* part = a.ws + ((int64_t)(bi * a.n_heads + head) * n_splits + split) * (HD + 2);
+      if (t == 0) { part[0] = M; part[1] = l; }
+      part[2 + t] = o;
+    }
+  }
+}
+
 template <int HD>
 __global__ void attn_merge_kernel(AttnArgs a, int n_splits) {
   const int head = blockIdx.x, bi = blockIdx.y, t = threadIdx.x;
@@ -379,8 +489,13 @@ int launch_attention_decode(const AttnArgs& a, cudaStream_t st) {
   n_splits = (L + per - 1) / per;
   if (n_splits > 1 && (int64_t)pairs * n_splits * (hd + 2) > a.ws_floats) return -1;
   dim3 grid(a.n_heads, a.b, n_splits);
-  if (hd == 64) attn_decode_kernel<64><<<grid, 128, 0, st>>>(a, n_splits, per);
-  else attn_decode_kernel<128><<<grid, 128, 0, st>>>(a, n_splits, per);
+  if (a.use_cuda_cores) {   // v1 (one row per warp), kept for A/B
+    if (hd == 64) attn_decode_kernel<64><<<grid, 128, 0, st>>>(a, n_splits, per);
+    else attn_decode_kernel<128><<<grid, 128, 0, st>>>(a, n_splits, per);
+  } else {
+    if (hd == 64) attn_decode_v2_kernel<64><<<grid, 128, 0, st>>>(a, n_splits, per);
+    else attn_decode_v2_kernel<128><<<grid, 128, 0, st>>>(a, n_splits, per);
+  }
   if (n_splits == 1) return 1;
   dim3 g2(a.n_heads, a.b);
   if (hd == 64) attn_merge_kernel<64><<<g2, 64, 0, st>>>(a, n_splits);

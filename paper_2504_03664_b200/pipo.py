@@ -95,7 +95,9 @@ _sig("pipo_linear", C.c_int, _P, C.c_int32, C.c_int32, _u16, _f, _f, C.c_int32, 
 _sig("pipo_bench_linear", C.c_int, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
      C.POINTER(C.c_double))
 _sig("pipo_probe_bulk", C.c_int, _P, C.c_int32, C.c_int32, C.POINTER(C.c_double))
-_sig("pipo_attention_decode", C.c_int, _P, _u16, _u16, _u16, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _f)
+_sig("pipo_bench_attention", C.c_int, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+     C.POINTER(C.c_double))
+_sig("pipo_attention_decode", C.c_int, _P, _u16, _u16, _u16, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _f)
 _sig("pipo_attention_prefill", C.c_int, _P, _u16, _u16, _u16, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
      C.c_int32, C.c_int32, _f)
 _sig("pipo_debug_capture", C.c_int, _P, C.c_int32, _f)
@@ -104,7 +106,7 @@ _sig("pipo_probe_h2d", C.c_int, _P, C.c_int64, C.c_int32, C.POINTER(C.c_double))
 EXPORTED = ["pipo_last_error", "pipo_abi_version", "pipeline_init", "pipeline_destroy", "load_layer_weights",
             "pipo_load_synthetic", "prefill", "decode_step", "decode_step_dev", "pipeline_stats",
             "pipeline_stats_reset", "pipo_stream", "pipo_kernel_stats", "pipo_quantize_int4_g64", "pipo_quantize_int4_g64_gpu",
-            "pipo_unpack_int4_g64", "pipo_linear", "pipo_bench_linear", "pipo_probe_bulk", "pipo_attention_decode", "pipo_attention_prefill", "pipo_debug_capture", "pipo_probe_h2d"]
+            "pipo_unpack_int4_g64", "pipo_linear", "pipo_bench_linear", "pipo_probe_bulk", "pipo_bench_attention", "pipo_attention_decode", "pipo_attention_prefill", "pipo_debug_capture", "pipo_probe_h2d"]
 
 
 class PipoError(RuntimeError):
@@ -259,7 +261,13 @@ def pipo_probe_bulk(ctx, chunk: int, stages: int) -> float:
     return g.value
 
 
-def pipo_attention_decode(ctx, q, k, v, n_heads):
+def pipo_bench_attention(ctx, b, L, d, n_heads, variant=0, iters=10) -> float:
+    us = C.c_double()
+    _check(_lib.pipo_bench_attention(ctx, b, L, d, n_heads, variant, iters, C.byref(us)))
+    return us.value
+
+
+def pipo_attention_decode(ctx, q, k, v, n_heads, variant=0):
     q = _c(np.asarray(q, dtype=np.float16).view(np.uint16), np.uint16)
     k = _c(np.asarray(k, dtype=np.float16).view(np.uint16), np.uint16)
     v = _c(np.asarray(v, dtype=np.float16).view(np.uint16), np.uint16)
@@ -267,7 +275,7 @@ def pipo_attention_decode(ctx, q, k, v, n_heads):
     L = k.shape[0]
     o = np.empty((b, d), dtype=np.float32)
     _check(_lib.pipo_attention_decode(ctx, _ptr(q, C.c_uint16), _ptr(k, C.c_uint16), _ptr(v, C.c_uint16),
-                                      b, L, d, n_heads, _ptr(o, C.c_float)))
+                                      b, L, d, n_heads, variant, _ptr(o, C.c_float)))
     return o
 
 

@@ -113,13 +113,14 @@ def test_linear_special_cases_exact(env, path):
 
 @pytest.mark.parametrize("b,L,d,H", [(1, 1, 128, 2), (2, 7, 256, 4), (3, 65, 256, 2), (4, 300, 512, 4),
                                      (2, 544, 1024, 8), (64, 40, 512, 8)])
-def test_attention_decode_vs_oracle(env, b, L, d, H):
+@pytest.mark.parametrize("variant", [0, 1])
+def test_attention_decode_vs_oracle(env, b, L, d, H, variant):
     pipo, pl = env
     rng = np.random.default_rng(b * 1000 + L)
     q = (rng.standard_normal((b, d)) * (d // H) ** -0.5).astype(np.float16)
     k = rng.standard_normal((L, b, d)).astype(np.float16)
     v = rng.standard_normal((L, b, d)).astype(np.float16)
-    o = pipo.pipo_attention_decode(pl.ctx, q, k, v, H)
+    o = pipo.pipo_attention_decode(pl.ctx, q, k, v, H, variant)
     ref = opt.attention(q.astype(np.float64)[:, None], k.astype(np.float64).transpose(1, 0, 2),
                         v.astype(np.float64).transpose(1, 0, 2), L - 1, H)[:, 0]
     assert rel_inf(o, ref) < 2e-2

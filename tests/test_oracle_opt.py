@@ -179,3 +179,29 @@ def test_generate_prefill_then_decode_steps():
     ids, logits = opt.generate(m, synth.prompts(2, 6, TINY.vocab), 5)
     assert ids.shape == (2, 5) and len(logits) == 5
     assert m.past == 6 + 4       # prefill 6 positions, then G-1 = 4 decode steps
+
+
+def test_int4_kv_cache_semantics():
+    """INT4 KV (reading Q17b): prefill logits are untouched (fresh K/V), the cache
+    holds exactly the weight encoder's quant->dequant of the fresh rows, and a decode
+    step reads that cache; its logits stay within the 4-bit error of the fp KV path."""
+    m_fp, _, _ = _tiny_model()
+    m_q = opt.OracleOPT.from_masters(TINY.n_heads, synth.embed_masters(TINY),
+                                     [synth.layer_masters(TINY, j) for j in range(TINY.n_layers)],
+                                     "int4", 48, kv_int4=True)
+    ids = synth.prompts(2, 10, TINY.vocab)
+    a = m_fp.prefill(ids)
+    b = m_q.prefill(ids)
+    assert np.array_equal(a, b)
+    for j in range(TINY.n_layers):
+        # the fp path's cache row and the int4 path's cache row come from the same fresh K
+        assert np.array_equal(m_q.kc[j][:, :10], opt.kv_quant_dequant(m_fp.kc[j][:, :10]))
+    nxt = opt.greedy(a)
+    da = m_fp.decode(nxt)
+    db = m_q.decode(nxt)
+    rel = np.abs(da - db).max() / np.abs(da).max()
+    assert 0 < rel < 0.2
+    # one cached position per sequence: attention output = the dequantized V row
+    q = np.random.default_rng(1).standard_normal((1, 1, 64))
+    v = opt.kv_quant_dequant(np.random.default_rng(2).standard_normal((1, 1, 64)))
+    assert np.array_equal(opt.attention(q, v, v, 0, 1)[0, 0], v[0, 0])
