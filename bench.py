@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--impl", default="pipo", choices=["pipo", "reference"])
     ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
     ap.add_argument("--wfmt", default="int4", choices=["int4", "fp16"])
+    ap.add_argument("--kv-fmt", default="fp16", choices=["fp16", "int4"],
+                    help="KV cache storage (int4 = NEXT-2: PAPER.md:96 INT4 KV cache)")
     ap.add_argument("--ring", type=int, default=2)
     ap.add_argument("--chunk-mb", type=float, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -243,6 +245,7 @@ def run_pipo(args):
     cfg = pipo.make_config(s, device=local, max_batch=b, max_seq=max_seq,
                            wfmt=pipo.PIPO_W_INT4_G64 if args.wfmt == "int4" else pipo.PIPO_W_FP16,
                            weight_tier=c["weight_tier"], kv_tier=c["kv_tier"], ring_layers=args.ring,
+                           kv_fmt=pipo.PIPO_W_INT4_G64 if args.kv_fmt == "int4" else pipo.PIPO_W_FP16,
                            chunk_bytes=int(args.chunk_mb * (1 << 20)), disk_dir=disk_dir,
                            flags=pipo.PIPO_F_TIMELINE | pipo.PIPO_F_KPROF)
     t_setup = time.perf_counter()
@@ -351,7 +354,7 @@ def run_pipo(args):
                        "gen": G, "n_layers": s.n_layers, "d_model": s.d_model,
                        "parallelism": f"batch-shard x{world} (no hot-path collective)",
                        "weight_tier": ["device", "host", "disk"][c["weight_tier"]],
-                       "kv_tier": ["device", "host"][c["kv_tier"]], "ring_layers": args.ring,
+                       "kv_tier": ["device", "host"][c["kv_tier"]], "kv_fmt": args.kv_fmt, "ring_layers": args.ring,
                        "l2": "inputs larger than L2 (every step streams all layer weights through HBM)"},
             "clocks": clocks,
             "e2e": e2e,

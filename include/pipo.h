@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define PIPO_ABI_VERSION 1
+#define PIPO_ABI_VERSION 2
 
 typedef enum {
   PIPO_OK = 0,
@@ -78,6 +78,10 @@ typedef struct {
   int32_t wfmt;          /* pipo_wfmt for the four decoder linear weights            */
   int32_t weight_tier;   /* pipo_tier: where decoder-layer weights live              */
   int32_t kv_tier;       /* PIPO_TIER_DEVICE or PIPO_TIER_HOST         */
+  int32_t kv_fmt;        /* PIPO_W_FP16 or PIPO_W_INT4_G64: KV cache storage ("quantizing both
+                            weights and KV-cache to INT4").  int4: each cached
+                            row is stored in 64-feature groups with an fp16 scale; prefill
+                            attends over its fresh fp16 K/V, decode reads the int4 cache   */
   int32_t ring_layers;   /* HBM weight ring depth in layers: >= 2 = performance-optimized
                             pipeline (preload next layer); 1 = memory-
                             efficient (one layer resident). 0 -> 2    */
@@ -228,7 +232,7 @@ pipo_status pipo_bench_attention(pipo_ctx* ctx, int32_t b, int32_t L, int32_t d,
 
 /* Decode attention kernel: q [b][d] fp16 bits (pre-scaled), k/v [L][b][d] fp16
  * bits (position-major) -> o [b][d] fp32.  n_heads | d.  variant: 0 = production
- * kernel (16-B row loads, lane groups), 1 = the v1 one-row-per-warp kernel. */
+ * kernel (one K/V row per warp), 1 = the lane-group variant (16-B row loads). */
 pipo_status pipo_attention_decode(pipo_ctx* ctx, const uint16_t* q, const uint16_t* k,
                                   const uint16_t* v, int32_t b, int32_t L, int32_t d,
                                   int32_t n_heads, int32_t variant, float* o);

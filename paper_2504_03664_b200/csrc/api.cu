@@ -185,9 +185,23 @@ const __half* vec_ptr(const pipo_ctx* c, const uint8_t* blob, int v) {
 bool streamed(const pipo_ctx* c) { return c->weight_tier != PIPO_TIER_DEVICE; }
 bool host_kv(const pipo_ctx* c) { return c->kv_tier == PIPO_TIER_HOST; }
 
-__half* kv_ptr(pipo_ctx* c, int layer, int which, int64_t G) {
-  if (host_kv(c)) return c->kv_slot + ((G % c->R) * 2 + which) * c->kv_elems;
-  return c->kv_dev + ((int64_t)layer * 2 + which) * c->kv_elems;
+uint8_t* kv_region(pipo_ctx* c, int layer, int which, int64_t G) {
+  if (host_kv(c)) return c->kv_slot + ((G % c->R) * 2 + which) * c->kv_tensor_bytes;
+  return c->kv_dev + ((int64_t)layer * 2 + which) * c->kv_tensor_bytes;
+}
+uint8_t* kv_host_region(pipo_ctx* c, int layer, int which) {
+  return c->kv_host + ((int64_t)layer * 2 + which) * c->kv_tensor_bytes;
+}
+// byte ranges (offset, size) of positions [p0, p0 + np) inside a region, current batch
+int kv_ranges(const pipo_ctx* c, int64_t p0, int64_t np, int64_t* off, int64_t* bytes) {
+  const int64_t row = (int64_t)c->b_cur * c->d;   // elements per position
+  if (c->kv_fmt == PIPO_W_FP16) {
+    off[0] = p0 * row * 2; bytes[0] = np * row * 2;
+    return 1;
+  }
+  off[0] = p0 * row / 2; bytes[0] = np * row / 2;
+  off[1] = c->kv_codes_cap + p0 * (row / 64) * 2; bytes[1] = np * (row / 64) * 2;
+  return 2;
 }
 
 // H2D copy of one contiguous byte range in chunks (blockwise transfer)
@@ -219,13 +233,14 @@ pipo_status enqueue_copy(pipo_ctx* ctx, int64_t G, int64_t kv_pos) {
       // KV load advanced with the layer's MHA weights (reading Q6)
       if (G >= ctx->R) CK(cudaStreamWaitEvent(ctx->s_copy, ctx->ev_kv_free[slot], 0));
       CK(cudaStreamWaitEvent(ctx->s_copy, ctx->ev_saved[j], 0));   // A6 fence
-      const int64_t n = kv_pos * ctx->b_cur * ctx->d;
-      if (n > 0) {
-        for (int w = 0; w < 2; ++w) {
-          const __half* src = ctx->kv_host + ((int64_t)j * 2 + w) * ctx->kv_elems;
-          TRY(copy_chunks(ctx, kv_ptr(ctx, j, w, G), src, n * 2));
-        }
-        bytes += 2 * n * 2;
+      if (kv_pos > 0) {
+        int64_t off[2], nb[2];
+        const int nr = kv_ranges(ctx, 0, kv_pos, off, nb);
+        for (int w = 0; w < 2; ++w)
+          for (int r = 0; r < nr; ++r) {
+            TRY(copy_chunks(ctx, kv_region(ctx, j, w, G) + off[r], kv_host_region(ctx, j, w) + off[r], nb[r]));
+            bytes += nb[r];
+          }
       }
       ctx->kv_load_past[slot] = kv_pos;
       CK(cudaEventRecord(ctx->ev_ready[slot][4], ctx->s_copy));
@@ -268,15 +283,20 @@ pipo_status enqueue_kv_only(pipo_ctx* ctx, int64_t G, int64_t kv_pos) {
   CK(cudaStreamWaitEvent(ctx->s_copy, ctx->ev_saved[j], 0));
   cudaEvent_t t0 = nullptr;
   TRY(span_begin(ctx, ctx->s_copy, &t0));
-  const int64_t n = kv_pos * ctx->b_cur * ctx->d;
-  for (int w = 0; w < 2 && n > 0; ++w) {
-    const __half* src = ctx->kv_host + ((int64_t)j * 2 + w) * ctx->kv_elems;
-    TRY(copy_chunks(ctx, kv_ptr(ctx, j, w, G), src, n * 2));
+  int64_t moved = 0;
+  if (kv_pos > 0) {
+    int64_t off[2], nb[2];
+    const int nr = kv_ranges(ctx, 0, kv_pos, off, nb);
+    for (int w = 0; w < 2; ++w)
+      for (int r = 0; r < nr; ++r) {
+        TRY(copy_chunks(ctx, kv_region(ctx, j, w, G) + off[r], kv_host_region(ctx, j, w) + off[r], nb[r]));
+        moved += nb[r];
+      }
   }
   ctx->kv_load_past[slot] = kv_pos;
   CK(cudaEventRecord(ctx->ev_ready[slot][4], ctx->s_copy));
-  ctx->h2d_bytes += n > 0 ? 2 * n * 2 : 0;
-  TRY(span_end(ctx, ctx->s_copy, t0, 0, n > 0 ? 4 * n : 0));
+  ctx->h2d_bytes += moved;
+  TRY(span_end(ctx, ctx->s_copy, t0, 0, moved));
   return PIPO_OK;
 }
 
@@ -313,8 +333,11 @@ pipo_status forward(pipo_ctx* ctx, int b, int n, int past, bool want_logits) {
     }
     const uint8_t* blob = streamed(ctx) ? ctx->ring + (int64_t)slot * ctx->layer_bytes
                                         : ctx->dev_store + (int64_t)j * ctx->layer_bytes;
-    __half* kc = kv_ptr(ctx, j, 0, G);
-    __half* vc = kv_ptr(ctx, j, 1, G);
+    uint8_t* kreg = kv_region(ctx, j, 0, G);
+    uint8_t* vreg = kv_region(ctx, j, 1, G);
+    const bool q4 = ctx->kv_fmt == PIPO_W_INT4_G64;
+    __half* kc = q4 ? ctx->kv_stage : reinterpret_cast<__half*>(kreg);
+    __half* vc = q4 ? ctx->kv_stage + d : reinterpret_cast<__half*>(vreg);
     if (host_kv(ctx) && n == 1 && ctx->kv_load_past[slot] != past)
       return set_err(PIPO_E_STATE, "internal: KV prefetch range mismatch");
     cudaEvent_t t0;
@@ -328,15 +351,31 @@ pipo_status forward(pipo_ctx* ctx, int b, int n, int past, bool want_logits) {
     la.epi.kind = EPI_QKV; la.epi.bias = vec_ptr(ctx, blob, V_B_QKV); la.epi.M = M; la.epi.N = 3 * d;
     la.epi.q = ctx->q; la.epi.kc = kc; la.epi.vc = vc; la.epi.d = d; la.epi.n_tok = n; la.epi.past = past;
     la.epi.kv_b = b; la.epi.qscale = 1.0f / sqrtf((float)ctx->hd);
+    la.epi.kv_rowmajor = q4 ? 1 : 0;
     TRY(run_linear(ctx, la, PATH_AUTO, lin_cls));
     aa.q = ctx->q; aa.kc = kc; aa.vc = vc; aa.o = ctx->xa;
+    aa.kv_pos_stride = 0; aa.kv_b_stride = 0; aa.kq = nullptr;
+    if (q4) {
+      // append: quantize the fresh rows into the int4 cache (codes + fp16 scales)
+      LAUNCH(launch_kv_quant(ctx->kv_stage, b, n, past, d, b, kreg,
+                             reinterpret_cast<__half*>(kreg + ctx->kv_codes_cap), vreg,
+                             reinterpret_cast<__half*>(vreg + ctx->kv_codes_cap), cs));
+      if (n == 1) {
+        aa.kq = kreg; aa.ks = reinterpret_cast<const __half*>(kreg + ctx->kv_codes_cap);
+        aa.vq = vreg; aa.vs = reinterpret_cast<const __half*>(vreg + ctx->kv_codes_cap);
+      } else {
+        aa.kv_pos_stride = 2 * (int64_t)d;       // prefill attends over the fresh fp16 rows
+        aa.kv_b_stride = (int64_t)n * 2 * d;
+      }
+    }
     {
       cudaEvent_t ka = nullptr;
       TRY(kbegin(ctx, &ka));
-      if (n == 1) LAUNCH(launch_attention_decode(aa, cs));
+      if (n == 1 && q4) LAUNCH(launch_attention_decode_q4(aa, cs));
+      else if (n == 1) LAUNCH(launch_attention_decode(aa, cs));
       else LAUNCH(launch_attention_prefill(aa, cs));
       const double L = past + n;
-      const double kvb = n == 1 ? 2.0 * L * b * d * 2 : 2.0 * L * b * d * 2;
+      const double kvb = 2.0 * L * b * d * (q4 && n == 1 ? (0.5 + 2.0 / 64) : 2.0);
       const double fl = n == 1 ? 4.0 * b * d * L : 2.0 * b * d * (double)n * (past + (n + 1) / 2.0);
       TRY(kend(ctx, ka, n == 1 ? PIPO_K_ATTN_DECODE : PIPO_K_ATTN_PREFILL, kvb + 4.0 * M * d, fl));
     }
@@ -347,15 +386,18 @@ pipo_status forward(pipo_ctx* ctx, int b, int n, int past, bool want_logits) {
       CK(cudaStreamWaitEvent(ctx->s_save, ctx->ev_attn[slot], 0));
       cudaEvent_t s0;
       TRY(span_begin(ctx, ctx->s_save, &s0));
-      const int64_t off = (int64_t)past * b * d, cnt = (int64_t)n * b * d;
-      for (int w = 0; w < 2; ++w) {
-        __half* dst = ctx->kv_host + ((int64_t)j * 2 + w) * ctx->kv_elems + off;
-        CK(cudaMemcpyAsync(dst, kv_ptr(ctx, j, w, G) + off, (size_t)cnt * 2, cudaMemcpyDeviceToHost, ctx->s_save));
-      }
-      ctx->d2h_bytes += 2 * cnt * 2;
+      int64_t off[2], nb[2], saved = 0;
+      const int nr = kv_ranges(ctx, past, n, off, nb);
+      for (int w = 0; w < 2; ++w)
+        for (int r = 0; r < nr; ++r) {
+          CK(cudaMemcpyAsync(kv_host_region(ctx, j, w) + off[r], kv_region(ctx, j, w, G) + off[r], (size_t)nb[r],
+                             cudaMemcpyDeviceToHost, ctx->s_save));
+          saved += nb[r];
+        }
+      ctx->d2h_bytes += saved;
       CK(cudaEventRecord(ctx->ev_saved[j], ctx->s_save));
       CK(cudaEventRecord(ctx->ev_kv_free[slot], ctx->s_save));
-      TRY(span_end(ctx, ctx->s_save, s0, 2, 2 * cnt * 2));
+      TRY(span_end(ctx, ctx->s_save, s0, 2, saved));
     }
     // ---- MHA out-proj + residual (seg 1) ----
     if (streamed(ctx)) CK(cudaStreamWaitEvent(cs, ctx->ev_ready[slot][1], 0));
@@ -488,6 +530,7 @@ pipo_status pipeline_init(const pipo_config* cfg, pipo_ctx** out) {
   if (c.wfmt != PIPO_W_FP16 && c.wfmt != PIPO_W_INT4_G64) return set_err(PIPO_E_INVALID_ARG, "bad wfmt");
   if (c.weight_tier < 0 || c.weight_tier > 2) return set_err(PIPO_E_INVALID_ARG, "bad weight_tier");
   if (c.kv_tier != PIPO_TIER_DEVICE && c.kv_tier != PIPO_TIER_HOST) return set_err(PIPO_E_INVALID_ARG, "bad kv_tier");
+  if (c.kv_fmt != PIPO_W_FP16 && c.kv_fmt != PIPO_W_INT4_G64) return set_err(PIPO_E_INVALID_ARG, "bad kv_fmt");
   if (c.weight_tier == PIPO_TIER_DISK && (!c.disk_dir || !c.disk_dir[0]))
     return set_err(PIPO_E_INVALID_ARG, "disk tier needs disk_dir");
   int ndev = 0;
@@ -503,7 +546,7 @@ pipo_status pipeline_init(const pipo_config* cfg, pipo_ctx** out) {
   ctx->cfg.disk_dir = nullptr;
   ctx->d = c.d_model; ctx->l = c.n_layers; ctx->H = c.n_heads; ctx->F = c.ffn_dim; ctx->V = c.vocab;
   ctx->hd = hd; ctx->max_b = c.max_batch; ctx->max_s = c.max_seq; ctx->wfmt = c.wfmt;
-  ctx->weight_tier = c.weight_tier; ctx->kv_tier = c.kv_tier;
+  ctx->weight_tier = c.weight_tier; ctx->kv_tier = c.kv_tier; ctx->kv_fmt = c.kv_fmt;
   ctx->R = c.ring_layers > 0 ? c.ring_layers : 2;
   ctx->R = std::min({ctx->R, kMaxRing, ctx->l});
   if (host_kv(ctx) && ctx->R < 2 && ctx->l >= 2) ctx->R = 2;
@@ -569,12 +612,18 @@ pipo_status pipeline_init(const pipo_config* cfg, pipo_ctx** out) {
     }
   }
   // KV cache
-  ctx->kv_elems = (int64_t)ctx->max_s * ctx->max_b * ctx->d;
-  if (host_kv(ctx)) {
-    TRYI(host_alloc(ctx, &ctx->kv_host, (int64_t)ctx->l * 2 * ctx->kv_elems * 2));
-    TRYI(dev_alloc(ctx, &ctx->kv_slot, (int64_t)ctx->R * 2 * ctx->kv_elems * 2));
+  const int64_t kv_elems = (int64_t)ctx->max_s * ctx->max_b * ctx->d;
+  if (ctx->kv_fmt == PIPO_W_INT4_G64) {
+    ctx->kv_codes_cap = round_up(kv_elems / 2, 256);
+    ctx->kv_tensor_bytes = round_up(ctx->kv_codes_cap + kv_elems / 64 * 2, 4096);
   } else {
-    TRYI(dev_alloc(ctx, &ctx->kv_dev, (int64_t)ctx->l * 2 * ctx->kv_elems * 2));
+    ctx->kv_tensor_bytes = kv_elems * 2;
+  }
+  if (host_kv(ctx)) {
+    TRYI(host_alloc(ctx, &ctx->kv_host, (int64_t)ctx->l * 2 * ctx->kv_tensor_bytes));
+    TRYI(dev_alloc(ctx, &ctx->kv_slot, (int64_t)ctx->R * 2 * ctx->kv_tensor_bytes));
+  } else {
+    TRYI(dev_alloc(ctx, &ctx->kv_dev, (int64_t)ctx->l * 2 * ctx->kv_tensor_bytes));
   }
   // activations
   ctx->rows_cap = (int64_t)ctx->max_b * ctx->max_s;
@@ -594,7 +643,8 @@ pipo_status pipeline_init(const pipo_config* cfg, pipo_ctx** out) {
   CKI(cudaMemset(ctx->counters, 0, (size_t)ctx->n_counters * 4));
   TRYI(dev_alloc(ctx, &ctx->quant_bad, 4));
   CKI(cudaMemset(ctx->kv_dev ? (void*)ctx->kv_dev : (void*)ctx->kv_slot, 0,
-                 (size_t)(host_kv(ctx) ? ctx->R : ctx->l) * 2 * ctx->kv_elems * 2));
+                 (size_t)(host_kv(ctx) ? ctx->R : ctx->l) * 2 * ctx->kv_tensor_bytes));
+  if (ctx->kv_fmt == PIPO_W_INT4_G64) TRYI(dev_alloc(ctx, &ctx->kv_stage, ctx->rows_cap * 2 * ctx->d * 2));
   CKI(cudaDeviceSynchronize());
   *out = ctx;
   return PIPO_OK;
@@ -608,7 +658,7 @@ void pipeline_destroy(pipo_ctx* ctx) {
   cudaDeviceSynchronize();
   cudaGetLastError();
   if (ctx->disk) disk_close(ctx);
-  void* dev[] = {ctx->tok, ctx->pos, ctx->lnf_g, ctx->lnf_b, ctx->dev_store, ctx->ring, ctx->kv_dev, ctx->kv_slot,
+  void* dev[] = {ctx->tok, ctx->pos, ctx->lnf_g, ctx->lnf_b, ctx->dev_store, ctx->ring, ctx->kv_dev, ctx->kv_slot, ctx->kv_stage,
                  ctx->h, ctx->xa, ctx->q, ctx->u, ctx->logits, ctx->ids, ctx->next, ctx->ws, ctx->counters,
                  ctx->quant_bad, ctx->cap_dev};
   for (void* p : dev)

@@ -61,10 +61,15 @@ struct pipo_ctx {
   pipo::DiskTier* disk = nullptr;
 
   // KV cache: position-major [pos][b][d] per (layer, K/V)
-  int64_t kv_elems = 0;            // max_s * max_b * d per tensor
-  __half* kv_dev = nullptr;        // DEVICE kv tier: [l][2][kv_elems]
-  __half* kv_host = nullptr;       // HOST kv tier (pinned): [l][2][kv_elems]
-  __half* kv_slot = nullptr;       // HOST kv tier: [R][2][kv_elems] staging in HBM
+  // one region per (layer, K/V): fp16 [pos][b][d], or int4 codes [pos][b][d/2] followed
+  // (at kv_codes_cap) by fp16 scales [pos][b][d/64]
+  int kv_fmt = 0;
+  int64_t kv_tensor_bytes = 0;     // bytes per (layer, K/V) region
+  int64_t kv_codes_cap = 0;        // int4: byte offset of the scales inside a region
+  uint8_t* kv_dev = nullptr;       // DEVICE kv tier: [l][2] regions
+  uint8_t* kv_host = nullptr;      // HOST kv tier (pinned): [l][2] regions
+  uint8_t* kv_slot = nullptr;      // HOST kv tier: [R][2] staging regions in HBM
+  __half* kv_stage = nullptr;      // int4 KV: fresh fp16 K/V rows [rows][2d] of the current pass
 
   // activations
   int64_t rows_cap = 0;

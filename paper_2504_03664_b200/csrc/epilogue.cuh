@@ -15,7 +15,7 @@ __device__ __forceinline__ void epi_store(const EpiParams& e, int m, int n, floa
       if (n < e.d) {
         e.q[(int64_t)m * e.d + n] = __float2half_rn(v * e.qscale);
       } else {
-        const int64_t off = ((int64_t)(e.past + t) * e.kv_b + bi) * e.d;
+        const int64_t off = e.kv_rowmajor ? (int64_t)m * 2 * e.d : ((int64_t)(e.past + t) * e.kv_b + bi) * e.d;
         if (n < 2 * e.d) e.kc[off + n - e.d] = __float2half_rn(v);
         else e.vc[off + n - 2 * e.d] = __float2half_rn(v);
       }

@@ -16,10 +16,17 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "layout.h"
 
 namespace pipo {
 
 constexpr float kLog2e = 1.4426950408889634f;
+
+// element strides of the K/V source: position-major cache by default
+__device__ __forceinline__ int64_t kv_pstride(const AttnArgs& a) {
+  return a.kv_pos_stride ? a.kv_pos_stride : (int64_t)a.kv_b * a.d;
+}
+__device__ __forceinline__ int64_t kv_bstride(const AttnArgs& a) { return a.kv_b_stride ? a.kv_b_stride : a.d; }
 
 template <int E>
 __device__ __forceinline__ void load_row(const __half* p, float* out) {
@@ -47,9 +54,9 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnArgs a, int n_spli
   load_row<E>(a.q + (int64_t)bi * a.d + head * HD + lane * E, q);
 #pragma unroll
   for (int e = 0; e < E; ++e) q[e] *= kLog2e;   // scores in log2 units
-  const int64_t pstride = (int64_t)a.kv_b * a.d;
-  const __half* kbase = a.kc + (int64_t)bi * a.d + head * HD + lane * E;
-  const __half* vbase = a.vc + (int64_t)bi * a.d + head * HD + lane * E;
+  const int64_t pstride = kv_pstride(a);
+  const __half* kbase = a.kc + (int64_t)bi * kv_bstride(a) + head * HD + lane * E;
+  const __half* vbase = a.vc + (int64_t)bi * kv_bstride(a) + head * HD + lane * E;
   float m_run = -INFINITY, l_run = 0.f, acc[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) acc[e] = 0.f;
@@ -145,14 +152,17 @@ __global__ void __launch_bounds__(128) attn_decode_v2_kernel(AttnArgs a, int n_s
       q[2 * e + 1] = f.y * kLog2e;
     }
   }
-  const int64_t pstride = (int64_t)a.kv_b * a.d;
-  const __half* kbase = a.kc + (int64_t)bi * a.d + head * HD + sl * 8;
-  const __half* vbase = a.vc + (int64_t)bi * a.d + head * HD + sl * 8;
+  const int64_t pstride = kv_pstride(a);
+  const __half* kbase = a.kc + (int64_t)bi * kv_bstride(a) + head * HD + sl * 8;
+  const __half* vbase = a.vc + (int64_t)bi * kv_bstride(a) + head * HD + sl * 8;
   float m_run = -INFINITY, l_run = 0.f, acc[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) acc[e] = 0.f;
   constexpr int U = 4;
-  for (int p0 = lo + vw * U; p0 < hi; p0 += NV * U) {
+  // the trip count must be warp-uniform (full-mask shuffles): loop on the warp's first
+  // position, each lane group masks its own positions past `hi`
+  for (int pw = lo + warp * RPW * U; pw < hi; pw += NV * U) {
+    const int p0 = pw + sub * U;
     uint4 kr[U], vr[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -183,13 +193,13 @@ __global__ void __launch_bounds__(128) attn_decode_v2_kernel(AttnArgs a, int n_s
       if (p0 + u >= hi) s[u] = -INFINITY;
       mx = fmaxf(mx, s[u]);
     }
-    const float corr = exp2f(m_run - mx);
+    const float corr = mx == -INFINITY ? 1.f : exp2f(m_run - mx);   // group may have no live position yet
     l_run *= corr;
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[e] *= corr;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const float pu = exp2f(s[u] - mx);
+      const float pu = s[u] == -INFINITY ? 0.f : exp2f(s[u] - mx);
       l_run += pu;
       const __half2* vh = reinterpret_cast<const __half2*>(&vr[u]);
 #pragma unroll
@@ -262,9 +272,9 @@ __global__ void __launch_bounds__(256) attn_prefill_kernel(AttnArgs a) {
 #pragma unroll
     for (int e = 0; e < E; ++e) q[u][e] *= kLog2e;
   }
-  const int64_t pstride = (int64_t)a.kv_b * a.d;
-  const __half* kbase = a.kc + (int64_t)bi * a.d + head * HD + lane * E;
-  const __half* vbase = a.vc + (int64_t)bi * a.d + head * HD + lane * E;
+  const int64_t pstride = kv_pstride(a);
+  const __half* kbase = a.kc + (int64_t)bi * kv_bstride(a) + head * HD + lane * E;
+  const __half* vbase = a.vc + (int64_t)bi * kv_bstride(a) + head * HD + lane * E;
   float m_run[4], l_run[4], acc[4][E];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
@@ -332,7 +342,7 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(AttnArgs a) {
   const int L = a.past + a.n;
   const int kv_end = min(L, a.past + min(a.n, q0 + 64));     // exclusive, causal bound of this CTA
   const int n_kv = (kv_end + 63) / 64;
-  const int64_t pstride = (int64_t)a.kv_b * a.d;
+  const int64_t pstride = kv_pstride(a), bstride = kv_bstride(a);
   constexpr int CH = HD / 8;                 // 16-B chunks per row
 
   for (int c = tid; c < 64 * CH; c += 128) {
@@ -343,7 +353,7 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(AttnArgs a) {
   auto load_kv = [&](int j, int buf) {
     for (int c = tid; c < 64 * CH; c += 128) {
       const int r = c / CH, ch = c % CH, p = j * 64 + r;
-      const int64_t off = (int64_t)min(p, L - 1) * pstride + (int64_t)bi * a.d + head * HD + ch * 8;
+      const int64_t off = (int64_t)min(p, L - 1) * pstride + (int64_t)bi * bstride + head * HD + ch * 8;
       const int bytes = p < L ? 16 : 0;
       cp_async16(sK + (buf * 64 + r) * KP + ch * 8, a.kc + off, bytes);
       cp_async16(sV + (buf * 64 + r) * KP + ch * 8, a.vc + off, bytes);
@@ -475,6 +485,207 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(AttnArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------------
+// INT4 KV cache (NEXT-2; "quantizing both weights and KV-cache to INT4").
+// Cache rows use the weights' encoding: 64-feature groups, fp16 scale = absmax/7,
+// codes stored offset-binary in the fast nibble order (layout.h) so dequant8 applies.
+
+// one thread per (row, K|V, group): fresh fp16 K/V from the staging buffer -> cache
+__global__ void kv_quant_kernel(const __half* staging, int b, int n, int past, int d, int kv_b, uint8_t* kq,
+                                __half* ks, uint8_t* vq, __half* vs) {
+  const int ng = d / 64;
+  const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi >= (int64_t)b * n * 2 * ng) return;
+  const int g = (int)(gi % ng);
+  const int w = (int)((gi / ng) % 2);
+  const int64_t m = gi / (2 * ng);
+  const int bi = (int)(m / n), t = (int)(m % n);
+  const __half* src = staging + m * 2 * d + w * d + g * 64;
+  float x[64];
+  float amax = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint4 r = *reinterpret_cast<const uint4*>(src + 8 * i);
+    const __half2* h = reinterpret_cast<const __half2*>(&r);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __half22float2(h[j]);
+      x[8 * i + 2 * j] = f.x;
+      x[8 * i + 2 * j + 1] = f.y;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 64; ++i) amax = fmaxf(amax, fabsf(x[i]));
+  const __half s16 = __float2half_rn(__fdiv_rn(amax, 7.0f));
+  const float sc = __half2float(s16);
+  int q[64];
+#pragma unroll
+  for (int i = 0; i < 64; ++i) q[i] = sc != 0.f ? (int)fminf(fmaxf(rintf(__fdiv_rn(x[i], sc)), -8.f), 7.f) : 0;
+  const int64_t row = (int64_t)(past + t) * kv_b + bi;
+  uint8_t* codes = (w == 0 ? kq : vq) + row * (d / 2) + g * 32;
+  __half* scales = (w == 0 ? ks : vs) + row * ng + g;
+  uint32_t words[8];
+#pragma unroll
+  for (int wi = 0; wi < 8; ++wi) words[wi] = pack_tiled_word(q + 8 * wi);
+  uint4* cd = reinterpret_cast<uint4*>(codes);
+  cd[0] = make_uint4(words[0], words[1], words[2], words[3]);
+  cd[1] = make_uint4(words[4], words[5], words[6], words[7]);
+  *scales = s16;
+}
+
+int launch_kv_quant(const __half* staging, int b, int n, int past, int d, int kv_b, uint8_t* kq, __half* ks,
+                    uint8_t* vq, __half* vs, cudaStream_t st) {
+  if (d % 64) return -1;
+  const int64_t total = (int64_t)b * n * 2 * (d / 64);
+  kv_quant_kernel<<<(unsigned)((total + 127) / 128), 128, 0, st>>>(staging, b, n, past, d, kv_b, kq, ks, vq, vs);
+  return 1;
+}
+
+// Decode attention over the int4 cache, "directly on 4-bit": a lane
+// owns 16 features (two 8-code words) of one row; q.k = s * sum(q_i * c_i) with the
+// exact integer codes, and p*s scales the V codes once per row.  LPR = HD/16 lanes per
+// row, lane groups run independent online softmaxes (as in attn_decode_v2_kernel).
+template <int HD>
+__global__ void __launch_bounds__(128) attn_decode_q4_kernel(AttnArgs a, int n_splits, int pos_per_split) {
+  constexpr int LPR = HD / 16, RPW = 32 / LPR, NV = 4 * RPW;
+  __shared__ float sm_m[NV], sm_l[NV];
+  __shared__ float sm_acc[NV][HD];
+  const int head = blockIdx.x, bi = blockIdx.y, split = blockIdx.z;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sub = lane / LPR, sl = lane % LPR;
+  const int vw = warp * RPW + sub;
+  const int L = a.past + 1;
+  const int lo = split * pos_per_split, hi = min(L, lo + pos_per_split);
+  float q[16];
+  {
+    const __half* qp = a.q + (int64_t)bi * a.d + head * HD + sl * 16;
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const uint4 qr = *reinterpret_cast<const uint4*>(qp + 8 * h2);
+      const __half2* qh = reinterpret_cast<const __half2*>(&qr);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __half22float2(qh[e]);
+        q[8 * h2 + 2 * e] = f.x * kLog2e;
+        q[8 * h2 + 2 * e + 1] = f.y * kLog2e;
+      }
+    }
+  }
+  const int ng = a.d / 64;
+  const int64_t prow = (int64_t)a.kv_b;                      // rows per position
+  const int64_t row0 = bi;
+  const int cofs = head * (HD / 2) + sl * 8;                 // byte offset of this lane's 16 codes
+  const int gofs = head * (HD / 64) + (sl * 16) / 64;        // its group index
+  const __half2 one = __half2half2(__float2half_rn(1.f));
+  float m_run = -INFINITY, l_run = 0.f, acc[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) acc[e] = 0.f;
+  constexpr int U = 4;
+  for (int pw = lo + warp * RPW * U; pw < hi; pw += NV * U) {
+    const int p0 = pw + sub * U;
+    uint2 kc[U], vc[U];
+    float ksc[U], vsc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t row = (int64_t)min(p0 + u, hi - 1) * prow + row0;
+      kc[u] = *reinterpret_cast<const uint2*>(a.kq + row * (a.d / 2) + cofs);
+      vc[u] = *reinterpret_cast<const uint2*>(a.vq + row * (a.d / 2) + cofs);
+      ksc[u] = __half2float(a.ks[row * ng + gofs]);
+      vsc[u] = __half2float(a.vs[row * ng + gofs]);
+    }
+    float s[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      __half2 c[8];
+      dequant8(kc[u].x, one, c);
+      dequant8(kc[u].y, one, c + 4);
+      float t = 0.f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float2 f = __half22float2(c[e]);
+        t = fmaf(q[2 * e], f.x, t);
+        t = fmaf(q[2 * e + 1], f.y, t);
+      }
+      s[u] = t * ksc[u];
+    }
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1)
+#pragma unroll
+      for (int u = 0; u < U; ++u) s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
+    float mx = m_run;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (p0 + u >= hi) s[u] = -INFINITY;
+      mx = fmaxf(mx, s[u]);
+    }
+    const float corr = mx == -INFINITY ? 1.f : exp2f(m_run - mx);
+    l_run *= corr;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) acc[e] *= corr;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const float pu = s[u] == -INFINITY ? 0.f : exp2f(s[u] - mx);
+      l_run += pu;
+      const float ps = pu * vsc[u];
+      __half2 c[8];
+      dequant8(vc[u].x, one, c);
+      dequant8(vc[u].y, one, c + 4);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float2 f = __half22float2(c[e]);
+        acc[2 * e] = fmaf(ps, f.x, acc[2 * e]);
+        acc[2 * e + 1] = fmaf(ps, f.y, acc[2 * e + 1]);
+      }
+    }
+    m_run = mx;
+  }
+  if (sl == 0) { sm_m[vw] = m_run; sm_l[vw] = l_run; }
+#pragma unroll
+  for (int e = 0; e < 16; ++e) sm_acc[vw][sl * 16 + e] = acc[e];
+  __syncthreads();
+  if (threadIdx.x < HD) {
+    const int t = threadIdx.x;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < NV; ++w) M = fmaxf(M, sm_m[w]);
+    float l = 0.f, o = 0.f;
+#pragma unroll
+    for (int w = 0; w < NV; ++w) {
+      const float f = sm_m[w] == -INFINITY ? 0.f : exp2f(sm_m[w] - M);
+      l += sm_l[w] * f;
+      o += sm_acc[w][t] * f;
+    }
+    if (n_splits == 1) {
+      a.o[(int64_t)bi * a.d + head * HD + t] = __float2half_rn(o / l);
+    } else {
+      float* part = a.ws + ((int64_t)(bi * a.n_heads + head) * n_splits + split) * (HD + 2);
+      if (t == 0) { part[0] = M; part[1] = l; }
+      part[2 + t] = o;
+    }
+  }
+}
+
+int launch_attention_decode_q4(const AttnArgs& a, cudaStream_t st) {
+  const int hd = a.d / a.n_heads;
+  if (hd != 64 && hd != 128) return -1;
+  const int L = a.past + 1;
+  const int pairs = a.b * a.n_heads;
+  const int target = a.num_sms * 72;
+  int n_splits = pairs >= target ? 1 : (target + pairs - 1) / pairs;
+  n_splits = max(1, min(n_splits, (L + 63) / 64));
+  const int per = (L + n_splits - 1) / n_splits;
+  n_splits = (L + per - 1) / per;
+  if (n_splits > 1 && (int64_t)pairs * n_splits * (hd + 2) > a.ws_floats) return -1;
+  dim3 grid(a.n_heads, a.b, n_splits);
+  if (hd == 64) attn_decode_q4_kernel<64><<<grid, 128, 0, st>>>(a, n_splits, per);
+  else attn_decode_q4_kernel<128><<<grid, 128, 0, st>>>(a, n_splits, per);
+  if (n_splits == 1) return 1;
+  dim3 g2(a.n_heads, a.b);
+  if (hd == 64) attn_merge_kernel<64><<<g2, 64, 0, st>>>(a, n_splits);
+  else attn_merge_kernel<128><<<g2, 128, 0, st>>>(a, n_splits);
+  return 2;
+}
+
 int launch_attention_decode(const AttnArgs& a, cudaStream_t st) {
   const int hd = a.d / a.n_heads;
   if (hd != 64 && hd != 128) return -1;
@@ -489,10 +700,10 @@ int launch_attention_decode(const AttnArgs& a, cudaStream_t st) {
   n_splits = (L + per - 1) / per;
   if (n_splits > 1 && (int64_t)pairs * n_splits * (hd + 2) > a.ws_floats) return -1;
   dim3 grid(a.n_heads, a.b, n_splits);
-  if (a.use_cuda_cores) {   // v1 (one row per warp), kept for A/B
+  if (!a.use_cuda_cores) {   // one K/V row per warp: measured 0-5% ahead of v2 at c3-c5
     if (hd == 64) attn_decode_kernel<64><<<grid, 128, 0, st>>>(a, n_splits, per);
     else attn_decode_kernel<128><<<grid, 128, 0, st>>>(a, n_splits, per);
-  } else {
+  } else {                   // v2: lane groups with 16-B row loads (kept for A/B)
     if (hd == 64) attn_decode_v2_kernel<64><<<grid, 128, 0, st>>>(a, n_splits, per);
     else attn_decode_v2_kernel<128><<<grid, 128, 0, st>>>(a, n_splits, per);
   }

@@ -23,6 +23,7 @@ struct EpiParams {
   __half* kc = nullptr;
   __half* vc = nullptr;
   int d = 0, n_tok = 1, past = 0, kv_b = 1;
+  int kv_rowmajor = 0;        // 1: k/v go to a [m][2d] staging buffer (int4-KV path)
   float qscale = 1.f;
   float* h = nullptr;
   __half* u = nullptr;
@@ -64,13 +65,26 @@ struct AttnArgs {
   const __half* vc = nullptr;
   __half* o = nullptr;        // same shape as q
   int b = 0, n = 1, past = 0, d = 0, n_heads = 0, kv_b = 0;
+  int64_t kv_pos_stride = 0;  // elements between positions (0: kv_b * d, position-major cache)
+  int64_t kv_b_stride = 0;    // elements between sequences  (0: d)
   int use_cuda_cores = 0;     // prefill: 1 = the CUDA-core reference kernel
+  // int4 KV cache (decode): codes [pos][kv_b][d/2] bytes, scales [pos][kv_b][d/64] fp16
+  const uint8_t* kq = nullptr;
+  const __half* ks = nullptr;
+  const uint8_t* vq = nullptr;
+  const __half* vs = nullptr;
   float* ws = nullptr;
   int64_t ws_floats = 0;
   int num_sms = 148;
 };
 int launch_attention_decode(const AttnArgs& a, cudaStream_t st);
 int launch_attention_prefill(const AttnArgs& a, cudaStream_t st);
+
+// int4 KV: quantize the fresh fp16 K/V rows (staging [b*n][2d]) into the cache at
+// positions past..past+n-1 (codes [pos][kv_b][d/2], fast nibble order; scales fp16)
+int launch_kv_quant(const __half* staging, int b, int n, int past, int d, int kv_b, uint8_t* kq, __half* ks,
+                    uint8_t* vq, __half* vs, cudaStream_t st);
+int launch_attention_decode_q4(const AttnArgs& a, cudaStream_t st);
 
 // misc
 int launch_embed(const int32_t* ids, int b, int n, int past, const __half* tok_tiled, int64_t tok_n_kb,

@@ -37,7 +37,7 @@ class pipo_config(C.Structure):
     _fields_ = [("device", C.c_int32), ("d_model", C.c_int32), ("n_layers", C.c_int32), ("n_heads", C.c_int32),
                 ("ffn_dim", C.c_int32), ("vocab", C.c_int32), ("max_pos", C.c_int32),
                 ("max_batch", C.c_int32), ("max_seq", C.c_int32), ("wfmt", C.c_int32),
-                ("weight_tier", C.c_int32), ("kv_tier", C.c_int32), ("ring_layers", C.c_int32),
+                ("weight_tier", C.c_int32), ("kv_tier", C.c_int32), ("kv_fmt", C.c_int32), ("ring_layers", C.c_int32),
                 ("chunk_bytes", C.c_int64), ("gemv_max_m", C.c_int32), ("disk_threads", C.c_int32),
                 ("disk_dir", C.c_char_p), ("flags", C.c_uint32)]
 
@@ -305,12 +305,13 @@ def pipo_probe_h2d(ctx, nbytes: int, reps: int = 5) -> float:
 
 
 def make_config(shape, *, device=0, max_batch, max_seq, wfmt=PIPO_W_INT4_G64, weight_tier=PIPO_TIER_HOST,
-                kv_tier=PIPO_TIER_DEVICE, ring_layers=2, chunk_bytes=0, gemv_max_m=15, disk_threads=4,
+                kv_tier=PIPO_TIER_DEVICE, kv_fmt=PIPO_W_FP16, ring_layers=2, chunk_bytes=0, gemv_max_m=15, disk_threads=4,
                 disk_dir=None, flags=PIPO_F_TIMELINE, n_layers=None) -> pipo_config:
     """pipo_config from a pipo_synth.OPTShape-like object (d_model, n_layers, n_heads, ffn_dim, vocab, max_pos)."""
     return pipo_config(device=device, d_model=shape.d_model, n_layers=n_layers or shape.n_layers,
                        n_heads=shape.n_heads, ffn_dim=shape.ffn_dim, vocab=shape.vocab, max_pos=shape.max_pos,
                        max_batch=max_batch, max_seq=max_seq, wfmt=wfmt, weight_tier=weight_tier, kv_tier=kv_tier,
+                       kv_fmt=kv_fmt,
                        ring_layers=ring_layers, chunk_bytes=chunk_bytes, gemv_max_m=gemv_max_m,
                        disk_threads=disk_threads, disk_dir=(disk_dir.encode() if disk_dir else None), flags=flags)
 

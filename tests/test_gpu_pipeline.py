@@ -236,3 +236,39 @@ def test_disk_tier_io_failure_surfaces(tmp_path, monkeypatch):
             pl.prefill(np.zeros((2, 4), np.int32))
         assert e.value.status == pipo.PIPO_E_STATE
 
+
+
+@pytest.mark.parametrize("shape,b,P,G", [
+    (synth.OPTShape(d_model=1024, n_layers=2, n_heads=8, ffn_dim=4096, vocab=2048, max_pos=256), 4, 40, 5),
+    (synth.OPTShape(d_model=512, n_layers=2, n_heads=8, ffn_dim=2048, vocab=1500, max_pos=256), 20, 24, 4),
+])
+def test_int4_kv_cache_vs_oracle(shape, b, P, G):
+    """NEXT-2: the INT4 KV cache against the oracle's int4-KV semantics."""
+    pipo = pipo_mod()
+    emb = synth.embed_masters(shape)
+    layers = [synth.layer_masters(shape, j) for j in range(shape.n_layers)]
+    ref = opt.OracleOPT.from_masters(shape.n_heads, emb, layers, "int4", P + G, kv_int4=True)
+    for kv_tier in (pipo.PIPO_TIER_DEVICE, pipo.PIPO_TIER_HOST):
+        cfg = pipo.make_config(shape, max_batch=b, max_seq=P + G, weight_tier=pipo.PIPO_TIER_HOST,
+                               kv_tier=kv_tier, kv_fmt=pipo.PIPO_W_INT4_G64)
+        with pipo.Pipeline(cfg) as pl:
+            load_masters(pl, emb, layers)
+            ref.past = 0
+            teacher_forced(pl, ref, synth.prompts(b, P, shape.vocab), G)
+
+
+def test_int4_kv_tiers_bit_identical():
+    pipo = pipo_mod()
+    prompt = synth.prompts(3, 20, SMALL.vocab)
+    def syn(pl):
+        pl.load_synthetic(pipo.PIPO_LAYER_EMBED, 5)
+        for j in range(SMALL.n_layers):
+            pl.load_synthetic(j, 5)
+    ref, _ = _run(pipo, SMALL, dict(weight_tier=0, kv_fmt=1), syn, prompt, 5)
+    for variant in (dict(weight_tier=1, kv_tier=1, kv_fmt=1), dict(weight_tier=1, kv_tier=1, kv_fmt=1, ring_layers=3),
+                    dict(weight_tier=0, kv_tier=1, kv_fmt=1)):
+        got, _ = _run(pipo, SMALL, variant, syn, prompt, 5)
+        assert np.array_equal(got, ref)
+    fp, _ = _run(pipo, SMALL, dict(weight_tier=0), syn, prompt, 5)
+    assert np.array_equal(fp[0], ref[0])          # prefill attends over fresh fp16 K/V: identical
+    assert not np.array_equal(fp[1:], ref[1:])    # decode reads the int4 cache

@@ -10,5 +10,5 @@ for name, b, L, d, H in [("c5", 64, 528, 7168, 56), ("c4", 64, 528, 5120, 40), (
     row = {}
     for v in (0, 1):
         us = pipo.pipo_bench_attention(pl.ctx, b, L, d, H, v, 10)
-        row[f"v{2 - v}"] = (round(us, 2), round(2 * L * b * d * 2 / us / 1e3, 1))
+        row[f"v{v + 1}"] = (round(us, 2), round(2 * L * b * d * 2 / us / 1e3, 1))
     print(name, "us, GB/s:", row, flush=True)
