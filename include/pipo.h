@@ -210,14 +210,18 @@ pipo_status pipo_unpack_int4_g64(pipo_ctx* ctx, const uint8_t* codes, const uint
  * path: 0 = automatic (as the pipeline chooses), 1 = int4 GEMV (CUDA cores),
  * 2 = mma.sync GEMM (legacy baseline), 3 = tcgen05/TMEM GEMM (synchronous pipeline),
  * 4 = warp-specialized stream-K tcgen05 GEMM (int4, A in shared memory),
- * 5 = same with A in TMEM (int4, M <= 64). */
+ * 5 = same with A in TMEM (int4, M <= 64), 6 = prefill tcgen05 GEMM with A in TMEM
+ * (int4, any M; static persistent tile schedule). */
 pipo_status pipo_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, const uint16_t* x,
                         const float* w, const float* bias, int32_t M, int32_t N, int32_t K,
                         float* y);
 
 /* Kernel micro-benchmark: one linear layer y[M][N] = x . W^T on device-resident
  * synthetic data (weights drawn + quantized on the GPU), `iters` back-to-back
- * launches on the compute stream, average microseconds per launch in *us. */
+ * launches on the compute stream, average microseconds per launch in *us.
+ * Successive launches read different copies of the weights (>= 384 MB in total,
+ * more than L2), so every launch streams its weights from HBM as in the pipeline;
+ * environment PIPO_BENCH_HOT=1 re-reads one copy instead (L2-warm upper bound). */
 pipo_status pipo_bench_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, int32_t M, int32_t N, int32_t K,
                               int32_t iters, double* us);
 
@@ -253,6 +257,64 @@ pipo_status pipo_debug_capture(pipo_ctx* ctx, int32_t on, float* out);
 /* H2D probe: best-of-`reps` pinned->device cudaMemcpyAsync bandwidth (GB/s) for
  * `bytes`-sized copies on the weight-copy stream (App. A sweep). */
 pipo_status pipo_probe_h2d(pipo_ctx* ctx, int64_t bytes, int32_t reps, double* gbs);
+
+/* ---- automatic configuration (NEXT-3): memory model + Eq. (1) ---------------
+ * Host-only pure functions (no context, no GPU).  The paper states them for
+ * LLaMA3.1 (§3.5, App. B); readings Q23-Q27 in
+ * DESIGN.md.  All sizes in bytes (doubles, exact for the integer-valued results). */
+typedef struct {
+  int64_t n_layers, d_model, vocab;   /* l, d, V                                         */
+  int64_t n_heads, n_kv_heads;        /* h, h_kv (h_kv | h; OPT: h_kv = h)               */
+  int64_t ffn_hidden;                 /* d_h (LLaMA: pipo_ffn_hidden_dim; OPT: ffn_dim)  */
+  int32_t mlp_mats;                   /* 3 = the paper's SwiGLU MLP, 2 = OPT fc1/fc2 (Q27) */
+  double p_weight, p_act;             /* bytes/element: weights (2 fp16, 0.53125 int4-g64),
+                                         activations and KV cache          */
+} pipo_mem_spec;
+
+typedef struct {
+  double w_embed, w_mha, w_mlp, w_total;   /* W_embed, W_mha, W_mlp, W (§3.5)          */
+  double c_total;                          /* C = 2 p b s l d h_kv / h                  */
+  double m_mha, m_mlp, m_embed, m_peak;    /* App. B peaks; m_peak = max of the three   */
+} pipo_mem_report;
+
+#define PIPO_STAGE_PREFILL 0
+#define PIPO_STAGE_DECODE 1
+
+/* d_h = m * ceil(gamma * floor(8d/3) / m); -1 on bad arguments. */
+int64_t pipo_ffn_hidden_dim(int64_t d, int64_t m, double gamma);
+
+/* App. B memory model for batch b, sequence s (prompt + generated), stage
+ * PIPO_STAGE_*, with (preload != 0) or without preloading.  INVALID_ARG on a bad spec. */
+pipo_status pipo_memory_model(const pipo_mem_spec* spec, int64_t b, int64_t s, int32_t stage,
+                              int32_t preload, pipo_mem_report* out);
+
+typedef struct {
+  double m_gpu, m_cpu;   /* available device / host memory, bytes (M_GPU, M_CPU)   */
+  double b_gpu, b_ssd;   /* host->device and disk bandwidth, bytes/s (B_GPU, B_SSD) */
+} pipo_hw_spec;
+
+typedef struct {
+  int32_t weight_tier;        /* pipo_tier chosen by Eq. (1)                              */
+  int32_t ring_layers;        /* 2 = performance-optimized, 1 = memory-efficient pipeline */
+  int32_t use_quant_kernel;   /* int4 weights and b < 16                   */
+  int32_t gemv_max_m;         /* pipo_config.gemv_max_m to use (15)                       */
+  int64_t block_bytes;        /* transfer block size from the probe (App. A); 0 if none   */
+  double w_total, c_total;    /* W, C                                                     */
+  double m_peak;              /* M (prefill with preloading)                 */
+  double m_peak_no_preload;   /* prefill peak of the memory-efficient pipeline            */
+} pipo_plan;
+
+/* Smallest probed block size whose min-over-edges throughput (h2d, and disk when
+ * disk_bps != NULL) is within 5 % of the best (App. A, reading Q26); -1 if n < 1. */
+int64_t pipo_choose_block_size(const int64_t* sizes, const double* h2d_bps, const double* disk_bps,
+                               int32_t n);
+
+/* Eq. (1): weight tier and pipeline mode for workload (b, s) on
+ * hardware hw; optional bandwidth profile (n_sizes entries, may be 0) picks the
+ * block size.  INFEASIBLE when even the memory-efficient pipeline exceeds M_GPU. */
+pipo_status pipo_choose_plan(const pipo_mem_spec* spec, int64_t b, int64_t s, const pipo_hw_spec* hw,
+                             const int64_t* block_sizes, const double* h2d_bps, const double* disk_bps,
+                             int32_t n_sizes, pipo_plan* out);
 
 #ifdef __cplusplus
 }

@@ -40,4 +40,7 @@ struct BlobFileHeader {
 static_assert(sizeof(BlobFileHeader) == 4096, "header must be one O_DIRECT block");
 std::string blob_path(const std::string& dir, int layer);
 
+// thread-local pipo_last_error() message (defined in api.cu); returns s
+pipo_status set_last_error(pipo_status s, const char* msg);
+
 }  // namespace pipo

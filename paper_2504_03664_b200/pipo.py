@@ -25,7 +25,7 @@ PIPO_F_TIMELINE = 1
 PIPO_F_KPROF = 2
 K_CLASSES = ["linear_decode", "attn_decode", "lm_head", "linear_prefill", "attn_prefill", "misc"]
 PIPO_LAYER_EMBED = -1
-PATH_AUTO, PATH_GEMV, PATH_GEMM, PATH_TC, PATH_WS, PATH_TM = 0, 1, 2, 3, 4, 5
+PATH_AUTO, PATH_GEMV, PATH_GEMM, PATH_TC, PATH_WS, PATH_TM, PATH_TP = 0, 1, 2, 3, 4, 5, 6
 
 _f = C.POINTER(C.c_float)
 _u8 = C.POINTER(C.c_uint8)
@@ -67,6 +67,36 @@ class pipo_stats(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class pipo_mem_spec(C.Structure):
+    _fields_ = [("n_layers", C.c_int64), ("d_model", C.c_int64), ("vocab", C.c_int64), ("n_heads", C.c_int64),
+                ("n_kv_heads", C.c_int64), ("ffn_hidden", C.c_int64), ("mlp_mats", C.c_int32),
+                ("p_weight", C.c_double), ("p_act", C.c_double)]
+
+
+class pipo_mem_report(C.Structure):
+    _fields_ = [(k, C.c_double) for k in ("w_embed", "w_mha", "w_mlp", "w_total", "c_total", "m_mha", "m_mlp",
+                                          "m_embed", "m_peak")]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class pipo_hw_spec(C.Structure):
+    _fields_ = [("m_gpu", C.c_double), ("m_cpu", C.c_double), ("b_gpu", C.c_double), ("b_ssd", C.c_double)]
+
+
+class pipo_plan(C.Structure):
+    _fields_ = [("weight_tier", C.c_int32), ("ring_layers", C.c_int32), ("use_quant_kernel", C.c_int32),
+                ("gemv_max_m", C.c_int32), ("block_bytes", C.c_int64), ("w_total", C.c_double),
+                ("c_total", C.c_double), ("m_peak", C.c_double), ("m_peak_no_preload", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+PIPO_STAGE_PREFILL, PIPO_STAGE_DECODE = 0, 1
+
+
 def _sig(name, restype, *args):
     fn = getattr(_lib, name)
     fn.restype = restype
@@ -102,11 +132,19 @@ _sig("pipo_attention_prefill", C.c_int, _P, _u16, _u16, _u16, C.c_int32, C.c_int
      C.c_int32, C.c_int32, _f)
 _sig("pipo_debug_capture", C.c_int, _P, C.c_int32, _f)
 _sig("pipo_probe_h2d", C.c_int, _P, C.c_int64, C.c_int32, C.POINTER(C.c_double))
+_sig("pipo_ffn_hidden_dim", C.c_int64, C.c_int64, C.c_int64, C.c_double)
+_sig("pipo_memory_model", C.c_int, C.POINTER(pipo_mem_spec), C.c_int64, C.c_int64, C.c_int32, C.c_int32,
+     C.POINTER(pipo_mem_report))
+_sig("pipo_choose_block_size", C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_double), C.POINTER(C.c_double),
+     C.c_int32)
+_sig("pipo_choose_plan", C.c_int, C.POINTER(pipo_mem_spec), C.c_int64, C.c_int64, C.POINTER(pipo_hw_spec),
+     C.POINTER(C.c_int64), C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int32, C.POINTER(pipo_plan))
 
 EXPORTED = ["pipo_last_error", "pipo_abi_version", "pipeline_init", "pipeline_destroy", "load_layer_weights",
             "pipo_load_synthetic", "prefill", "decode_step", "decode_step_dev", "pipeline_stats",
             "pipeline_stats_reset", "pipo_stream", "pipo_kernel_stats", "pipo_quantize_int4_g64", "pipo_quantize_int4_g64_gpu",
-            "pipo_unpack_int4_g64", "pipo_linear", "pipo_bench_linear", "pipo_probe_bulk", "pipo_bench_attention", "pipo_attention_decode", "pipo_attention_prefill", "pipo_debug_capture", "pipo_probe_h2d"]
+            "pipo_unpack_int4_g64", "pipo_linear", "pipo_bench_linear", "pipo_probe_bulk", "pipo_bench_attention", "pipo_attention_decode", "pipo_attention_prefill", "pipo_debug_capture", "pipo_probe_h2d",
+            "pipo_ffn_hidden_dim", "pipo_memory_model", "pipo_choose_block_size", "pipo_choose_plan"]
 
 
 class PipoError(RuntimeError):
@@ -302,6 +340,41 @@ def pipo_probe_h2d(ctx, nbytes: int, reps: int = 5) -> float:
     g = C.c_double()
     _check(_lib.pipo_probe_h2d(ctx, nbytes, reps, C.byref(g)))
     return g.value
+
+
+def mem_spec(*, l, d, V, h, h_kv, d_h, mlp_mats=3, p_weight=2.0, p_act=2.0) -> pipo_mem_spec:
+    """pipo_mem_spec in the paper's notation."""
+    return pipo_mem_spec(n_layers=l, d_model=d, vocab=V, n_heads=h, n_kv_heads=h_kv, ffn_hidden=d_h,
+                         mlp_mats=mlp_mats, p_weight=float(p_weight), p_act=float(p_act))
+
+
+def pipo_ffn_hidden_dim(d: int, m: int, gamma: float) -> int:
+    return _lib.pipo_ffn_hidden_dim(d, m, gamma)
+
+
+def pipo_memory_model(spec: pipo_mem_spec, b: int, s: int, stage: int, preload: bool) -> dict:
+    r = pipo_mem_report()
+    _check(_lib.pipo_memory_model(C.byref(spec), b, s, stage, int(preload), C.byref(r)))
+    return r.as_dict()
+
+
+def _dbl(a):
+    return (C.c_double * len(a))(*a) if a is not None else None
+
+
+def pipo_choose_block_size(sizes, h2d_bps, disk_bps=None) -> int:
+    n = len(sizes)
+    return _lib.pipo_choose_block_size((C.c_int64 * n)(*sizes), _dbl(h2d_bps), _dbl(disk_bps), n)
+
+
+def pipo_choose_plan(spec: pipo_mem_spec, b: int, s: int, *, m_gpu, m_cpu, b_gpu, b_ssd,
+                     sizes=(), h2d_bps=None, disk_bps=None) -> dict:
+    hw = pipo_hw_spec(m_gpu=float(m_gpu), m_cpu=float(m_cpu), b_gpu=float(b_gpu), b_ssd=float(b_ssd))
+    out = pipo_plan()
+    n = len(sizes)
+    _check(_lib.pipo_choose_plan(C.byref(spec), b, s, C.byref(hw), (C.c_int64 * n)(*sizes) if n else None,
+                                 _dbl(h2d_bps) if n else None, _dbl(disk_bps) if n else None, n, C.byref(out)))
+    return out.as_dict()
 
 
 def make_config(shape, *, device=0, max_batch, max_seq, wfmt=PIPO_W_INT4_G64, weight_tier=PIPO_TIER_HOST,

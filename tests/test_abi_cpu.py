@@ -29,7 +29,7 @@ def pipo():
 def _declared():
     src = open(os.path.join(ROOT, "include", "pipo.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    names = re.findall(r"^\s*(?:pipo_status|void\s*\*?|const char\s*\*|int32_t)\s+(\w+)\s*\(", src, flags=re.M)
+    names = re.findall(r"^\s*(?:pipo_status|void\s*\*?|const char\s*\*|int32_t|int64_t)\s+(\w+)\s*\(", src, flags=re.M)
     return sorted(set(names))
 
 
