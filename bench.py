@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--kv-fmt", default="fp16", choices=["fp16", "int4"],
                     help="KV cache storage (int4 = NEXT-2: PAPER.md:96 INT4 KV cache)")
     ap.add_argument("--ring", type=int, default=2)
+    ap.add_argument("--weight-tier", default=None, choices=["device", "host", "disk"],
+                    help="override the config's weight tier (device = no streaming: isolates H2D interference)")
     ap.add_argument("--chunk-mb", type=float, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -239,6 +241,8 @@ def run_pipo(args):
     s, b, P, G = c["shape"], c["b"], c["P"], c["G"]
     steps_needed = args.warmup + args.steps * (1 if args.no_e2e else 2)
     max_seq = P + max(G, steps_needed + 1)
+    if args.weight_tier:
+        c = {**c, "weight_tier": ["device", "host", "disk"].index(args.weight_tier)}
     disk_dir = f"{args.disk_dir}/rank{rank}" if c["weight_tier"] == 2 else None
     if disk_dir:
         os.makedirs(disk_dir, exist_ok=True)
@@ -255,6 +259,10 @@ def run_pipo(args):
         pl.load_synthetic(j, synth.WEIGHT_SEED)
     t_load = time.perf_counter() - t_setup
     link_probe = pipo.pipo_probe_h2d(pl.ctx, 256 << 20, 5)
+    # App. A block-size sweep + Eq. (1) on this box (NEXT-3 planner, informational:
+    # the configs force the streamed tier, reading Q19)
+    sweep = [1 << 20, 4 << 20, 16 << 20, 32 << 20, 64 << 20, 128 << 20, 256 << 20]
+    sweep_gbs = [pipo.pipo_probe_h2d(pl.ctx, n, 3) for n in sweep]
     # batch shard: rank r owns sequences [r*b, (r+1)*b) of the global prompt batch
     lo, hi = shard_range(b * world, world, rank)
     prompt = synth.prompts(b * world, P, s.vocab)[lo:hi]
@@ -376,6 +384,25 @@ def run_pipo(args):
         line["disk_roofline"] = {"bound": "disk (O_DIRECT, 4 readers, 32 MiB)", "probe_gbs": dgbs,
                                  "achieved_gbs": layer_bytes / (ms / 1e3) / 1e9,
                                  "frac": layer_bytes / (dgbs * 1e9) / (ms / 1e3)}
+    if rank == 0:
+        try:
+            mem_cpu = int(open("/proc/meminfo").read().split("MemTotal:")[1].split()[0]) * 1024
+        except (OSError, IndexError, ValueError):
+            mem_cpu = 0
+        b_ssd = (line.get("disk_roofline") or {}).get("probe_gbs")
+        spec = pipo.mem_spec(l=s.n_layers, d=s.d_model, V=s.vocab, h=s.n_heads, h_kv=s.n_heads, d_h=s.ffn_dim,
+                             mlp_mats=2, p_weight=17 / 32 if args.wfmt == "int4" else 2.0, p_act=2.0)
+        try:
+            plan = pipo.pipo_choose_plan(spec, b, P + G, m_gpu=torch.cuda.get_device_properties(local).total_memory,
+                                         m_cpu=mem_cpu or 1, b_gpu=link_probe * 1e9,
+                                         b_ssd=(b_ssd or link_probe / 10) * 1e9,
+                                         sizes=sweep, h2d_bps=[g * 1e9 for g in sweep_gbs])
+            plan["weight_tier"] = ["device", "host", "disk"][plan["weight_tier"]]
+            plan["b_ssd"] = "probed" if b_ssd else "not probed (assumed B_GPU/10)"
+            plan["h2d_sweep_gbs"] = dict(zip([f"{n >> 20}MiB" for n in sweep], sweep_gbs))
+            line["plan_eq1"] = plan
+        except pipo.PipoError as e:
+            line["plan_eq1"] = {"error": str(e)}
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         sample = OracleSample(args.config, args.wfmt)
         t = min(sample.step() for _ in range(2))

@@ -110,7 +110,32 @@ __device__ __forceinline__ int cta_of_unit(int64_t u, int64_t U, int64_t G) {
   return (int)c;
 }
 
+// Programmatic dependent launch (PDL): a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start (prologue: barrier init,
+// TMEM alloc, descriptor prefetch) while its predecessor in the stream drains;
+// griddep_wait() blocks until the predecessor grid has completed and its memory is
+// visible, so every read of a predecessor's output and every global write comes after
+// it.  griddep_launch() lets this grid's dependents be scheduled early.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 }  // namespace ws
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 
 constexpr int WS_THREADS = 448;   // producer, MMA, 8 unpack warps, 4 epilogue warps
 
@@ -179,6 +204,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
   __syncthreads();
   ws::tc_after();
   const uint32_t tmem = *tmem_slot;
+  ws::griddep_wait();     // predecessor (producer of x, reader of the partials) has finished
+  ws::griddep_launch();   // the stream-K reduce may be scheduled now
   uint64_t* tsbuf = (dbg & 32) ? reinterpret_cast<uint64_t*>(a.ws + (15ll << 20)) + blockIdx.x * 8 : nullptr;
   auto stamp = [&](int k) {
     if (tsbuf) {
@@ -359,13 +386,24 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
 // (pair, m-tile) was split across CTAs cf..cl; their partial accumulators are summed
 // in k order (deterministic) and the fused epilogue runs.  grid = (tiles, BN/16).
 template <int BN>
-__global__ void __launch_bounds__(256) ws_reduce_kernel(LinearArgs a, int n_rt, int m_tiles, int G, int kbu) {
+__global__ void __launch_bounds__(256) ws_reduce_kernel(LinearArgs a, int n_rt, int m_tiles, int G, int kbu, int dbg) {
+  ws::griddep_wait();     // launched as a programmatic dependent of the GEMM: its partials
+  ws::griddep_launch();
+  if ((dbg & 128) && threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMin(reinterpret_cast<unsigned long long*>(a.ws + (15ll << 20)) + 148 * 16, (unsigned long long)t);
+  }
   // grid = (tiles, BN/8): each thread owns one weight row of one tile and 8 columns;
   // contributors are loaded 4 at a time (32 loads in flight), summed in k order.
+  // One block per CTA boundary c = blockIdx.x + 1: the tile holding unit u_begin(c) is
+  // shared iff the boundary falls inside it; the first such boundary owns the reduce.
   __shared__ int s_cf, s_cl, s_first;
-  const int64_t tile = blockIdx.x;
   const int n_ku = a.K / 64 / kbu, n_pairs = (n_rt + 1) >> 1;
   const int64_t U = (int64_t)n_pairs * m_tiles * n_ku;
+  const int64_t ub = ws::u_begin(blockIdx.x + 1, U, G);
+  const int64_t tile = ub / n_ku;
+  if (ub == tile * n_ku || ws::u_begin(blockIdx.x, U, G) > tile * n_ku) return;
   if (threadIdx.x == 0) {
     s_cf = ws::cta_of_unit(tile * n_ku, U, G);
     s_cl = ws::cta_of_unit((tile + 1) * n_ku - 1, U, G);
@@ -402,6 +440,11 @@ __global__ void __launch_bounds__(256) ws_reduce_kernel(LinearArgs a, int n_rt, 
   }
 #pragma unroll
   for (int j = 0; j < 8; ++j) epi_store(a.epi, m0 + c0 + j, n, acc[j]);
+  if ((dbg & 128) && threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(reinterpret_cast<unsigned long long*>(a.ws + (15ll << 20)) + 148 * 16 + 1, (unsigned long long)t);
+  }
 }
 
 // ---------------------------------------------------------------------------------
@@ -410,11 +453,15 @@ __global__ void __launch_bounds__(256) ws_reduce_kernel(LinearArgs a, int n_rt, 
 // 64 fp16 values = 32 columns), and the MMA reads A from TMEM (tcgen05.mma ... [a_tmem]).
 // No shared-memory A ring, no swizzled STS, no generic->async proxy fence, and the
 // freed shared memory deepens the raw-weight ring (NR stages in flight).
-constexpr int TM_THREADS = 480;   // 0 raw producer, 1 MMA, 2-9 unpack, 10-13 epilogue, 14 x producer
-
+// Roles: warp 0 raw producer, 1 MMA, 2 .. 2+UW-1 unpack, then 4 epilogue warps, then
+// the x producer.
 // One unit = 2 weight tiles (256 rows) x KBU k-blocks: the per-unit synchronisation
 // (mbarrier waits, tcgen05.commit, producer bookkeeping) is amortised over 8*KBU MMAs.
-template <int BN, int KBU>
+// NACC accumulator buffers (2: the epilogue of one tile overlaps the next tile's MMAs;
+// 1: more TMEM for the A ring).  UW unpack warps: 8 (warp -> tile x lane quarter, all
+// KBU k-blocks) or 16 (warp -> tile x lane quarter x k-block (KBU = 2) or 32-code half
+// (KBU = 1)), i.e. twice the warps to hide the dequant latency chain.
+template <int BN, int KBU, int NACC = 2, int UW = 8>
 struct TmCfg {
   static constexpr int RAW_T = KBU * (int)kInt4BlockBytes;     // one tile's blocks (contiguous)
   static constexpr int RAW = 2 * RAW_T;
@@ -422,13 +469,17 @@ struct TmCfg {
   static constexpr int X_KB = BN * 128;                         // x tile of one k-block
   static constexpr int X_TILE = KBU * X_KB;
   static constexpr int NX = (KBU == 1 ? 8 : 4);
-  static constexpr int ACC_COLS = 2 * 2 * BN;                   // 2 buffers x 2 tiles
+  static constexpr int ACC_COLS = NACC * 2 * BN;                // NACC buffers x 2 tiles
   static constexpr int A_COLS = 2 * 32 * KBU;                   // per A stage (2 tiles x KBU x 32 cols)
-  static constexpr int NA = (512 - ACC_COLS) / A_COLS < 6 ? (512 - ACC_COLS) / A_COLS : 6;
+  static constexpr int NA = (512 - ACC_COLS) / A_COLS < 8 ? (512 - ACC_COLS) / A_COLS : 8;
+  static constexpr int E0 = 2 + UW;                              // first epilogue warp
+  static constexpr int XW = E0 + 4;                              // x producer warp
+  static constexpr int THREADS = (XW + 1) * 32;
   static constexpr int SMEM = 1024 + NX * X_TILE + NR * RAW + 512;
   static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
   static_assert(NA >= 2, "TMEM budget");
+  static_assert(UW == 8 || UW == 16, "unpack warps");
 };
 
 __device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc, uint32_t acc) {
@@ -449,16 +500,25 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
       : "memory");
 }
 
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(
+          taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+
 __device__ __forceinline__ uint64_t clk() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
   return t;
 }
 
-template <int BN, int KBU>
-__global__ void __launch_bounds__(TM_THREADS, 1)
+template <int BN, int KBU, int NACC, int UW>
+__global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
     gemm_tm_kernel(const __grid_constant__ CUtensorMap xmap, LinearArgs a, int n_rt, int m_tiles, int G, int dbg) {
-  using C = TmCfg<BN, KBU>;
+  using C = TmCfg<BN, KBU, NACC, UW>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* base = smem_raw + (base_u32 - smem_u32(smem_raw));
@@ -473,19 +533,29 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
   uint64_t* a_empty = a_full + C::NA;
   uint64_t* acc_full = a_empty + C::NA;
   uint64_t* acc_empty = acc_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + NACC);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n_kb = a.K / 64, n_ku = n_kb / KBU;
   const int n_pairs = (n_rt + 1) >> 1;
   const int64_t U = (int64_t)n_pairs * m_tiles * n_ku;
-  const int64_t u0 = ws::u_begin(blockIdx.x, U, G), u1 = ws::u_begin(blockIdx.x + 1, U, G);
+  const int64_t u0 = ws::u_begin(blockIdx.x, U, G);
+  const int64_t u1 = (dbg & 256) ? u0 : ws::u_begin(blockIdx.x + 1, U, G);   // debug: no work
+  uint64_t* ts = (dbg & 128) ? reinterpret_cast<uint64_t*>(a.ws + (15ll << 20)) + blockIdx.x * 16 : nullptr;
+  auto gstamp = [&](int k) {
+    if (ts) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      ts[k] = t;
+    }
+  };
+  if (tid == 0) gstamp(9);
 
   if (tid == 0) {
-    for (int i = 0; i < C::NR; ++i) { ws::mbar_init(&raw_full[i], 1); ws::mbar_init(&raw_empty[i], 8); }
+    for (int i = 0; i < C::NR; ++i) { ws::mbar_init(&raw_full[i], 1); ws::mbar_init(&raw_empty[i], UW); }
     for (int i = 0; i < C::NX; ++i) { ws::mbar_init(&x_full[i], 1); ws::mbar_init(&x_empty[i], 1); }
-    for (int i = 0; i < C::NA; ++i) { ws::mbar_init(&a_full[i], 8); ws::mbar_init(&a_empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { ws::mbar_init(&acc_full[i], 1); ws::mbar_init(&acc_empty[i], 4); }
+    for (int i = 0; i < C::NA; ++i) { ws::mbar_init(&a_full[i], UW); ws::mbar_init(&a_empty[i], 1); }
+    for (int i = 0; i < NACC; ++i) { ws::mbar_init(&acc_full[i], 1); ws::mbar_init(&acc_empty[i], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&xmap) : "memory");
   }
@@ -498,7 +568,10 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
   __syncthreads();
   ws::tc_after();
   const uint32_t tmem = *tmem_slot;
+  ws::griddep_wait();     // predecessor (producer of x, reader of the partials) has finished
+  ws::griddep_launch();   // the stream-K reduce may be scheduled now
   const uint32_t a_base = tmem + C::ACC_COLS;           // A ring columns
+  if (tid == 0) gstamp(10);
   uint64_t* wt = (dbg & 32) ? reinterpret_cast<uint64_t*>(a.ws + (15ll << 20)) + blockIdx.x * 16 : nullptr;
   uint64_t w_acc[2] = {0, 0};
   const uint64_t t_begin = clk();
@@ -534,7 +607,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
         if (++s == C::NR) { s = 0; ph ^= 1; }
       }
     }
-  } else if (warp == 14) {
+  } else if (warp == C::XW) {
     // ---------------- x producer (TMA 2D, SWIZZLE_128B, KBU boxes per unit) ----------------
     if (lane == 0) {
       int64_t tile = u0 / n_ku;
@@ -567,8 +640,8 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
       const int64_t tile = u / n_ku;
       const int64_t seg_end = min(u1, (tile + 1) * n_ku);
       const bool two = 2 * (int)(tile % n_pairs) + 1 < n_rt;
-      const int ab = seg & 1;
-      ws::mbar_wait(&acc_empty[ab], ((seg >> 1) & 1) ^ 1);
+      const int ab = seg % NACC;
+      ws::mbar_wait(&acc_empty[ab], ((seg / NACC) & 1) ^ 1);
       ws::tc_after();
       const uint32_t d = tmem + ab * (2 * BN);
       for (int64_t v = u; v < seg_end; ++v) {
@@ -584,8 +657,10 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
             for (int kk = 0; kk < 4; ++kk) {
               const uint32_t acc = (v > u || k > 0 || kk > 0) ? 1u : 0u;
               const uint64_t db = db0 + (uint64_t)((k * C::X_KB + kk * 32) >> 4);
-              mma_f16_ts(d, at + k * 64 + kk * 8, db, C::IDESC, acc);
-              if (two) mma_f16_ts(d + BN, at + k * 64 + 32 + kk * 8, db, C::IDESC, acc);
+              if (!(dbg & 2)) {   // debug: skip the MMAs (commits still flow)
+                mma_f16_ts(d, at + k * 64 + kk * 8, db, C::IDESC, acc);
+                if (two) mma_f16_ts(d + BN, at + k * 64 + 32 + kk * 8, db, C::IDESC, acc);
+              }
             }
           ws::mma_commit(&a_empty[sa]);
           ws::mma_commit(&x_empty[sx]);
@@ -599,36 +674,61 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
       u = seg_end;
       ++seg;
     }
-  } else if (warp < 10) {
+    if (lane == 0) gstamp(11);
+  } else if (warp < C::E0) {
     // ---------------- unpack + scale straight into TMEM ----------------
-    // warp w: tile t = (w-2)/4, TMEM lanes 32*(w%4).. (a warp may only touch its lane quarter)
-    const int t = (warp - 2) >> 2, q = warp & 3;
+    // a warp may only touch its TMEM lane quarter (warp % 4).  UW = 8: warp -> (tile,
+    // quarter), all KBU k-blocks; UW = 16: warp -> (tile, quarter) and one k-block
+    // (KBU = 2) or one 32-code half (KBU = 1).
+    const int g = (warp - 2) >> 2, q = warp & 3;
+    const int t = UW == 8 ? g : (g >> 1), sub = UW == 8 ? 0 : (g & 1);
     const int r = q * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     int s = 0, sa = 0;
     uint32_t ph_r = 0, ph_a = 1;
     for (int64_t u = u0; u < u1; ++u) {
       TWAIT(0, &raw_full[s], ph_r);
-      uint4 cw[KBU][2];
-      __half2 s2[KBU];
+      constexpr int NK = UW == 8 ? KBU : (KBU == 2 ? 1 : 1);
+      uint4 cw[NK][2];
+      __half2 s2[NK];
 #pragma unroll
-      for (int k = 0; k < KBU; ++k) {
+      for (int kk = 0; kk < NK; ++kk) {
+        const int k = UW == 8 ? kk : (KBU == 2 ? sub : 0);
         const uint8_t* rs = raw + s * C::RAW + t * C::RAW_T + k * kInt4BlockBytes;
-        cw[k][0] = *reinterpret_cast<const uint4*>(rs + r * 16);
-        cw[k][1] = *reinterpret_cast<const uint4*>(rs + (128 + r) * 16);
-        s2[k] = __half2half2(*reinterpret_cast<const __half*>(rs + 4096 + r * 2));
+        if (UW == 8 || KBU == 2) {
+          cw[kk][0] = *reinterpret_cast<const uint4*>(rs + r * 16);
+          cw[kk][1] = *reinterpret_cast<const uint4*>(rs + (128 + r) * 16);
+        } else {
+          cw[kk][0] = *reinterpret_cast<const uint4*>(rs + (sub * 128 + r) * 16);
+        }
+        s2[kk] = __half2half2(*reinterpret_cast<const __half*>(rs + 4096 + r * 2));
       }
       __syncwarp();
       if (lane == 0) ws::mbar_arrive(&raw_empty[s]);
       TWAIT(1, &a_empty[sa], ph_a);
       ws::tc_after();
 #pragma unroll
-      for (int k = 0; k < KBU; ++k) {
-        uint32_t o[32];
-        const uint32_t w[8] = {cw[k][0].x, cw[k][0].y, cw[k][0].z, cw[k][0].w,
-                               cw[k][1].x, cw[k][1].y, cw[k][1].z, cw[k][1].w};
+      for (int kk = 0; kk < NK; ++kk) {
+        const int k = UW == 8 ? kk : (KBU == 2 ? sub : 0);
+        if (UW == 8 || KBU == 2) {
+          uint32_t o[32];
+          const uint32_t w[8] = {cw[kk][0].x, cw[kk][0].y, cw[kk][0].z, cw[kk][0].w,
+                                 cw[kk][1].x, cw[kk][1].y, cw[kk][1].z, cw[kk][1].w};
+          if (dbg & 4) {   // debug: skip the dequant arithmetic
 #pragma unroll
-        for (int ch = 0; ch < 8; ++ch) dequant8(w[ch], s2[k], reinterpret_cast<__half2*>(o + ch * 4));
-        tmem_st32(a_base + sa * C::A_COLS + k * 64 + t * 32 + ((uint32_t)(q * 32) << 16), o);
+            for (int ch = 0; ch < 8; ++ch) o[4 * ch] = o[4 * ch + 1] = o[4 * ch + 2] = o[4 * ch + 3] = w[ch];
+          } else {
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) dequant8(w[ch], s2[kk], reinterpret_cast<__half2*>(o + ch * 4));
+          }
+          if (!(dbg & 1)) tmem_st32(a_base + sa * C::A_COLS + k * 64 + t * 32 + lane_off, o);   // debug: skip
+        } else {
+          uint32_t o[16];
+          const uint32_t w[4] = {cw[kk][0].x, cw[kk][0].y, cw[kk][0].z, cw[kk][0].w};
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) dequant8(w[ch], s2[kk], reinterpret_cast<__half2*>(o + ch * 4));
+          if (!(dbg & 1)) tmem_st16(a_base + sa * C::A_COLS + t * 32 + sub * 16 + lane_off, o);
+        }
       }
       asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
       ws::tc_before();
@@ -651,10 +751,10 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
       const int pr = (int)(tile % n_pairs), mt = (int)(tile / n_pairs);
       const int m0 = mt * BN;
       const int ntile = (2 * pr + 1 < n_rt) ? 2 : 1;
-      const int ab = seg & 1;
+      const int ab = seg % NACC;
       {
         uint32_t done = 0;
-        const uint32_t addr = smem_u32(&acc_full[ab]), par = (seg >> 1) & 1;
+        const uint32_t addr = smem_u32(&acc_full[ab]), par = (seg / NACC) & 1;
         while (true) {
           asm volatile(
               "{\n.reg .pred P1;\nmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
@@ -689,11 +789,12 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
       u = seg_end;
       ++seg;
     }
+    if (warp == C::E0 && lane == 0) gstamp(12);
   }
   if (wt && lane == 0) {
     // slots: 0/1 raw producer, 2/3 MMA (a_full, x_full), 4/5 unpack warp 2 (raw_full, a_empty),
     // 6/7 x producer, 8 = total cycles of the MMA thread
-    const int role = warp == 0 ? 0 : warp == 1 ? 1 : warp == 2 ? 2 : warp == 14 ? 3 : -1;
+    const int role = warp == 0 ? 0 : warp == 1 ? 1 : warp == 2 ? 2 : warp == C::XW ? 3 : -1;
     if (role >= 0) { wt[2 * role] = w_acc[0]; wt[2 * role + 1] = w_acc[1]; }
     if (warp == 1) wt[8] = clk() - t_begin;
   }
@@ -701,6 +802,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
   __syncwarp();
   ws::tc_before();
   __syncthreads();
+  if (tid == 0) gstamp(13);
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512u));
 }
@@ -752,35 +854,39 @@ static int run_ws(const LinearArgs& a, cudaStream_t st) {
   CUtensorMap map;   // rows >= M are out of bounds: TMA zero-fills them
   if (!make_xmap(&map, a.x, a.M, a.K, BN)) return -1;
   static const int dbg = getenv("PIPO_WS_DEBUG") ? atoi(getenv("PIPO_WS_DEBUG")) : 0;
-  gemm_ws_kernel<BN><<<G, WS_THREADS, C::SMEM, st>>>(map, a, n_rt, m_tiles, dbg);
+  launch_pdl(gemm_ws_kernel<BN>, dim3(G), dim3(WS_THREADS), C::SMEM, st, map, a, n_rt, m_tiles, dbg);
   if (dbg & 64) return 1;   // debug: main kernel only
-  dim3 rg((unsigned)tiles, BN / 8);
-  ws_reduce_kernel<BN><<<rg, 256, 0, st>>>(a, n_rt, m_tiles, G, 1);
-  return 2;
+  if (G > 1) {
+    dim3 rg((unsigned)(G - 1), BN / 8);
+    launch_pdl(ws_reduce_kernel<BN>, rg, dim3(256), 0, st, a, n_rt, m_tiles, G, 1, 0);
+  }
+  return G > 1 ? 2 : 1;
 }
 
 
-template <int BN, int KBU>
+template <int BN, int KBU, int NACC = 2, int UW = 8>
 static int run_tm(const LinearArgs& a, cudaStream_t st) {
-  using C = TmCfg<BN, KBU>;
+  using C = TmCfg<BN, KBU, NACC, UW>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(gemm_tm_kernel<BN, KBU>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(gemm_tm_kernel<BN, KBU, NACC, UW>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr_set = true;
   }
   const int n_rt = (a.N + 127) / 128, m_tiles = (a.M + BN - 1) / BN, n_kb = a.K / 64;
   const int n_pairs = (n_rt + 1) / 2, n_ku = n_kb / KBU;
   const int64_t U = (int64_t)n_pairs * m_tiles * n_ku;
   const int G = (int)std::max<int64_t>(1, std::min<int64_t>(a.num_sms, U / (8 / KBU)));
-  const int64_t tiles = (int64_t)n_pairs * m_tiles;
   if ((int64_t)2 * G * 2 * BN * 128 > a.ws_floats || U * G >= (1ll << 32)) return -1;
   CUtensorMap map;
   if (!make_xmap(&map, a.x, a.M, a.K, BN)) return -1;
   static const int dbg = getenv("PIPO_WS_DEBUG") ? atoi(getenv("PIPO_WS_DEBUG")) : 0;
-  gemm_tm_kernel<BN, KBU><<<G, TM_THREADS, C::SMEM, st>>>(map, a, n_rt, m_tiles, G, dbg);
-  dim3 rg((unsigned)tiles, BN / 8);
-  ws_reduce_kernel<BN><<<rg, 256, 0, st>>>(a, n_rt, m_tiles, G, KBU);
-  return 2;
+  launch_pdl(gemm_tm_kernel<BN, KBU, NACC, UW>, dim3(G), dim3(C::THREADS), C::SMEM, st, map, a, n_rt, m_tiles, G, dbg);
+  if (dbg & 64) return 1;   // debug: main kernel only
+  if (G > 1) {
+    dim3 rg((unsigned)(G - 1), BN / 8);
+    launch_pdl(ws_reduce_kernel<BN>, rg, dim3(256), 0, st, a, n_rt, m_tiles, G, KBU, dbg);
+  }
+  return G > 1 ? 2 : 1;
 }
 
 int launch_linear_tm(const LinearArgs& a, cudaStream_t st) {
@@ -788,8 +894,301 @@ int launch_linear_tm(const LinearArgs& a, cudaStream_t st) {
   const bool even = (a.K / 64) % 2 == 0;
   if (a.M <= 16) return even ? run_tm<16, 2>(a, st) : run_tm<16, 1>(a, st);
   if (a.M <= 32) return even ? run_tm<32, 2>(a, st) : run_tm<32, 1>(a, st);
-  if (a.M <= 64) return even ? run_tm<64, 2>(a, st) : run_tm<64, 1>(a, st);
+  if (a.M <= 64) {
+    const char* env = getenv("PIPO_TM_CFG");   // tuning hook: (NACC, unpack warps) variants
+    switch (env ? atoi(env) : 0) {
+      case 1: return even ? run_tm<64, 2, 1, 8>(a, st) : run_tm<64, 1, 1, 8>(a, st);
+      case 2: return even ? run_tm<64, 2, 2, 16>(a, st) : run_tm<64, 1, 2, 16>(a, st);
+      case 3: return even ? run_tm<64, 2, 1, 16>(a, st) : run_tm<64, 1, 1, 16>(a, st);
+      case 4: return run_tm<64, 1, 2, 16>(a, st);
+      default: return even ? run_tm<64, 2>(a, st) : run_tm<64, 1>(a, st);
+    }
+  }
   return -1;
+}
+
+// ---------------------------------------------------------------------------------
+// Prefill: the same roles as gemm_tm_kernel (A = dequantized weights in TMEM, x by TMA,
+// one elected MMA lane), scheduled for M = b*P >> 128 where the GEMM is tensor-bound.
+//  * static persistent schedule: CTA c owns output tiles c, c+G, ... and the whole K
+//    of each (no stream-K partials, no reduce pass);
+//  * tile order = weight-tile group fastest: at any moment the 148 CTAs work on ~2
+//    token tiles, so the x tile is read from HBM about once and the weights (<= 110 MB
+//    per matrix) stay resident in the 126 MB L2 across token tiles;
+//  * TILES weight tiles (128 rows each) share one x stage: x is reused 128*TILES times
+//    per load, each dequantized weight BN times;
+//  * NACC accumulator sets (TILES*BN TMEM columns each); with NACC = 2 the epilogue of
+//    tile i overlaps the MMAs of tile i+1;
+//  * EPW epilogue warps (4 or 8): with 8, two warps share each TMEM lane quarter and
+//    split the columns.
+template <int BN, int TILES, int NACC, int EPW>
+struct TpCfg {
+  static constexpr int RAW_T = (int)kInt4BlockBytes;
+  static constexpr int RAW = TILES * RAW_T;
+  static constexpr int NR = 12;
+  static constexpr int X_KB = BN * 128;
+  static constexpr int NX_MAX = (200 * 1024 - NR * RAW) / X_KB;
+  static constexpr int NX = NX_MAX > 8 ? 8 : NX_MAX;
+  static constexpr int ACC_COLS = NACC * TILES * BN;
+  static constexpr int A_COLS = TILES * 32;
+  static constexpr int NA = (512 - ACC_COLS) / A_COLS < 8 ? (512 - ACC_COLS) / A_COLS : 8;
+  static constexpr int THREADS = (10 + EPW + 1) * 32;   // x producer is the last warp
+  static constexpr int XW = 10 + EPW;
+  static constexpr int SMEM = 1024 + NX * X_KB + NR * RAW + 512;
+  static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
+  static_assert(NX >= 3, "x ring depth");
+  static_assert(NA >= 2, "TMEM budget");
+  static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "MMA N");
+  static_assert(EPW == 4 || EPW == 8, "epilogue warps");
+};
+
+
+template <int BN, int TILES, int NACC, int EPW>
+__global__ void __launch_bounds__(TpCfg<BN, TILES, NACC, EPW>::THREADS, 1)
+    gemm_tp_kernel(const __grid_constant__ CUtensorMap xmap, LinearArgs a, int n_rt, int m_tiles) {
+  using C = TpCfg<BN, TILES, NACC, EPW>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  uint8_t* base = smem_raw + (base_u32 - smem_u32(smem_raw));
+  uint8_t* xs = base;
+  uint8_t* raw = xs + C::NX * C::X_KB;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(raw + C::NR * C::RAW);
+  uint64_t* raw_full = bar;
+  uint64_t* raw_empty = raw_full + C::NR;
+  uint64_t* x_full = raw_empty + C::NR;
+  uint64_t* x_empty = x_full + C::NX;
+  uint64_t* a_full = x_empty + C::NX;
+  uint64_t* a_empty = a_full + C::NA;
+  uint64_t* acc_full = a_empty + C::NA;
+  uint64_t* acc_empty = acc_full + NACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + NACC);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n_kb = a.K / 64;
+  const int n_grp = (n_rt + TILES - 1) / TILES;
+  const int n_tiles = n_grp * m_tiles;
+  const int G = gridDim.x;
+
+  if (tid == 0) {
+    for (int i = 0; i < C::NR; ++i) { ws::mbar_init(&raw_full[i], 1); ws::mbar_init(&raw_empty[i], 8); }
+    for (int i = 0; i < C::NX; ++i) { ws::mbar_init(&x_full[i], 1); ws::mbar_init(&x_empty[i], 1); }
+    for (int i = 0; i < C::NA; ++i) { ws::mbar_init(&a_full[i], 8); ws::mbar_init(&a_empty[i], 1); }
+    for (int i = 0; i < NACC; ++i) { ws::mbar_init(&acc_full[i], 1); ws::mbar_init(&acc_empty[i], EPW); }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&xmap) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512u));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  ws::tc_before();
+  __syncthreads();
+  ws::tc_after();
+  const uint32_t tmem = *tmem_slot;
+  ws::griddep_wait();     // predecessor (producer of x, reader of the partials) has finished
+  ws::griddep_launch();   // the stream-K reduce may be scheduled now
+  const uint32_t a_base = tmem + C::ACC_COLS;
+
+  if (warp == 0) {
+    // ---------------- raw int4 producer: one bulk copy per weight tile and k-block ----------------
+    if (lane == 0) {
+      const int64_t tile_stride = (int64_t)n_kb * kInt4BlockBytes;
+      int s = 0;
+      uint32_t ph = 1;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += G) {
+        const int grp = tile % n_grp;
+        const int nt = min(TILES, n_rt - grp * TILES);
+        const uint8_t* wsrc = a.w + (int64_t)(grp * TILES) * tile_stride;
+        for (int kb = 0; kb < n_kb; ++kb) {
+          ws::mbar_wait(&raw_empty[s], ph);
+          ws::mbar_expect_tx(&raw_full[s], nt * C::RAW_T);
+          for (int t = 0; t < nt; ++t)
+            ws::bulk_g2s(raw + s * C::RAW + t * C::RAW_T, wsrc + t * tile_stride, C::RAW_T, &raw_full[s]);
+          wsrc += kInt4BlockBytes;
+          if (++s == C::NR) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == C::XW) {
+    // ---------------- x producer (TMA 2D, SWIZZLE_128B; rows >= M zero-filled) ----------------
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 1;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += G) {
+        const int mt = tile / n_grp;
+        for (int kb = 0; kb < n_kb; ++kb) {
+          ws::mbar_wait(&x_empty[s], ph);
+          ws::mbar_expect_tx(&x_full[s], C::X_KB);
+          ws::tma_2d(xs + s * C::X_KB, &xmap, kb * 64, mt * BN, &x_full[s]);
+          if (++s == C::NX) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    int sa = 0, sx = 0, seg = 0;
+    uint32_t ph_a = 0, ph_x = 0;
+    const uint32_t xs_base = smem_u32(xs);
+    for (int tile = blockIdx.x; tile < n_tiles; tile += G, ++seg) {
+      const int grp = tile % n_grp;
+      const int nt = min(TILES, n_rt - grp * TILES);
+      const int ab = seg % NACC;
+      ws::mbar_wait(&acc_empty[ab], ((seg / NACC) & 1) ^ 1);
+      ws::tc_after();
+      const uint32_t d = tmem + ab * (TILES * BN);
+      for (int kb = 0; kb < n_kb; ++kb) {
+        ws::mbar_wait(&a_full[sa], ph_a);
+        ws::mbar_wait(&x_full[sx], ph_x);
+        ws::tc_after();
+        if (ws::elect_one()) {
+          const uint32_t at = a_base + sa * C::A_COLS;
+          const uint64_t db0 = ws::sw128_desc(xs_base + sx * C::X_KB);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
+            const uint64_t db = db0 + (uint64_t)((kk * 32) >> 4);
+#pragma unroll
+            for (int t = 0; t < TILES; ++t)
+              if (t < nt) mma_f16_ts(d + t * BN, at + t * 32 + kk * 8, db, C::IDESC, acc);
+          }
+          ws::mma_commit(&a_empty[sa]);
+          ws::mma_commit(&x_empty[sx]);
+        }
+        __syncwarp();
+        if (++sa == C::NA) { sa = 0; ph_a ^= 1; }
+        if (++sx == C::NX) { sx = 0; ph_x ^= 1; }
+      }
+      if (ws::elect_one()) ws::mma_commit(&acc_full[ab]);
+      __syncwarp();
+    }
+  } else if (warp < 10) {
+    // ---------------- unpack + scale into TMEM ----------------
+    // TILES = 2: warp -> (tile (w-2)/4, lane quarter w%4), both 32-code halves of a row;
+    // TILES = 1: warp -> (half (w-2)/4, lane quarter w%4), one 32-code half.
+    const int g = (warp - 2) >> 2, q = warp & 3;
+    const int r = q * 32 + lane;
+    const int t = TILES == 2 ? g : 0;
+    int s = 0, sa = 0;
+    uint32_t ph_r = 0, ph_a = 1;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += G) {
+      for (int kb = 0; kb < n_kb; ++kb) {
+        ws::mbar_wait(&raw_full[s], ph_r);
+        const uint8_t* rs = raw + s * C::RAW + t * C::RAW_T;
+        uint4 cw0, cw1;
+        if (TILES == 2) {
+          cw0 = *reinterpret_cast<const uint4*>(rs + r * 16);
+          cw1 = *reinterpret_cast<const uint4*>(rs + (128 + r) * 16);
+        } else {
+          cw0 = *reinterpret_cast<const uint4*>(rs + (g * 128 + r) * 16);
+        }
+        const __half2 s2 = __half2half2(*reinterpret_cast<const __half*>(rs + 4096 + r * 2));
+        __syncwarp();
+        if (lane == 0) ws::mbar_arrive(&raw_empty[s]);
+        ws::mbar_wait(&a_empty[sa], ph_a);
+        ws::tc_after();
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        if (TILES == 2) {
+          uint32_t o[32];
+          const uint32_t w[8] = {cw0.x, cw0.y, cw0.z, cw0.w, cw1.x, cw1.y, cw1.z, cw1.w};
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch) dequant8(w[ch], s2, reinterpret_cast<__half2*>(o + ch * 4));
+          tmem_st32(a_base + sa * C::A_COLS + t * 32 + lane_off, o);
+        } else {
+          uint32_t o[16];
+          const uint32_t w[4] = {cw0.x, cw0.y, cw0.z, cw0.w};
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) dequant8(w[ch], s2, reinterpret_cast<__half2*>(o + ch * 4));
+          tmem_st16(a_base + sa * C::A_COLS + g * 16 + lane_off, o);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        ws::tc_before();
+        __syncwarp();
+        if (lane == 0) ws::mbar_arrive(&a_full[sa]);
+        if (++s == C::NR) { s = 0; ph_r ^= 1; }
+        if (++sa == C::NA) { sa = 0; ph_a ^= 1; }
+      }
+    }
+  } else if (warp < C::XW) {
+    // ---------------- epilogue ----------------
+    const int quarter = warp & 3, part = (warp - 10) >> 2;
+    constexpr int PARTS = EPW / 4;
+    const int row = quarter * 32 + lane;
+    int seg = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += G, ++seg) {
+      const int grp = tile % n_grp, mt = tile / n_grp;
+      const int nt = min(TILES, n_rt - grp * TILES);
+      const int ab = seg % NACC;
+      {
+        uint32_t done = 0;
+        const uint32_t addr = smem_u32(&acc_full[ab]), par = (seg / NACC) & 1;
+        while (true) {
+          asm volatile(
+              "{\n.reg .pred P1;\nmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
+              : "=r"(done)
+              : "r"(addr), "r"(par)
+              : "memory");
+          if (done) break;
+          __nanosleep(64);
+        }
+      }
+      ws::tc_after();
+      const int m0 = mt * BN;
+      for (int tt = 0; tt < nt; ++tt) {
+        const uint32_t t_row = tmem + ab * (TILES * BN) + tt * BN + ((uint32_t)(quarter * 32) << 16);
+        const int n = (grp * TILES + tt) * 128 + row;
+        for (int c0 = part * 16; c0 < BN; c0 += 16 * PARTS) {
+          if (m0 + c0 >= a.M) break;
+          float v[16];
+          ws::tmem_ld16(t_row + c0, v);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) epi_store(a.epi, m0 + c0 + j, n, v[j]);
+        }
+      }
+      ws::tc_before();
+      __syncwarp();
+      if (lane == 0) ws::mbar_arrive(&acc_empty[ab]);
+    }
+  }
+  __syncwarp();
+  ws::tc_before();
+  __syncthreads();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512u));
+}
+
+template <int BN, int TILES, int NACC, int EPW>
+static int run_tp(const LinearArgs& a, cudaStream_t st) {
+  using C = TpCfg<BN, TILES, NACC, EPW>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(gemm_tp_kernel<BN, TILES, NACC, EPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    attr_set = true;
+  }
+  const int n_rt = (a.N + 127) / 128, m_tiles = (a.M + BN - 1) / BN;
+  const int64_t n_tiles = (int64_t)((n_rt + TILES - 1) / TILES) * m_tiles;
+  if (n_tiles >= (1ll << 31)) return -1;
+  const int G = (int)std::min<int64_t>(a.num_sms, n_tiles);
+  CUtensorMap map;
+  if (!make_xmap(&map, a.x, a.M, a.K, BN)) return -1;
+  launch_pdl(gemm_tp_kernel<BN, TILES, NACC, EPW>, dim3(G), dim3(C::THREADS), C::SMEM, st, map, a, n_rt, m_tiles);
+  return 1;
+}
+
+int launch_linear_tp(const LinearArgs& a, cudaStream_t st) {
+  if (a.wfmt != 1) return -1;
+  const char* env = getenv("PIPO_TP_CFG");   // tuning / test hook: tile configuration
+  const int cfg = env ? atoi(env) : 0;
+  // measured at the OPT prefill shapes (tools/tpbench.py, profiles/r01): 256-token x
+  // 128-row tiles with 8 epilogue warps win (1.15-1.32 PFLOP/s at c5)
+  switch (cfg) {
+    case 1: return run_tp<96, 2, 2, 4>(a, st);
+    case 2: return run_tp<128, 2, 1, 8>(a, st);
+    case 3: return run_tp<128, 1, 2, 4>(a, st);
+    case 4: return run_tp<128, 2, 1, 4>(a, st);
+    default: return run_tp<256, 1, 1, 8>(a, st);
+  }
 }
 
 int launch_linear_ws(const LinearArgs& a, cudaStream_t st) {

@@ -328,6 +328,7 @@ int launch_linear(const LinearArgs& a, int path, int gemv_max_m, cudaStream_t st
   bool gemv = false;
   if (path == PATH_GEMV) gemv = true;
   else if (path == PATH_AUTO) gemv = (a.wfmt == 1 && a.M <= gemv_max_m);
+  if (path == PATH_TP || (path == PATH_AUTO && !gemv && a.wfmt == 1 && a.M > 128)) return launch_linear_tp(a, st);
   if (path == PATH_TM || (path == PATH_AUTO && !gemv && a.wfmt == 1 && a.M <= 64)) return launch_linear_tm(a, st);
   if (path == PATH_WS || (path == PATH_AUTO && !gemv && a.wfmt == 1 && a.M <= 128)) return launch_linear_ws(a, st);
   if (path == PATH_TC || (path == PATH_AUTO && !gemv)) return launch_linear_tc(a, st);

@@ -44,10 +44,11 @@ struct LinearArgs {
   int num_sms = 148;
 };
 
-enum LinearPath { PATH_AUTO = 0, PATH_GEMV = 1, PATH_GEMM = 2, PATH_TC = 3, PATH_WS = 4, PATH_TM = 5 };
+enum LinearPath { PATH_AUTO = 0, PATH_GEMV = 1, PATH_GEMM = 2, PATH_TC = 3, PATH_WS = 4, PATH_TM = 5, PATH_TP = 6 };
 
 // warp-specialized stream-K tcgen05 GEMM with A in TMEM, int4 weights, M <= 64
 int launch_linear_tm(const LinearArgs& a, cudaStream_t st);
+int launch_linear_tp(const LinearArgs& a, cudaStream_t st);
 
 // warp-specialized stream-K tcgen05 GEMM, int4 weights (k_gemm_ws.cu)
 int launch_linear_ws(const LinearArgs& a, cudaStream_t st);

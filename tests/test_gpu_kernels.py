@@ -60,7 +60,8 @@ def _ref_linear(x16, w, bias, wfmt):
 
 
 SHAPES = [(1, 128, 64), (3, 200, 256), (4, 384, 1024), (13, 130, 512), (16, 256, 256), (17, 384, 320),
-          (40, 200, 1024), (64, 512, 2048), (100, 256, 192), (130, 384, 512), (300, 256, 320), (64, 7168, 7168)]
+          (40, 200, 1024), (64, 512, 2048), (100, 256, 192), (130, 384, 512), (300, 256, 320), (64, 7168, 7168), (1000, 640, 384),
+          (512, 1152, 1024)]
 
 
 @pytest.mark.parametrize("M,N,K", SHAPES)
@@ -73,7 +74,8 @@ def test_linear_vs_oracle(env, M, N, K, wfmt):
     bias = (rng.uniform(-0.02, 0.02, N)).astype(np.float32)
     ref = _ref_linear(x, w, bias, wfmt)
     paths = [pipo.PATH_TC, pipo.PATH_GEMM] + ([pipo.PATH_GEMV] if wfmt == 1 and M <= 16 else []) + \
-        ([pipo.PATH_WS] if wfmt == 1 and M <= 128 else []) + ([pipo.PATH_TM] if wfmt == 1 and M <= 64 else [])
+        ([pipo.PATH_WS] if wfmt == 1 and M <= 128 else []) + ([pipo.PATH_TM] if wfmt == 1 and M <= 64 else []) + \
+        ([pipo.PATH_TP] if wfmt == 1 else [])
     for path in paths:
         y = pipo.pipo_linear(pl.ctx, wfmt, path, x, w, bias)
         err = rel_inf(y, ref)
@@ -82,10 +84,56 @@ def test_linear_vs_oracle(env, M, N, K, wfmt):
         assert err < (2e-3 if wfmt == 1 else 1e-4), (path, err)
 
 
-@pytest.mark.parametrize("path", ["gemv", "gemm", "tc", "ws", "tm"])
+TM_CFGS = ["0", "1", "2", "3", "4"]   # PIPO_TM_CFG: decode TMEM-A variants (accumulators, unpack warps)
+
+
+@pytest.mark.parametrize("cfg", TM_CFGS)
+@pytest.mark.parametrize("M,N,K", [(64, 512, 2048), (40, 200, 1024), (33, 384, 320), (64, 2304, 7168)])
+def test_linear_tm_configs(env, cfg, M, N, K, monkeypatch):
+    pipo, pl = env
+    monkeypatch.setenv("PIPO_TM_CFG", cfg)
+    rng = np.random.default_rng(M * 3 + N + K)
+    x = rng.standard_normal((M, K)).astype(np.float16)
+    w = (rng.standard_normal((N, K)) * 0.02).astype(np.float16).astype(np.float32)
+    bias = (rng.uniform(-0.02, 0.02, N)).astype(np.float32)
+    y = pipo.pipo_linear(pl.ctx, 1, pipo.PATH_TM, x, w, bias)
+    assert rel_inf(y, _ref_linear(x, w, bias, 1)) < 2e-3
+    # deterministic stream-K: identical to the default configuration bit for bit
+    monkeypatch.setenv("PIPO_TM_CFG", "0")
+    assert np.array_equal(y, pipo.pipo_linear(pl.ctx, 1, pipo.PATH_TM, x, w, bias))
+
+
+TP_CFGS = ["0", "1", "2", "3", "4"]   # PIPO_TP_CFG: prefill tile configurations (k_gemm_ws.cu)
+
+
+@pytest.mark.parametrize("cfg", TP_CFGS)
+@pytest.mark.parametrize("M,N,K", [(1, 128, 64), (97, 384, 320), (300, 640, 512), (1000, 1152, 256)])
+def test_linear_prefill_configs(env, cfg, M, N, K, monkeypatch):
+    pipo, pl = env
+    monkeypatch.setenv("PIPO_TP_CFG", cfg)
+    rng = np.random.default_rng(M + N + K)
+    x = rng.standard_normal((M, K)).astype(np.float16)
+    w = (rng.standard_normal((N, K)) * 0.02).astype(np.float16).astype(np.float32)
+    bias = (rng.uniform(-0.02, 0.02, N)).astype(np.float32)
+    ref = _ref_linear(x, w, bias, 1)
+    y = pipo.pipo_linear(pl.ctx, 1, pipo.PATH_TP, x, w, bias)
+    assert rel_inf(y, ref) < 2e-3
+    # one-hot rows -> dequantized columns exactly (fp16_rne(q*s) + bias, one rounding)
+    q, s = quant.quantize_int4_g64(w)
+    col = quant.dequantize(q, s).astype(np.float16).astype(np.float32)
+    xo = np.zeros((M, K), np.float16)
+    ks = np.arange(M) % K
+    xo[np.arange(M), ks] = 1
+    yo = pipo.pipo_linear(pl.ctx, 1, pipo.PATH_TP, xo, w, bias)
+    b16 = bias.astype(np.float16).astype(np.float32)          # the library stores biases in fp16
+    assert np.array_equal(yo, (col[:, ks].T + b16).astype(np.float32))
+
+
+@pytest.mark.parametrize("path", ["gemv", "gemm", "tc", "ws", "tm", "tp"])
 def test_linear_special_cases_exact(env, path):
     pipo, pl = env
-    p = {"gemv": pipo.PATH_GEMV, "gemm": pipo.PATH_GEMM, "tc": pipo.PATH_TC, "ws": pipo.PATH_WS, "tm": pipo.PATH_TM}[path]
+    p = {"gemv": pipo.PATH_GEMV, "gemm": pipo.PATH_GEMM, "tc": pipo.PATH_TC, "ws": pipo.PATH_WS, "tm": pipo.PATH_TM,
+         "tp": pipo.PATH_TP}[path]
     rng = np.random.default_rng(5)
     N, K = 200, 256
     w = (rng.standard_normal((N, K)) * 0.02).astype(np.float16).astype(np.float32)
