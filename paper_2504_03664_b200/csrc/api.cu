@@ -1138,6 +1138,16 @@ pipo_status pipo_bench_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, int32_t
       std::sort(v.begin(), v.end());
       if (!v.empty()) fprintf(stderr, "tm-stamp %-8s min %7.2f med %7.2f max %7.2f us (n=%zu)\n", nm[k - 9], v.front(), v[v.size() / 2], v.back(), v.size());
     }
+    {   // same-CTA ordering check: exit (after the final __syncthreads) minus MMA / epilogue end
+      double lo = 1e30, hi = -1e30, lo2 = 1e30;
+      for (int c = 0; c < 148; ++c) {
+        if (!ts[c * 16 + 13] || !ts[c * 16 + 11]) continue;
+        const double dm = (double)(int64_t)(ts[c * 16 + 13] - ts[c * 16 + 11]) * 1e-3;
+        const double de = (double)(int64_t)(ts[c * 16 + 13] - ts[c * 16 + 12]) * 1e-3;
+        lo = std::min(lo, dm); hi = std::max(hi, dm); lo2 = std::min(lo2, de);
+      }
+      fprintf(stderr, "tm-stamp per-CTA exit-mma_end min %.2f max %.2f us, exit-epi_end min %.2f us\n", lo, hi, lo2);
+    }
     fprintf(stderr, "reduce first start %.2f last end %.2f us\n", (double)(int64_t)(ts[148 * 16] - t0) * 1e-3, (double)(int64_t)(ts[148 * 16 + 1] - t0) * 1e-3);
   } else if (getenv("PIPO_WS_DEBUG") && (atoi(getenv("PIPO_WS_DEBUG")) & 32) && path == 5) {
     std::vector<uint64_t> wt(148 * 16);

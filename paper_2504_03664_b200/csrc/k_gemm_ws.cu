@@ -595,9 +595,13 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
       for (int64_t u = u0; u < u1; ++u) {
         const bool two = 2 * pr + 1 < n_rt;
         TWAIT(0, &raw_empty[s], ph);
-        ws::mbar_expect_tx(&raw_full[s], two ? C::RAW : C::RAW_T);
-        ws::bulk_g2s(raw + s * C::RAW, wsrc, C::RAW_T, &raw_full[s]);
-        if (two) ws::bulk_g2s(raw + s * C::RAW + C::RAW_T, wsrc + tile_stride, C::RAW_T, &raw_full[s]);
+        if (dbg & 16) {   // debug: no weight traffic (stale stage contents)
+          ws::mbar_arrive(&raw_full[s]);
+        } else {
+          ws::mbar_expect_tx(&raw_full[s], two ? C::RAW : C::RAW_T);
+          ws::bulk_g2s(raw + s * C::RAW, wsrc, C::RAW_T, &raw_full[s]);
+          if (two) ws::bulk_g2s(raw + s * C::RAW + C::RAW_T, wsrc + tile_stride, C::RAW_T, &raw_full[s]);
+        }
         wsrc += C::RAW_T;
         if (++ku == n_ku) {
           ku = 0;
@@ -617,10 +621,14 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
       uint32_t ph = 1;
       for (int64_t u = u0; u < u1; ++u) {
         TWAIT(0, &x_empty[s], ph);
-        ws::mbar_expect_tx(&x_full[s], C::X_TILE);
+        if (dbg & 8) {   // debug: no activation traffic (stale stage contents)
+          ws::mbar_arrive(&x_full[s]);
+        } else {
+          ws::mbar_expect_tx(&x_full[s], C::X_TILE);
 #pragma unroll
-        for (int k = 0; k < KBU; ++k)
-          ws::tma_2d(xs + s * C::X_TILE + k * C::X_KB, &xmap, (ku * KBU + k) * 64, mt * BN, &x_full[s]);
+          for (int k = 0; k < KBU; ++k)
+            ws::tma_2d(xs + s * C::X_TILE + k * C::X_KB, &xmap, (ku * KBU + k) * 64, mt * BN, &x_full[s]);
+        }
         if (++ku == n_ku) {
           ku = 0;
           if (++pr == n_pairs) { pr = 0; ++mt; }
