@@ -1131,8 +1131,8 @@ pipo_status pipo_bench_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, int32_t
     CK(cudaMemcpy(ts.data(), ctx->ws + (15ll << 20), ts.size() * 8, cudaMemcpyDeviceToHost));
     uint64_t t0 = ~0ull;
     for (int c = 0; c < 148; ++c) if (ts[c * 16 + 9]) t0 = std::min(t0, ts[c * 16 + 9]);
-    const char* nm[5] = {"entry", "setup", "mma_end", "epi_end", "exit"};
-    for (int k = 9; k <= 13; ++k) {
+    const char* nm[6] = {"entry", "setup", "mma_end", "epi_end", "exit", "fixup_end"};
+    for (int k = 9; k <= 14; ++k) {
       std::vector<double> v;
       for (int c = 0; c < 148; ++c) if (ts[c * 16 + k] >= t0 && ts[c * 16 + k] - t0 < 10000000ull) v.push_back((ts[c * 16 + k] - t0) * 1e-3);
       std::sort(v.begin(), v.end());
@@ -1147,6 +1147,12 @@ pipo_status pipo_bench_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, int32_t
         lo = std::min(lo, dm); hi = std::max(hi, dm); lo2 = std::min(lo2, de);
       }
       fprintf(stderr, "tm-stamp per-CTA exit-mma_end min %.2f max %.2f us, exit-epi_end min %.2f us\n", lo, hi, lo2);
+      double fx = 0, bm = 0;
+      for (int c = 0; c < 148; ++c) { fx += (double)ts[c * 16] / 148; bm += (double)(int64_t)ts[c * 16 + 1] / 148; }
+      fprintf(stderr, "tm-clk fixup %.0f cycles, barrier-after-MMA-end %.0f cycles (avg over CTAs)\n", fx, bm);
+      double sp = 0, lp = 0, ww = 0;
+      for (int c = 0; c < 148; ++c) { sp += (double)ts[c * 16 + 3] / 148; lp += (double)ts[c * 16 + 4] / 148; ww += (double)ts[c * 16 + 5] / 148; }
+      fprintf(stderr, "tm-clk fixup spin %.0f loop %.0f cycles, items %.0f\n", sp, lp, ww);
     }
     fprintf(stderr, "reduce first start %.2f last end %.2f us\n", (double)(int64_t)(ts[148 * 16] - t0) * 1e-3, (double)(int64_t)(ts[148 * 16 + 1] - t0) * 1e-3);
   } else if (getenv("PIPO_WS_DEBUG") && (atoi(getenv("PIPO_WS_DEBUG")) & 32) && path == 5) {

@@ -515,9 +515,121 @@ __device__ __forceinline__ uint64_t clk() {
   return t;
 }
 
+// In-kernel stream-K fixup (replaces the ws_reduce_kernel launch).  Every CTA has written
+// the partial accumulators of its shared tiles (<= 2: the tile it entered mid-way and the
+// one it left mid-way) to its ws slots and fenced them.  For each shared tile t with
+// contributors cf..cl it bumps arrive[t]; once all n = cl-cf+1 have arrived, contributor
+// i sums the n partials of element share i (contiguous ws range, coalesced) in k order —
+// the same order for every share and every run, so results are bit-reproducible — and
+// runs the fused epilogue on it.  The n contributors reduce in parallel (no single
+// last-arriver serialising the whole tile).  Spinning is safe: grid <= #SMs with one CTA
+// per SM, and the CTAs waited on never wait on anything scheduled after them.
+// done[t] (second half of the counter array) lets the last finisher reset both counters.
+template <int BN>
+__device__ __forceinline__ void tm_fixup(const LinearArgs& a, int64_t u0, int64_t u1, int n_ku, int n_pairs,
+                                         int n_rt, int64_t U, int G, uint64_t* dbgts) {
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  int* arrive = a.counters;
+  int* done = a.counters + (a.n_counters >> 1);
+  // the CTA's shared tiles: at most its first and its last tile
+  int64_t pt[2];
+  int np = 0;
+  const int64_t t_first = u0 / n_ku, t_last = (u1 - 1) / n_ku;
+  if (u0 > t_first * n_ku || u1 < (t_first + 1) * n_ku) pt[np++] = t_first;
+  if (t_last != t_first && u1 < (t_last + 1) * n_ku) pt[np++] = t_last;
+  if (np == 0) return;
+  int cf[2], n[2], i0[2], w0[2], w1[2], base[2];
+  bool cff[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    if (k >= np) { w0[k] = w1[k] = 0; continue; }
+    const int64_t t = pt[k];
+    cf[k] = ws::cta_of_unit(t * n_ku, U, G);
+    n[k] = ws::cta_of_unit((t + 1) * n_ku - 1, U, G) - cf[k] + 1;
+    i0[k] = (int)blockIdx.x - cf[k];
+    cff[k] = ws::u_begin(cf[k], U, G) / n_ku == t;   // t is cf's first tile -> its slot 0
+    const int pr = (int)(t % n_pairs);
+    const int E4 = ((2 * pr + 1 < n_rt) ? 2 : 1) * BN * 32;   // float4 items of the tile
+    w0[k] = (int)((int64_t)E4 * i0[k] / n[k]);
+    w1[k] = (int)((int64_t)E4 * (i0[k] + 1) / n[k]);
+  }
+  base[0] = 0;
+  base[1] = w1[0] - w0[0];
+  const int W = base[1] + (w1[1] - w0[1]);
+  const uint64_t c0 = clk();
+  if (tid == 0) {
+    for (int k = 0; k < np; ++k) atomicAdd(&arrive[pt[k]], 1);
+    for (int k = 0; k < np; ++k)
+      while (*reinterpret_cast<volatile int*>(&arrive[pt[k]]) < n[k]) __nanosleep(20);
+    __threadfence();
+  }
+  __syncthreads();
+  const uint64_t c1 = clk();
+  // each thread: up to 2 float4 items, contributors in batches of 4, all loads issued
+  // before the (k-ordered) sums
+  for (int wb = 0; wb < W; wb += 2 * nthr) {
+    float4 acc[2];
+    int kk[2], e4[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int w = wb + tid + j * nthr;
+      acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      kk[j] = w < W ? (w >= base[1] ? 1 : 0) : -1;
+      e4[j] = kk[j] >= 0 ? w0[kk[j]] + (w - base[kk[j]]) : 0;
+    }
+    const int nmax = max(kk[0] >= 0 ? n[kk[0]] : 0, kk[1] >= 0 ? n[kk[1]] : 0);
+    for (int cb = 0; cb < nmax; cb += 4) {
+      float4 v[2][4];
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int k = kk[j];
+          const int cc = cb + q;
+          if (k >= 0 && cc < n[k]) {
+            const int c = cf[k] + cc;
+            const int sl = 2 * c + ((cc == 0 && !cff[k]) ? 1 : 0);
+            v[j][q] = __ldcg(reinterpret_cast<const float4*>(a.ws + (int64_t)sl * (2 * BN * 128)) + e4[j]);
+          } else {
+            v[j][q] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (kk[j] >= 0 && cb + q < n[kk[j]]) {
+            acc[j].x += v[j][q].x; acc[j].y += v[j][q].y; acc[j].z += v[j][q].z; acc[j].w += v[j][q].w;
+          }
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (kk[j] < 0) continue;
+      const int64_t t = pt[kk[j]];
+      const int pr = (int)(t % n_pairs), mt = (int)(t / n_pairs);
+      const int e = e4[j] * 4;
+      const int tt = e / (BN * 128), col = (e / 128) % BN, row = e & 127;
+      const int nn = (2 * pr + tt) * 128 + row, m = mt * BN + col;
+      epi_store(a.epi, m, nn, acc[j].x);
+      epi_store(a.epi, m, nn + 1, acc[j].y);
+      epi_store(a.epi, m, nn + 2, acc[j].z);
+      epi_store(a.epi, m, nn + 3, acc[j].w);
+    }
+  }
+  __syncthreads();
+  if (dbgts && tid == 0) { dbgts[3] = c1 - c0; dbgts[4] = clk() - c1; dbgts[5] = W; }
+  if (tid == 0)
+    for (int k = 0; k < np; ++k)
+      if (atomicAdd(&done[pt[k]], 1) == n[k] - 1) {   // every contributor is past its wait
+        arrive[pt[k]] = 0;
+        done[pt[k]] = 0;
+      }
+}
+
 template <int BN, int KBU, int NACC, int UW>
 __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
-    gemm_tm_kernel(const __grid_constant__ CUtensorMap xmap, LinearArgs a, int n_rt, int m_tiles, int G, int dbg) {
+    gemm_tm_kernel(const __grid_constant__ CUtensorMap xmap, LinearArgs a, int n_rt, int m_tiles, int G, int dbg,
+                   int fix) {
   using C = TmCfg<BN, KBU, NACC, UW>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -683,6 +795,7 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
       ++seg;
     }
     if (lane == 0) gstamp(11);
+    if (lane == 0 && ts) ts[2] = clk();
   } else if (warp < C::E0) {
     // ---------------- unpack + scale straight into TMEM ----------------
     // a warp may only touch its TMEM lane quarter (warp % 4).  UW = 8: warp -> (tile,
@@ -809,10 +922,15 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
 #undef TWAIT
   __syncwarp();
   ws::tc_before();
+  if (fix) __threadfence();   // partials visible device-wide before the arrival counters move
   __syncthreads();
   if (tid == 0) gstamp(13);
+  const uint64_t c13 = ts ? clk() : 0;
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512u));
+  if (fix && u1 > u0) tm_fixup<BN>(a, u0, u1, n_ku, n_pairs, n_rt, U, G, ts);
+  if (tid == 0) gstamp(14);
+  if (tid == 0 && ts) { ts[0] = clk() - c13; ts[1] = c13 - ts[2]; }   // cycles: fixup, barrier - MMA end
 }
 
 // ---------------------------------------------------------------------------------
@@ -888,8 +1006,17 @@ static int run_tm(const LinearArgs& a, cudaStream_t st) {
   CUtensorMap map;
   if (!make_xmap(&map, a.x, a.M, a.K, BN)) return -1;
   static const int dbg = getenv("PIPO_WS_DEBUG") ? atoi(getenv("PIPO_WS_DEBUG")) : 0;
-  launch_pdl(gemm_tm_kernel<BN, KBU, NACC, UW>, dim3(G), dim3(C::THREADS), C::SMEM, st, map, a, n_rt, m_tiles, G, dbg);
-  if (dbg & 64) return 1;   // debug: main kernel only
+  // stream-K fixup as a separate ws_reduce_kernel launch (default) or inside the GEMM
+  // (PIPO_TM_FIXUP=1: measured SLOWER on B200 — c5 QKV 48 vs 39 us; the partial reads
+  // right after the all-CTA partial-write burst run ~15k cycles per CTA, see DESIGN.md
+  // §6); the in-kernel fixup spins on other CTAs, so it needs every CTA co-resident:
+  // G <= #SMs, one CTA per SM.
+  static const int fix_env = getenv("PIPO_TM_FIXUP") ? atoi(getenv("PIPO_TM_FIXUP")) : 0;
+  const int64_t tiles = (int64_t)n_pairs * m_tiles;
+  const int fix = fix_env && G > 1 && G <= a.num_sms && 2 * tiles <= a.n_counters && !(dbg & 64) ? 1 : 0;
+  launch_pdl(gemm_tm_kernel<BN, KBU, NACC, UW>, dim3(G), dim3(C::THREADS), C::SMEM, st, map, a, n_rt, m_tiles, G, dbg,
+             fix);
+  if ((dbg & 64) || fix) return 1;   // debug: main kernel only / fixup done in-kernel
   if (G > 1) {
     dim3 rg((unsigned)(G - 1), BN / 8);
     launch_pdl(ws_reduce_kernel<BN>, rg, dim3(256), 0, st, a, n_rt, m_tiles, G, KBU, dbg);
