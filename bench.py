@@ -344,7 +344,7 @@ def run_pipo(args):
         tc = peaks.get("bf16_tflops_sustained") or 1400.0
         ach = per_unit_bytes / per_unit_s / 1e9
         roofline = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                    "frac": ach / hbm, "traffic": None,
+                    "frac": ach / hbm, "traffic": ncu_traffic(dom),
                     "bytes_per_unit": per_unit_bytes, "us_per_unit": per_unit_s * 1e6,
                     "tflops": kd["flops"] / kd["units"] / per_unit_s / 1e12,
                     "tflops_frac_of_fp16_peak": kd["flops"] / kd["units"] / per_unit_s / 1e12 / tc,
@@ -413,6 +413,18 @@ def run_pipo(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def ncu_traffic(cls):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the
+    class's kernel from the committed `ncu --set full` capture (profiles/ncu_traffic.json,
+    written by hand from tools/ncu_summary.py output), or None if not captured."""
+    try:
+        t = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")))
+    except (OSError, ValueError):
+        return None
+    e = t.get(cls)
+    return None if e is None else e["traffic_bytes_per_unit"]
 
 
 def main():

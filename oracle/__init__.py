@@ -20,5 +20,7 @@ SURVEY.md §8(c) step 1 / SPEC.md:485-493 define it.
 Modules:
   quant.py  — int4 group-64 symmetric quantize / pack / unpack / dequantize.
   opt.py    — OPT decoder forward (embed, pre-LN layers, LM head, greedy).
+  llama.py  — LLaMA3.1 decoder forward (NEXT-4: GQA, RoPE llama3, RMSNorm, SwiGLU,
+              untied LM head), pinned to transformers' LlamaForCausalLM.
   memory.py — PAPER.md §3.5 / App. B memory model (Eq. 1 planner inputs).
 """

@@ -197,3 +197,69 @@ def prompts(b: int, p: int, vocab: int, seed: int = PROMPT_SEED) -> np.ndarray:
     h = _hash(key, np.arange(b * p, dtype=np.uint64))
     ids = np.uint64(4) + h % np.uint64(vocab - 4)
     return ids.astype(np.int32).reshape(b, p)
+
+
+# ---------------------------------------------------------------------------------
+# LLaMA3.1-shaped models (NEXT-4; PAPER.md:318-331 §3.5, :390 §4.1).
+# Same generator and distributions ([ext] LlamaConfig initializer_range = 0.02; RMSNorm
+# weights drawn like LN gamma); tensor ids reuse the OPT slots where the role matches.
+T_LM_HEAD = 4   # embedding slot: untied LM head [V][d]
+
+
+@dataclass(frozen=True)
+class LlamaShape:
+    """LLaMA3.1 decoder shape ([ext] public Llama-3.1 configs): GQA with n_kv_heads,
+    SwiGLU MLP of width ffn_dim (= d_h), RoPE (llama3 frequency rule),
+    RMSNorm, untied LM head, no biases."""
+    d_model: int
+    n_layers: int
+    n_heads: int
+    n_kv_heads: int
+    ffn_dim: int
+    vocab: int = 128256
+    max_pos: int = 131072
+    rope_theta: float = 500000.0
+    rope_factor: float = 8.0          # llama3 rope_scaling (0 -> plain RoPE)
+    rope_low_freq: float = 1.0
+    rope_high_freq: float = 4.0
+    rope_orig_max_pos: int = 8192
+
+    @property
+    def head_dim(self) -> int:
+        return self.d_model // self.n_heads
+
+    @property
+    def d_kv(self) -> int:
+        return self.n_kv_heads * self.head_dim
+
+
+LLAMA31_8B = LlamaShape(4096, 32, 32, 8, 14336)
+
+
+def llama_layer_tensor_specs(s: LlamaShape):
+    d, f, dkv = s.d_model, s.ffn_dim, s.d_kv
+    return {
+        "ln1_g": (T_LN1_G, KIND_GAMMA, LN_A, (d,)),
+        "w_qkv": (T_W_QKV, KIND_NORMAL, W_STD, (d + 2 * dkv, d)),   # rows q | k | v
+        "w_out": (T_W_OUT, KIND_NORMAL, W_STD, (d, d)),
+        "ln2_g": (T_LN2_G, KIND_GAMMA, LN_A, (d,)),
+        "w_fc1": (T_W_FC1, KIND_NORMAL, W_STD, (2 * f, d)),         # rows gate | up
+        "w_fc2": (T_W_FC2, KIND_NORMAL, W_STD, (d, f)),             # down
+    }
+
+
+def llama_embed_tensor_specs(s: LlamaShape):
+    d = s.d_model
+    return {
+        "tok": (T_TOK, KIND_NORMAL, W_STD, (s.vocab, d)),
+        "lnf_g": (T_LNF_G, KIND_GAMMA, LN_A, (d,)),
+        "lm_head": (T_LM_HEAD, KIND_NORMAL, W_STD, (s.vocab, d)),
+    }
+
+
+def llama_layer_masters(s: LlamaShape, layer: int, seed: int = WEIGHT_SEED) -> dict:
+    return {k: _draw_spec(seed, layer + 1, v) for k, v in llama_layer_tensor_specs(s).items()}
+
+
+def llama_embed_masters(s: LlamaShape, seed: int = WEIGHT_SEED) -> dict:
+    return {k: _draw_spec(seed, 0, v) for k, v in llama_embed_tensor_specs(s).items()}
