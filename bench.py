@@ -40,6 +40,12 @@ CONFIGS = {
                desc="configs[3]: OPT-13B streamed weights from disk -> pinned host ring, b=64, P=512, gen 32"),
     "c5": dict(shape=synth.OPT_30B, b=64, P=512, G=32, weight_tier=1, kv_tier=0,
                desc="configs[4]: OPT-30B streamed weights, b=64/GPU, P=512, gen 32 (batch-sharded)"),
+    # NEXT-4: the paper's LLaMA3.1 family (§4.1)
+    "c6": dict(shape=synth.LLAMA31_8B, b=64, P=512, G=32, weight_tier=1, kv_tier=0,
+               desc="NEXT-4: LLaMA3.1-8B streamed int4 weights (GQA 32/8, SwiGLU 14336, RoPE llama3), b=64, P=512, gen 32"),
+    "c7": dict(shape=synth.LLAMA31_8B, b=1, P=512, G=32, weight_tier=1, kv_tier=0,
+               desc="NEXT-4: LLaMA3.1-8B streamed int4 weights, b=1, context 512, gen 32 (the paper's latency "
+                    "table PAPER.md:697-713: TTFT + per-token decode latency)"),
 }
 
 
@@ -165,30 +171,49 @@ class OracleSample:
     n_layers * t_layer + t_head.  Weights are drawn once (setup, untimed)."""
 
     def __init__(self, cfg_name: str, wfmt: str):
-        from oracle import opt
-        self.opt = opt
         c = CONFIGS[cfg_name]
         self.s, self.b, P, G = c["shape"], c["b"], c["P"], c["G"]
+        self.llama = isinstance(self.s, synth.LlamaShape)
         self.cores = len(os.sched_getaffinity(0))
-        self.lw = opt.layer_from_masters(synth.layer_masters(self.s, 0), wfmt)
-        emb = synth.embed_masters(self.s)
-        self.lnf = (emb["lnf_g"].astype(np.float64), emb["lnf_b"].astype(np.float64))
-        self.tok = emb["tok"].astype(np.float64)
+        d = self.s.d_model
+        if self.llama:
+            from oracle import llama
+            self.mod = llama
+            self.lw = llama.layer_from_masters(synth.llama_layer_masters(self.s, 0), wfmt)
+            spec = synth.llama_embed_tensor_specs(self.s)
+            self.lnf = synth._draw_spec(synth.WEIGHT_SEED, 0, spec["lnf_g"]).astype(np.float64)
+            self.head_w = synth._draw_spec(synth.WEIGHT_SEED, 0, spec["lm_head"]).astype(np.float64)
+            self.inv = llama.rope_inv_freq(self.s.head_dim, self.s.rope_theta, self.s.rope_factor,
+                                           self.s.rope_low_freq, self.s.rope_high_freq, self.s.rope_orig_max_pos)
+            dkv = self.s.d_kv
+        else:
+            from oracle import opt
+            self.mod = opt
+            self.lw = opt.layer_from_masters(synth.layer_masters(self.s, 0), wfmt)
+            emb = synth.embed_masters(self.s)
+            self.lnf = (emb["lnf_g"].astype(np.float64), emb["lnf_b"].astype(np.float64))
+            self.head_w = emb["tok"].astype(np.float64)
+            dkv = d
         self.past = P + G // 2 - 1
         rng = np.random.default_rng(0)
-        d = self.s.d_model
-        self.kc = rng.standard_normal((self.b, self.past + 1, d)) * 0.5
-        self.vc = rng.standard_normal((self.b, self.past + 1, d)) * 0.5
+        self.kc = rng.standard_normal((self.b, self.past + 1, dkv)) * 0.5
+        self.vc = rng.standard_normal((self.b, self.past + 1, dkv)) * 0.5
         self.h = rng.standard_normal((self.b, 1, d))
-        self.desc = (f"oracle/opt.py fp64: 1 of {self.s.n_layers} decoder layers + LM head at b={self.b}, "
-                     f"L={self.past + 1}, extrapolated x{self.s.n_layers} layers")
+        self.desc = (f"oracle/{'llama' if self.llama else 'opt'}.py fp64: 1 of {self.s.n_layers} decoder layers + "
+                     f"LM head at b={self.b}, L={self.past + 1}, extrapolated x{self.s.n_layers} layers")
 
     def step(self) -> float:
-        opt = self.opt
+        m = self.mod
         t0 = time.perf_counter()
-        h2 = opt.decoder_layer(self.h, self.lw, self.kc, self.vc, self.past, self.s.n_heads)
-        t1 = time.perf_counter()
-        opt.greedy(opt.layer_norm(h2[:, 0], *self.lnf) @ self.tok.T)
+        if self.llama:
+            h2 = m.decoder_layer(self.h, self.lw, self.kc, self.vc, self.past, self.s.n_heads, self.s.n_kv_heads,
+                                 self.inv)
+            t1 = time.perf_counter()
+            np.argmax(m.rms_norm(h2[:, 0], self.lnf) @ self.head_w.T, axis=-1)
+        else:
+            h2 = m.decoder_layer(self.h, self.lw, self.kc, self.vc, self.past, self.s.n_heads)
+            t1 = time.perf_counter()
+            m.greedy(m.layer_norm(h2[:, 0], *self.lnf) @ self.head_w.T)
         t2 = time.perf_counter()
         return (t1 - t0) * self.s.n_layers + (t2 - t1)
 
@@ -354,6 +379,7 @@ def run_pipo(args):
         line = {
             "metric": "decode tokens/s, OPT-30B streamed weights (int4-g64), b=64/GPU, P=512" if args.config == "c5"
             else f"decode tokens/s, {c['desc']}",
+            "decode_latency_ms": ms,
             "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f16", "weights": args.wfmt + ("-g64" if args.wfmt == "int4" else ""),
@@ -390,8 +416,10 @@ def run_pipo(args):
         except (OSError, IndexError, ValueError):
             mem_cpu = 0
         b_ssd = (line.get("disk_roofline") or {}).get("probe_gbs")
-        spec = pipo.mem_spec(l=s.n_layers, d=s.d_model, V=s.vocab, h=s.n_heads, h_kv=s.n_heads, d_h=s.ffn_dim,
-                             mlp_mats=2, p_weight=17 / 32 if args.wfmt == "int4" else 2.0, p_act=2.0)
+        llama = isinstance(s, synth.LlamaShape)
+        spec = pipo.mem_spec(l=s.n_layers, d=s.d_model, V=s.vocab, h=s.n_heads,
+                             h_kv=s.n_kv_heads if llama else s.n_heads, d_h=s.ffn_dim,
+                             mlp_mats=3 if llama else 2, p_weight=17 / 32 if args.wfmt == "int4" else 2.0, p_act=2.0)
         try:
             plan = pipo.pipo_choose_plan(spec, b, P + G, m_gpu=torch.cuda.get_device_properties(local).total_memory,
                                          m_cpu=mem_cpu or 1, b_gpu=link_probe * 1e9,

@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define PIPO_ABI_VERSION 2
+#define PIPO_ABI_VERSION 3
 
 typedef enum {
   PIPO_OK = 0,
@@ -69,7 +69,7 @@ typedef enum { PIPO_TIER_DEVICE = 0, PIPO_TIER_HOST = 1, PIPO_TIER_DISK = 2 } pi
 
 typedef struct {
   int32_t device;        /* CUDA ordinal */
-  /* model shape (OPT): d_model % 64 == 0, ffn_dim % 64 == 0, n_heads | d_model,
+  /* model shape: d_model % 64 == 0, ffn_dim % 64 == 0, n_heads | d_model,
    * head_dim = d_model / n_heads in {64, 128}                                  */
   int32_t d_model, n_layers, n_heads, ffn_dim, vocab, max_pos;  /* OPT: max_pos 2048 */
   /* workload capacity: KV cache holds max_batch x max_seq positions
@@ -92,19 +92,39 @@ typedef struct {
   int32_t disk_threads;  /* DISK tier reader threads; 0 -> 4        */
   const char* disk_dir;  /* DISK tier directory (copied at init)                      */
   uint32_t flags;        /* PIPO_F_*                                                   */
+  /* ---- model family (ABI 3).  PIPO_ARCH_OPT (default, 0): the OPT block above.
+   * PIPO_ARCH_LLAMA: the LLaMA3.1 block the paper also evaluates (PAPER.md:318-331
+   * §3.5, :390 §4.1; NEXT-4): GQA with n_kv_heads, RoPE with the llama3
+   * frequency rule, RMSNorm (eps 1e-5), SwiGLU MLP with ffn_dim = d_h (PAPER.md:323,
+   * ffn_dim % 128 == 0), no biases, untied LM head, no position table (max_pos only
+   * bounds positions).  LLaMA + kv_fmt INT4 is not built (PIPO_E_INVALID_ARG).       */
+  int32_t arch;          /* pipo_arch                                                  */
+  int32_t n_kv_heads;    /* LLaMA: KV heads, divides n_heads; 0 -> n_heads             */
+  float rope_theta;      /* LLaMA: RoPE base (Llama-3.1: 500000); 0 -> 10000           */
+  float rope_factor;     /* llama3 rope scaling factor (8); 0 -> plain RoPE             */
+  float rope_low_freq, rope_high_freq;   /* llama3 low/high_freq_factor (1, 4)          */
+  int32_t rope_orig_max_pos;             /* llama3 original_max_position_embeddings (8192) */
 } pipo_config;
 
+typedef enum { PIPO_ARCH_OPT = 0, PIPO_ARCH_LLAMA = 1 } pipo_arch;
+
 /* fp32 masters (values must be finite; fp16-representable for exact parity).
- * Row-major.  w_qkv rows are q | k | v ([3d][d]); w_out [d][d]; w_fc1 [F][d];
- * w_fc2 [d][F]; vectors have the obvious lengths. */
+ * Row-major.  OPT: w_qkv rows are q | k | v ([3d][d]); w_out [d][d]; w_fc1 [F][d];
+ * w_fc2 [d][F]; vectors have the obvious lengths.
+ * LLaMA: w_qkv [d + 2 d_kv][d] (d_kv = n_kv_heads * head_dim), w_out [d][d],
+ * w_fc1 [2F][d] = gate rows then up rows, w_fc2 [d][F] (down); ln1_g / ln2_g are the
+ * RMSNorm weights; every bias and ln*_b must be NULL (ignored). */
 typedef struct {
   const float *ln1_g, *ln1_b, *w_qkv, *b_qkv, *w_out, *b_out;
   const float *ln2_g, *ln2_b, *w_fc1, *b_fc1, *w_fc2, *b_fc2;
 } pipo_layer_weights;
 
-/* tok [vocab][d], pos [max_pos + 2][d] (OPT learned positions, offset 2), final LN. */
+/* tok [vocab][d], pos [max_pos + 2][d] (OPT learned positions, offset 2), final LN.
+ * LLaMA: pos and lnf_b NULL, lnf_g = final RMSNorm weight, lm_head [vocab][d] (untied;
+ * NULL for OPT, whose LM head is tok). */
 typedef struct {
   const float *tok, *pos, *lnf_g, *lnf_b;
+  const float *lm_head;
 } pipo_embed_weights;
 
 #define PIPO_LAYER_EMBED (-1)
@@ -248,6 +268,23 @@ pipo_status pipo_attention_decode(pipo_ctx* ctx, const uint16_t* q, const uint16
 pipo_status pipo_attention_prefill(pipo_ctx* ctx, const uint16_t* q, const uint16_t* k, const uint16_t* v,
                                    int32_t b, int32_t n, int32_t past, int32_t d, int32_t n_heads, int32_t cuda_cores,
                                    float* o);
+
+/* Grouped-query attention (LLaMA; NEXT-4) through the production
+ * kernels: q [b][n][n_heads*head_dim] fp16 bits (pre-scaled, rotated) at positions
+ * past..past+n-1; k/v [past+n][b][n_kv_heads*head_dim] position-major; query head j
+ * reads KV head j / (n_heads / n_kv_heads).  n == 1 runs the decode kernel, n > 1 the
+ * causal prefill kernel.  o [b][n][n_heads*head_dim] fp32.  n_kv_heads | n_heads,
+ * head_dim in {64, 128}. */
+pipo_status pipo_attention_gqa(pipo_ctx* ctx, const uint16_t* q, const uint16_t* k, const uint16_t* v, int32_t b,
+                               int32_t n, int32_t past, int32_t n_heads, int32_t n_kv_heads, int32_t head_dim,
+                               float* o);
+
+/* RoPE kernel of a LLaMA context (its n_heads, n_kv_heads, head_dim, llama3 frequencies):
+ * q [b][n][n_heads*hd] fp16 bits at positions past..past+n-1 and k [past+n][b][n_kv_heads*hd]
+ * (position-major; only positions past.. are rotated) -> q_out, k_out fp32, same shapes.
+ * Errors: STATE (not a LLaMA context), INVALID_ARG. */
+pipo_status pipo_rope(pipo_ctx* ctx, const uint16_t* q, const uint16_t* k, int32_t b, int32_t n, int32_t past,
+                      float* q_out, float* k_out);
 
 /* Capture per-layer hidden states of the next prefill/decode call:
  * on != 0 -> after that call, out receives [n_layers][b][n][d] fp32 (n = P for

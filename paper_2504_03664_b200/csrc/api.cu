@@ -179,7 +179,7 @@ pipo_status run_linear(pipo_ctx* ctx, const LinearArgs& la, int path, int cls) {
 
 // ---- pointers into a layer blob -----------------------------------------------
 const __half* vec_ptr(const pipo_ctx* c, const uint8_t* blob, int v) {
-  return reinterpret_cast<const __half*>(blob + c->lay.vec_off[v]);
+  return c->lay.vec_len[v] ? reinterpret_cast<const __half*>(blob + c->lay.vec_off[v]) : nullptr;   // LLaMA: none
 }
 
 bool streamed(const pipo_ctx* c) { return c->weight_tier != PIPO_TIER_DEVICE; }
@@ -194,7 +194,7 @@ uint8_t* kv_host_region(pipo_ctx* c, int layer, int which) {
 }
 // byte ranges (offset, size) of positions [p0, p0 + np) inside a region, current batch
 int kv_ranges(const pipo_ctx* c, int64_t p0, int64_t np, int64_t* off, int64_t* bytes) {
-  const int64_t row = (int64_t)c->b_cur * c->d;   // elements per position
+  const int64_t row = (int64_t)c->b_cur * c->dkv;   // elements per position
   if (c->kv_fmt == PIPO_W_FP16) {
     off[0] = p0 * row * 2; bytes[0] = np * row * 2;
     return 1;
@@ -305,12 +305,15 @@ pipo_status forward(pipo_ctx* ctx, int b, int n, int past, bool want_logits) {
   const int M = b * n, d = ctx->d;
   cudaStream_t cs = ctx->s_comp;
   const int64_t next_pass_kv = past + n;   // KV positions the next (decode) pass loads
+  const bool llama = ctx->arch == PIPO_ARCH_LLAMA;
+  const int dkv = ctx->dkv;
   LAUNCH(launch_embed(ctx->ids, b, n, past, ctx->tok, ctx->tok_lay.n_kb, ctx->pos, d, ctx->h, cs));
   LinearArgs la;
   la.ws = ctx->ws; la.ws_floats = ctx->ws_floats; la.counters = ctx->counters; la.n_counters = ctx->n_counters;
   la.num_sms = ctx->num_sms; la.M = M;
   AttnArgs aa;
   aa.b = b; aa.n = n; aa.past = past; aa.d = d; aa.n_heads = ctx->H; aa.kv_b = b;
+  aa.dkv = dkv; aa.group = ctx->H / ctx->Hkv;
   aa.ws = ctx->ws; aa.ws_floats = ctx->ws_floats; aa.num_sms = ctx->num_sms;
   const int64_t pass_base = ctx->g_comp;
   const int lin_cls = n == 1 ? PIPO_K_LINEAR_DECODE : PIPO_K_LINEAR_PREFILL;
@@ -337,7 +340,7 @@ pipo_status forward(pipo_ctx* ctx, int b, int n, int past, bool want_logits) {
     uint8_t* vreg = kv_region(ctx, j, 1, G);
     const bool q4 = ctx->kv_fmt == PIPO_W_INT4_G64;
     __half* kc = q4 ? ctx->kv_stage : reinterpret_cast<__half*>(kreg);
-    __half* vc = q4 ? ctx->kv_stage + d : reinterpret_cast<__half*>(vreg);
+    __half* vc = q4 ? ctx->kv_stage + dkv : reinterpret_cast<__half*>(vreg);
     if (host_kv(ctx) && n == 1 && ctx->kv_load_past[slot] != past)
       return set_err(PIPO_E_STATE, "internal: KV prefetch range mismatch");
     cudaEvent_t t0;
@@ -346,13 +349,16 @@ pipo_status forward(pipo_ctx* ctx, int b, int n, int past, bool want_logits) {
     if (host_kv(ctx)) CK(cudaStreamWaitEvent(cs, ctx->ev_ready[slot][4], 0));
     TRY(span_begin(ctx, cs, &t0));
     LAUNCH(launch_layernorm(ctx->h, d, M, d, vec_ptr(ctx, blob, V_LN1_G), vec_ptr(ctx, blob, V_LN1_B), ctx->xa, cs));
-    la.x = ctx->xa; la.w = blob + ctx->lay.mat_off[M_QKV]; la.wfmt = ctx->wfmt; la.N = 3 * d; la.K = d;
+    la.x = ctx->xa; la.w = blob + ctx->lay.mat_off[M_QKV]; la.wfmt = ctx->wfmt; la.N = d + 2 * dkv; la.K = d;
     la.epi = EpiParams{};
-    la.epi.kind = EPI_QKV; la.epi.bias = vec_ptr(ctx, blob, V_B_QKV); la.epi.M = M; la.epi.N = 3 * d;
+    la.epi.kind = EPI_QKV; la.epi.bias = vec_ptr(ctx, blob, V_B_QKV); la.epi.M = M; la.epi.N = d + 2 * dkv;
+    la.epi.dkv = dkv;
     la.epi.q = ctx->q; la.epi.kc = kc; la.epi.vc = vc; la.epi.d = d; la.epi.n_tok = n; la.epi.past = past;
     la.epi.kv_b = b; la.epi.qscale = 1.0f / sqrtf((float)ctx->hd);
     la.epi.kv_rowmajor = q4 ? 1 : 0;
     TRY(run_linear(ctx, la, PATH_AUTO, lin_cls));
+    if (llama)   // RoPE on q and the fresh K rows (q already carries hd^-0.5: rotation is linear)
+      LAUNCH(launch_rope(ctx->q, kc, ctx->rope_inv, b, n, past, ctx->H, ctx->Hkv, ctx->hd, b, cs));
     aa.q = ctx->q; aa.kc = kc; aa.vc = vc; aa.o = ctx->xa;
     aa.kv_pos_stride = 0; aa.kv_b_stride = 0; aa.kq = nullptr;
     if (q4) {
@@ -375,7 +381,7 @@ pipo_status forward(pipo_ctx* ctx, int b, int n, int past, bool want_logits) {
       else if (n == 1) LAUNCH(launch_attention_decode(aa, cs));
       else LAUNCH(launch_attention_prefill(aa, cs));
       const double L = past + n;
-      const double kvb = 2.0 * L * b * d * (q4 && n == 1 ? (0.5 + 2.0 / 64) : 2.0);
+      const double kvb = 2.0 * L * b * dkv * (q4 && n == 1 ? (0.5 + 2.0 / 64) : 2.0);
       const double fl = n == 1 ? 4.0 * b * d * L : 2.0 * b * d * (double)n * (past + (n + 1) / 2.0);
       TRY(kend(ctx, ka, n == 1 ? PIPO_K_ATTN_DECODE : PIPO_K_ATTN_PREFILL, kvb + 4.0 * M * d, fl));
     }
@@ -411,10 +417,12 @@ pipo_status forward(pipo_ctx* ctx, int b, int n, int past, bool want_logits) {
     if (streamed(ctx)) CK(cudaStreamWaitEvent(cs, ctx->ev_ready[slot][2], 0));
     TRY(span_begin(ctx, cs, &t0));
     LAUNCH(launch_layernorm(ctx->h, d, M, d, vec_ptr(ctx, blob, V_LN2_G), vec_ptr(ctx, blob, V_LN2_B), ctx->xa, cs));
-    la.x = ctx->xa; la.w = blob + ctx->lay.mat_off[M_FC1]; la.N = ctx->F; la.K = d;
+    la.x = ctx->xa; la.w = blob + ctx->lay.mat_off[M_FC1]; la.N = llama ? 2 * ctx->F : ctx->F; la.K = d;
     la.epi = EpiParams{};
-    la.epi.kind = EPI_RELU; la.epi.bias = vec_ptr(ctx, blob, V_B_FC1); la.epi.M = M; la.epi.N = ctx->F; la.epi.u = ctx->u;
+    la.epi.kind = llama ? EPI_HALF : EPI_RELU; la.epi.bias = vec_ptr(ctx, blob, V_B_FC1); la.epi.M = M;
+    la.epi.N = la.N; la.epi.u = llama ? ctx->gu : ctx->u;
     TRY(run_linear(ctx, la, PATH_AUTO, lin_cls));
+    if (llama) LAUNCH(launch_swiglu(ctx->gu, M, ctx->F, ctx->u, cs));   // u = silu(gate) * up
     TRY(span_end(ctx, cs, t0, 1, 0));
     // ---- MLP: FC2 + residual (seg 3) ----
     if (streamed(ctx)) CK(cudaStreamWaitEvent(cs, ctx->ev_ready[slot][3], 0));
@@ -432,7 +440,7 @@ pipo_status forward(pipo_ctx* ctx, int b, int n, int past, bool want_logits) {
   cudaEvent_t t0;
   TRY(span_begin(ctx, cs, &t0));
   LAUNCH(launch_layernorm(ctx->h + (int64_t)(n - 1) * d, (int64_t)n * d, b, d, ctx->lnf_g, ctx->lnf_b, ctx->xa, cs));
-  la.x = ctx->xa; la.w = reinterpret_cast<const uint8_t*>(ctx->tok); la.wfmt = 0; la.M = b; la.N = ctx->V; la.K = d;
+  la.x = ctx->xa; la.w = reinterpret_cast<const uint8_t*>(ctx->head); la.wfmt = 0; la.M = b; la.N = ctx->V; la.K = d;
   la.epi = EpiParams{};
   la.epi.kind = EPI_F32; la.epi.M = b; la.epi.N = ctx->V; la.epi.y = ctx->logits; la.epi.ldy = ctx->V;
   TRY(run_linear(ctx, la, PATH_GEMM, PIPO_K_HEAD));
@@ -535,6 +543,13 @@ pipo_status pipeline_init(const pipo_config* cfg, pipo_ctx** out) {
   if (c.kv_fmt != PIPO_W_FP16 && c.kv_fmt != PIPO_W_INT4_G64) return set_err(PIPO_E_INVALID_ARG, "bad kv_fmt");
   if (c.weight_tier == PIPO_TIER_DISK && (!c.disk_dir || !c.disk_dir[0]))
     return set_err(PIPO_E_INVALID_ARG, "disk tier needs disk_dir");
+  if (c.arch != PIPO_ARCH_OPT && c.arch != PIPO_ARCH_LLAMA) return set_err(PIPO_E_INVALID_ARG, "bad arch");
+  const int n_kv = c.arch == PIPO_ARCH_LLAMA && c.n_kv_heads > 0 ? c.n_kv_heads : c.n_heads;
+  if (c.arch == PIPO_ARCH_LLAMA) {
+    if (c.n_heads % n_kv) return set_err(PIPO_E_INVALID_ARG, "n_kv_heads must divide n_heads");
+    if (c.ffn_dim % 128) return set_err(PIPO_E_INVALID_ARG, "LLaMA ffn_dim must be a multiple of 128");
+    if (c.kv_fmt != PIPO_W_FP16) return set_err(PIPO_E_INVALID_ARG, "LLaMA with an int4 KV cache is not built");
+  }
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
     cudaGetLastError();
@@ -548,6 +563,7 @@ pipo_status pipeline_init(const pipo_config* cfg, pipo_ctx** out) {
   ctx->cfg.disk_dir = nullptr;
   ctx->d = c.d_model; ctx->l = c.n_layers; ctx->H = c.n_heads; ctx->F = c.ffn_dim; ctx->V = c.vocab;
   ctx->hd = hd; ctx->max_b = c.max_batch; ctx->max_s = c.max_seq; ctx->wfmt = c.wfmt;
+  ctx->arch = c.arch; ctx->Hkv = n_kv; ctx->dkv = n_kv * hd;
   ctx->weight_tier = c.weight_tier; ctx->kv_tier = c.kv_tier; ctx->kv_fmt = c.kv_fmt;
   ctx->R = c.ring_layers > 0 ? c.ring_layers : 2;
   ctx->R = std::min({ctx->R, kMaxRing, ctx->l});
@@ -556,7 +572,7 @@ pipo_status pipeline_init(const pipo_config* cfg, pipo_ctx** out) {
   ctx->gemv_max_m = c.gemv_max_m > 0 ? std::min(c.gemv_max_m, 16) : 15;
   ctx->timeline = (c.flags & PIPO_F_TIMELINE) != 0;
   ctx->kprof = (c.flags & PIPO_F_KPROF) != 0;
-  ctx->lay = layer_layout(ctx->d, ctx->F, ctx->wfmt);
+  ctx->lay = layer_layout(ctx->d, ctx->F, ctx->wfmt, ctx->dkv, ctx->arch == PIPO_ARCH_LLAMA);
   ctx->layer_bytes = ctx->lay.total;
   ctx->layer_loaded.assign(ctx->l, 0);
   ctx->ev_saved.assign(ctx->l, nullptr);
@@ -598,9 +614,35 @@ pipo_status pipeline_init(const pipo_config* cfg, pipo_ctx** out) {
   // resident embeddings
   ctx->tok_lay = mat_layout(ctx->V, ctx->d, 0);
   TRYI(dev_alloc(ctx, &ctx->tok, ctx->tok_lay.bytes));
-  TRYI(dev_alloc(ctx, &ctx->pos, (int64_t)(c.max_pos + 2) * ctx->d * 2));
   TRYI(dev_alloc(ctx, &ctx->lnf_g, ctx->d * 2));
-  TRYI(dev_alloc(ctx, &ctx->lnf_b, ctx->d * 2));
+  if (ctx->arch == PIPO_ARCH_OPT) {
+    TRYI(dev_alloc(ctx, &ctx->pos, (int64_t)(c.max_pos + 2) * ctx->d * 2));
+    TRYI(dev_alloc(ctx, &ctx->lnf_b, ctx->d * 2));
+    ctx->head = ctx->tok;   // tied LM head
+  } else {
+    TRYI(dev_alloc(ctx, &ctx->head, ctx->tok_lay.bytes));
+    // llama3 inverse frequencies in double on the host ([ext] transformers
+    // _compute_llama3_parameters), uploaded as fp32 (the RoPE kernel multiplies in fp32)
+    const double theta = c.rope_theta > 0 ? c.rope_theta : 10000.0;
+    std::vector<float> inv((size_t)hd / 2);
+    for (int i = 0; i < hd / 2; ++i) {
+      double f = 1.0 / std::pow(theta, (2.0 * i) / hd);
+      if (c.rope_factor > 0) {
+        const double lo = c.rope_low_freq > 0 ? c.rope_low_freq : 1.0, hi = c.rope_high_freq > 0 ? c.rope_high_freq : 4.0;
+        const double orig = c.rope_orig_max_pos > 0 ? c.rope_orig_max_pos : 8192;
+        const double wl = 2.0 * M_PI / f;
+        if (wl > orig / lo) {
+          f = f / c.rope_factor;
+        } else if (!(wl < orig / hi)) {
+          const double sm = (orig / wl - lo) / (hi - lo);
+          f = (1.0 - sm) * f / c.rope_factor + sm * f;
+        }
+      }
+      inv[i] = (float)f;
+    }
+    TRYI(dev_alloc(ctx, &ctx->rope_inv, (int64_t)hd / 2 * 4));
+    CKI(cudaMemcpy(ctx->rope_inv, inv.data(), inv.size() * 4, cudaMemcpyHostToDevice));
+  }
   // weights
   if (ctx->weight_tier == PIPO_TIER_DEVICE) {
     TRYI(dev_alloc(ctx, &ctx->dev_store, (int64_t)ctx->l * ctx->layer_bytes));
@@ -614,7 +656,7 @@ pipo_status pipeline_init(const pipo_config* cfg, pipo_ctx** out) {
     }
   }
   // KV cache
-  const int64_t kv_elems = (int64_t)ctx->max_s * ctx->max_b * ctx->d;
+  const int64_t kv_elems = (int64_t)ctx->max_s * ctx->max_b * ctx->dkv;
   if (ctx->kv_fmt == PIPO_W_INT4_G64) {
     ctx->kv_codes_cap = round_up(kv_elems / 2, 256);
     ctx->kv_tensor_bytes = round_up(ctx->kv_codes_cap + kv_elems / 64 * 2, 4096);
@@ -633,6 +675,7 @@ pipo_status pipeline_init(const pipo_config* cfg, pipo_ctx** out) {
   TRYI(dev_alloc(ctx, &ctx->xa, ctx->rows_cap * ctx->d * 2));
   TRYI(dev_alloc(ctx, &ctx->q, ctx->rows_cap * ctx->d * 2));
   TRYI(dev_alloc(ctx, &ctx->u, ctx->rows_cap * ctx->F * 2));
+  if (ctx->arch == PIPO_ARCH_LLAMA) TRYI(dev_alloc(ctx, &ctx->gu, ctx->rows_cap * 2 * ctx->F * 2));
   TRYI(dev_alloc(ctx, &ctx->logits, (int64_t)ctx->max_b * ctx->V * 4));
   TRYI(dev_alloc(ctx, &ctx->ids, ctx->rows_cap * 4));
   TRYI(dev_alloc(ctx, &ctx->next, (int64_t)ctx->max_b * 4));
@@ -646,7 +689,7 @@ pipo_status pipeline_init(const pipo_config* cfg, pipo_ctx** out) {
   TRYI(dev_alloc(ctx, &ctx->quant_bad, 4));
   CKI(cudaMemset(ctx->kv_dev ? (void*)ctx->kv_dev : (void*)ctx->kv_slot, 0,
                  (size_t)(host_kv(ctx) ? ctx->R : ctx->l) * 2 * ctx->kv_tensor_bytes));
-  if (ctx->kv_fmt == PIPO_W_INT4_G64) TRYI(dev_alloc(ctx, &ctx->kv_stage, ctx->rows_cap * 2 * ctx->d * 2));
+  if (ctx->kv_fmt == PIPO_W_INT4_G64) TRYI(dev_alloc(ctx, &ctx->kv_stage, ctx->rows_cap * 2 * ctx->dkv * 2));
   CKI(cudaDeviceSynchronize());
   *out = ctx;
   return PIPO_OK;
@@ -660,7 +703,8 @@ void pipeline_destroy(pipo_ctx* ctx) {
   cudaDeviceSynchronize();
   cudaGetLastError();
   if (ctx->disk) disk_close(ctx);
-  void* dev[] = {ctx->tok, ctx->pos, ctx->lnf_g, ctx->lnf_b, ctx->dev_store, ctx->ring, ctx->kv_dev, ctx->kv_slot, ctx->kv_stage,
+  if (ctx->head == ctx->tok) ctx->head = nullptr;
+  void* dev[] = {ctx->tok, ctx->head, ctx->gu, ctx->rope_inv, ctx->pos, ctx->lnf_g, ctx->lnf_b, ctx->dev_store, ctx->ring, ctx->kv_dev, ctx->kv_slot, ctx->kv_stage,
                  ctx->h, ctx->xa, ctx->q, ctx->u, ctx->logits, ctx->ids, ctx->next, ctx->ws, ctx->counters,
                  ctx->quant_bad, ctx->cap_dev};
   for (void* p : dev)
@@ -691,18 +735,28 @@ pipo_status load_layer_weights(pipo_ctx* ctx, int32_t layer, const void* w) {
   CK(cudaSetDevice(ctx->cfg.device));
   if (layer == PIPO_LAYER_EMBED) {
     const pipo_embed_weights* e = static_cast<const pipo_embed_weights*>(w);
-    if (!e->tok || !e->pos || !e->lnf_g || !e->lnf_b) return set_err(PIPO_E_INVALID_ARG, "NULL embedding tensor");
+    const bool llama = ctx->arch == PIPO_ARCH_LLAMA;
+    if (!e->tok || !e->lnf_g || (llama ? !e->lm_head : (!e->pos || !e->lnf_b)))
+      return set_err(PIPO_E_INVALID_ARG, "NULL embedding tensor");
     std::vector<uint8_t> tiled((size_t)ctx->tok_lay.bytes);
     tile_fp16(e->tok, ctx->V, ctx->d, tiled.data());
     CK(cudaMemcpy(ctx->tok, tiled.data(), tiled.size(), cudaMemcpyHostToDevice));
-    const int64_t npos = (int64_t)(ctx->cfg.max_pos + 2) * ctx->d;
-    std::vector<uint16_t> tmp((size_t)npos);
-    for (int64_t i = 0; i < npos; ++i) tmp[i] = f32_to_f16_rne(e->pos[i]);
-    CK(cudaMemcpy(ctx->pos, tmp.data(), (size_t)npos * 2, cudaMemcpyHostToDevice));
+    if (llama) {
+      tile_fp16(e->lm_head, ctx->V, ctx->d, tiled.data());
+      CK(cudaMemcpy(ctx->head, tiled.data(), tiled.size(), cudaMemcpyHostToDevice));
+    }
+    const int64_t npos = llama ? ctx->d : (int64_t)(ctx->cfg.max_pos + 2) * ctx->d;
+    std::vector<uint16_t> tmp((size_t)std::max<int64_t>(npos, ctx->d));
+    if (!llama) {
+      for (int64_t i = 0; i < npos; ++i) tmp[i] = f32_to_f16_rne(e->pos[i]);
+      CK(cudaMemcpy(ctx->pos, tmp.data(), (size_t)npos * 2, cudaMemcpyHostToDevice));
+    }
     for (int64_t i = 0; i < ctx->d; ++i) tmp[i] = f32_to_f16_rne(e->lnf_g[i]);
     CK(cudaMemcpy(ctx->lnf_g, tmp.data(), (size_t)ctx->d * 2, cudaMemcpyHostToDevice));
-    for (int64_t i = 0; i < ctx->d; ++i) tmp[i] = f32_to_f16_rne(e->lnf_b[i]);
-    CK(cudaMemcpy(ctx->lnf_b, tmp.data(), (size_t)ctx->d * 2, cudaMemcpyHostToDevice));
+    if (!llama) {
+      for (int64_t i = 0; i < ctx->d; ++i) tmp[i] = f32_to_f16_rne(e->lnf_b[i]);
+      CK(cudaMemcpy(ctx->lnf_b, tmp.data(), (size_t)ctx->d * 2, cudaMemcpyHostToDevice));
+    }
     ctx->embed_loaded = true;
     return PIPO_OK;
   }
@@ -716,7 +770,7 @@ pipo_status load_layer_weights(pipo_ctx* ctx, int32_t layer, const void* w) {
     tmp.resize((size_t)ctx->layer_bytes);
     dst = tmp.data();
   }
-  if (!build_layer_blob(lw, ctx->lay, ctx->d, ctx->F, ctx->wfmt, dst))
+  if (!build_layer_blob(lw, ctx->lay, ctx->wfmt, dst))
     return set_err(PIPO_E_INVALID_ARG, "non-finite weight, NULL tensor or fp16-overflowing group scale");
   if (ctx->weight_tier == PIPO_TIER_DEVICE)
     CK(cudaMemcpy(ctx->dev_store + (int64_t)layer * ctx->layer_bytes, dst, (size_t)ctx->layer_bytes,
@@ -738,20 +792,28 @@ pipo_status pipo_load_synthetic(pipo_ctx* ctx, int32_t layer, uint64_t seed) {
     LAUNCH(launch_synth(dst, 0, count, synth_key(seed, slot, tid), kind, synth_scale(kind, param), st));
     return PIPO_OK;
   };
+  const bool llama = ctx->arch == PIPO_ARCH_LLAMA;
   if (layer == PIPO_LAYER_EMBED) {
-    const int64_t ntok = (int64_t)ctx->V * d, npos = (int64_t)(ctx->cfg.max_pos + 2) * d;
+    const int64_t ntok = (int64_t)ctx->V * d, npos = llama ? 0 : (int64_t)(ctx->cfg.max_pos + 2) * d;
     float* buf = nullptr;
     TRY(dev_alloc(ctx, &buf, std::max(ntok, npos) * 4));
     pipo_status s = PIPO_OK;
-    do {
+    do {   // pipo_synth tensor ids: tok 0, pos 1, lnf_g 2, lnf_b 3, lm_head 4
       if ((s = draw(buf, 0, 0, 0, 0.02, ntok)) != PIPO_OK) break;
       LAUNCH(launch_tile_fp16(buf, ctx->V, d, reinterpret_cast<uint8_t*>(ctx->tok), st));
-      if ((s = draw(buf, 0, 1, 0, 0.02, npos)) != PIPO_OK) break;
-      LAUNCH(launch_f32_to_f16(buf, ctx->pos, npos, st));
+      if (llama) {
+        if ((s = draw(buf, 0, 4, 0, 0.02, ntok)) != PIPO_OK) break;
+        LAUNCH(launch_tile_fp16(buf, ctx->V, d, reinterpret_cast<uint8_t*>(ctx->head), st));
+      } else {
+        if ((s = draw(buf, 0, 1, 0, 0.02, npos)) != PIPO_OK) break;
+        LAUNCH(launch_f32_to_f16(buf, ctx->pos, npos, st));
+      }
       if ((s = draw(buf, 0, 2, 2, 0.1, d)) != PIPO_OK) break;
       LAUNCH(launch_f32_to_f16(buf, ctx->lnf_g, d, st));
-      if ((s = draw(buf, 0, 3, 1, 0.1, d)) != PIPO_OK) break;
-      LAUNCH(launch_f32_to_f16(buf, ctx->lnf_b, d, st));
+      if (!llama) {
+        if ((s = draw(buf, 0, 3, 1, 0.1, d)) != PIPO_OK) break;
+        LAUNCH(launch_f32_to_f16(buf, ctx->lnf_b, d, st));
+      }
     } while (0);
     CK(cudaStreamSynchronize(st));
     cudaFree(buf);
@@ -768,7 +830,9 @@ pipo_status pipo_load_synthetic(pipo_ctx* ctx, int32_t layer, uint64_t seed) {
   } else {
     TRY(dev_alloc(ctx, &blob, ctx->layer_bytes));
   }
-  const int64_t big = std::max(3 * d * d, F * d);
+  int64_t big = 0;
+  for (int m = 0; m < M_COUNT; ++m) big = std::max(big, ctx->lay.mat[m].N * ctx->lay.mat[m].K);
+  (void)F;
   float* buf = nullptr;
   pipo_status s = dev_alloc(ctx, &buf, big * 4);
   const uint32_t slot = (uint32_t)layer + 1;
@@ -776,11 +840,13 @@ pipo_status pipo_load_synthetic(pipo_ctx* ctx, int32_t layer, uint64_t seed) {
   const double vparams[V_COUNT] = {0.1, 0.1, 0.02, 0.02, 0.1, 0.1, 0.02, 0.02};
   const uint32_t vtids[V_COUNT] = {0, 1, 3, 5, 6, 7, 9, 11};
   const uint32_t mtids[M_COUNT] = {2, 4, 8, 10};
-  const int64_t mrows[M_COUNT] = {3 * d, d, F, d}, mcols[M_COUNT] = {d, d, d, F};
+  int64_t mrows[M_COUNT], mcols[M_COUNT];
+  for (int m = 0; m < M_COUNT; ++m) { mrows[m] = ctx->lay.mat[m].N; mcols[m] = ctx->lay.mat[m].K; }
   if (s == PIPO_OK) {
     CK(cudaMemsetAsync(blob, 0, (size_t)ctx->layer_bytes, st));
     CK(cudaMemsetAsync(ctx->quant_bad, 0, 4, st));
     for (int v = 0; v < V_COUNT && s == PIPO_OK; ++v) {
+      if (ctx->lay.vec_len[v] == 0) continue;   // LLaMA: no biases / betas
       s = draw(buf, slot, vtids[v], vkinds[v], vparams[v], ctx->lay.vec_len[v]);
       if (s == PIPO_OK)
         LAUNCH(launch_f32_to_f16(buf, reinterpret_cast<__half*>(blob + ctx->lay.vec_off[v]), ctx->lay.vec_len[v], st));
@@ -788,10 +854,23 @@ pipo_status pipo_load_synthetic(pipo_ctx* ctx, int32_t layer, uint64_t seed) {
     for (int m = 0; m < M_COUNT && s == PIPO_OK; ++m) {
       s = draw(buf, slot, mtids[m], 0, 0.02, mrows[m] * mcols[m]);
       if (s != PIPO_OK) break;
-      if (ctx->wfmt == PIPO_W_INT4_G64)
-        LAUNCH(launch_quantize(buf, mrows[m], mcols[m], nullptr, nullptr, blob + ctx->lay.mat_off[m], ctx->quant_bad, st));
-      else
-        LAUNCH(launch_tile_fp16(buf, mrows[m], mcols[m], blob + ctx->lay.mat_off[m], st));
+      uint8_t* dst = blob + ctx->lay.mat_off[m];
+      if (ctx->lay.glu && m == M_FC1) {
+        // tile-interleaved [gate; up] (layout.h): tile 2p <- gate rows 128p.., 2p+1 <- up rows F+128p..
+        const MatLayout& ml = ctx->lay.mat[m];
+        const int64_t Fh = mrows[m] / 2, tile_bytes = ml.n_kb * ml.block_bytes;
+        for (int64_t t = 0; t < ml.n_rt; ++t) {
+          const float* src = buf + ((t & 1) * Fh + (t >> 1) * 128) * mcols[m];
+          if (ctx->wfmt == PIPO_W_INT4_G64)
+            LAUNCH(launch_quantize(src, 128, mcols[m], nullptr, nullptr, dst + t * tile_bytes, ctx->quant_bad, st));
+          else
+            LAUNCH(launch_tile_fp16(src, 128, mcols[m], dst + t * tile_bytes, st));
+        }
+      } else if (ctx->wfmt == PIPO_W_INT4_G64) {
+        LAUNCH(launch_quantize(buf, mrows[m], mcols[m], nullptr, nullptr, dst, ctx->quant_bad, st));
+      } else {
+        LAUNCH(launch_tile_fp16(buf, mrows[m], mcols[m], dst, st));
+      }
     }
   }
   if (s == PIPO_OK && !direct) {
@@ -1317,6 +1396,69 @@ pipo_status pipo_attention_prefill(pipo_ctx* ctx, const uint16_t* q, const uint1
   CK(cudaStreamSynchronize(st));
   cudaFree(dq); cudaFree(dk); cudaFree(dv); cudaFree(dout); cudaFree(df);
   ctx->hbm_bytes -= nq * 2 * 2 + nkv * 2 * 2 + nq * 4;
+  return PIPO_OK;
+}
+
+pipo_status pipo_attention_gqa(pipo_ctx* ctx, const uint16_t* q, const uint16_t* k, const uint16_t* v, int32_t b,
+                               int32_t n, int32_t past, int32_t n_heads, int32_t n_kv_heads, int32_t head_dim,
+                               float* o) {
+  CHECK_CTX();
+  if (!q || !k || !v || !o || b <= 0 || n <= 0 || past < 0 || n_heads <= 0 || n_kv_heads <= 0 ||
+      n_heads % n_kv_heads || (head_dim != 64 && head_dim != 128))
+    return set_err(PIPO_E_INVALID_ARG, "bad attention arguments");
+  CK(cudaSetDevice(ctx->cfg.device));
+  const int d = n_heads * head_dim, dkv = n_kv_heads * head_dim;
+  __half *dq = nullptr, *dk = nullptr, *dv = nullptr, *dout = nullptr;
+  float* df = nullptr;
+  const int64_t L = past + n, nq = (int64_t)b * n * d, nkv = L * b * dkv;
+  TRY(dev_alloc(ctx, &dq, nq * 2));
+  TRY(dev_alloc(ctx, &dk, nkv * 2));
+  TRY(dev_alloc(ctx, &dv, nkv * 2));
+  TRY(dev_alloc(ctx, &dout, nq * 2));
+  TRY(dev_alloc(ctx, &df, nq * 4));
+  cudaStream_t st = ctx->s_comp;
+  CK(cudaMemcpyAsync(dq, q, (size_t)nq * 2, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dk, k, (size_t)nkv * 2, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dv, v, (size_t)nkv * 2, cudaMemcpyHostToDevice, st));
+  AttnArgs aa;
+  aa.q = dq; aa.kc = dk; aa.vc = dv; aa.o = dout; aa.b = b; aa.n = n; aa.past = past; aa.d = d;
+  aa.n_heads = n_heads; aa.kv_b = b; aa.dkv = dkv; aa.group = n_heads / n_kv_heads;
+  aa.ws = ctx->ws; aa.ws_floats = ctx->ws_floats; aa.num_sms = ctx->num_sms;
+  if (n == 1) LAUNCH(launch_attention_decode(aa, st));
+  else LAUNCH(launch_attention_prefill(aa, st));
+  LAUNCH(launch_f16_to_f32(dout, df, nq, st));
+  CK(cudaMemcpyAsync(o, df, (size_t)nq * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  cudaFree(dq); cudaFree(dk); cudaFree(dv); cudaFree(dout); cudaFree(df);
+  ctx->hbm_bytes -= nq * 2 * 2 + nkv * 2 * 2 + nq * 4;
+  return PIPO_OK;
+}
+
+pipo_status pipo_rope(pipo_ctx* ctx, const uint16_t* q, const uint16_t* k, int32_t b, int32_t n, int32_t past,
+                      float* q_out, float* k_out) {
+  CHECK_CTX();
+  if (ctx->arch != PIPO_ARCH_LLAMA) return set_err(PIPO_E_STATE, "pipo_rope needs a LLaMA context");
+  if (!q || !k || !q_out || !k_out || b <= 0 || n <= 0 || past < 0 || past + n > ctx->max_s)
+    return set_err(PIPO_E_INVALID_ARG, "bad rope arguments");
+  CK(cudaSetDevice(ctx->cfg.device));
+  __half *dq = nullptr, *dk = nullptr;
+  float* df = nullptr;
+  const int64_t nq = (int64_t)b * n * ctx->d, nk = (int64_t)(past + n) * b * ctx->dkv;
+  TRY(dev_alloc(ctx, &dq, nq * 2));
+  TRY(dev_alloc(ctx, &dk, nk * 2));
+  TRY(dev_alloc(ctx, &df, std::max(nq, nk) * 4));
+  cudaStream_t st = ctx->s_comp;
+  CK(cudaMemcpyAsync(dq, q, (size_t)nq * 2, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dk, k, (size_t)nk * 2, cudaMemcpyHostToDevice, st));
+  LAUNCH(launch_rope(dq, dk, ctx->rope_inv, b, n, past, ctx->H, ctx->Hkv, ctx->hd, b, st));
+  LAUNCH(launch_f16_to_f32(dq, df, nq, st));
+  CK(cudaMemcpyAsync(q_out, df, (size_t)nq * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  LAUNCH(launch_f16_to_f32(dk, df, nk, st));
+  CK(cudaMemcpyAsync(k_out, df, (size_t)nk * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  cudaFree(dq); cudaFree(dk); cudaFree(df);
+  ctx->hbm_bytes -= nq * 2 + nk * 2 + std::max(nq, nk) * 4;
   return PIPO_OK;
 }
 

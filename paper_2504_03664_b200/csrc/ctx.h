@@ -36,6 +36,9 @@ struct pipo_ctx {
   pipo_config cfg{};
   std::string disk_dir;
   int d = 0, l = 0, H = 0, F = 0, V = 0, hd = 0, max_b = 0, max_s = 0, wfmt = 1;
+  int arch = 0;                    // PIPO_ARCH_OPT / PIPO_ARCH_LLAMA
+  int Hkv = 0, dkv = 0;            // KV heads, K/V row width (OPT: H, d)
+  float* rope_inv = nullptr;       // LLaMA: device [hd/2] inverse frequencies (llama3 rule)
   int weight_tier = 1, kv_tier = 0, R = 2, gemv_max_m = 15;
   int64_t chunk = 0;
   pipo::LayerLayout lay;
@@ -51,6 +54,7 @@ struct pipo_ctx {
   __half* pos = nullptr;      // [max_pos + 2][d]
   __half* lnf_g = nullptr;
   __half* lnf_b = nullptr;
+  __half* head = nullptr;     // LM head weight, tiled [V_pad x d]: == tok (OPT, tied) or own (LLaMA)
   bool embed_loaded = false;
   std::vector<char> layer_loaded;
 
@@ -77,6 +81,7 @@ struct pipo_ctx {
   __half* xa = nullptr;            // [rows][d] LN output / attention output
   __half* q = nullptr;             // [rows][d]
   __half* u = nullptr;             // [rows][F]
+  __half* gu = nullptr;            // LLaMA: FC1 gate|up output [rows][2F] (tile-interleaved)
   float* logits = nullptr;         // [max_b][V]
   int32_t* ids = nullptr;          // [rows]
   int32_t* next = nullptr;         // [max_b]

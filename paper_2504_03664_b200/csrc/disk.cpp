@@ -68,7 +68,7 @@ struct DiskTier {
 static uint64_t layout_hash(const pipo_ctx* ctx) {
   uint64_t h = 1469598103934665603ull;
   auto mix = [&](int64_t v) { h = (h ^ (uint64_t)v) * 1099511628211ull; };
-  mix(ctx->d); mix(ctx->F); mix(ctx->wfmt); mix(ctx->layer_bytes);
+  mix(ctx->d); mix(ctx->F); mix(ctx->wfmt); mix(ctx->layer_bytes); mix(ctx->arch); mix(ctx->dkv);
   return h;
 }
 

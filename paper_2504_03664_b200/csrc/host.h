@@ -25,8 +25,7 @@ bool quantize_tiled(const float* w, int64_t rows, int64_t cols, uint8_t* tiled);
 void tile_fp16(const float* w, int64_t rows, int64_t cols, uint8_t* tiled);
 
 // Build a decoder layer's merged blob (layout.h) from fp32 masters.
-bool build_layer_blob(const pipo_layer_weights* w, const LayerLayout& L, int64_t d, int64_t F, int wfmt,
-                      uint8_t* blob);
+bool build_layer_blob(const pipo_layer_weights* w, const LayerLayout& L, int wfmt, uint8_t* blob);
 
 // Disk tier: one file per layer, header + payload, O_DIRECT-aligned.
 struct BlobFileHeader {

@@ -117,51 +117,71 @@ bool quantize_canonical(const float* w, int64_t rows, int64_t cols, uint8_t* cod
   return ok;
 }
 
-bool quantize_tiled(const float* w, int64_t rows, int64_t cols, uint8_t* tiled) {
+// One 128-row tile of the tiled layout: `src` -> rows 0..nrows-1 (zero rows beyond),
+// n_kb k-blocks written at `dst` (the tile's first block).
+static bool quantize_one_tile(const float* src, int64_t nrows, int64_t cols, uint8_t* dst) {
+  const int64_t n_kb = cols / 64;
+  const float zeros[64] = {0};
+  bool good = true;
+  for (int64_t kb = 0; kb < n_kb; ++kb) {
+    uint8_t* blk = dst + kb * kInt4BlockBytes;
+    for (int rr = 0; rr < 128; ++rr) {
+      uint16_t sb;
+      int q[64];
+      good &= quant_codes(rr < nrows ? src + rr * cols + kb * 64 : zeros, q, &sb);
+      uint32_t words[8];
+      for (int wi = 0; wi < 8; ++wi) words[wi] = pack_tiled_word(q + wi * 8);
+      std::memcpy(blk + (0 * 128 + rr) * 16, words, 16);
+      std::memcpy(blk + (1 * 128 + rr) * 16, words + 4, 16);
+      std::memcpy(blk + 4096 + rr * 2, &sb, 2);
+    }
+  }
+  return good;
+}
+
+static void tile_fp16_one(const float* src, int64_t nrows, int64_t cols, uint8_t* dst) {
+  const int64_t n_kb = cols / 64;
+  uint16_t* out = reinterpret_cast<uint16_t*>(dst);
+  for (int64_t rr = 0; rr < 128; ++rr)
+    for (int64_t k = 0; k < cols; ++k)
+      out[fp16_tiled_index(rr, k, n_kb)] = rr < nrows ? f32_to_f16_rne(src[rr * cols + k]) : 0;
+}
+
+// tile t of the stored matrix <- master rows row_of_tile(t) .. +127 (identity order, or
+// the GLU interleave: tile 2p = gate rows 128p.., tile 2p+1 = up rows F + 128p..)
+static bool tile_matrix(const float* w, int64_t rows, int64_t cols, int wfmt, bool glu, uint8_t* tiled) {
   if (cols % 64 != 0) return false;
-  const MatLayout m = mat_layout(rows, cols, 1);
+  const MatLayout m = mat_layout(rows, cols, wfmt);
+  const int64_t half = rows / 2;
   std::atomic<bool> ok{true};
   parallel_for(m.n_rt, [&](int64_t t0, int64_t t1) {
     bool good = true;
-    const float zeros[64] = {0};
-    for (int64_t rt = t0; rt < t1; ++rt)
-      for (int64_t kb = 0; kb < m.n_kb; ++kb) {
-        uint8_t* blk = tiled + (rt * m.n_kb + kb) * kInt4BlockBytes;
-        for (int rr = 0; rr < 128; ++rr) {
-          const int64_t r = rt * 128 + rr;
-          uint16_t sb;
-          int q[64];
-          good &= quant_codes(r < rows ? w + r * cols + kb * 64 : zeros, q, &sb);
-          uint32_t words[8];
-          for (int wi = 0; wi < 8; ++wi) words[wi] = pack_tiled_word(q + wi * 8);
-          std::memcpy(blk + (0 * 128 + rr) * 16, words, 16);
-          std::memcpy(blk + (1 * 128 + rr) * 16, words + 4, 16);
-          std::memcpy(blk + 4096 + rr * 2, &sb, 2);
-        }
-      }
+    for (int64_t t = t0; t < t1; ++t) {
+      const int64_t r0 = glu ? (t & 1) * half + (t >> 1) * 128 : t * 128;
+      const int64_t end = glu ? (t & 1) * half + half : rows;
+      const int64_t nr = std::min<int64_t>(128, end - r0);
+      uint8_t* dst = tiled + t * m.n_kb * m.block_bytes;
+      if (wfmt == PIPO_W_INT4_G64) good &= quantize_one_tile(w + r0 * cols, nr, cols, dst);
+      else tile_fp16_one(w + r0 * cols, nr, cols, dst);
+    }
     if (!good) ok = false;
   });
   return ok;
 }
 
-void tile_fp16(const float* w, int64_t rows, int64_t cols, uint8_t* tiled) {
-  const MatLayout m = mat_layout(rows, cols, 0);
-  uint16_t* out = reinterpret_cast<uint16_t*>(tiled);
-  parallel_for(m.n_rt, [&](int64_t t0, int64_t t1) {
-    for (int64_t rt = t0; rt < t1; ++rt)
-      for (int64_t rr = 0; rr < 128; ++rr) {
-        const int64_t r = rt * 128 + rr;
-        for (int64_t k = 0; k < cols; ++k)
-          out[fp16_tiled_index(r, k, m.n_kb)] = r < rows ? f32_to_f16_rne(w[r * cols + k]) : 0;
-      }
-  });
+bool quantize_tiled(const float* w, int64_t rows, int64_t cols, uint8_t* tiled) {
+  return tile_matrix(w, rows, cols, PIPO_W_INT4_G64, false, tiled);
 }
 
-bool build_layer_blob(const pipo_layer_weights* w, const LayerLayout& L, int64_t d, int64_t F, int wfmt,
-                      uint8_t* blob) {
+void tile_fp16(const float* w, int64_t rows, int64_t cols, uint8_t* tiled) {
+  tile_matrix(w, rows, cols, PIPO_W_FP16, false, tiled);
+}
+
+bool build_layer_blob(const pipo_layer_weights* w, const LayerLayout& L, int wfmt, uint8_t* blob) {
   std::memset(blob, 0, (size_t)L.total);
   const float* vecs[V_COUNT] = {w->ln1_g, w->ln1_b, w->b_qkv, w->b_out, w->ln2_g, w->ln2_b, w->b_fc1, w->b_fc2};
   for (int v = 0; v < V_COUNT; ++v) {
+    if (L.vec_len[v] == 0) continue;   // LLaMA: no biases / betas
     if (!vecs[v]) return false;
     uint16_t* dst = reinterpret_cast<uint16_t*>(blob + L.vec_off[v]);
     for (int64_t i = 0; i < L.vec_len[v]; ++i) {
@@ -170,14 +190,9 @@ bool build_layer_blob(const pipo_layer_weights* w, const LayerLayout& L, int64_t
     }
   }
   const float* mats[M_COUNT] = {w->w_qkv, w->w_out, w->w_fc1, w->w_fc2};
-  const int64_t rows[M_COUNT] = {3 * d, d, F, d}, cols[M_COUNT] = {d, d, d, F};
   for (int i = 0; i < M_COUNT; ++i) {
     if (!mats[i]) return false;
-    if (wfmt == PIPO_W_INT4_G64) {
-      if (!quantize_tiled(mats[i], rows[i], cols[i], blob + L.mat_off[i])) return false;
-    } else {
-      tile_fp16(mats[i], rows[i], cols[i], blob + L.mat_off[i]);
-    }
+    if (!tile_matrix(mats[i], L.mat[i].N, L.mat[i].K, wfmt, L.glu && i == M_FC1, blob + L.mat_off[i])) return false;
   }
   return true;
 }

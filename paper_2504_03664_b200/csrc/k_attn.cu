@@ -23,10 +23,13 @@ namespace pipo {
 constexpr float kLog2e = 1.4426950408889634f;
 
 // element strides of the K/V source: position-major cache by default
+// GQA (LLaMA): K/V rows are dkv = n_kv_heads * hd wide and query head j
+// reads KV head j / group; OPT is dkv = d, group = 1.
+__device__ __forceinline__ int kv_width(const AttnArgs& a) { return a.dkv ? a.dkv : a.d; }
 __device__ __forceinline__ int64_t kv_pstride(const AttnArgs& a) {
-  return a.kv_pos_stride ? a.kv_pos_stride : (int64_t)a.kv_b * a.d;
+  return a.kv_pos_stride ? a.kv_pos_stride : (int64_t)a.kv_b * kv_width(a);
 }
-__device__ __forceinline__ int64_t kv_bstride(const AttnArgs& a) { return a.kv_b_stride ? a.kv_b_stride : a.d; }
+__device__ __forceinline__ int64_t kv_bstride(const AttnArgs& a) { return a.kv_b_stride ? a.kv_b_stride : kv_width(a); }
 
 template <int E>
 __device__ __forceinline__ void load_row(const __half* p, float* out) {
@@ -55,8 +58,8 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnArgs a, int n_spli
 #pragma unroll
   for (int e = 0; e < E; ++e) q[e] *= kLog2e;   // scores in log2 units
   const int64_t pstride = kv_pstride(a);
-  const __half* kbase = a.kc + (int64_t)bi * kv_bstride(a) + head * HD + lane * E;
-  const __half* vbase = a.vc + (int64_t)bi * kv_bstride(a) + head * HD + lane * E;
+  const __half* kbase = a.kc + (int64_t)bi * kv_bstride(a) + (head / a.group) * HD + lane * E;
+  const __half* vbase = a.vc + (int64_t)bi * kv_bstride(a) + (head / a.group) * HD + lane * E;
   float m_run = -INFINITY, l_run = 0.f, acc[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) acc[e] = 0.f;
@@ -153,8 +156,8 @@ __global__ void __launch_bounds__(128) attn_decode_v2_kernel(AttnArgs a, int n_s
     }
   }
   const int64_t pstride = kv_pstride(a);
-  const __half* kbase = a.kc + (int64_t)bi * kv_bstride(a) + head * HD + sl * 8;
-  const __half* vbase = a.vc + (int64_t)bi * kv_bstride(a) + head * HD + sl * 8;
+  const __half* kbase = a.kc + (int64_t)bi * kv_bstride(a) + (head / a.group) * HD + sl * 8;
+  const __half* vbase = a.vc + (int64_t)bi * kv_bstride(a) + (head / a.group) * HD + sl * 8;
   float m_run = -INFINITY, l_run = 0.f, acc[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) acc[e] = 0.f;
@@ -273,8 +276,8 @@ __global__ void __launch_bounds__(256) attn_prefill_kernel(AttnArgs a) {
     for (int e = 0; e < E; ++e) q[u][e] *= kLog2e;
   }
   const int64_t pstride = kv_pstride(a);
-  const __half* kbase = a.kc + (int64_t)bi * kv_bstride(a) + head * HD + lane * E;
-  const __half* vbase = a.vc + (int64_t)bi * kv_bstride(a) + head * HD + lane * E;
+  const __half* kbase = a.kc + (int64_t)bi * kv_bstride(a) + (head / a.group) * HD + lane * E;
+  const __half* vbase = a.vc + (int64_t)bi * kv_bstride(a) + (head / a.group) * HD + lane * E;
   float m_run[4], l_run[4], acc[4][E];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
@@ -353,7 +356,7 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(AttnArgs a) {
   auto load_kv = [&](int j, int buf) {
     for (int c = tid; c < 64 * CH; c += 128) {
       const int r = c / CH, ch = c % CH, p = j * 64 + r;
-      const int64_t off = (int64_t)min(p, L - 1) * pstride + (int64_t)bi * bstride + head * HD + ch * 8;
+      const int64_t off = (int64_t)min(p, L - 1) * pstride + (int64_t)bi * bstride + (head / a.group) * HD + ch * 8;
       const int bytes = p < L ? 16 : 0;
       cp_async16(sK + (buf * 64 + r) * KP + ch * 8, a.kc + off, bytes);
       cp_async16(sV + (buf * 64 + r) * KP + ch * 8, a.vc + off, bytes);

@@ -16,10 +16,10 @@ __global__ void embed_kernel(const int32_t* ids, int n, int past, const __half* 
   const int m = blockIdx.x;
   const int t = m % n;
   const int64_t id = ids[m];
-  const __half* prow = pos + (int64_t)(past + t + 2) * d;
+  const __half* prow = pos ? pos + (int64_t)(past + t + 2) * d : nullptr;   // LLaMA: no position table
   for (int k = threadIdx.x; k < d; k += blockDim.x) {
     const float a = __half2float(tok[fp16_tiled_index(id, k, n_kb)]);
-    h[(int64_t)m * d + k] = a + __half2float(prow[k]);
+    h[(int64_t)m * d + k] = prow ? a + __half2float(prow[k]) : a;
   }
 }
 
@@ -59,7 +59,8 @@ __global__ void __launch_bounds__(LN_THREADS) layernorm_kernel(const float* h, i
     v[i] = k < d ? row[k] : 0.f;
     s += v[i];
   }
-  const float mean = block_sum(s, red) / d;
+  // RMSNorm (LLaMA, beta == nullptr): x / sqrt(mean(x^2) + eps) * g, i.e. mean taken as 0
+  const float mean = beta ? block_sum(s, red) / d : 0.f;
   float q = 0.f;
 #pragma unroll
   for (int i = 0; i < LN_MAX_PER_THREAD; ++i) {
@@ -73,7 +74,7 @@ __global__ void __launch_bounds__(LN_THREADS) layernorm_kernel(const float* h, i
 #pragma unroll
   for (int i = 0; i < LN_MAX_PER_THREAD; ++i) {
     const int k = threadIdx.x + i * LN_THREADS;
-    if (k < d) out[k] = __float2half_rn((v[i] - mean) * rstd * __half2float(g[k]) + __half2float(beta[k]));
+    if (k < d) out[k] = __float2half_rn((v[i] - mean) * rstd * __half2float(g[k]) + (beta ? __half2float(beta[k]) : 0.f));
   }
 }
 
@@ -81,6 +82,69 @@ int launch_layernorm(const float* h, int64_t row_stride, int rows, int d, const 
                      const __half* beta, __half* x, cudaStream_t st) {
   if (d > LN_THREADS * LN_MAX_PER_THREAD) return -1;
   layernorm_kernel<<<rows, LN_THREADS, 0, st>>>(h, row_stride, d, g, beta, x);
+  return 1;
+}
+
+// LLaMA RoPE (NEXT-4): one thread per (row, head, pair i); x1 = x[i], x2 = x[i + hd/2],
+// angle = pos * inv_freq[i] in fp32 (sincosf, full precision), results rounded to fp16.
+// q heads first, then the KV heads of the new K rows in the cache.
+__global__ void rope_kernel(__half* q, __half* kc, const float* inv_freq, int n, int past, int n_heads,
+                            int n_kv_heads, int hd, int kv_b, int64_t total) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const int half = hd >> 1;
+  const int i = (int)(idx % half);
+  const int64_t rest = idx / half;
+  const int heads = n_heads + n_kv_heads;
+  const int hh = (int)(rest % heads);
+  const int m = (int)(rest / heads);
+  const int bi = m / n, t = m - bi * n;
+  __half* x = hh < n_heads ? q + (int64_t)m * n_heads * hd + hh * hd
+                           : kc + ((int64_t)(past + t) * kv_b + bi) * n_kv_heads * hd + (hh - n_heads) * hd;
+  float sn, cs;
+  sincosf((float)(past + t) * inv_freq[i], &sn, &cs);
+  const float x1 = __half2float(x[i]), x2 = __half2float(x[i + half]);
+  x[i] = __float2half_rn(x1 * cs - x2 * sn);
+  x[i + half] = __float2half_rn(x2 * cs + x1 * sn);
+}
+
+int launch_rope(__half* q, __half* kc, const float* inv_freq, int b, int n, int past, int n_heads, int n_kv_heads,
+                int hd, int kv_b, cudaStream_t st) {
+  const int64_t total = (int64_t)b * n * (n_heads + n_kv_heads) * (hd / 2);
+  if (total == 0) return 0;
+  rope_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(q, kc, inv_freq, n, past, n_heads, n_kv_heads, hd,
+                                                                kv_b, total);
+  return 1;
+}
+
+// SwiGLU (NEXT-4): 8 features per thread (16-B loads of gate and up, 16-B store).
+__global__ void swiglu_kernel(const __half* gu, int F, int64_t total8, __half* u) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total8) return;
+  const int f8 = F / 8;
+  const int64_t m = idx / f8;
+  const int f = (int)(idx - m * f8) * 8;
+  const int p = f >> 7, j = f & 127;
+  const __half* row = gu + m * 2 * (int64_t)F;
+  const uint4 gv = *reinterpret_cast<const uint4*>(row + p * 256 + j);
+  const uint4 uv = *reinterpret_cast<const uint4*>(row + p * 256 + 128 + j);
+  const __half2* g2 = reinterpret_cast<const __half2*>(&gv);
+  const __half2* u2 = reinterpret_cast<const __half2*>(&uv);
+  uint4 ov;
+  __half2* o2 = reinterpret_cast<__half2*>(&ov);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 g = __half22float2(g2[k]), up = __half22float2(u2[k]);
+    const float a = g.x / (1.f + expf(-g.x)) * up.x, c = g.y / (1.f + expf(-g.y)) * up.y;
+    o2[k] = __floats2half2_rn(a, c);
+  }
+  *reinterpret_cast<uint4*>(u + m * F + f) = ov;
+}
+
+int launch_swiglu(const __half* gu, int M, int F, __half* u, cudaStream_t st) {
+  const int64_t total8 = (int64_t)M * F / 8;
+  if (total8 == 0) return 0;
+  swiglu_kernel<<<(unsigned)((total8 + 255) / 256), 256, 0, st>>>(gu, F, total8, u);
   return 1;
 }
 

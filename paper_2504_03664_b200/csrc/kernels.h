@@ -6,7 +6,7 @@
 
 namespace pipo {
 
-enum EpiKind { EPI_QKV = 0, EPI_RESID = 1, EPI_RELU = 2, EPI_F32 = 3 };
+enum EpiKind { EPI_QKV = 0, EPI_RESID = 1, EPI_RELU = 2, EPI_F32 = 3, EPI_HALF = 4 };
 
 // Fused epilogue of a linear layer (acc = x . W^T for output row m, feature n):
 //  EPI_QKV  : v = acc + b; n < d -> q[m][n] = fp16(v * qscale);  d <= n < 2d -> K cache;
@@ -15,6 +15,8 @@ enum EpiKind { EPI_QKV = 0, EPI_RESID = 1, EPI_RELU = 2, EPI_F32 = 3 };
 //  EPI_RESID: h[m][n] += acc + b          (out-proj, FC2: residual add, fp32 stream)
 //  EPI_RELU : u[m][n] = fp16(relu(acc + b))  (FC1)
 //  EPI_F32  : y[m][n] = acc               (LM head logits; pipo_linear hook)
+//  EPI_HALF : u[m][n] = fp16(acc + b)     (LLaMA FC1 gate|up, consumed by the SwiGLU kernel)
+// GQA (LLaMA): the K and V parts are dkv = n_kv_heads * head_dim wide (dkv = d for OPT).
 struct EpiParams {
   int kind = EPI_F32;
   const __half* bias = nullptr;
@@ -23,6 +25,7 @@ struct EpiParams {
   __half* kc = nullptr;
   __half* vc = nullptr;
   int d = 0, n_tok = 1, past = 0, kv_b = 1;
+  int dkv = 0;                // K / V width (0 -> d)
   int kv_rowmajor = 0;        // 1: k/v go to a [m][2d] staging buffer (int4-KV path)
   float qscale = 1.f;
   float* h = nullptr;
@@ -66,6 +69,7 @@ struct AttnArgs {
   const __half* vc = nullptr;
   __half* o = nullptr;        // same shape as q
   int b = 0, n = 1, past = 0, d = 0, n_heads = 0, kv_b = 0;
+  int dkv = 0, group = 1;     // GQA: K/V rows dkv wide (0 -> d), query head j reads KV head j / group
   int64_t kv_pos_stride = 0;  // elements between positions (0: kv_b * d, position-major cache)
   int64_t kv_b_stride = 0;    // elements between sequences  (0: d)
   int use_cuda_cores = 0;     // prefill: 1 = the CUDA-core reference kernel
@@ -93,6 +97,15 @@ int launch_embed(const int32_t* ids, int b, int n, int past, const __half* tok_t
 int launch_layernorm(const float* h, int64_t row_stride, int rows, int d, const __half* g,
                      const __half* beta, __half* x, cudaStream_t st);
 int launch_argmax(const float* logits, int rows, int V, int ldl, int32_t* out, cudaStream_t st);
+// LLaMA (NEXT-4): RMSNorm = launch_layernorm with beta == nullptr (mean taken as 0).
+// RoPE (rotate-half, angle = pos * inv_freq[i], fp32 math) in place on q [b*n][n_heads*hd]
+// (row m = bi*n + t at position past + t) and on the fresh K rows of the position-major
+// cache [pos][kv_b][n_kv_heads*hd] at positions past .. past+n-1.
+int launch_rope(__half* q, __half* kc, const float* inv_freq, int b, int n, int past, int n_heads, int n_kv_heads,
+                int hd, int kv_b, cudaStream_t st);
+// SwiGLU: u[m][f] = fp16(silu(g) * up) from the tile-interleaved FC1 output gu [M][2F]
+// (gate of feature f = 128p + j at column 256p + j, up at 256p + 128 + j; layout.h).
+int launch_swiglu(const __half* gu, int M, int F, __half* u, cudaStream_t st);
 int launch_unpack_int4(const uint8_t* codes, const uint16_t* scales, int64_t rows, int64_t cols,
                        __half* out, cudaStream_t st);
 // quantize fp32 masters [rows][cols] (device) -> canonical codes/scales and/or tiled blob

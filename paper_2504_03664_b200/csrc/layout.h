@@ -84,17 +84,26 @@ struct LayerLayout {
   int64_t mat_off[M_COUNT];
   MatLayout mat[M_COUNT];
   int64_t total = 0;
+  bool glu = false;   // LLaMA: W_fc1 is [gate | up], stored tile-interleaved (below)
 };
 
-inline LayerLayout layer_layout(int64_t d, int64_t F, int wfmt) {
+// OPT (llama = false): QKV [3d x d], FC1 [F x d], every bias and LN beta present.
+// LLaMA (NEXT-4): QKV [(d + 2 dkv) x d] (GQA), no biases / betas (length
+// 0), FC1 = [gate; up] [2F x d] stored TILE-INTERLEAVED: 128-row tile 2p holds gate rows
+// 128p..128p+127 and tile 2p+1 the up rows of the same features, so the two
+// accumulators a SwiGLU output needs sit in adjacent tiles (F % 128 == 0).
+inline LayerLayout layer_layout(int64_t d, int64_t F, int wfmt, int64_t dkv = -1, bool llama = false) {
   LayerLayout L;
-  L.mat[M_QKV] = mat_layout(3 * d, d, wfmt);
+  if (dkv < 0) dkv = d;
+  L.glu = llama;
+  L.mat[M_QKV] = mat_layout(d + 2 * dkv, d, wfmt);
   L.mat[M_OUT] = mat_layout(d, d, wfmt);
-  L.mat[M_FC1] = mat_layout(F, d, wfmt);
+  L.mat[M_FC1] = mat_layout(llama ? 2 * F : F, d, wfmt);
   L.mat[M_FC2] = mat_layout(d, F, wfmt);
   const int seg_vecs[4][3] = {{V_LN1_G, V_LN1_B, V_B_QKV}, {V_B_OUT, -1, -1},
                               {V_LN2_G, V_LN2_B, V_B_FC1}, {V_B_FC2, -1, -1}};
-  const int64_t len[V_COUNT] = {d, d, 3 * d, d, d, d, F, d};
+  const int64_t z = llama ? 0 : 1;
+  const int64_t len[V_COUNT] = {d, z * d, z * (d + 2 * dkv), z * d, d, z * d, z * F, z * d};
   int64_t off = 0;
   for (int s = 0; s < 4; ++s) {
     off = round_up(off, 4096);

@@ -39,7 +39,12 @@ class pipo_config(C.Structure):
                 ("max_batch", C.c_int32), ("max_seq", C.c_int32), ("wfmt", C.c_int32),
                 ("weight_tier", C.c_int32), ("kv_tier", C.c_int32), ("kv_fmt", C.c_int32), ("ring_layers", C.c_int32),
                 ("chunk_bytes", C.c_int64), ("gemv_max_m", C.c_int32), ("disk_threads", C.c_int32),
-                ("disk_dir", C.c_char_p), ("flags", C.c_uint32)]
+                ("disk_dir", C.c_char_p), ("flags", C.c_uint32),
+                ("arch", C.c_int32), ("n_kv_heads", C.c_int32), ("rope_theta", C.c_float), ("rope_factor", C.c_float),
+                ("rope_low_freq", C.c_float), ("rope_high_freq", C.c_float), ("rope_orig_max_pos", C.c_int32)]
+
+
+PIPO_ARCH_OPT, PIPO_ARCH_LLAMA = 0, 1
 
 
 class pipo_layer_weights(C.Structure):
@@ -48,7 +53,7 @@ class pipo_layer_weights(C.Structure):
 
 
 class pipo_embed_weights(C.Structure):
-    _fields_ = [(n, _f) for n in ("tok", "pos", "lnf_g", "lnf_b")]
+    _fields_ = [(n, _f) for n in ("tok", "pos", "lnf_g", "lnf_b", "lm_head")]
 
 
 class pipo_kstats(C.Structure):
@@ -130,6 +135,9 @@ _sig("pipo_bench_attention", C.c_int, _P, C.c_int32, C.c_int32, C.c_int32, C.c_i
 _sig("pipo_attention_decode", C.c_int, _P, _u16, _u16, _u16, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _f)
 _sig("pipo_attention_prefill", C.c_int, _P, _u16, _u16, _u16, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
      C.c_int32, C.c_int32, _f)
+_sig("pipo_attention_gqa", C.c_int, _P, _u16, _u16, _u16, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+     C.c_int32, _f)
+_sig("pipo_rope", C.c_int, _P, _u16, _u16, C.c_int32, C.c_int32, C.c_int32, _f, _f)
 _sig("pipo_debug_capture", C.c_int, _P, C.c_int32, _f)
 _sig("pipo_probe_h2d", C.c_int, _P, C.c_int64, C.c_int32, C.POINTER(C.c_double))
 _sig("pipo_ffn_hidden_dim", C.c_int64, C.c_int64, C.c_int64, C.c_double)
@@ -144,7 +152,7 @@ EXPORTED = ["pipo_last_error", "pipo_abi_version", "pipeline_init", "pipeline_de
             "pipo_load_synthetic", "prefill", "decode_step", "decode_step_dev", "pipeline_stats",
             "pipeline_stats_reset", "pipo_stream", "pipo_kernel_stats", "pipo_quantize_int4_g64", "pipo_quantize_int4_g64_gpu",
             "pipo_unpack_int4_g64", "pipo_linear", "pipo_bench_linear", "pipo_probe_bulk", "pipo_bench_attention", "pipo_attention_decode", "pipo_attention_prefill", "pipo_debug_capture", "pipo_probe_h2d",
-            "pipo_ffn_hidden_dim", "pipo_memory_model", "pipo_choose_block_size", "pipo_choose_plan"]
+            "pipo_attention_gqa", "pipo_rope", "pipo_ffn_hidden_dim", "pipo_memory_model", "pipo_choose_block_size", "pipo_choose_plan"]
 
 
 class PipoError(RuntimeError):
@@ -186,11 +194,12 @@ def pipeline_destroy(ctx):
 
 def load_layer_weights(ctx, layer: int, w: dict):
     if layer == PIPO_LAYER_EMBED:
-        keep = {k: _c(w[k], np.float32) for k in ("tok", "pos", "lnf_g", "lnf_b")}
+        # absent tensors (LLaMA: pos, lnf_b; OPT: lm_head) are passed as NULL
+        keep = {k: _c(w[k], np.float32) for k in ("tok", "pos", "lnf_g", "lnf_b", "lm_head") if w.get(k) is not None}
         st = pipo_embed_weights(**{k: _ptr(v, C.c_float) for k, v in keep.items()})
     else:
         names = [n for n, _ in pipo_layer_weights._fields_]
-        keep = {k: _c(w[k], np.float32) for k in names}
+        keep = {k: _c(w[k], np.float32) for k in names if w.get(k) is not None}   # LLaMA: no biases
         st = pipo_layer_weights(**{k: _ptr(v, C.c_float) for k, v in keep.items()})
     _check(_lib.load_layer_weights(ctx, layer, C.byref(st)))
 
@@ -328,6 +337,30 @@ def pipo_attention_prefill(ctx, q, k, v, past, n_heads, cuda_cores=False):
     return o
 
 
+def pipo_attention_gqa(ctx, q, k, v, past, n_heads, n_kv_heads):
+    """q [b][n][h*hd], k/v [past+n][b][h_kv*hd] (fp16 values) -> o [b][n][h*hd] fp32."""
+    q = _c(np.asarray(q, dtype=np.float16).view(np.uint16), np.uint16)
+    k = _c(np.asarray(k, dtype=np.float16).view(np.uint16), np.uint16)
+    v = _c(np.asarray(v, dtype=np.float16).view(np.uint16), np.uint16)
+    b, n, d = q.shape
+    o = np.empty((b, n, d), dtype=np.float32)
+    _check(_lib.pipo_attention_gqa(ctx, _ptr(q, C.c_uint16), _ptr(k, C.c_uint16), _ptr(v, C.c_uint16), b, n, past,
+                                   n_heads, n_kv_heads, d // n_heads, _ptr(o, C.c_float)))
+    return o
+
+
+def pipo_rope(ctx, q, k, past):
+    """q [b][n][h*hd], k [past+n][b][h_kv*hd] (fp16 values) -> (q_rot, k_rot) fp32."""
+    q = _c(np.asarray(q, dtype=np.float16).view(np.uint16), np.uint16)
+    k = _c(np.asarray(k, dtype=np.float16).view(np.uint16), np.uint16)
+    b, n, _ = q.shape
+    qo = np.empty(q.shape, dtype=np.float32)
+    ko = np.empty(k.shape, dtype=np.float32)
+    _check(_lib.pipo_rope(ctx, _ptr(q, C.c_uint16), _ptr(k, C.c_uint16), b, n, past, _ptr(qo, C.c_float),
+                          _ptr(ko, C.c_float)))
+    return qo, ko
+
+
 def pipo_debug_capture(ctx, out: np.ndarray | None):
     if out is None:
         _check(_lib.pipo_debug_capture(ctx, 0, None))
@@ -380,13 +413,19 @@ def pipo_choose_plan(spec: pipo_mem_spec, b: int, s: int, *, m_gpu, m_cpu, b_gpu
 def make_config(shape, *, device=0, max_batch, max_seq, wfmt=PIPO_W_INT4_G64, weight_tier=PIPO_TIER_HOST,
                 kv_tier=PIPO_TIER_DEVICE, kv_fmt=PIPO_W_FP16, ring_layers=2, chunk_bytes=0, gemv_max_m=15, disk_threads=4,
                 disk_dir=None, flags=PIPO_F_TIMELINE, n_layers=None) -> pipo_config:
-    """pipo_config from a pipo_synth.OPTShape-like object (d_model, n_layers, n_heads, ffn_dim, vocab, max_pos)."""
+    """pipo_config from a pipo_synth.OPTShape-like object (d_model, n_layers, n_heads, ffn_dim, vocab, max_pos)
+    or a pipo_synth.LlamaShape (adds n_kv_heads and the llama3 RoPE parameters -> arch LLAMA)."""
+    llama = hasattr(shape, "n_kv_heads")
+    extra = dict(arch=PIPO_ARCH_LLAMA, n_kv_heads=shape.n_kv_heads, rope_theta=shape.rope_theta,
+                 rope_factor=shape.rope_factor, rope_low_freq=shape.rope_low_freq, rope_high_freq=shape.rope_high_freq,
+                 rope_orig_max_pos=shape.rope_orig_max_pos) if llama else dict(arch=PIPO_ARCH_OPT)
     return pipo_config(device=device, d_model=shape.d_model, n_layers=n_layers or shape.n_layers,
                        n_heads=shape.n_heads, ffn_dim=shape.ffn_dim, vocab=shape.vocab, max_pos=shape.max_pos,
                        max_batch=max_batch, max_seq=max_seq, wfmt=wfmt, weight_tier=weight_tier, kv_tier=kv_tier,
                        kv_fmt=kv_fmt,
                        ring_layers=ring_layers, chunk_bytes=chunk_bytes, gemv_max_m=gemv_max_m,
-                       disk_threads=disk_threads, disk_dir=(disk_dir.encode() if disk_dir else None), flags=flags)
+                       disk_threads=disk_threads, disk_dir=(disk_dir.encode() if disk_dir else None), flags=flags,
+                       **extra)
 
 
 class Pipeline:
