@@ -1202,6 +1202,26 @@ pipo_status pipo_bench_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, int32_t
   CK(cudaEventSynchronize(e1));
   float ms = 0;
   CK(cudaEventElapsedTime(&ms, e0, e1));
+  // PIPO_BENCH_IDLE_US > 0: time each launch alone after the GPU sat idle that long
+  // (the pipeline's situation when the link is the bottleneck), average of iters
+  const int idle_us = getenv("PIPO_BENCH_IDLE_US") ? atoi(getenv("PIPO_BENCH_IDLE_US")) : 0;
+  if (idle_us > 0) {
+    double tot = 0;
+    for (int i = 0; i < iters; ++i) {
+      la.w = wcopy(i + 1);
+      CK(cudaStreamSynchronize(st));
+      const auto t_end = std::chrono::steady_clock::now() + std::chrono::microseconds(idle_us);
+      while (std::chrono::steady_clock::now() < t_end) {}
+      CK(cudaEventRecord(e0, st));
+      LAUNCH(launch_linear(la, path, ctx->gemv_max_m, st));
+      CK(cudaEventRecord(e1, st));
+      CK(cudaEventSynchronize(e1));
+      float m1 = 0;
+      CK(cudaEventElapsedTime(&m1, e0, e1));
+      tot += m1;
+    }
+    ms = (float)tot;
+  }
   cudaEventDestroy(e0); cudaEventDestroy(e1);
   if (getenv("PIPO_WS_DEBUG") && (atoi(getenv("PIPO_WS_DEBUG")) & 128) && path == 5) {
     // globaltimer stamps of the last launch: 9 entry, 10 after setup, 11 MMA done,
@@ -1229,9 +1249,11 @@ pipo_status pipo_bench_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, int32_t
       double fx = 0, bm = 0;
       for (int c = 0; c < 148; ++c) { fx += (double)ts[c * 16] / 148; bm += (double)(int64_t)ts[c * 16 + 1] / 148; }
       fprintf(stderr, "tm-clk fixup %.0f cycles, barrier-after-MMA-end %.0f cycles (avg over CTAs)\n", fx, bm);
-      double sp = 0, lp = 0, ww = 0;
-      for (int c = 0; c < 148; ++c) { sp += (double)ts[c * 16 + 3] / 148; lp += (double)ts[c * 16 + 4] / 148; ww += (double)ts[c * 16 + 5] / 148; }
-      fprintf(stderr, "tm-clk fixup spin %.0f loop %.0f cycles, items %.0f\n", sp, lp, ww);
+      for (int c = 0; c < 148; ++c)
+        if (ts[c * 16 + 6] && ts[c * 16 + 6] < 1000)
+          fprintf(stderr, "tm-fin cta %d: n_fin %llu spin %llu copy %llu process %llu cycles\n", c,
+                  (unsigned long long)ts[c * 16 + 6], (unsigned long long)ts[c * 16 + 3],
+                  (unsigned long long)ts[c * 16 + 4], (unsigned long long)ts[c * 16 + 5]);
     }
     fprintf(stderr, "reduce first start %.2f last end %.2f us\n", (double)(int64_t)(ts[148 * 16] - t0) * 1e-3, (double)(int64_t)(ts[148 * 16 + 1] - t0) * 1e-3);
   } else if (getenv("PIPO_WS_DEBUG") && (atoi(getenv("PIPO_WS_DEBUG")) & 32) && path == 5) {

@@ -44,27 +44,41 @@ __device__ __forceinline__ void load_row(const __half* p, float* out) {
   }
 }
 
-template <int HD>
+// G > 1 (GQA): one CTA per (KV head, b, split) serves the G query heads
+// that share the KV head, so each K/V row is read from HBM once for all G heads (G = 1:
+// blockIdx.x is the query head; a group size without a G instance also runs G = 1 with
+// the head -> KV-head mapping, re-reading shared rows through L2).
+template <int HD, int G>
 __global__ void __launch_bounds__(128) attn_decode_kernel(AttnArgs a, int n_splits, int pos_per_split) {
   constexpr int E = HD / 32;
-  __shared__ float sm_m[4], sm_l[4];
-  __shared__ float sm_acc[4][HD];
-  const int head = blockIdx.x, bi = blockIdx.y, split = blockIdx.z;
+  __shared__ float sm_m[G][4], sm_l[G][4];
+  __shared__ float sm_acc[G][4][HD];
+  const int bi = blockIdx.y, split = blockIdx.z;
+  const int head0 = G == 1 ? blockIdx.x : blockIdx.x * G;            // first query head
+  const int kvh = G == 1 ? blockIdx.x / a.group : blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int L = a.past + 1;
   const int lo = split * pos_per_split, hi = min(L, lo + pos_per_split);
-  float q[E];
-  load_row<E>(a.q + (int64_t)bi * a.d + head * HD + lane * E, q);
+  float q[G][E];
 #pragma unroll
-  for (int e = 0; e < E; ++e) q[e] *= kLog2e;   // scores in log2 units
+  for (int g = 0; g < G; ++g) {
+    load_row<E>(a.q + (int64_t)bi * a.d + (head0 + g) * HD + lane * E, q[g]);
+#pragma unroll
+    for (int e = 0; e < E; ++e) q[g][e] *= kLog2e;   // scores in log2 units
+  }
   const int64_t pstride = kv_pstride(a);
-  const __half* kbase = a.kc + (int64_t)bi * kv_bstride(a) + (head / a.group) * HD + lane * E;
-  const __half* vbase = a.vc + (int64_t)bi * kv_bstride(a) + (head / a.group) * HD + lane * E;
-  float m_run = -INFINITY, l_run = 0.f, acc[E];
+  const __half* kbase = a.kc + (int64_t)bi * kv_bstride(a) + kvh * HD + lane * E;
+  const __half* vbase = a.vc + (int64_t)bi * kv_bstride(a) + kvh * HD + lane * E;
+  float m_run[G], l_run[G], acc[G][E];
 #pragma unroll
-  for (int e = 0; e < E; ++e) acc[e] = 0.f;
+  for (int g = 0; g < G; ++g) {
+    m_run[g] = -INFINITY;
+    l_run[g] = 0.f;
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[g][e] = 0.f;
+  }
   for (int p0 = lo + 4 * warp; p0 < hi; p0 += 16) {
-    float kr[4][E], vr[4][E], s[4];
+    float kr[4][E], vr[4][E], s[G][4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int p = min(p0 + u, hi - 1);
@@ -72,50 +86,60 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnArgs a, int n_spli
       load_row<E>(vbase + p * pstride, vr[u]);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      float t = 0.f;
+    for (int g = 0; g < G; ++g)
 #pragma unroll
-      for (int e = 0; e < E; ++e) t = fmaf(q[e], kr[u][e], t);
-      s[u] = t;
-    }
+      for (int u = 0; u < 4; ++u) {
+        float t = 0.f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) t = fmaf(q[g][e], kr[u][e], t);
+        s[g][u] = t;
+      }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-      for (int u = 0; u < 4; ++u) s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
-    float mx = m_run;
+      for (int g = 0; g < G; ++g)
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (p0 + u >= hi) s[u] = -INFINITY;
-      mx = fmaxf(mx, s[u]);
+        for (int u = 0; u < 4; ++u) s[g][u] += __shfl_xor_sync(0xffffffffu, s[g][u], o);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      float mx = m_run[g];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (p0 + u >= hi) s[g][u] = -INFINITY;
+        mx = fmaxf(mx, s[g][u]);
+      }
+      const float corr = exp2f(m_run[g] - mx);   // m_run=-inf, mx finite -> 0
+      l_run[g] *= corr;
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc[g][e] *= corr;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float pu = exp2f(s[g][u] - mx);     // -inf -> 0
+        l_run[g] += pu;
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[g][e] = fmaf(pu, vr[u][e], acc[g][e]);
+      }
+      m_run[g] = mx;
     }
-    const float corr = exp2f(m_run - mx);   // m_run=-inf, mx finite -> 0
-    l_run *= corr;
-#pragma unroll
-    for (int e = 0; e < E; ++e) acc[e] *= corr;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const float pu = exp2f(s[u] - mx);     // -inf -> 0
-      l_run += pu;
-#pragma unroll
-      for (int e = 0; e < E; ++e) acc[e] = fmaf(pu, vr[u][e], acc[e]);
-    }
-    m_run = mx;
   }
-  if (lane == 0) { sm_m[warp] = m_run; sm_l[warp] = l_run; }
 #pragma unroll
-  for (int e = 0; e < E; ++e) sm_acc[warp][lane * E + e] = acc[e];
+  for (int g = 0; g < G; ++g) {
+    if (lane == 0) { sm_m[g][warp] = m_run[g]; sm_l[g][warp] = l_run[g]; }
+#pragma unroll
+    for (int e = 0; e < E; ++e) sm_acc[g][warp][lane * E + e] = acc[g][e];
+  }
   __syncthreads();
-  if (threadIdx.x < HD) {
-    const int t = threadIdx.x;
+  for (int i = threadIdx.x; i < G * HD; i += 128) {
+    const int g = i / HD, t = i - g * HD, head = head0 + g;
     float M = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) M = fmaxf(M, sm_m[w]);
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, sm_m[g][w]);
     float l = 0.f, o = 0.f;
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
-      const float f = sm_m[w] == -INFINITY ? 0.f : exp2f(sm_m[w] - M);
-      l += sm_l[w] * f;
-      o += sm_acc[w][t] * f;
+      const float f = sm_m[g][w] == -INFINITY ? 0.f : exp2f(sm_m[g][w] - M);
+      l += sm_l[g][w] * f;
+      o += sm_acc[g][w][t] * f;
     }
     if (n_splits == 1) {
       a.o[(int64_t)bi * a.d + head * HD + t] = __float2half_rn(o / l);
@@ -693,7 +717,9 @@ int launch_attention_decode(const AttnArgs& a, cudaStream_t st) {
   const int hd = a.d / a.n_heads;
   if (hd != 64 && hd != 128) return -1;
   const int L = a.past + 1;
-  const int pairs = a.b * a.n_heads;
+  // GQA: one CTA per KV head serves its whole query-head group (group sizes 2, 4, 8)
+  const int G = (a.group == 2 || a.group == 4 || a.group == 8) && !a.use_cuda_cores ? a.group : 1;
+  const int pairs = a.b * a.n_heads / G;
   // enough CTAs for ~8 waves of resident blocks (9 per SM): the block scheduler then
   // balances the tail to within ~1/8 of the kernel; splits merge in a second kernel
   const int target = a.num_sms * 72;
@@ -701,11 +727,18 @@ int launch_attention_decode(const AttnArgs& a, cudaStream_t st) {
   n_splits = max(1, min(n_splits, (L + 63) / 64));
   const int per = (L + n_splits - 1) / n_splits;
   n_splits = (L + per - 1) / per;
-  if (n_splits > 1 && (int64_t)pairs * n_splits * (hd + 2) > a.ws_floats) return -1;
-  dim3 grid(a.n_heads, a.b, n_splits);
+  if (n_splits > 1 && (int64_t)a.b * a.n_heads * n_splits * (hd + 2) > a.ws_floats) return -1;
+  dim3 grid(a.n_heads / G, a.b, n_splits);
   if (!a.use_cuda_cores) {   // one K/V row per warp: measured 0-5% ahead of v2 at c3-c5
-    if (hd == 64) attn_decode_kernel<64><<<grid, 128, 0, st>>>(a, n_splits, per);
-    else attn_decode_kernel<128><<<grid, 128, 0, st>>>(a, n_splits, per);
+#define PIPO_DECODE(HDV, GV) attn_decode_kernel<HDV, GV><<<grid, 128, 0, st>>>(a, n_splits, per)
+    if (hd == 64) {
+      if (G == 1) PIPO_DECODE(64, 1); else if (G == 2) PIPO_DECODE(64, 2); else if (G == 4) PIPO_DECODE(64, 4);
+      else PIPO_DECODE(64, 8);
+    } else {
+      if (G == 1) PIPO_DECODE(128, 1); else if (G == 2) PIPO_DECODE(128, 2); else if (G == 4) PIPO_DECODE(128, 4);
+      else PIPO_DECODE(128, 8);
+    }
+#undef PIPO_DECODE
   } else {                   // v2: lane groups with 16-B row loads (kept for A/B)
     if (hd == 64) attn_decode_v2_kernel<64><<<grid, 128, 0, st>>>(a, n_splits, per);
     else attn_decode_v2_kernel<128><<<grid, 128, 0, st>>>(a, n_splits, per);

@@ -475,11 +475,12 @@ struct TmCfg {
   static constexpr int E0 = 2 + UW;                              // first epilogue warp
   static constexpr int XW = E0 + 4;                              // x producer warp
   static constexpr int THREADS = (XW + 1) * 32;
-  static constexpr int SMEM = 1024 + NX * X_TILE + NR * RAW + 512;
+  static constexpr int SMEM = 1024 + NX * X_TILE + NR * RAW + 1024;   // + mbarriers (<= 70) and TMEM slot
   static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
   static_assert(NA >= 2, "TMEM budget");
   static_assert(UW == 8 || UW == 16, "unpack warps");
+  static_assert((2 * NR + 2 * NX + 2 * NA + 2 + NACC + 1) * 8 + 4 <= 1024, "barrier area");
 };
 
 __device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc, uint32_t acc) {
@@ -515,115 +516,21 @@ __device__ __forceinline__ uint64_t clk() {
   return t;
 }
 
-// In-kernel stream-K fixup (replaces the ws_reduce_kernel launch).  Every CTA has written
-// the partial accumulators of its shared tiles (<= 2: the tile it entered mid-way and the
-// one it left mid-way) to its ws slots and fenced them.  For each shared tile t with
-// contributors cf..cl it bumps arrive[t]; once all n = cl-cf+1 have arrived, contributor
-// i sums the n partials of element share i (contiguous ws range, coalesced) in k order —
-// the same order for every share and every run, so results are bit-reproducible — and
-// runs the fused epilogue on it.  The n contributors reduce in parallel (no single
-// last-arriver serialising the whole tile).  Spinning is safe: grid <= #SMs with one CTA
-// per SM, and the CTAs waited on never wait on anything scheduled after them.
-// done[t] (second half of the counter array) lets the last finisher reset both counters.
-template <int BN>
-__device__ __forceinline__ void tm_fixup(const LinearArgs& a, int64_t u0, int64_t u1, int n_ku, int n_pairs,
-                                         int n_rt, int64_t U, int G, uint64_t* dbgts) {
-  const int tid = threadIdx.x, nthr = blockDim.x;
-  int* arrive = a.counters;
-  int* done = a.counters + (a.n_counters >> 1);
-  // the CTA's shared tiles: at most its first and its last tile
-  int64_t pt[2];
-  int np = 0;
-  const int64_t t_first = u0 / n_ku, t_last = (u1 - 1) / n_ku;
-  if (u0 > t_first * n_ku || u1 < (t_first + 1) * n_ku) pt[np++] = t_first;
-  if (t_last != t_first && u1 < (t_last + 1) * n_ku) pt[np++] = t_last;
-  if (np == 0) return;
-  int cf[2], n[2], i0[2], w0[2], w1[2], base[2];
-  bool cff[2];
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    if (k >= np) { w0[k] = w1[k] = 0; continue; }
-    const int64_t t = pt[k];
-    cf[k] = ws::cta_of_unit(t * n_ku, U, G);
-    n[k] = ws::cta_of_unit((t + 1) * n_ku - 1, U, G) - cf[k] + 1;
-    i0[k] = (int)blockIdx.x - cf[k];
-    cff[k] = ws::u_begin(cf[k], U, G) / n_ku == t;   // t is cf's first tile -> its slot 0
-    const int pr = (int)(t % n_pairs);
-    const int E4 = ((2 * pr + 1 < n_rt) ? 2 : 1) * BN * 32;   // float4 items of the tile
-    w0[k] = (int)((int64_t)E4 * i0[k] / n[k]);
-    w1[k] = (int)((int64_t)E4 * (i0[k] + 1) / n[k]);
-  }
-  base[0] = 0;
-  base[1] = w1[0] - w0[0];
-  const int W = base[1] + (w1[1] - w0[1]);
-  const uint64_t c0 = clk();
-  if (tid == 0) {
-    for (int k = 0; k < np; ++k) atomicAdd(&arrive[pt[k]], 1);
-    for (int k = 0; k < np; ++k)
-      while (*reinterpret_cast<volatile int*>(&arrive[pt[k]]) < n[k]) __nanosleep(20);
-    __threadfence();
-  }
-  __syncthreads();
-  const uint64_t c1 = clk();
-  // each thread: up to 2 float4 items, contributors in batches of 4, all loads issued
-  // before the (k-ordered) sums
-  for (int wb = 0; wb < W; wb += 2 * nthr) {
-    float4 acc[2];
-    int kk[2], e4[2];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int w = wb + tid + j * nthr;
-      acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-      kk[j] = w < W ? (w >= base[1] ? 1 : 0) : -1;
-      e4[j] = kk[j] >= 0 ? w0[kk[j]] + (w - base[kk[j]]) : 0;
-    }
-    const int nmax = max(kk[0] >= 0 ? n[kk[0]] : 0, kk[1] >= 0 ? n[kk[1]] : 0);
-    for (int cb = 0; cb < nmax; cb += 4) {
-      float4 v[2][4];
-#pragma unroll
-      for (int j = 0; j < 2; ++j)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int k = kk[j];
-          const int cc = cb + q;
-          if (k >= 0 && cc < n[k]) {
-            const int c = cf[k] + cc;
-            const int sl = 2 * c + ((cc == 0 && !cff[k]) ? 1 : 0);
-            v[j][q] = __ldcg(reinterpret_cast<const float4*>(a.ws + (int64_t)sl * (2 * BN * 128)) + e4[j]);
-          } else {
-            v[j][q] = make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-        }
-#pragma unroll
-      for (int j = 0; j < 2; ++j)
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (kk[j] >= 0 && cb + q < n[kk[j]]) {
-            acc[j].x += v[j][q].x; acc[j].y += v[j][q].y; acc[j].z += v[j][q].z; acc[j].w += v[j][q].w;
-          }
-    }
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      if (kk[j] < 0) continue;
-      const int64_t t = pt[kk[j]];
-      const int pr = (int)(t % n_pairs), mt = (int)(t / n_pairs);
-      const int e = e4[j] * 4;
-      const int tt = e / (BN * 128), col = (e / 128) % BN, row = e & 127;
-      const int nn = (2 * pr + tt) * 128 + row, m = mt * BN + col;
-      epi_store(a.epi, m, nn, acc[j].x);
-      epi_store(a.epi, m, nn + 1, acc[j].y);
-      epi_store(a.epi, m, nn + 2, acc[j].z);
-      epi_store(a.epi, m, nn + 3, acc[j].w);
-    }
-  }
-  __syncthreads();
-  if (dbgts && tid == 0) { dbgts[3] = c1 - c0; dbgts[4] = clk() - c1; dbgts[5] = W; }
-  if (tid == 0)
-    for (int k = 0; k < np; ++k)
-      if (atomicAdd(&done[pt[k]], 1) == n[k] - 1) {   // every contributor is past its wait
-        arrive[pt[k]] = 0;
-        done[pt[k]] = 0;
-      }
+// In-kernel stream-K fixup ("finisher" scheme, fix = 1).  A shared tile t is split
+// over CTAs cf..cl.  cf (the CTA holding t's first unit) processes t's head as the LAST
+// segment of its range; every other contributor holds t's tail as the FIRST segment of
+// its range (or its whole range), so their partials are written early — each CTA writes
+// at most one partial, to its own ws slot, then releases arrive[t].  cf keeps its own
+// part in TMEM: when its accumulator is ready it waits for arrive[t] == n - 1, adds the
+// partials of cf+1 .. cl in that order to its accumulator and runs the fused epilogue.
+// The sum is acc_cf + p_cf+1 + ... + p_cl — the same operands in the same order as the
+// separate ws_reduce_kernel (0 + p_cf + ...), so both modes are bit-identical and
+// deterministic.  Spinning is safe: grid <= #SMs with one CTA per SM (all co-resident),
+// and contributors never wait on anything.
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 
 template <int BN, int KBU, int NACC, int UW>
@@ -645,7 +552,8 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
   uint64_t* a_empty = a_full + C::NA;
   uint64_t* acc_full = a_empty + C::NA;
   uint64_t* acc_empty = acc_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + NACC);
+  uint64_t* fin_bar = acc_empty + NACC;                     // fixup: partials landed in smem
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin_bar + 1);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n_kb = a.K / 64, n_ku = n_kb / KBU;
@@ -668,6 +576,7 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
     for (int i = 0; i < C::NX; ++i) { ws::mbar_init(&x_full[i], 1); ws::mbar_init(&x_empty[i], 1); }
     for (int i = 0; i < C::NA; ++i) { ws::mbar_init(&a_full[i], UW); ws::mbar_init(&a_empty[i], 1); }
     for (int i = 0; i < NACC; ++i) { ws::mbar_init(&acc_full[i], 1); ws::mbar_init(&acc_empty[i], 4); }
+    ws::mbar_init(fin_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&xmap) : "memory");
   }
@@ -863,6 +772,7 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     int seg = 0;
+    uint32_t fin_phase = 0;
     int64_t u = u0;
     const int64_t first_tile_mine = u0 / n_ku;
     while (u < u1) {
@@ -887,9 +797,75 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
         }
       }
       ws::tc_after();
-      const int slot = 2 * (int)blockIdx.x + (tile == first_tile_mine ? 0 : 1);
+      // fix = 1: a segment starting at the tile's first unit belongs to cf (finisher);
+      // a partial segment starting mid-tile is a contributor (writes ws slot blockIdx.x)
+      const bool finisher = fix && !full && u == tile * n_ku;
+      if (finisher) {
+        // all of this CTA's MMAs are done, so the raw-weight ring is idle: land the other
+        // contributors' partials there with bulk copies (2 per batch), add them to the
+        // TMEM accumulator in contributor order (k order), epilogue after the last batch
+        const int n_fin = ws::cta_of_unit((tile + 1) * n_ku - 1, U, G) - (int)blockIdx.x;
+        const uint32_t pbytes = (uint32_t)(ntile * BN * 128 * 4);
+        const uint64_t f0 = clk();
+        uint64_t f1 = 0, f2 = 0;
+        if (warp == C::E0 && lane == 0) {
+          if (!(dbg & 512))   // debug: no wait (wrong results; timing only)
+            while (ld_acquire(&a.counters[tile]) < n_fin) __nanosleep(32);
+          a.counters[tile] = 0;                                 // every contributor has arrived
+          asm volatile("fence.proxy.async.global;\n" ::: "memory");
+        }
+        __syncwarp();   // reconverge before the .aligned tcgen05 / bar.sync instructions
+        constexpr int NB = (C::NR * C::RAW) / (2 * BN * 128 * 4) < 2 ? 1 : 2;
+        for (int b0 = (dbg & 1024) ? n_fin : 1; b0 <= n_fin; b0 += NB) {   // debug 1024: one batch only
+          const int nb = min(NB, n_fin - b0 + 1);
+          const bool last = b0 + nb > n_fin;
+          if (warp == C::E0 && lane == 0) {
+            ws::mbar_expect_tx(fin_bar, pbytes * nb);
+            for (int k = 0; k < nb; ++k)
+              ws::bulk_g2s(raw + k * pbytes, a.ws + (int64_t)((int)blockIdx.x + b0 + k) * (2 * BN * 128), pbytes,
+                           fin_bar);
+          }
+          __syncwarp();
+          if (!f1) f1 = clk();
+          ws::mbar_wait(fin_bar, fin_phase);
+          fin_phase ^= 1;
+          if (!f2) f2 = clk();
+          const float* land = reinterpret_cast<const float*>(raw);
+          for (int tt = 0; tt < ntile; ++tt) {
+            const uint32_t t_row = tmem + ab * (2 * BN) + tt * BN + ((uint32_t)(quarter * 32) << 16);
+            const int n = (2 * pr + tt) * 128 + row;
+            for (int c0 = 0; c0 < BN; c0 += 16) {
+              float v[16];
+              if (dbg & 16384) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[j] = 0.f;
+              } else {
+                ws::tmem_ld16(t_row + c0, v);
+              }
+              if (!(dbg & 8192))
+                for (int k = 0; k < nb; ++k)
+#pragma unroll
+                  for (int j = 0; j < 16; ++j) v[j] += land[k * (pbytes / 4) + (tt * BN + c0 + j) * 128 + row];
+              if (last) {
+                if (!(dbg & 4096))
+#pragma unroll
+                  for (int j = 0; j < 16; ++j) epi_store(a.epi, m0 + c0 + j, n, v[j]);
+              } else {
+                uint32_t w[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) w[j] = __float_as_uint(v[j]);
+                tmem_st16(t_row + c0, w);
+                asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+              }
+            }
+          }
+          ws::named_bar(1, 128);   // the landing buffer is free for the next batch
+        }
+        if (ts && warp == C::E0 && lane == 0) { ts[3] = f1 - f0; ts[4] = f2 - f1; ts[5] = clk() - f2; ts[6] = n_fin; }
+      }
+      const int slot = fix ? (int)blockIdx.x : 2 * (int)blockIdx.x + (tile == first_tile_mine ? 0 : 1);
       float* part = a.ws + (int64_t)slot * (2 * BN * 128);
-      for (int tt = 0; tt < ntile; ++tt) {
+      for (int tt = 0; tt < ntile && !finisher; ++tt) {
         const uint32_t t_row = tmem + ab * (2 * BN) + tt * BN + ((uint32_t)(quarter * 32) << 16);
         const int n = (2 * pr + tt) * 128 + row;
         for (int c0 = 0; c0 < BN; c0 += 16) {
@@ -905,6 +881,12 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
         }
       }
       ws::tc_before();
+      if (fix && !full && !finisher) {   // contributor: release the partial
+        if (!(dbg & 2048)) __threadfence();   // debug: no fence
+        ws::named_bar(1, 128);
+        if (warp == C::E0 && lane == 0) atomicAdd(&a.counters[tile], 1);
+        __syncwarp();
+      }
       __syncwarp();
       if (lane == 0) ws::mbar_arrive(&acc_empty[ab]);
       u = seg_end;
@@ -922,15 +904,13 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
 #undef TWAIT
   __syncwarp();
   ws::tc_before();
-  if (fix) __threadfence();   // partials visible device-wide before the arrival counters move
   __syncthreads();
   if (tid == 0) gstamp(13);
   const uint64_t c13 = ts ? clk() : 0;
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512u));
-  if (fix && u1 > u0) tm_fixup<BN>(a, u0, u1, n_ku, n_pairs, n_rt, U, G, ts);
   if (tid == 0) gstamp(14);
-  if (tid == 0 && ts) { ts[0] = clk() - c13; ts[1] = c13 - ts[2]; }   // cycles: fixup, barrier - MMA end
+  if (tid == 0 && ts) { ts[0] = clk() - c13; ts[1] = c13 - ts[2]; }   // cycles: teardown, barrier - MMA end
 }
 
 // ---------------------------------------------------------------------------------
@@ -1006,14 +986,15 @@ static int run_tm(const LinearArgs& a, cudaStream_t st) {
   CUtensorMap map;
   if (!make_xmap(&map, a.x, a.M, a.K, BN)) return -1;
   static const int dbg = getenv("PIPO_WS_DEBUG") ? atoi(getenv("PIPO_WS_DEBUG")) : 0;
-  // stream-K fixup as a separate ws_reduce_kernel launch (default) or inside the GEMM
-  // (PIPO_TM_FIXUP=1: measured SLOWER on B200 — c5 QKV 48 vs 39 us; the partial reads
-  // right after the all-CTA partial-write burst run ~15k cycles per CTA, see DESIGN.md
-  // §6); the in-kernel fixup spins on other CTAs, so it needs every CTA co-resident:
-  // G <= #SMs, one CTA per SM.
+  // stream-K fixup as a separate ws_reduce_kernel launch (default, 0) or inside the GEMM
+  // by the tile's first CTA (PIPO_TM_FIXUP=1, the "finisher" scheme above).  Measured on
+  // B200 (profiles/r01/fixup/): the finisher is SLOWER (c5 QKV 52 vs 40 us, out-proj 41 vs
+  // 22 us) — clock64 stamps put ~30k cycles in the finisher's final-output stores at the
+  // kernel tail (partial spin ~3k, bulk copy ~1.2k), so the separate reduce stays default.
+  // The in-kernel fixup spins on other CTAs: it needs G <= #SMs, one CTA per SM.
   static const int fix_env = getenv("PIPO_TM_FIXUP") ? atoi(getenv("PIPO_TM_FIXUP")) : 0;
   const int64_t tiles = (int64_t)n_pairs * m_tiles;
-  const int fix = fix_env && G > 1 && G <= a.num_sms && 2 * tiles <= a.n_counters && !(dbg & 64) ? 1 : 0;
+  const int fix = fix_env && G > 1 && G <= a.num_sms && tiles <= a.n_counters && !(dbg & 64) ? 1 : 0;
   launch_pdl(gemm_tm_kernel<BN, KBU, NACC, UW>, dim3(G), dim3(C::THREADS), C::SMEM, st, map, a, n_rt, m_tiles, G, dbg,
              fix);
   if ((dbg & 64) || fix) return 1;   // debug: main kernel only / fixup done in-kernel
