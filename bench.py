@@ -63,6 +63,9 @@ def parse():
     ap.add_argument("--weight-tier", default=None, choices=["device", "host", "disk"],
                     help="override the config's weight tier (device = no streaming: isolates H2D interference)")
     ap.add_argument("--chunk-mb", type=float, default=0)
+    ap.add_argument("--shard-stream", action="store_true",
+                    help="NEXT-1: each rank streams 1/N of every layer over its host link and all-gathers the "
+                         "rest over NVLink (NCCL); compute stays batch-sharded (host weight tier only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--disk-dir", default="/tmp/pipo_disk")
@@ -279,6 +282,13 @@ def run_pipo(args):
                            flags=pipo.PIPO_F_TIMELINE | pipo.PIPO_F_KPROF)
     t_setup = time.perf_counter()
     pl = pipo.Pipeline(cfg)
+    if args.shard_stream:
+        uid = pipo.pipo_nccl_unique_id() if rank == 0 else bytes(128)
+        if world > 1:
+            t = torch.tensor(list(uid), dtype=torch.uint8, device="cpu" if shared_gpu else f"cuda:{local}")
+            dist.broadcast(t, 0)
+            uid = bytes(t.cpu().tolist())
+        pipo.pipo_shard_stream_init(pl.ctx, rank, world, uid)
     pl.load_synthetic(pipo.PIPO_LAYER_EMBED, synth.WEIGHT_SEED)
     for j in range(s.n_layers):
         pl.load_synthetic(j, synth.WEIGHT_SEED)
@@ -369,7 +379,7 @@ def run_pipo(args):
         tc = peaks.get("bf16_tflops_sustained") or 1400.0
         ach = per_unit_bytes / per_unit_s / 1e9
         roofline = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                    "frac": ach / hbm, "traffic": ncu_traffic(dom),
+                    "frac": ach / hbm, "traffic": ncu_traffic(dom, args),
                     "bytes_per_unit": per_unit_bytes, "us_per_unit": per_unit_s * 1e6,
                     "tflops": kd["flops"] / kd["units"] / per_unit_s / 1e12,
                     "tflops_frac_of_fp16_peak": kd["flops"] / kd["units"] / per_unit_s / 1e12 / tc,
@@ -386,7 +396,9 @@ def run_pipo(args):
             "data": "synthetic (seeded counter-based OPT weights + prompts, pipo_synth)",
             "config": {"workload": f"{args.config}: {c['desc']}", "global_batch": b * world, "seq_len": P,
                        "gen": G, "n_layers": s.n_layers, "d_model": s.d_model,
-                       "parallelism": f"batch-shard x{world} (no hot-path collective)",
+                       "parallelism": (f"batch-shard x{world} + sharded streaming (1/{world} of each layer over "
+                                       f"PCIe, NCCL all-gather over NVLink)") if args.shard_stream
+                       else f"batch-shard x{world} (no hot-path collective)",
                        "weight_tier": ["device", "host", "disk"][c["weight_tier"]],
                        "kv_tier": ["device", "host"][c["kv_tier"]], "kv_fmt": args.kv_fmt, "ring_layers": args.ring,
                        "l2": "inputs larger than L2 (every step streams all layer weights through HBM)"},
@@ -443,13 +455,17 @@ def run_pipo(args):
     return 0
 
 
-def ncu_traffic(cls):
+def ncu_traffic(cls, args):
     """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the
     class's kernel from the committed `ncu --set full` capture (profiles/ncu_traffic.json,
-    written by hand from tools/ncu_summary.py output), or None if not captured."""
+    written by hand from tools/ncu_summary.py output), or None if that capture was not
+    taken on this workload."""
     try:
         t = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")))
     except (OSError, ValueError):
+        return None
+    want = t.get("applies_to", {})
+    if (want.get("config"), want.get("wfmt"), want.get("kv_fmt")) != (args.config, args.wfmt, args.kv_fmt):
         return None
     e = t.get(cls)
     return None if e is None else e["traffic_bytes_per_unit"]

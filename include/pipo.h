@@ -295,6 +295,30 @@ pipo_status pipo_debug_capture(pipo_ctx* ctx, int32_t on, float* out);
  * `bytes`-sized copies on the weight-copy stream (App. A sweep). */
 pipo_status pipo_probe_h2d(pipo_ctx* ctx, int64_t bytes, int32_t reps, double* gbs);
 
+/* ---- NEXT-1: sharded weight streaming across the GPUs of one node ----------
+ * App. D: with data parallelism "every GPU loads the layer", so each
+ * GPU's host link carries the whole model every step.  Sharded streaming keeps the
+ * batch-sharded compute (results bit-identical to one GPU) but splits the transfer:
+ * rank r of `world` streams only bytes [r*S, (r+1)*S) of every layer blob (blob padded
+ * to world * 4 KiB; S = padded / world) over its own host link into its HBM ring slot,
+ * then an NCCL all-gather over NVLink on the copy stream fills in the other ranks'
+ * ranges before the layer's segments are marked ready.  Per-rank link bytes drop by
+ * `world`x; the pinned host store shrinks to l * S per rank.
+ * NCCL is loaded at run time (dlopen "libnccl.so.2"; PIPO_E_CUDA if unavailable). */
+
+/* Host-only: the rank's byte range of a blob of `layer_bytes` (after padding). */
+pipo_status pipo_shard_range(int64_t layer_bytes, int32_t world, int32_t rank, int64_t* offset, int64_t* bytes);
+
+/* ncclGetUniqueId: rank 0 creates the 128-byte id; the caller broadcasts it. */
+pipo_status pipo_nccl_unique_id(uint8_t id[128]);
+
+/* Switch a HOST-tier context to sharded streaming: call after pipeline_init and
+ * before any weights are loaded, on every rank (collective: blocks until all `world`
+ * ranks have joined the NCCL communicator).  world == 1 is allowed (a 1-rank
+ * all-gather).  Errors: INVALID_ARG (rank/world, weight tier not HOST), STATE (weights
+ * already loaded), OOM, CUDA (NCCL missing or failing). */
+pipo_status pipo_shard_stream_init(pipo_ctx* ctx, int32_t rank, int32_t world, const uint8_t id[128]);
+
 /* ---- automatic configuration (NEXT-3): memory model + Eq. (1) ---------------
  * Host-only pure functions (no context, no GPU).  The paper states them for
  * LLaMA3.1 (§3.5, App. B); readings Q23-Q27 in

@@ -35,6 +35,7 @@
 
 #include "ctx.h"
 #include "disk.h"
+#include "nccl_rt.h"
 
 using namespace pipo;
 
@@ -258,6 +259,19 @@ pipo_status enqueue_copy(pipo_ctx* ctx, int64_t G, int64_t kv_pos) {
       bytes += ctx->lay.seg_bytes[s];
       TRY(after_segment(s));
     }
+  } else if (ctx->nccl_comm) {
+    // NEXT-1 sharded streaming: this rank's 1/world of the blob over its own host link,
+    // then the other ranks' ranges over NVLink (in-place NCCL all-gather on the copy
+    // stream); every segment is ready once the gather has completed
+    const int64_t S = ctx->shard_bytes;
+    TRY(copy_chunks(ctx, dst + (int64_t)ctx->shard_rank * S, ctx->host_store + (int64_t)j * S, S));
+    bytes += S;
+    const int rc = nccl_allgather_bytes(dst + (int64_t)ctx->shard_rank * S, dst, (size_t)S, ctx->nccl_comm, ctx->s_copy);
+    if (rc != 0) {
+      ctx->poisoned = true;
+      return set_err(PIPO_E_CUDA, std::string("ncclAllGather failed: ") + nccl_error_string(rc));
+    }
+    for (int s = 0; s < 4; ++s) TRY(after_segment(s));
   } else {
     const uint8_t* src = ctx->host_store + (int64_t)j * ctx->layer_bytes;
     const int64_t total = ctx->lay.seg_off[3] + ctx->lay.seg_bytes[3];
@@ -344,8 +358,12 @@ pipo_status forward(pipo_ctx* ctx, int b, int n, int past, bool want_logits) {
     if (host_kv(ctx) && n == 1 && ctx->kv_load_past[slot] != past)
       return set_err(PIPO_E_STATE, "internal: KV prefetch range mismatch");
     cudaEvent_t t0;
-    // ---- MHA: LN1 + QKV + attention (seg 0) ----
-    if (streamed(ctx)) CK(cudaStreamWaitEvent(cs, ctx->ev_ready[slot][0], 0));
+    // SynchronizeLoadTask granularity: per segment (the paper's tasks, default for the
+    // memory-efficient ring R = 1) or per layer (R >= 2: one wait on the layer's last
+    // segment — same-stream events are ordered — so the compute stream wakes once per
+    // layer instead of before every linear; the copy stream is still R-1 layers ahead)
+    const bool seg_wait = ctx->layer_wait ? false : true;
+    if (streamed(ctx)) CK(cudaStreamWaitEvent(cs, ctx->ev_ready[slot][seg_wait ? 0 : 3], 0));
     if (host_kv(ctx)) CK(cudaStreamWaitEvent(cs, ctx->ev_ready[slot][4], 0));
     TRY(span_begin(ctx, cs, &t0));
     LAUNCH(launch_layernorm(ctx->h, d, M, d, vec_ptr(ctx, blob, V_LN1_G), vec_ptr(ctx, blob, V_LN1_B), ctx->xa, cs));
@@ -406,7 +424,7 @@ pipo_status forward(pipo_ctx* ctx, int b, int n, int past, bool want_logits) {
       TRY(span_end(ctx, ctx->s_save, s0, 2, saved));
     }
     // ---- MHA out-proj + residual (seg 1) ----
-    if (streamed(ctx)) CK(cudaStreamWaitEvent(cs, ctx->ev_ready[slot][1], 0));
+    if (streamed(ctx) && seg_wait) CK(cudaStreamWaitEvent(cs, ctx->ev_ready[slot][1], 0));
     TRY(span_begin(ctx, cs, &t0));
     la.x = ctx->xa; la.w = blob + ctx->lay.mat_off[M_OUT]; la.N = d; la.K = d;
     la.epi = EpiParams{};
@@ -414,7 +432,7 @@ pipo_status forward(pipo_ctx* ctx, int b, int n, int past, bool want_logits) {
     TRY(run_linear(ctx, la, PATH_AUTO, lin_cls));
     TRY(span_end(ctx, cs, t0, 1, 0));
     // ---- MLP: LN2 + FC1 + ReLU (seg 2) ----
-    if (streamed(ctx)) CK(cudaStreamWaitEvent(cs, ctx->ev_ready[slot][2], 0));
+    if (streamed(ctx) && seg_wait) CK(cudaStreamWaitEvent(cs, ctx->ev_ready[slot][2], 0));
     TRY(span_begin(ctx, cs, &t0));
     LAUNCH(launch_layernorm(ctx->h, d, M, d, vec_ptr(ctx, blob, V_LN2_G), vec_ptr(ctx, blob, V_LN2_B), ctx->xa, cs));
     la.x = ctx->xa; la.w = blob + ctx->lay.mat_off[M_FC1]; la.N = llama ? 2 * ctx->F : ctx->F; la.K = d;
@@ -425,7 +443,7 @@ pipo_status forward(pipo_ctx* ctx, int b, int n, int past, bool want_logits) {
     if (llama) LAUNCH(launch_swiglu(ctx->gu, M, ctx->F, ctx->u, cs));   // u = silu(gate) * up
     TRY(span_end(ctx, cs, t0, 1, 0));
     // ---- MLP: FC2 + residual (seg 3) ----
-    if (streamed(ctx)) CK(cudaStreamWaitEvent(cs, ctx->ev_ready[slot][3], 0));
+    if (streamed(ctx) && seg_wait) CK(cudaStreamWaitEvent(cs, ctx->ev_ready[slot][3], 0));
     TRY(span_begin(ctx, cs, &t0));
     la.x = ctx->u; la.w = blob + ctx->lay.mat_off[M_FC2]; la.N = d; la.K = ctx->F;
     la.epi = EpiParams{};
@@ -569,6 +587,10 @@ pipo_status pipeline_init(const pipo_config* cfg, pipo_ctx** out) {
   ctx->R = std::min({ctx->R, kMaxRing, ctx->l});
   if (host_kv(ctx) && ctx->R < 2 && ctx->l >= 2) ctx->R = 2;
   ctx->chunk = c.chunk_bytes;
+  {
+    const char* lw = getenv("PIPO_LAYER_WAIT");   // 1 = per-layer wait (R >= 2), 0 = per segment
+    ctx->layer_wait = (lw ? atoi(lw) : 0) && ctx->R >= 2;
+  }
   ctx->gemv_max_m = c.gemv_max_m > 0 ? std::min(c.gemv_max_m, 16) : 15;
   ctx->timeline = (c.flags & PIPO_F_TIMELINE) != 0;
   ctx->kprof = (c.flags & PIPO_F_KPROF) != 0;
@@ -703,6 +725,7 @@ void pipeline_destroy(pipo_ctx* ctx) {
   cudaDeviceSynchronize();
   cudaGetLastError();
   if (ctx->disk) disk_close(ctx);
+  if (ctx->nccl_comm) nccl_comm_destroy(ctx->nccl_comm);
   if (ctx->head == ctx->tok) ctx->head = nullptr;
   void* dev[] = {ctx->tok, ctx->head, ctx->gu, ctx->rope_inv, ctx->pos, ctx->lnf_g, ctx->lnf_b, ctx->dev_store, ctx->ring, ctx->kv_dev, ctx->kv_slot, ctx->kv_stage,
                  ctx->h, ctx->xa, ctx->q, ctx->u, ctx->logits, ctx->ids, ctx->next, ctx->ws, ctx->counters,
@@ -764,7 +787,7 @@ pipo_status load_layer_weights(pipo_ctx* ctx, int32_t layer, const void* w) {
   const pipo_layer_weights* lw = static_cast<const pipo_layer_weights*>(w);
   uint8_t* dst = nullptr;
   std::vector<uint8_t> tmp;
-  if (ctx->weight_tier == PIPO_TIER_HOST) {
+  if (ctx->weight_tier == PIPO_TIER_HOST && !ctx->nccl_comm) {
     dst = ctx->host_store + (int64_t)layer * ctx->layer_bytes;
   } else {
     tmp.resize((size_t)ctx->layer_bytes);
@@ -772,6 +795,9 @@ pipo_status load_layer_weights(pipo_ctx* ctx, int32_t layer, const void* w) {
   }
   if (!build_layer_blob(lw, ctx->lay, ctx->wfmt, dst))
     return set_err(PIPO_E_INVALID_ARG, "non-finite weight, NULL tensor or fp16-overflowing group scale");
+  if (ctx->nccl_comm)   // sharded streaming: keep only this rank's range (padding is zero)
+    std::memcpy(ctx->host_store + (int64_t)layer * ctx->shard_bytes, dst + (int64_t)ctx->shard_rank * ctx->shard_bytes,
+                (size_t)ctx->shard_bytes);
   if (ctx->weight_tier == PIPO_TIER_DEVICE)
     CK(cudaMemcpy(ctx->dev_store + (int64_t)layer * ctx->layer_bytes, dst, (size_t)ctx->layer_bytes,
                   cudaMemcpyHostToDevice));
@@ -874,7 +900,12 @@ pipo_status pipo_load_synthetic(pipo_ctx* ctx, int32_t layer, uint64_t seed) {
     }
   }
   if (s == PIPO_OK && !direct) {
-    if (ctx->weight_tier == PIPO_TIER_HOST) {
+    if (ctx->nccl_comm) {   // sharded streaming: this rank's range only
+      CK(cudaMemcpyAsync(ctx->host_store + (int64_t)layer * ctx->shard_bytes,
+                         blob + (int64_t)ctx->shard_rank * ctx->shard_bytes, (size_t)ctx->shard_bytes,
+                         cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    } else if (ctx->weight_tier == PIPO_TIER_HOST) {
       CK(cudaMemcpyAsync(ctx->host_store + (int64_t)layer * ctx->layer_bytes, blob, (size_t)ctx->layer_bytes,
                          cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
@@ -1481,6 +1512,54 @@ pipo_status pipo_rope(pipo_ctx* ctx, const uint16_t* q, const uint16_t* k, int32
   CK(cudaStreamSynchronize(st));
   cudaFree(dq); cudaFree(dk); cudaFree(df);
   ctx->hbm_bytes -= nq * 2 + nk * 2 + std::max(nq, nk) * 4;
+  return PIPO_OK;
+}
+
+pipo_status pipo_shard_range(int64_t layer_bytes, int32_t world, int32_t rank, int64_t* offset, int64_t* bytes) {
+  if (layer_bytes <= 0 || world <= 0 || rank < 0 || rank >= world || !offset || !bytes)
+    return set_err(PIPO_E_INVALID_ARG, "bad shard arguments");
+  const int64_t padded = round_up(layer_bytes, (int64_t)world * 4096);
+  *bytes = padded / world;
+  *offset = (int64_t)rank * *bytes;
+  return PIPO_OK;
+}
+
+pipo_status pipo_nccl_unique_id(uint8_t id[128]) {
+  if (!id) return set_err(PIPO_E_INVALID_ARG, "id is NULL");
+  const int rc = nccl_unique_id(id);
+  if (rc != 0) return set_err(PIPO_E_CUDA, std::string("ncclGetUniqueId: ") + nccl_error_string(rc));
+  return PIPO_OK;
+}
+
+pipo_status pipo_shard_stream_init(pipo_ctx* ctx, int32_t rank, int32_t world, const uint8_t id[128]) {
+  CHECK_CTX();
+  if (!id || world <= 0 || rank < 0 || rank >= world) return set_err(PIPO_E_INVALID_ARG, "bad rank/world");
+  if (ctx->weight_tier != PIPO_TIER_HOST) return set_err(PIPO_E_INVALID_ARG, "sharded streaming needs the HOST tier");
+  if (ctx->nccl_comm) return set_err(PIPO_E_STATE, "sharded streaming already initialised");
+  for (int j = 0; j < ctx->l; ++j)
+    if (ctx->layer_loaded[j]) return set_err(PIPO_E_STATE, "call pipo_shard_stream_init before loading weights");
+  CK(cudaSetDevice(ctx->cfg.device));
+  int64_t off = 0, S = 0;
+  TRY(pipo_shard_range(ctx->lay.total, world, rank, &off, &S));
+  // re-size the ring (padded slots) and the host store (this rank's ranges only)
+  CK(cudaDeviceSynchronize());
+  if (ctx->ring) { cudaFree(ctx->ring); ctx->hbm_bytes -= (int64_t)ctx->R * ctx->layer_bytes; ctx->ring = nullptr; }
+  if (ctx->host_store) {
+    cudaFreeHost(ctx->host_store);
+    ctx->pinned_bytes -= (int64_t)ctx->l * ctx->layer_bytes;
+    ctx->host_store = nullptr;
+  }
+  ctx->layer_bytes = S * world;
+  ctx->shard_bytes = S;
+  ctx->shard_rank = rank;
+  ctx->shard_world = world;
+  TRY(dev_alloc(ctx, &ctx->ring, (int64_t)ctx->R * ctx->layer_bytes));
+  CK(cudaMemset(ctx->ring, 0, (size_t)((int64_t)ctx->R * ctx->layer_bytes)));
+  TRY(host_alloc(ctx, &ctx->host_store, (int64_t)ctx->l * S));
+  void* comm = nullptr;
+  const int rc = nccl_comm_init(&comm, world, id, rank);
+  if (rc != 0) return set_err(PIPO_E_CUDA, std::string("ncclCommInitRank: ") + nccl_error_string(rc));
+  ctx->nccl_comm = comm;
   return PIPO_OK;
 }
 

@@ -41,6 +41,7 @@ struct pipo_ctx {
   float* rope_inv = nullptr;       // LLaMA: device [hd/2] inverse frequencies (llama3 rule)
   int weight_tier = 1, kv_tier = 0, R = 2, gemv_max_m = 15;
   int64_t chunk = 0;
+  bool layer_wait = false;         // compute waits once per layer (see forward())
   pipo::LayerLayout lay;
   int64_t layer_bytes = 0;
   int num_sms = 148;
@@ -62,6 +63,11 @@ struct pipo_ctx {
   uint8_t* host_store = nullptr;   // pinned, l * layer_bytes (HOST tier)
   uint8_t* dev_store = nullptr;    // HBM, l * layer_bytes (DEVICE tier)
   uint8_t* ring = nullptr;         // HBM, R * layer_bytes (HOST / DISK tiers)
+  // NEXT-1 sharded streaming: this rank streams bytes [shard_rank*shard_bytes, +shard_bytes)
+  // of every (padded) layer blob and all-gathers the rest from its peers (NCCL, copy stream)
+  int shard_rank = 0, shard_world = 1;
+  int64_t shard_bytes = 0;         // per-rank range; host_store holds l * shard_bytes
+  void* nccl_comm = nullptr;       // ncclComm_t
   pipo::DiskTier* disk = nullptr;
 
   // KV cache: position-major [pos][b][d] per (layer, K/V)

@@ -138,6 +138,9 @@ _sig("pipo_attention_prefill", C.c_int, _P, _u16, _u16, _u16, C.c_int32, C.c_int
 _sig("pipo_attention_gqa", C.c_int, _P, _u16, _u16, _u16, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
      C.c_int32, _f)
 _sig("pipo_rope", C.c_int, _P, _u16, _u16, C.c_int32, C.c_int32, C.c_int32, _f, _f)
+_sig("pipo_shard_range", C.c_int, C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64))
+_sig("pipo_nccl_unique_id", C.c_int, _u8)
+_sig("pipo_shard_stream_init", C.c_int, _P, C.c_int32, C.c_int32, _u8)
 _sig("pipo_debug_capture", C.c_int, _P, C.c_int32, _f)
 _sig("pipo_probe_h2d", C.c_int, _P, C.c_int64, C.c_int32, C.POINTER(C.c_double))
 _sig("pipo_ffn_hidden_dim", C.c_int64, C.c_int64, C.c_int64, C.c_double)
@@ -152,7 +155,8 @@ EXPORTED = ["pipo_last_error", "pipo_abi_version", "pipeline_init", "pipeline_de
             "pipo_load_synthetic", "prefill", "decode_step", "decode_step_dev", "pipeline_stats",
             "pipeline_stats_reset", "pipo_stream", "pipo_kernel_stats", "pipo_quantize_int4_g64", "pipo_quantize_int4_g64_gpu",
             "pipo_unpack_int4_g64", "pipo_linear", "pipo_bench_linear", "pipo_probe_bulk", "pipo_bench_attention", "pipo_attention_decode", "pipo_attention_prefill", "pipo_debug_capture", "pipo_probe_h2d",
-            "pipo_attention_gqa", "pipo_rope", "pipo_ffn_hidden_dim", "pipo_memory_model", "pipo_choose_block_size", "pipo_choose_plan"]
+            "pipo_attention_gqa", "pipo_rope", "pipo_shard_range", "pipo_nccl_unique_id", "pipo_shard_stream_init",
+            "pipo_ffn_hidden_dim", "pipo_memory_model", "pipo_choose_block_size", "pipo_choose_plan"]
 
 
 class PipoError(RuntimeError):
@@ -359,6 +363,25 @@ def pipo_rope(ctx, q, k, past):
     _check(_lib.pipo_rope(ctx, _ptr(q, C.c_uint16), _ptr(k, C.c_uint16), b, n, past, _ptr(qo, C.c_float),
                           _ptr(ko, C.c_float)))
     return qo, ko
+
+
+def pipo_shard_range(layer_bytes: int, world: int, rank: int):
+    """(offset, bytes) of rank's range of a padded layer blob (host-only, NEXT-1)."""
+    off, n = C.c_int64(), C.c_int64()
+    _check(_lib.pipo_shard_range(layer_bytes, world, rank, C.byref(off), C.byref(n)))
+    return off.value, n.value
+
+
+def pipo_nccl_unique_id() -> bytes:
+    buf = np.zeros(128, dtype=np.uint8)
+    _check(_lib.pipo_nccl_unique_id(_ptr(buf, C.c_uint8)))
+    return buf.tobytes()
+
+
+def pipo_shard_stream_init(ctx, rank: int, world: int, uid: bytes):
+    buf = np.frombuffer(uid, dtype=np.uint8).copy()
+    assert buf.size == 128
+    _check(_lib.pipo_shard_stream_init(ctx, rank, world, _ptr(buf, C.c_uint8)))
 
 
 def pipo_debug_capture(ctx, out: np.ndarray | None):

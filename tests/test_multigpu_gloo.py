@@ -60,3 +60,52 @@ def test_gloo_world2_max_and_shards():
         assert mx == 1.5
         assert np.array_equal(allp, full)
     assert aggregate_throughput(64, 2, 10, 2.0) == 640.0
+
+
+# ---- NEXT-1 sharded weight streaming: host logic under a real 2-process collective ----
+def test_shard_range_tiles_padded_blob():
+    from paper_2504_03664_b200 import pipo
+    for lb in (1, 4095, 4096, 3_780_096, 327_757_824, 115_900_416):
+        for world in (1, 2, 3, 4, 8):
+            spans = [pipo.pipo_shard_range(lb, world, r) for r in range(world)]
+            S = spans[0][1]
+            assert all(n == S for _, n in spans) and S % 4096 == 0
+            assert [o for o, _ in spans] == [r * S for r in range(world)]
+            assert lb <= S * world < lb + world * 4096          # padding < one 4 KiB page per rank
+    with pytest.raises(pipo.PipoError):
+        pipo.pipo_shard_range(100, 2, 2)
+
+
+def _shard_worker(rank, world, port, q):
+    """Emulates the copy stream of a sharded rank on CPU: stream own range, then the
+    in-place all-gather (gloo standing in for NCCL over NVLink) must rebuild the blob."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import torch
+    from paper_2504_03664_b200 import pipo
+    lb = 3_780_096 + 123                                   # a c1 blob, not 4 KiB aligned
+    off, S = pipo.pipo_shard_range(lb, world, rank)
+    blob = np.zeros(S * world, dtype=np.uint8)
+    blob[:lb] = np.random.default_rng(7).integers(0, 256, lb, dtype=np.uint8)   # same host store on every rank
+    slot = torch.zeros(S * world, dtype=torch.uint8)
+    slot[off:off + S] = torch.from_numpy(blob[off:off + S])                      # this rank's H2D range
+    parts = [torch.zeros(S, dtype=torch.uint8) for _ in range(world)]
+    dist.all_gather(parts, slot[off:off + S].clone())
+    full = torch.cat(parts).numpy()
+    q.put((rank, bool(np.array_equal(full, blob)), int(S)))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_sharded_stream_rebuilds_blob():
+    world = 2
+    port = 30500 + os.getpid() % 1000
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_shard_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok, _ in res)
