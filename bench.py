@@ -68,6 +68,7 @@ def parse():
                          "rest over NVLink (NCCL); compute stays batch-sharded (host weight tier only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cupti", action="store_true", help="skip the torch.profiler kernel-duration pass")
     ap.add_argument("--disk-dir", default="/tmp/pipo_disk")
     ap.add_argument("--profile", action="store_true",
                     help="cudaProfilerStart/Stop around the timed region (ncu --profile-from-start off)")
@@ -267,7 +268,7 @@ def run_pipo(args):
     torch.cuda.set_device(local)
     c = CONFIGS[args.config]
     s, b, P, G = c["shape"], c["b"], c["P"], c["G"]
-    steps_needed = args.warmup + args.steps * (1 if args.no_e2e else 2)
+    steps_needed = args.warmup + args.steps * (1 if args.no_e2e else 2) + (0 if args.no_cupti else 2)
     max_seq = P + max(G, steps_needed + 1)
     if args.weight_tier:
         c = {**c, "weight_tier": ["device", "host", "disk"].index(args.weight_tier)}
@@ -358,6 +359,12 @@ def run_pipo(args):
                "h2d_bytes_per_step": int(per_step_h2d), "d2h_bytes_per_step": int(b * 4),
                "note": "decode_step(host tokens) -> host next ids; h2d counts the streamed weights too"}
 
+    # CUPTI (torch.profiler) view of 2 extra untimed steps: true per-kernel GPU durations
+    # with the copy stream running (context for the event-bracketed roofline above)
+    cupti = None
+    if not args.no_cupti and rank == 0:
+        cupti = cupti_kernel_times(pl, tok_dev, 2, args.steps, kst)
+
     value = aggregate_throughput(b, world, args.steps, t_dev)
     ms = t_dev / args.steps * 1e3
     peaks = measured_peaks()
@@ -407,6 +414,7 @@ def run_pipo(args):
             "gpu_launches": int(st["kernel_launches"]),
             "roofline": roofline,
             "kernels": kernels,
+            "roofline_cupti": cupti,
             "link_roofline": {"bound": "host-link", "bytes_per_step": int(layer_bytes),
                               "probe_gbs": link_probe, "achieved_gbs": layer_bytes / (ms / 1e3) / 1e9,
                               "frac": link_floor_s / (ms / 1e3), "copy_engine_gbs": st["h2d_gbs"]},
@@ -453,6 +461,43 @@ def run_pipo(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+_CLASS_KERNELS = {"linear_decode": ("gemm_tm_kernel", "gemm_ws_kernel", "gemv_int4_kernel", "ws_reduce_kernel",
+                                     "gemm_tc_kernel"),
+                  "attn_decode": ("attn_decode", "attn_merge")}
+
+
+def cupti_kernel_times(pl, tok_dev, steps, timed_steps, kst):
+    """Kernel-only GPU time per unit of each class from a CUPTI trace of `steps` extra
+    decode steps (all of a class's kernels summed, e.g. the GEMM and its stream-K reduce;
+    a PDL-launched reduce's span includes its wait, so this is an upper bound).  Units and
+    algorithmic bytes per unit come from the event-timed region (`timed_steps` steps)."""
+    import torch
+    from paper_2504_03664_b200 import pipo
+    try:
+        with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
+            for _ in range(steps):
+                pipo.decode_step_dev(pl.ctx, tok_dev.data_ptr(), tok_dev.data_ptr())
+            torch.cuda.synchronize()
+    except Exception as e:  # noqa: BLE001  (profiler unavailable: report, do not fail the bench)
+        return {"error": str(e)[:200]}
+    tot = {c: 0.0 for c in _CLASS_KERNELS}
+    for e in prof.events():
+        if e.device_type != torch.autograd.DeviceType.CUDA:
+            continue
+        for c, names in _CLASS_KERNELS.items():
+            if any(n in e.name for n in names):
+                tot[c] += (e.time_range.end - e.time_range.start) * 1e-6
+    out = {"source": f"torch.profiler CUDA activity (CUPTI), {steps} untimed steps after the timed region"}
+    for c, t in tot.items():
+        k = kst.get(c)
+        if not k or not k["units"] or t <= 0:
+            continue
+        units_per_step = k["units"] / timed_steps
+        us = t / steps / units_per_step * 1e6
+        out[c] = {"us_per_unit": us, "gbs": k["bytes"] / k["units"] / (us * 1e-6) / 1e9}
+    return out
 
 
 def ncu_traffic(cls, args):

@@ -622,7 +622,15 @@ pipo_status pipeline_init(const pipo_config* cfg, pipo_ctx** out) {
   CKI(cudaGetDeviceProperties(&prop, c.device));
   if (prop.major < 10) return fail(set_err(PIPO_E_CUDA, "device is not sm_100-class (built for sm_100a only)"));
   ctx->num_sms = prop.multiProcessorCount;
-  CKI(cudaStreamCreateWithFlags(&ctx->s_comp, cudaStreamNonBlocking));
+  {
+    // compute stream at the highest priority (PIPO_COMP_PRIO=0 disables): the copy
+    // stream runs multi-ms DMA commands, the compute stream short kernels and events
+    int lo = 0, hi = 0;
+    CKI(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    const char* pe = getenv("PIPO_COMP_PRIO");
+    const bool prio = pe ? atoi(pe) != 0 : true;
+    CKI(cudaStreamCreateWithPriority(&ctx->s_comp, cudaStreamNonBlocking, prio ? hi : lo));
+  }
   CKI(cudaStreamCreateWithFlags(&ctx->s_copy, cudaStreamNonBlocking));
   CKI(cudaStreamCreateWithFlags(&ctx->s_save, cudaStreamNonBlocking));
   for (int i = 0; i < kMaxRing; ++i) {

@@ -49,32 +49,51 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 __global__ void __launch_bounds__(LN_THREADS) layernorm_kernel(const float* h, int64_t row_stride, int d,
                                                                  const __half* g, const __half* beta,
                                                                  __half* x) {
+  // 16-B loads: float4 of h and 4 halves of gamma / beta per item, all issued before the
+  // first reduction (one memory round trip); RMSNorm when beta == nullptr (mean = 0)
+  constexpr int NV = LN_MAX_PER_THREAD / 4;   // float4 items per thread (d <= 8192)
   __shared__ float red[LN_THREADS / 32];
-  const float* row = h + blockIdx.x * row_stride;
-  float v[LN_MAX_PER_THREAD];
+  const float4* row = reinterpret_cast<const float4*>(h + blockIdx.x * row_stride);
+  const int d4 = d >> 2;
+  float4 v[NV];
+  uint2 gv[NV], bv[NV];
   float s = 0.f;
 #pragma unroll
-  for (int i = 0; i < LN_MAX_PER_THREAD; ++i) {
+  for (int i = 0; i < NV; ++i) {
     const int k = threadIdx.x + i * LN_THREADS;
-    v[i] = k < d ? row[k] : 0.f;
-    s += v[i];
+    const bool in = k < d4;
+    v[i] = in ? row[k] : make_float4(0.f, 0.f, 0.f, 0.f);
+    gv[i] = in ? reinterpret_cast<const uint2*>(g)[k] : make_uint2(0, 0);
+    bv[i] = in && beta ? reinterpret_cast<const uint2*>(beta)[k] : make_uint2(0, 0);
+    s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
   }
-  // RMSNorm (LLaMA, beta == nullptr): x / sqrt(mean(x^2) + eps) * g, i.e. mean taken as 0
   const float mean = beta ? block_sum(s, red) / d : 0.f;
   float q = 0.f;
 #pragma unroll
-  for (int i = 0; i < LN_MAX_PER_THREAD; ++i) {
-    const int k = threadIdx.x + i * LN_THREADS;
-    const float c = k < d ? v[i] - mean : 0.f;
-    q = fmaf(c, c, q);
+  for (int i = 0; i < NV; ++i) {
+    if (threadIdx.x + i * LN_THREADS < d4) {
+      const float a = v[i].x - mean, b = v[i].y - mean, c = v[i].z - mean, e = v[i].w - mean;
+      q = fmaf(a, a, q); q = fmaf(b, b, q); q = fmaf(c, c, q); q = fmaf(e, e, q);
+    }
   }
   const float var = block_sum(q, red) / d;
   const float rstd = rsqrtf(var + 1e-5f);
-  __half* out = x + (int64_t)blockIdx.x * d;
+  uint2* out = reinterpret_cast<uint2*>(x + (int64_t)blockIdx.x * d);
 #pragma unroll
-  for (int i = 0; i < LN_MAX_PER_THREAD; ++i) {
+  for (int i = 0; i < NV; ++i) {
     const int k = threadIdx.x + i * LN_THREADS;
-    if (k < d) out[k] = __float2half_rn((v[i] - mean) * rstd * __half2float(g[k]) + (beta ? __half2float(beta[k]) : 0.f));
+    if (k < d4) {
+      const float2 g01 = __half22float2(*reinterpret_cast<const __half2*>(&gv[i].x));
+      const float2 g23 = __half22float2(*reinterpret_cast<const __half2*>(&gv[i].y));
+      const float2 b01 = __half22float2(*reinterpret_cast<const __half2*>(&bv[i].x));
+      const float2 b23 = __half22float2(*reinterpret_cast<const __half2*>(&bv[i].y));
+      const __half2 o01 = __floats2half2_rn((v[i].x - mean) * rstd * g01.x + b01.x, (v[i].y - mean) * rstd * g01.y + b01.y);
+      const __half2 o23 = __floats2half2_rn((v[i].z - mean) * rstd * g23.x + b23.x, (v[i].w - mean) * rstd * g23.y + b23.y);
+      uint2 o;
+      o.x = *reinterpret_cast<const uint32_t*>(&o01);
+      o.y = *reinterpret_cast<const uint32_t*>(&o23);
+      out[k] = o;
+    }
   }
 }
 
