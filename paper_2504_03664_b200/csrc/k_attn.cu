@@ -15,6 +15,7 @@
 #include <float.h>
 
 #include "common.cuh"
+#include "launch.cuh"
 #include "kernels.h"
 #include "layout.h"
 
@@ -53,6 +54,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnArgs a, int n_spli
   constexpr int E = HD / 32;
   __shared__ float sm_m[G][4], sm_l[G][4];
   __shared__ float sm_acc[G][4][HD];
+  pdl_wait();   // multi-wave: no early trigger (dependents would take SM slots)
   const int bi = blockIdx.y, split = blockIdx.z;
   const int head0 = G == 1 ? blockIdx.x : blockIdx.x * G;            // first query head
   const int kvh = G == 1 ? blockIdx.x / a.group : blockIdx.x;
@@ -266,6 +268,7 @@ __global__ void __launch_bounds__(128) attn_decode_v2_kernel(AttnArgs a, int n_s
 
 template <int HD>
 __global__ void attn_merge_kernel(AttnArgs a, int n_splits) {
+  pdl_wait();
   const int head = blockIdx.x, bi = blockIdx.y, t = threadIdx.x;
   const float* base = a.ws + (int64_t)(bi * a.n_heads + head) * n_splits * (HD + 2);
   float M = -INFINITY;
@@ -730,7 +733,7 @@ int launch_attention_decode(const AttnArgs& a, cudaStream_t st) {
   if (n_splits > 1 && (int64_t)a.b * a.n_heads * n_splits * (hd + 2) > a.ws_floats) return -1;
   dim3 grid(a.n_heads / G, a.b, n_splits);
   if (!a.use_cuda_cores) {   // one K/V row per warp: measured 0-5% ahead of v2 at c3-c5
-#define PIPO_DECODE(HDV, GV) attn_decode_kernel<HDV, GV><<<grid, 128, 0, st>>>(a, n_splits, per)
+#define PIPO_DECODE(HDV, GV) launch_pdl_k(attn_decode_kernel<HDV, GV>, grid, dim3(128), 0, st, a, n_splits, per)
     if (hd == 64) {
       if (G == 1) PIPO_DECODE(64, 1); else if (G == 2) PIPO_DECODE(64, 2); else if (G == 4) PIPO_DECODE(64, 4);
       else PIPO_DECODE(64, 8);
@@ -745,8 +748,8 @@ int launch_attention_decode(const AttnArgs& a, cudaStream_t st) {
   }
   if (n_splits == 1) return 1;
   dim3 g2(a.n_heads, a.b);
-  if (hd == 64) attn_merge_kernel<64><<<g2, 64, 0, st>>>(a, n_splits);
-  else attn_merge_kernel<128><<<g2, 128, 0, st>>>(a, n_splits);
+  if (hd == 64) launch_pdl_k(attn_merge_kernel<64>, g2, dim3(64), 0, st, a, n_splits);
+  else launch_pdl_k(attn_merge_kernel<128>, g2, dim3(128), 0, st, a, n_splits);
   return 2;
 }
 

@@ -4,6 +4,7 @@
 #include <float.h>
 
 #include "common.cuh"
+#include "launch.cuh"
 #include "kernels.h"
 #include "layout.h"
 
@@ -13,6 +14,8 @@ namespace pipo {
 // tok is the fp16 tiled LM-head matrix (layout.h), pos row-major fp16.
 __global__ void embed_kernel(const int32_t* ids, int n, int past, const __half* tok, int64_t n_kb,
                              const __half* pos, int d, float* h) {
+  pdl_wait();
+  pdl_trigger();
   const int m = blockIdx.x;
   const int t = m % n;
   const int64_t id = ids[m];
@@ -25,7 +28,8 @@ __global__ void embed_kernel(const int32_t* ids, int n, int past, const __half* 
 
 int launch_embed(const int32_t* ids, int b, int n, int past, const __half* tok_tiled, int64_t tok_n_kb,
                  const __half* pos, int d, float* h, cudaStream_t st) {
-  embed_kernel<<<b * n, 256, 0, st>>>(ids, n, past, tok_tiled, tok_n_kb, pos, d, h);
+  if (b * n <= 4096) launch_pdl_k(embed_kernel, dim3(b * n), dim3(256), 0, st, ids, n, past, tok_tiled, tok_n_kb, pos, d, h);
+  else embed_kernel<<<b * n, 256, 0, st>>>(ids, n, past, tok_tiled, tok_n_kb, pos, d, h);
   return 1;
 }
 
@@ -53,6 +57,8 @@ __global__ void __launch_bounds__(LN_THREADS) layernorm_kernel(const float* h, i
   // first reduction (one memory round trip); RMSNorm when beta == nullptr (mean = 0)
   constexpr int NV = LN_MAX_PER_THREAD / 4;   // float4 items per thread (d <= 8192)
   __shared__ float red[LN_THREADS / 32];
+  pdl_wait();
+  if (gridDim.x <= 1024) pdl_trigger();       // decode: one wave
   const float4* row = reinterpret_cast<const float4*>(h + blockIdx.x * row_stride);
   const int d4 = d >> 2;
   float4 v[NV];
@@ -100,7 +106,7 @@ __global__ void __launch_bounds__(LN_THREADS) layernorm_kernel(const float* h, i
 int launch_layernorm(const float* h, int64_t row_stride, int rows, int d, const __half* g,
                      const __half* beta, __half* x, cudaStream_t st) {
   if (d > LN_THREADS * LN_MAX_PER_THREAD) return -1;
-  layernorm_kernel<<<rows, LN_THREADS, 0, st>>>(h, row_stride, d, g, beta, x);
+  launch_pdl_k(layernorm_kernel, dim3(rows), dim3(LN_THREADS), 0, st, h, row_stride, d, g, beta, x);
   return 1;
 }
 
@@ -109,6 +115,7 @@ int launch_layernorm(const float* h, int64_t row_stride, int rows, int d, const 
 // q heads first, then the KV heads of the new K rows in the cache.
 __global__ void rope_kernel(__half* q, __half* kc, const float* inv_freq, int n, int past, int n_heads,
                             int n_kv_heads, int hd, int kv_b, int64_t total) {
+  pdl_wait();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= total) return;
   const int half = hd >> 1;
@@ -131,13 +138,14 @@ int launch_rope(__half* q, __half* kc, const float* inv_freq, int b, int n, int 
                 int hd, int kv_b, cudaStream_t st) {
   const int64_t total = (int64_t)b * n * (n_heads + n_kv_heads) * (hd / 2);
   if (total == 0) return 0;
-  rope_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(q, kc, inv_freq, n, past, n_heads, n_kv_heads, hd,
-                                                                kv_b, total);
+  launch_pdl_k(rope_kernel, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, st, q, kc, inv_freq, n, past, n_heads,
+               n_kv_heads, hd, kv_b, total);
   return 1;
 }
 
 // SwiGLU (NEXT-4): 8 features per thread (16-B loads of gate and up, 16-B store).
 __global__ void swiglu_kernel(const __half* gu, int F, int64_t total8, __half* u) {
+  pdl_wait();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= total8) return;
   const int f8 = F / 8;
@@ -163,7 +171,7 @@ __global__ void swiglu_kernel(const __half* gu, int F, int64_t total8, __half* u
 int launch_swiglu(const __half* gu, int M, int F, __half* u, cudaStream_t st) {
   const int64_t total8 = (int64_t)M * F / 8;
   if (total8 == 0) return 0;
-  swiglu_kernel<<<(unsigned)((total8 + 255) / 256), 256, 0, st>>>(gu, F, total8, u);
+  launch_pdl_k(swiglu_kernel, dim3((unsigned)((total8 + 255) / 256)), dim3(256), 0, st, gu, F, total8, u);
   return 1;
 }
 
@@ -172,6 +180,8 @@ int launch_swiglu(const __half* gu, int M, int F, __half* u, cudaStream_t st) {
 __global__ void __launch_bounds__(1024) argmax_kernel(const float* logits, int V, int ldl, int32_t* out) {
   __shared__ float sv[32];
   __shared__ int si[32];
+  pdl_wait();
+  pdl_trigger();
   const float* row = logits + (int64_t)blockIdx.x * ldl;
   float best = -INFINITY;
   int bi = 0x7fffffff;
@@ -196,7 +206,7 @@ __global__ void __launch_bounds__(1024) argmax_kernel(const float* logits, int V
 }
 
 int launch_argmax(const float* logits, int rows, int V, int ldl, int32_t* out, cudaStream_t st) {
-  argmax_kernel<<<rows, 1024, 0, st>>>(logits, V, ldl, out);
+  launch_pdl_k(argmax_kernel, dim3(rows), dim3(1024), 0, st, logits, V, ldl, out);
   return 1;
 }
 
