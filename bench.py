@@ -69,6 +69,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cupti", action="store_true", help="skip the torch.profiler kernel-duration pass")
+    ap.add_argument("--no-timeline", action="store_true",
+                    help="no per-phase span events (busy fractions unavailable); A/B of the event overhead")
     ap.add_argument("--disk-dir", default="/tmp/pipo_disk")
     ap.add_argument("--profile", action="store_true",
                     help="cudaProfilerStart/Stop around the timed region (ncu --profile-from-start off)")
@@ -280,7 +282,7 @@ def run_pipo(args):
                            weight_tier=c["weight_tier"], kv_tier=c["kv_tier"], ring_layers=args.ring,
                            kv_fmt=pipo.PIPO_W_INT4_G64 if args.kv_fmt == "int4" else pipo.PIPO_W_FP16,
                            chunk_bytes=int(args.chunk_mb * (1 << 20)), disk_dir=disk_dir,
-                           flags=pipo.PIPO_F_TIMELINE | pipo.PIPO_F_KPROF)
+                           flags=(0 if args.no_timeline else pipo.PIPO_F_TIMELINE) | pipo.PIPO_F_KPROF)
     t_setup = time.perf_counter()
     pl = pipo.Pipeline(cfg)
     if args.shard_stream:

@@ -447,6 +447,50 @@ __global__ void __launch_bounds__(256) ws_reduce_kernel(LinearArgs a, int n_rt, 
   }
 }
 
+// Stream-K reduce v2: one 128-thread block per (tile, 8-column group, weight tile) — only
+// the tiles that exist (no early-exit blocks for CTA boundaries, no shared-memory
+// broadcast), one resident wave.  Same operands and order as ws_reduce_kernel
+// (0 + p_cf + p_cf+1 + ... in CTA order), so the two are bit-identical.
+template <int BN>
+__global__ void __launch_bounds__(128) ws_reduce2_kernel(LinearArgs a, int n_rt, int m_tiles, int G, int kbu) {
+  ws::griddep_wait();
+  ws::griddep_launch();
+  const int n_ku = a.K / 64 / kbu, n_pairs = (n_rt + 1) >> 1;
+  const int64_t U = (int64_t)n_pairs * m_tiles * n_ku;
+  const int64_t tile = blockIdx.x;
+  const int t = blockIdx.z;
+  const int pr = (int)(tile % n_pairs), mt = (int)(tile / n_pairs);
+  if (2 * pr + t >= n_rt) return;
+  const int cf = ws::cta_of_unit(tile * n_ku, U, G), cl = ws::cta_of_unit((tile + 1) * n_ku - 1, U, G);
+  if (cf == cl) return;                                   // owned whole: stored by the GEMM
+  const bool cf_first = ws::u_begin(cf, U, G) / n_ku == tile;
+  const int row = threadIdx.x, c0 = blockIdx.y * 8;
+  const int n = (2 * pr + t) * 128 + row, m0 = mt * BN;
+  float acc[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+  for (int cb = cf; cb <= cl; cb += 4) {
+    float v[4][8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int cc = cb + q;
+      if (cc <= cl) {
+        const int sl = 2 * cc + ((cc == cf && !cf_first) ? 1 : 0);
+        const float* src = a.ws + (int64_t)sl * (2 * BN * 128) + (t * BN + c0) * 128 + row;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[q][j] = __ldcg(src + j * 128);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (cb + q <= cl)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += v[q][j];
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) epi_store(a.epi, m0 + c0 + j, n, acc[j]);
+}
+
 // ---------------------------------------------------------------------------------
 // v5: A operand in TMEM.  The unpack warps write each dequantized 128 x 64 tile row
 // straight into tensor memory with tcgen05.st (one 32x32b.x32 store per row: the row's
@@ -999,8 +1043,14 @@ static int run_tm(const LinearArgs& a, cudaStream_t st) {
              fix);
   if ((dbg & 64) || fix) return 1;   // debug: main kernel only / fixup done in-kernel
   if (G > 1) {
-    dim3 rg((unsigned)(G - 1), BN / 8);
-    launch_pdl(ws_reduce_kernel<BN>, rg, dim3(256), 0, st, a, n_rt, m_tiles, G, KBU, dbg);
+    static const int red_v = getenv("PIPO_REDUCE") ? atoi(getenv("PIPO_REDUCE")) : 2;   // 1 = the v1 reduce
+    if (red_v == 1 || (dbg & 128)) {
+      dim3 rg((unsigned)(G - 1), BN / 8);
+      launch_pdl(ws_reduce_kernel<BN>, rg, dim3(256), 0, st, a, n_rt, m_tiles, G, KBU, dbg);
+    } else {
+      dim3 rg((unsigned)tiles, BN / 8, 2);
+      launch_pdl(ws_reduce2_kernel<BN>, rg, dim3(128), 0, st, a, n_rt, m_tiles, G, KBU);
+    }
   }
   return G > 1 ? 2 : 1;
 }

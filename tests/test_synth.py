@@ -36,3 +36,22 @@ def test_prompts_range():
     assert p.shape == (16, 256) and p.dtype == np.int32
     assert p.min() >= 4 and p.max() < 50272
     assert np.array_equal(p, synth.prompts(16, 256, 50272))
+
+
+def test_llama_shapes_and_streams():
+    """LLaMA3.1 tensor set (NEXT-4): shapes from the public 8B config, and the streams
+    that share a role with OPT use the same tensor ids (so e.g. w_qkv rows of an 8B
+    layer are the same counter stream as any other matrix in that slot)."""
+    s = synth.LLAMA31_8B
+    assert (s.head_dim, s.d_kv) == (128, 1024)
+    spec = synth.llama_layer_tensor_specs(s)
+    assert spec["w_qkv"][3] == (4096 + 2 * 1024, 4096)
+    assert spec["w_fc1"][3] == (2 * 14336, 4096) and spec["w_fc2"][3] == (4096, 14336)
+    assert set(spec) == {"ln1_g", "w_qkv", "w_out", "ln2_g", "w_fc1", "w_fc2"}     # no biases
+    emb = synth.llama_embed_tensor_specs(s)
+    assert emb["lm_head"][0] == synth.T_LM_HEAD and emb["lm_head"][3] == (128256, 4096)
+    tiny = synth.LlamaShape(64, 1, 4, 2, 128, vocab=256, max_pos=64)
+    m = synth.llama_layer_masters(tiny, 0)
+    ref = synth.draw(synth.WEIGHT_SEED, 1, synth.T_W_QKV, synth.KIND_NORMAL, 0.02, 0, 128 * 64).reshape(128, 64)
+    assert np.array_equal(m["w_qkv"], ref)
+    assert np.all(np.abs(m["ln1_g"] - 1.0) <= 0.1 + 1e-3)

@@ -14,7 +14,8 @@ if os.environ.get("KBENCH_PATHS"):
     paths = {k: v for k, v in paths.items() if k in os.environ["KBENCH_PATHS"].split(",")}
 cases = [("c5_qkv", 64, 21504, 7168), ("c5_out", 64, 7168, 7168), ("c5_fc1", 64, 28672, 7168),
          ("c5_fc2", 64, 7168, 28672), ("c2_qkv", 16, 6144, 2048), ("c2_fc2", 16, 2048, 8192),
-         ("c3_qkv", 32, 12288, 4096), ("pre_c2_qkv", 4096, 6144, 2048)]
+         ("c3_qkv", 32, 12288, 4096), ("pre_c2_qkv", 4096, 6144, 2048), ("c5_head", 64, 50272, 7168),
+         ("c6_head", 64, 128256, 4096)]
 if len(sys.argv) > 1:
     cases = [c for c in cases if c[0] in sys.argv[1:]]
 out = {}
@@ -23,8 +24,10 @@ for name, M, N, K in cases:
     res = {}
     for pn, p in paths.items():
         try:
-            us = pipo.pipo_bench_linear(pl.ctx, 1, p, M, N, K, 10)
-            res[pn] = {"us": round(us, 2), "GBs": round(wbytes / us / 1e3, 1),
+            wf = int(os.environ.get("KBENCH_WFMT", "1"))
+            wb = wbytes if wf == 1 else N * K * 2
+            us = pipo.pipo_bench_linear(pl.ctx, wf, p, M, N, K, 10)
+            res[pn] = {"us": round(us, 2), "GBs": round(wb / us / 1e3, 1),
                        "TFLOPs": round(2 * M * N * K / us / 1e6, 1)}
         except pipo.PipoError as e:
             res[pn] = str(e)
