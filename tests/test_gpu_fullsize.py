@@ -1,0 +1,112 @@
+"""Full-size sampled parity: the kernels at the exact shapes and launch configurations
+bench.py times (c5 OPT-30B: d = 7168, F = 28672, 56 heads, b = 64, P = 512, L up to 543;
+c6 LLaMA3.1-8B: d = 4096, F = 14336, GQA 32/8), checked against the oracle's
+definitions on SAMPLED outputs the fp64 oracle computes one by one (selected output
+features / rows / sequences), since a full fp64 OPT-30B forward is out of reach.
+
+The decode linears go through PATH_AUTO at M = 64 — the stream-K tcgen05 kernel the
+pipeline launches — and the prefill linear through the persistent tcgen05 kernel at
+M = b * P = 32768.  Output-feature groups are independent in the int4 encoding (one
+scale per 64 weights of a row), so quantizing only the sampled rows on the oracle side
+is exactly the full quantization restricted to those rows.
+"""
+import numpy as np
+import pytest
+
+from oracle import llama, opt, quant
+from tests.gpu_util import pipo_mod, rel_inf
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+@pytest.fixture(scope="module")
+def env():
+    pipo = pipo_mod()
+    import pipo_synth as synth
+    shape = synth.OPTShape(d_model=256, n_layers=1, n_heads=4, ffn_dim=512, vocab=512, max_pos=64)
+    pl = pipo.Pipeline(pipo.make_config(shape, max_batch=4, max_seq=16, weight_tier=pipo.PIPO_TIER_DEVICE))
+    yield pipo, pl
+    pl.close()
+
+
+def _sampled_linear_check(pipo, pl, M, N, K, path, seed, n_rows=384, m_rows=None, tol=2e-3):
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((M, K), dtype=np.float32).astype(np.float16)
+    w = (rng.standard_normal((N, K), dtype=np.float32) * np.float32(0.02)).astype(np.float16).astype(np.float32)
+    bias = rng.uniform(-0.02, 0.02, N).astype(np.float32)
+    y = pipo.pipo_linear(pl.ctx, 1, path, x, w, bias)
+    rows = np.sort(rng.choice(N, n_rows, replace=False))
+    rows[0], rows[-1] = 0, N - 1                              # first and last (ragged) tile
+    ms = np.arange(M) if m_rows is None else np.sort(rng.choice(M, m_rows, replace=False))
+    wh = quant.quant_dequant(np.ascontiguousarray(w[rows])).astype(np.float64)
+    ref = x[ms].astype(np.float64) @ wh.T + bias[rows].astype(np.float16).astype(np.float64)
+    err = rel_inf(y[np.ix_(ms, rows)], ref)
+    assert err < 2e-2 and err < tol, (M, N, K, err)
+
+
+@pytest.mark.parametrize("name,N,K", [("c5_qkv", 21504, 7168), ("c5_out", 7168, 7168), ("c5_fc1", 28672, 7168),
+                                      ("c5_fc2", 7168, 28672), ("c6_qkv", 6144, 4096), ("c6_fc1", 28672, 4096),
+                                      ("c6_fc2", 4096, 14336)])
+def test_decode_linear_fullsize(env, name, N, K):
+    pipo, pl = env
+    _sampled_linear_check(pipo, pl, 64, N, K, pipo.PATH_AUTO, N + K)
+
+
+def test_decode_linear_fullsize_b1_gemv(env):
+    """c7 (b = 1): the CUDA-core GEMV at the LLaMA3.1-8B FC1 shape."""
+    pipo, pl = env
+    _sampled_linear_check(pipo, pl, 1, 28672, 4096, pipo.PATH_AUTO, 17)
+
+
+def test_prefill_linear_fullsize_sampled(env):
+    """c5 prefill out-proj: M = 64 x 512 tokens through the persistent tcgen05 kernel,
+    checked on 96 sampled token rows x 384 sampled features."""
+    pipo, pl = env
+    _sampled_linear_check(pipo, pl, 64 * 512, 7168, 7168, pipo.PATH_AUTO, 5, n_rows=384, m_rows=96)
+
+
+def test_decode_attention_fullsize(env):
+    """c5 decode attention: b = 64, 56 heads x 128, L = 528 (mid-generation), 8 sampled
+    sequences against the fp64 definition."""
+    pipo, pl = env
+    rng = np.random.default_rng(11)
+    b, L, d, H = 64, 528, 7168, 56
+    q = (rng.standard_normal((b, d), dtype=np.float32) * (d // H) ** -0.5).astype(np.float16)
+    k = rng.standard_normal((L, b, d), dtype=np.float32).astype(np.float16)
+    v = rng.standard_normal((L, b, d), dtype=np.float32).astype(np.float16)
+    o = pipo.pipo_attention_decode(pl.ctx, q, k, v, H)
+    seqs = np.array([0, 9, 17, 31, 32, 40, 55, 63])
+    ref = opt.attention(q[seqs].astype(np.float64)[:, None], k[:, seqs].astype(np.float64).transpose(1, 0, 2),
+                        v[:, seqs].astype(np.float64).transpose(1, 0, 2), L - 1, H)[:, 0]
+    assert rel_inf(o[seqs], ref) < 5e-3
+
+
+def test_gqa_decode_attention_fullsize(env):
+    """c6 decode attention: b = 64, 32 query heads over 8 KV heads x 128, L = 528."""
+    pipo, pl = env
+    rng = np.random.default_rng(12)
+    b, L, H, Hkv, hd = 64, 528, 32, 8, 128
+    q = (rng.standard_normal((b, 1, H * hd), dtype=np.float32) * hd ** -0.5).astype(np.float16)
+    k = rng.standard_normal((L, b, Hkv * hd), dtype=np.float32).astype(np.float16)
+    v = rng.standard_normal((L, b, Hkv * hd), dtype=np.float32).astype(np.float16)
+    o = pipo.pipo_attention_gqa(pl.ctx, q, k, v, L - 1, H, Hkv)
+    seqs = np.array([0, 13, 38, 63])
+    ref = llama.attention_gqa(q[seqs].astype(np.float64), k[:, seqs].astype(np.float64).transpose(1, 0, 2),
+                              v[:, seqs].astype(np.float64).transpose(1, 0, 2), L - 1, H, Hkv)
+    assert rel_inf(o[seqs], ref) < 5e-3
+
+
+def test_prefill_attention_fullsize_sampled(env):
+    """c5 prefill attention (causal, tensor-core kernel): b = 64, P = 512, 56 heads;
+    2 sampled sequences against the fp64 definition."""
+    pipo, pl = env
+    rng = np.random.default_rng(13)
+    b, n, d, H = 64, 512, 7168, 56
+    q = (rng.standard_normal((b, n, d), dtype=np.float32) * (d // H) ** -0.5).astype(np.float16)
+    k = rng.standard_normal((n, b, d), dtype=np.float32).astype(np.float16)
+    v = rng.standard_normal((n, b, d), dtype=np.float32).astype(np.float16)
+    o = pipo.pipo_attention_prefill(pl.ctx, q, k, v, 0, H)
+    seqs = np.array([5, 62])
+    ref = opt.attention(q[seqs].astype(np.float64), k[:, seqs].astype(np.float64).transpose(1, 0, 2),
+                        v[:, seqs].astype(np.float64).transpose(1, 0, 2), 0, H)
+    assert rel_inf(o[seqs], ref) < 1e-2
