@@ -1345,14 +1345,18 @@ static int run_tp(const LinearArgs& a, cudaStream_t st) {
 int launch_linear_tp(const LinearArgs& a, cudaStream_t st) {
   if (a.wfmt != 1) return -1;
   const char* env = getenv("PIPO_TP_CFG");   // tuning / test hook: tile configuration
-  const int cfg = env ? atoi(env) : 0;
-  // measured at the OPT prefill shapes (tools/tpbench.py, profiles/r01): 256-token x
-  // 128-row tiles with 8 epilogue warps win (1.15-1.32 PFLOP/s at c5)
+  // measured at the OPT prefill shapes (tools/tpbench.py, profiles/r01/prefill_nacc2):
+  // 224-token tiles with two accumulators (the epilogue of one tile overlaps the next
+  // tile's MMAs) win except for the long-K down-projection (K >= 4N: fewer, longer
+  // tiles, where 256-token tiles with one accumulator are 4 % faster)
+  const int cfg = env ? atoi(env) : (a.K >= 4 * a.N ? 0 : 5);
   switch (cfg) {
     case 1: return run_tp<96, 2, 2, 4>(a, st);
     case 2: return run_tp<128, 2, 1, 8>(a, st);
     case 3: return run_tp<128, 1, 2, 4>(a, st);
     case 4: return run_tp<128, 2, 1, 4>(a, st);
+    case 5: return run_tp<224, 1, 2, 8>(a, st);   // two accumulators: epilogue overlaps the next tile
+    case 6: return run_tp<192, 1, 2, 8>(a, st);
     default: return run_tp<256, 1, 1, 8>(a, st);
   }
 }
