@@ -172,3 +172,33 @@ def test_llama_rejects_int4_kv():
     cfg = pipo.make_config(TINY, max_batch=2, max_seq=8, kv_fmt=pipo.PIPO_W_INT4_G64)
     with pytest.raises(pipo.PipoError):
         pipo.Pipeline(cfg)
+
+
+def test_llama_disk_tier_bit_identical(tiny, tmp_path):
+    """LLaMA through the DISK tier (blob files -> reader pool -> pinned ring -> H2D):
+    same logits as the HOST tier."""
+    pipo = pipo_mod()
+    prompt = synth.prompts(20, 10, TINY.vocab)
+
+    def syn(pl):
+        pl.load_synthetic(pipo.PIPO_LAYER_EMBED, synth.WEIGHT_SEED)
+        for j in range(TINY.n_layers):
+            pl.load_synthetic(j, synth.WEIGHT_SEED)
+    base = _logits_run(pipo, TINY, syn, prompt, 4, weight_tier=pipo.PIPO_TIER_HOST)
+    got = _logits_run(pipo, TINY, syn, prompt, 4, weight_tier=pipo.PIPO_TIER_DISK, disk_dir=str(tmp_path),
+                      chunk_bytes=1 << 18, disk_threads=3)
+    assert np.array_equal(base, got)
+
+
+def test_llama_sharded_stream_world1_bit_identical(tiny):
+    """NEXT-1 sharded streaming (1-rank NCCL all-gather) on the LLaMA path."""
+    pipo = pipo_mod()
+    emb, layers = tiny
+    prompt = synth.prompts(20, 10, TINY.vocab)
+    base = _logits_run(pipo, TINY, lambda pl: load_masters(pl, emb, layers), prompt, 4, weight_tier=pipo.PIPO_TIER_HOST)
+
+    def sharded(pl):
+        pipo.pipo_shard_stream_init(pl.ctx, 0, 1, pipo.pipo_nccl_unique_id())
+        load_masters(pl, emb, layers)
+    got = _logits_run(pipo, TINY, sharded, prompt, 4, weight_tier=pipo.PIPO_TIER_HOST)
+    assert np.array_equal(base, got)
