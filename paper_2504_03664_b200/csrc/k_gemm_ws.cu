@@ -516,14 +516,19 @@ struct TmCfg {
   static constexpr int ACC_COLS = NACC * 2 * BN;                // NACC buffers x 2 tiles
   static constexpr int A_COLS = 2 * 32 * KBU;                   // per A stage (2 tiles x KBU x 32 cols)
   static constexpr int NA = (512 - ACC_COLS) / A_COLS < 8 ? (512 - ACC_COLS) / A_COLS : 8;
-  static constexpr int E0 = 2 + UW;                              // first epilogue warp
+  // UW = 8: 8 unpack warps; 16: 16 warps splitting each unit's k-blocks; 88: two groups of
+  // 8 warps taking alternate units (each warp's serial per-unit barrier/TMEM latency chain
+  // runs at half the unit rate)
+  static constexpr int UWW = UW == 88 ? 8 : UW;                  // unpack warps per unit
+  static constexpr int UG = UW == 88 ? 2 : 1;                    // unit-interleaved groups
+  static constexpr int E0 = 2 + UWW * UG;                        // first epilogue warp
   static constexpr int XW = E0 + 4;                              // x producer warp
   static constexpr int THREADS = (XW + 1) * 32;
   static constexpr int SMEM = 1024 + NX * X_TILE + NR * RAW + 1024;   // + mbarriers (<= 70) and TMEM slot
   static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
   static_assert(NA >= 2, "TMEM budget");
-  static_assert(UW == 8 || UW == 16, "unpack warps");
+  static_assert(UW == 8 || UW == 16 || UW == 88, "unpack warps");
   static_assert((2 * NR + 2 * NX + 2 * NA + 2 + NACC + 1) * 8 + 4 <= 1024, "barrier area");
 };
 
@@ -616,9 +621,9 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
   if (tid == 0) gstamp(9);
 
   if (tid == 0) {
-    for (int i = 0; i < C::NR; ++i) { ws::mbar_init(&raw_full[i], 1); ws::mbar_init(&raw_empty[i], UW); }
+    for (int i = 0; i < C::NR; ++i) { ws::mbar_init(&raw_full[i], 1); ws::mbar_init(&raw_empty[i], C::UWW); }
     for (int i = 0; i < C::NX; ++i) { ws::mbar_init(&x_full[i], 1); ws::mbar_init(&x_empty[i], 1); }
-    for (int i = 0; i < C::NA; ++i) { ws::mbar_init(&a_full[i], UW); ws::mbar_init(&a_empty[i], 1); }
+    for (int i = 0; i < C::NA; ++i) { ws::mbar_init(&a_full[i], C::UWW); ws::mbar_init(&a_empty[i], 1); }
     for (int i = 0; i < NACC; ++i) { ws::mbar_init(&acc_full[i], 1); ws::mbar_init(&acc_empty[i], 4); }
     ws::mbar_init(fin_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -754,22 +759,25 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
     // a warp may only touch its TMEM lane quarter (warp % 4).  UW = 8: warp -> (tile,
     // quarter), all KBU k-blocks; UW = 16: warp -> (tile, quarter) and one k-block
     // (KBU = 2) or one 32-code half (KBU = 1).
-    const int g = (warp - 2) >> 2, q = warp & 3;
-    const int t = UW == 8 ? g : (g >> 1), sub = UW == 8 ? 0 : (g & 1);
+    constexpr int UWW = C::UWW;
+    const int grp = (warp - 2) / UWW;                 // unit group (UW = 88: alternate units)
+    const int g = ((warp - 2) % UWW) >> 2, q = warp & 3;
+    const int t = UWW == 8 ? g : (g >> 1), sub = UWW == 8 ? 0 : (g & 1);
     const int r = q * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    int s = 0, sa = 0;
-    uint32_t ph_r = 0, ph_a = 1;
-    for (int64_t u = u0; u < u1; ++u) {
+    for (int64_t u = u0 + grp; u < u1; u += C::UG) {
+      const int64_t iu = u - u0;
+      const int s = (int)(iu % C::NR), sa = (int)(iu % C::NA);
+      const uint32_t ph_r = (uint32_t)((iu / C::NR) & 1), ph_a = (uint32_t)(((iu / C::NA) & 1) ^ 1);
       TWAIT(0, &raw_full[s], ph_r);
-      constexpr int NK = UW == 8 ? KBU : (KBU == 2 ? 1 : 1);
+      constexpr int NK = UWW == 8 ? KBU : (KBU == 2 ? 1 : 1);
       uint4 cw[NK][2];
       __half2 s2[NK];
 #pragma unroll
       for (int kk = 0; kk < NK; ++kk) {
-        const int k = UW == 8 ? kk : (KBU == 2 ? sub : 0);
+        const int k = UWW == 8 ? kk : (KBU == 2 ? sub : 0);
         const uint8_t* rs = raw + s * C::RAW + t * C::RAW_T + k * kInt4BlockBytes;
-        if (UW == 8 || KBU == 2) {
+        if (UWW == 8 || KBU == 2) {
           cw[kk][0] = *reinterpret_cast<const uint4*>(rs + r * 16);
           cw[kk][1] = *reinterpret_cast<const uint4*>(rs + (128 + r) * 16);
         } else {
@@ -783,8 +791,8 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
       ws::tc_after();
 #pragma unroll
       for (int kk = 0; kk < NK; ++kk) {
-        const int k = UW == 8 ? kk : (KBU == 2 ? sub : 0);
-        if (UW == 8 || KBU == 2) {
+        const int k = UWW == 8 ? kk : (KBU == 2 ? sub : 0);
+        if (UWW == 8 || KBU == 2) {
           uint32_t o[32];
           const uint32_t w[8] = {cw[kk][0].x, cw[kk][0].y, cw[kk][0].z, cw[kk][0].w,
                                  cw[kk][1].x, cw[kk][1].y, cw[kk][1].z, cw[kk][1].w};
@@ -808,8 +816,6 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
       ws::tc_before();
       __syncwarp();
       if (lane == 0) ws::mbar_arrive(&a_full[sa]);
-      if (++s == C::NR) { s = 0; ph_r ^= 1; }
-      if (++sa == C::NA) { sa = 0; ph_a ^= 1; }
     }
   } else {
     // ---------------- epilogue ----------------
@@ -1067,6 +1073,7 @@ int launch_linear_tm(const LinearArgs& a, cudaStream_t st) {
       case 2: return even ? run_tm<64, 2, 2, 16>(a, st) : run_tm<64, 1, 2, 16>(a, st);
       case 3: return even ? run_tm<64, 2, 1, 16>(a, st) : run_tm<64, 1, 1, 16>(a, st);
       case 4: return run_tm<64, 1, 2, 16>(a, st);
+      case 5: return even ? run_tm<64, 2, 2, 88>(a, st) : run_tm<64, 1, 2, 88>(a, st);
       default: return even ? run_tm<64, 2>(a, st) : run_tm<64, 1>(a, st);
     }
   }
