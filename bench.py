@@ -465,7 +465,7 @@ def run_pipo(args):
     return 0
 
 
-_CLASS_KERNELS = {"linear_decode": ("gemm_tm_kernel", "gemm_ws_kernel", "gemv_int4_kernel", "ws_reduce_kernel",
+_CLASS_KERNELS = {"linear_decode": ("gemm_tm_kernel", "gemm_ws_kernel", "gemv_int4_kernel", "ws_reduce",
                                      "gemm_tc_kernel"),
                   "attn_decode": ("attn_decode", "attn_merge")}
 
