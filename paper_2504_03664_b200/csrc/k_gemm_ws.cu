@@ -1094,38 +1094,44 @@ int launch_linear_tm(const LinearArgs& a, cudaStream_t st) {
 //    tile i overlaps the MMAs of tile i+1;
 //  * EPW epilogue warps (4 or 8): with 8, two warps share each TMEM lane quarter and
 //    split the columns.
-template <int BN, int TILES, int NACC, int EPW>
+// KBU k-blocks per pipeline unit (TILES = 1 only): one raw bulk copy, one x stage of KBU
+// TMA boxes, one A stage of KBU x 32 TMEM columns and ONE round of barrier hand-offs per
+// unit — the per-unit synchronisation chain (~700 cycles, see the decode anatomy in
+// DESIGN.md) is then paid once per 2 k-blocks = 8 MMAs instead of 4.
+template <int BN, int TILES, int NACC, int EPW, int KBU = 1>
 struct TpCfg {
   static constexpr int RAW_T = (int)kInt4BlockBytes;
-  static constexpr int RAW = TILES * RAW_T;
-  static constexpr int NR = 12;
-  static constexpr int X_KB = BN * 128;
-  static constexpr int NX_MAX = (200 * 1024 - NR * RAW) / X_KB;
+  static constexpr int RAW = TILES * RAW_T * KBU;
+  static constexpr int NR = 12 / KBU;
+  static constexpr int X_KB = BN * 128;                  // x of one k-block
+  static constexpr int X_ST = KBU * X_KB;                // x stage
+  static constexpr int NX_MAX = (200 * 1024 - NR * RAW) / X_ST;
   static constexpr int NX = NX_MAX > 8 ? 8 : NX_MAX;
   static constexpr int ACC_COLS = NACC * TILES * BN;
-  static constexpr int A_COLS = TILES * 32;
+  static constexpr int A_COLS = TILES * 32 * KBU;
   static constexpr int NA = (512 - ACC_COLS) / A_COLS < 8 ? (512 - ACC_COLS) / A_COLS : 8;
   static constexpr int THREADS = (10 + EPW + 1) * 32;   // x producer is the last warp
   static constexpr int XW = 10 + EPW;
-  static constexpr int SMEM = 1024 + NX * X_KB + NR * RAW + 512;
+  static constexpr int SMEM = 1024 + NX * X_ST + NR * RAW + 512;
   static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
-  static_assert(NX >= 3, "x ring depth");
+  static_assert(NX >= (KBU == 1 ? 3 : 2), "x ring depth");
+  static_assert(KBU == 1 || TILES == 1, "multi-k-block units with one weight tile per unit");
   static_assert(NA >= 2, "TMEM budget");
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "MMA N");
   static_assert(EPW == 4 || EPW == 8, "epilogue warps");
 };
 
 
-template <int BN, int TILES, int NACC, int EPW>
-__global__ void __launch_bounds__(TpCfg<BN, TILES, NACC, EPW>::THREADS, 1)
+template <int BN, int TILES, int NACC, int EPW, int KBU>
+__global__ void __launch_bounds__(TpCfg<BN, TILES, NACC, EPW, KBU>::THREADS, 1)
     gemm_tp_kernel(const __grid_constant__ CUtensorMap xmap, LinearArgs a, int n_rt, int m_tiles) {
-  using C = TpCfg<BN, TILES, NACC, EPW>;
+  using C = TpCfg<BN, TILES, NACC, EPW, KBU>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* base = smem_raw + (base_u32 - smem_u32(smem_raw));
   uint8_t* xs = base;
-  uint8_t* raw = xs + C::NX * C::X_KB;
+  uint8_t* raw = xs + C::NX * C::X_ST;
   uint64_t* bar = reinterpret_cast<uint64_t*>(raw + C::NR * C::RAW);
   uint64_t* raw_full = bar;
   uint64_t* raw_empty = raw_full + C::NR;
@@ -1138,7 +1144,7 @@ __global__ void __launch_bounds__(TpCfg<BN, TILES, NACC, EPW>::THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + NACC);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int n_kb = a.K / 64;
+  const int n_kb = a.K / 64;                 // n_kb % KBU == 0 (checked by the launcher)
   const int n_grp = (n_rt + TILES - 1) / TILES;
   const int n_tiles = n_grp * m_tiles;
   const int G = gridDim.x;
@@ -1174,12 +1180,12 @@ __global__ void __launch_bounds__(TpCfg<BN, TILES, NACC, EPW>::THREADS, 1)
         const int grp = tile % n_grp;
         const int nt = min(TILES, n_rt - grp * TILES);
         const uint8_t* wsrc = a.w + (int64_t)(grp * TILES) * tile_stride;
-        for (int kb = 0; kb < n_kb; ++kb) {
+        for (int kb = 0; kb < n_kb; kb += KBU) {
           ws::mbar_wait(&raw_empty[s], ph);
-          ws::mbar_expect_tx(&raw_full[s], nt * C::RAW_T);
-          for (int t = 0; t < nt; ++t)
-            ws::bulk_g2s(raw + s * C::RAW + t * C::RAW_T, wsrc + t * tile_stride, C::RAW_T, &raw_full[s]);
-          wsrc += kInt4BlockBytes;
+          ws::mbar_expect_tx(&raw_full[s], nt * C::RAW_T * KBU);
+          for (int t = 0; t < nt; ++t)   // a tile's KBU blocks are contiguous
+            ws::bulk_g2s(raw + s * C::RAW + t * C::RAW_T, wsrc + t * tile_stride, C::RAW_T * KBU, &raw_full[s]);
+          wsrc += kInt4BlockBytes * KBU;
           if (++s == C::NR) { s = 0; ph ^= 1; }
         }
       }
@@ -1191,10 +1197,12 @@ __global__ void __launch_bounds__(TpCfg<BN, TILES, NACC, EPW>::THREADS, 1)
       uint32_t ph = 1;
       for (int tile = blockIdx.x; tile < n_tiles; tile += G) {
         const int mt = tile / n_grp;
-        for (int kb = 0; kb < n_kb; ++kb) {
+        for (int kb = 0; kb < n_kb; kb += KBU) {
           ws::mbar_wait(&x_empty[s], ph);
-          ws::mbar_expect_tx(&x_full[s], C::X_KB);
-          ws::tma_2d(xs + s * C::X_KB, &xmap, kb * 64, mt * BN, &x_full[s]);
+          ws::mbar_expect_tx(&x_full[s], C::X_ST);
+#pragma unroll
+          for (int k = 0; k < KBU; ++k)
+            ws::tma_2d(xs + s * C::X_ST + k * C::X_KB, &xmap, (kb + k) * 64, mt * BN, &x_full[s]);
           if (++s == C::NX) { s = 0; ph ^= 1; }
         }
       }
@@ -1211,20 +1219,23 @@ __global__ void __launch_bounds__(TpCfg<BN, TILES, NACC, EPW>::THREADS, 1)
       ws::mbar_wait(&acc_empty[ab], ((seg / NACC) & 1) ^ 1);
       ws::tc_after();
       const uint32_t d = tmem + ab * (TILES * BN);
-      for (int kb = 0; kb < n_kb; ++kb) {
+      for (int kb = 0; kb < n_kb; kb += KBU) {
         ws::mbar_wait(&a_full[sa], ph_a);
         ws::mbar_wait(&x_full[sx], ph_x);
         ws::tc_after();
         if (ws::elect_one()) {
           const uint32_t at = a_base + sa * C::A_COLS;
-          const uint64_t db0 = ws::sw128_desc(xs_base + sx * C::X_KB);
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
-            const uint64_t db = db0 + (uint64_t)((kk * 32) >> 4);
+          for (int k = 0; k < KBU; ++k) {
+            const uint64_t db0 = ws::sw128_desc(xs_base + sx * C::X_ST + k * C::X_KB);
 #pragma unroll
-            for (int t = 0; t < TILES; ++t)
-              if (t < nt) mma_f16_ts(d + t * BN, at + t * 32 + kk * 8, db, C::IDESC, acc);
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint32_t acc = (kb > 0 || k > 0 || kk > 0) ? 1u : 0u;
+              const uint64_t db = db0 + (uint64_t)((kk * 32) >> 4);
+#pragma unroll
+              for (int t = 0; t < TILES; ++t)
+                if (t < nt) mma_f16_ts(d + t * BN, at + k * 32 + t * 32 + kk * 8, db, C::IDESC, acc);
+            }
           }
           ws::mma_commit(&a_empty[sa]);
           ws::mma_commit(&x_empty[sx]);
@@ -1246,8 +1257,38 @@ __global__ void __launch_bounds__(TpCfg<BN, TILES, NACC, EPW>::THREADS, 1)
     int s = 0, sa = 0;
     uint32_t ph_r = 0, ph_a = 1;
     for (int tile = blockIdx.x; tile < n_tiles; tile += G) {
-      for (int kb = 0; kb < n_kb; ++kb) {
+      for (int kb = 0; kb < n_kb; kb += KBU) {
         ws::mbar_wait(&raw_full[s], ph_r);
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        if (KBU > 1) {   // TILES == 1: all KBU blocks of the unit, one hand-off round
+          uint4 cw[KBU];
+          __half2 s2k[KBU];
+#pragma unroll
+          for (int k = 0; k < KBU; ++k) {
+            const uint8_t* rs = raw + s * C::RAW + k * C::RAW_T;
+            cw[k] = *reinterpret_cast<const uint4*>(rs + (g * 128 + r) * 16);
+            s2k[k] = __half2half2(*reinterpret_cast<const __half*>(rs + 4096 + r * 2));
+          }
+          __syncwarp();
+          if (lane == 0) ws::mbar_arrive(&raw_empty[s]);
+          ws::mbar_wait(&a_empty[sa], ph_a);
+          ws::tc_after();
+#pragma unroll
+          for (int k = 0; k < KBU; ++k) {
+            uint32_t o[16];
+            const uint32_t w[4] = {cw[k].x, cw[k].y, cw[k].z, cw[k].w};
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) dequant8(w[ch], s2k[k], reinterpret_cast<__half2*>(o + ch * 4));
+            tmem_st16(a_base + sa * C::A_COLS + k * 32 + g * 16 + lane_off, o);
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+          ws::tc_before();
+          __syncwarp();
+          if (lane == 0) ws::mbar_arrive(&a_full[sa]);
+          if (++s == C::NR) { s = 0; ph_r ^= 1; }
+          if (++sa == C::NA) { sa = 0; ph_a ^= 1; }
+          continue;
+        }
         const uint8_t* rs = raw + s * C::RAW + t * C::RAW_T;
         uint4 cw0, cw1;
         if (TILES == 2) {
@@ -1261,7 +1302,6 @@ __global__ void __launch_bounds__(TpCfg<BN, TILES, NACC, EPW>::THREADS, 1)
         if (lane == 0) ws::mbar_arrive(&raw_empty[s]);
         ws::mbar_wait(&a_empty[sa], ph_a);
         ws::tc_after();
-        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         if (TILES == 2) {
           uint32_t o[32];
           const uint32_t w[8] = {cw0.x, cw0.y, cw0.z, cw0.w, cw1.x, cw1.y, cw1.z, cw1.w};
@@ -1331,12 +1371,14 @@ __global__ void __launch_bounds__(TpCfg<BN, TILES, NACC, EPW>::THREADS, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512u));
 }
 
-template <int BN, int TILES, int NACC, int EPW>
+template <int BN, int TILES, int NACC, int EPW, int KBU = 1>
 static int run_tp(const LinearArgs& a, cudaStream_t st) {
-  using C = TpCfg<BN, TILES, NACC, EPW>;
+  using C = TpCfg<BN, TILES, NACC, EPW, KBU>;
+  if ((a.K / 64) % KBU) return -1;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(gemm_tp_kernel<BN, TILES, NACC, EPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(gemm_tp_kernel<BN, TILES, NACC, EPW, KBU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         C::SMEM);
     attr_set = true;
   }
   const int n_rt = (a.N + 127) / 128, m_tiles = (a.M + BN - 1) / BN;
@@ -1345,7 +1387,7 @@ static int run_tp(const LinearArgs& a, cudaStream_t st) {
   const int G = (int)std::min<int64_t>(a.num_sms, n_tiles);
   CUtensorMap map;
   if (!make_xmap(&map, a.x, a.M, a.K, BN)) return -1;
-  launch_pdl(gemm_tp_kernel<BN, TILES, NACC, EPW>, dim3(G), dim3(C::THREADS), C::SMEM, st, map, a, n_rt, m_tiles);
+  launch_pdl(gemm_tp_kernel<BN, TILES, NACC, EPW, KBU>, dim3(G), dim3(C::THREADS), C::SMEM, st, map, a, n_rt, m_tiles);
   return 1;
 }
 
@@ -1364,6 +1406,9 @@ int launch_linear_tp(const LinearArgs& a, cudaStream_t st) {
     case 4: return run_tp<128, 2, 1, 4>(a, st);
     case 5: return run_tp<224, 1, 2, 8>(a, st);   // two accumulators: epilogue overlaps the next tile
     case 6: return run_tp<192, 1, 2, 8>(a, st);
+    case 7: return (a.K / 64) % 2 ? run_tp<256, 1, 1, 8>(a, st) : run_tp<256, 1, 1, 8, 2>(a, st);   // 2-k-block units
+    case 8: return (a.K / 64) % 2 ? run_tp<192, 1, 2, 8>(a, st) : run_tp<192, 1, 2, 8, 2>(a, st);
+    case 9: return (a.K / 64) % 2 ? run_tp<128, 1, 2, 8>(a, st) : run_tp<128, 1, 2, 8, 2>(a, st);
     default: return run_tp<256, 1, 1, 8>(a, st);
   }
 }
