@@ -110,3 +110,79 @@ def test_prefill_attention_fullsize_sampled(env):
     ref = opt.attention(q[seqs].astype(np.float64), k[:, seqs].astype(np.float64).transpose(1, 0, 2),
                         v[:, seqs].astype(np.float64).transpose(1, 0, 2), 0, H)
     assert rel_inf(o[seqs], ref) < 1e-2
+
+
+def test_c2_full_model_sampled_sequences():
+    """configs[1] end to end: OPT-1.3B (24 layers, d = 2048), b = 16, P = 256, weights in
+    pinned host memory (streamed), through prefill + 3 decode steps.  Sequences are
+    independent, so the fp64 oracle runs only 2 sampled sequences of the batch; their
+    per-layer outputs (debug capture) and logits must be within 2e-2 of the oracle.  The
+    GPU is fed the oracle's greedy tokens for the sampled sequences (teacher forcing,
+    reading Q11) and its own for the rest."""
+    import pipo_synth as synth
+    from tests.gpu_util import load_masters
+    pipo = pipo_mod()
+    s = synth.OPT_1_3B
+    b, P, G = 16, 256, 4
+    seqs = np.array([3, 12])
+    emb = synth.embed_masters(s)
+    layers = [synth.layer_masters(s, j) for j in range(s.n_layers)]
+    ref = opt.OracleOPT.from_masters(s.n_heads, emb, layers, "int4", P + G)
+    prompt = synth.prompts(b, P, s.vocab)
+    cfg = pipo.make_config(s, max_batch=b, max_seq=P + G, weight_tier=pipo.PIPO_TIER_HOST)
+    with pipo.Pipeline(cfg) as pl:
+        load_masters(pl, emb, layers)
+        del layers
+        cap = np.zeros((s.n_layers, b, P, s.d_model), np.float32)
+        pipo.pipo_debug_capture(pl.ctx, cap)
+        nxt, lg = pl.prefill(prompt, want_logits=True)
+        rl = ref.prefill(prompt[seqs])
+        for j in (0, s.n_layers // 2, s.n_layers - 1):
+            assert rel_inf(cap[j][seqs], ref.capture[j]) < 2e-2, j
+        assert rel_inf(lg[seqs], rl) < 2e-2
+        for _ in range(G - 1):
+            tok = nxt.copy()
+            tok[seqs] = np.argmax(rl, -1)
+            nxt, lg = pl.decode_step(tok.astype(np.int32), want_logits=True)
+            rl = ref.decode(tok[seqs])
+            err = rel_inf(lg[seqs], rl)
+            assert err < 2e-2, err
+            srt = np.sort(rl, -1)
+            decided = (srt[:, -1] - srt[:, -2]) >= 4 * np.abs(lg[seqs] - rl).max()
+            assert np.array_equal(nxt[seqs][decided], np.argmax(rl, -1)[decided])
+
+
+def test_c6_llama8b_two_layers_sampled_sequences():
+    """c6 shapes end to end (LLaMA3.1-8B: d = 4096, GQA 32/8, SwiGLU 14336, V = 128256,
+    llama3 RoPE), 2 of the 32 decoder layers (the per-layer kernels and launch
+    configurations are the ones c6 runs), b = 64, P = 512, host-streamed int4 weights,
+    prefill + 2 decode steps; 2 sampled sequences against the fp64 oracle."""
+    import dataclasses
+
+    import pipo_synth as synth
+    from tests.gpu_util import load_masters
+    pipo = pipo_mod()
+    s = dataclasses.replace(synth.LLAMA31_8B, n_layers=2, max_pos=4096)
+    b, P, G = 64, 512, 3
+    seqs = np.array([7, 50])
+    emb = synth.llama_embed_masters(s)
+    layers = [synth.llama_layer_masters(s, j) for j in range(s.n_layers)]
+    ref = llama.OracleLlama.from_masters(s, emb, layers, "int4", P + G)
+    prompt = synth.prompts(b, P, s.vocab)
+    cfg = pipo.make_config(s, max_batch=b, max_seq=P + G, weight_tier=pipo.PIPO_TIER_HOST)
+    with pipo.Pipeline(cfg) as pl:
+        load_masters(pl, emb, layers)
+        del layers
+        cap = np.zeros((s.n_layers, b, P, s.d_model), np.float32)
+        pipo.pipo_debug_capture(pl.ctx, cap)
+        nxt, lg = pl.prefill(prompt, want_logits=True)
+        rl = ref.prefill(prompt[seqs])
+        for j in range(s.n_layers):
+            assert rel_inf(cap[j][seqs], ref.capture[j]) < 2e-2, j
+        assert rel_inf(lg[seqs], rl) < 2e-2
+        for _ in range(G - 1):
+            tok = nxt.copy()
+            tok[seqs] = np.argmax(rl, -1)
+            nxt, lg = pl.decode_step(tok.astype(np.int32), want_logits=True)
+            rl = ref.decode(tok[seqs])
+            assert rel_inf(lg[seqs], rl) < 2e-2
