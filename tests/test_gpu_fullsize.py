@@ -186,3 +186,38 @@ def test_c6_llama8b_two_layers_sampled_sequences():
             nxt, lg = pl.decode_step(tok.astype(np.int32), want_logits=True)
             rl = ref.decode(tok[seqs])
             assert rel_inf(lg[seqs], rl) < 2e-2
+
+
+def test_c5_opt30b_two_layers_sampled_sequences():
+    """The headline config's shapes end to end (OPT-30B: d = 7168, 56 heads, F = 28672,
+    V = 50272), 2 of the 48 decoder layers, b = 64, P = 512, host-streamed int4 weights,
+    prefill + 2 decode steps; 2 sampled sequences against the fp64 oracle."""
+    import dataclasses
+
+    import pipo_synth as synth
+    from tests.gpu_util import load_masters
+    pipo = pipo_mod()
+    s = dataclasses.replace(synth.OPT_30B, n_layers=2)
+    b, P, G = 64, 512, 3
+    seqs = np.array([1, 60])
+    emb = synth.embed_masters(s)
+    layers = [synth.layer_masters(s, j) for j in range(s.n_layers)]
+    ref = opt.OracleOPT.from_masters(s.n_heads, emb, layers, "int4", P + G)
+    prompt = synth.prompts(b, P, s.vocab)
+    cfg = pipo.make_config(s, max_batch=b, max_seq=P + G, weight_tier=pipo.PIPO_TIER_HOST)
+    with pipo.Pipeline(cfg) as pl:
+        load_masters(pl, emb, layers)
+        del layers
+        cap = np.zeros((s.n_layers, b, P, s.d_model), np.float32)
+        pipo.pipo_debug_capture(pl.ctx, cap)
+        nxt, lg = pl.prefill(prompt, want_logits=True)
+        rl = ref.prefill(prompt[seqs])
+        for j in range(s.n_layers):
+            assert rel_inf(cap[j][seqs], ref.capture[j]) < 2e-2, j
+        assert rel_inf(lg[seqs], rl) < 2e-2
+        for _ in range(G - 1):
+            tok = nxt.copy()
+            tok[seqs] = np.argmax(rl, -1)
+            nxt, lg = pl.decode_step(tok.astype(np.int32), want_logits=True)
+            rl = ref.decode(tok[seqs])
+            assert rel_inf(lg[seqs], rl) < 2e-2
