@@ -519,8 +519,9 @@ struct TmCfg {
   // UW = 8: 8 unpack warps; 16: 16 warps splitting each unit's k-blocks; 88: two groups of
   // 8 warps taking alternate units (each warp's serial per-unit barrier/TMEM latency chain
   // runs at half the unit rate)
-  static constexpr int UWW = UW == 88 ? 8 : UW;                  // unpack warps per unit
+  static constexpr int UWW = (UW == 88 || UW == 98) ? 8 : UW;   // unpack warps per unit
   static constexpr int UG = UW == 88 ? 2 : 1;                    // unit-interleaved groups
+  static constexpr bool PIPE = UW == 98;                         // 8 warps, software-pipelined
   static constexpr int E0 = 2 + UWW * UG;                        // first epilogue warp
   static constexpr int XW = E0 + 4;                              // x producer warp
   static constexpr int THREADS = (XW + 1) * 32;
@@ -528,7 +529,7 @@ struct TmCfg {
   static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
   static_assert(NA >= 2, "TMEM budget");
-  static_assert(UW == 8 || UW == 16 || UW == 88, "unpack warps");
+  static_assert(UW == 8 || UW == 16 || UW == 88 || UW == 98, "unpack warps");
   static_assert((2 * NR + 2 * NX + 2 * NA + 2 + NACC + 1) * 8 + 4 <= 1024, "barrier area");
 };
 
@@ -765,6 +766,47 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
     const int t = UWW == 8 ? g : (g >> 1), sub = UWW == 8 ? 0 : (g & 1);
     const int r = q * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    if constexpr (C::PIPE) {
+      // software-pipelined: unit u+1's raw wait + shared loads + ring release are issued
+      // while unit u's TMEM stores drain (before tcgen05.wait::st), so the per-unit
+      // barrier/latency chain overlaps the store completion
+      uint4 cw[KBU][2];
+      __half2 s2[KBU];
+      auto load_unit = [&](int64_t iu, uint4 (&c)[KBU][2], __half2 (&sc)[KBU]) {
+        const int s = (int)(iu % C::NR);
+        TWAIT(0, &raw_full[s], (uint32_t)((iu / C::NR) & 1));
+#pragma unroll
+        for (int k = 0; k < KBU; ++k) {
+          const uint8_t* rs = raw + s * C::RAW + t * C::RAW_T + k * kInt4BlockBytes;
+          c[k][0] = *reinterpret_cast<const uint4*>(rs + r * 16);
+          c[k][1] = *reinterpret_cast<const uint4*>(rs + (128 + r) * 16);
+          sc[k] = __half2half2(*reinterpret_cast<const __half*>(rs + 4096 + r * 2));
+        }
+        __syncwarp();
+        if (lane == 0) ws::mbar_arrive(&raw_empty[s]);
+      };
+      if (u0 < u1) load_unit(0, cw, s2);
+      for (int64_t u = u0; u < u1; ++u) {
+        const int64_t iu = u - u0;
+        const int sa = (int)(iu % C::NA);
+        TWAIT(1, &a_empty[sa], (uint32_t)(((iu / C::NA) & 1) ^ 1));
+        ws::tc_after();
+#pragma unroll
+        for (int k = 0; k < KBU; ++k) {
+          uint32_t o[32];
+          const uint32_t w[8] = {cw[k][0].x, cw[k][0].y, cw[k][0].z, cw[k][0].w,
+                                 cw[k][1].x, cw[k][1].y, cw[k][1].z, cw[k][1].w};
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch) dequant8(w[ch], s2[k], reinterpret_cast<__half2*>(o + ch * 4));
+          tmem_st32(a_base + sa * C::A_COLS + k * 64 + t * 32 + lane_off, o);
+        }
+        if (u + 1 < u1) load_unit(iu + 1, cw, s2);   // registers are free once the stores are issued
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        ws::tc_before();
+        __syncwarp();
+        if (lane == 0) ws::mbar_arrive(&a_full[sa]);
+      }
+    } else
     for (int64_t u = u0 + grp; u < u1; u += C::UG) {
       const int64_t iu = u - u0;
       const int s = (int)(iu % C::NR), sa = (int)(iu % C::NA);
@@ -1064,16 +1106,22 @@ static int run_tm(const LinearArgs& a, cudaStream_t st) {
 int launch_linear_tm(const LinearArgs& a, cudaStream_t st) {
   if (a.wfmt != 1) return -1;
   const bool even = (a.K / 64) % 2 == 0;
-  if (a.M <= 16) return even ? run_tm<16, 2>(a, st) : run_tm<16, 1>(a, st);
-  if (a.M <= 32) return even ? run_tm<32, 2>(a, st) : run_tm<32, 1>(a, st);
+  const char* env = getenv("PIPO_TM_CFG");   // tuning hook: (NACC, unpack warps) variants
+  const int cfg = env ? atoi(env) : 6;      // 6: software-pipelined unpack (3-5 % faster at c5)
+  if (a.M <= 16)
+    return cfg == 6 ? (even ? run_tm<16, 2, 2, 98>(a, st) : run_tm<16, 1, 2, 98>(a, st))
+                    : (even ? run_tm<16, 2>(a, st) : run_tm<16, 1>(a, st));
+  if (a.M <= 32)
+    return cfg == 6 ? (even ? run_tm<32, 2, 2, 98>(a, st) : run_tm<32, 1, 2, 98>(a, st))
+                    : (even ? run_tm<32, 2>(a, st) : run_tm<32, 1>(a, st));
   if (a.M <= 64) {
-    const char* env = getenv("PIPO_TM_CFG");   // tuning hook: (NACC, unpack warps) variants
-    switch (env ? atoi(env) : 0) {
+    switch (cfg) {
       case 1: return even ? run_tm<64, 2, 1, 8>(a, st) : run_tm<64, 1, 1, 8>(a, st);
       case 2: return even ? run_tm<64, 2, 2, 16>(a, st) : run_tm<64, 1, 2, 16>(a, st);
       case 3: return even ? run_tm<64, 2, 1, 16>(a, st) : run_tm<64, 1, 1, 16>(a, st);
       case 4: return run_tm<64, 1, 2, 16>(a, st);
       case 5: return even ? run_tm<64, 2, 2, 88>(a, st) : run_tm<64, 1, 2, 88>(a, st);
+      case 6: return even ? run_tm<64, 2, 2, 98>(a, st) : run_tm<64, 1, 2, 98>(a, st);
       default: return even ? run_tm<64, 2>(a, st) : run_tm<64, 1>(a, st);
     }
   }

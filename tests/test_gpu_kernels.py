@@ -84,7 +84,7 @@ def test_linear_vs_oracle(env, M, N, K, wfmt):
         assert err < (2e-3 if wfmt == 1 else 1e-4), (path, err)
 
 
-TM_CFGS = ["0", "1", "2", "3", "4", "5"]   # PIPO_TM_CFG: decode TMEM-A variants (accumulators, unpack warps)
+TM_CFGS = ["0", "1", "2", "3", "4", "5", "6"]   # PIPO_TM_CFG: decode TMEM-A variants (accumulators, unpack warps)
 
 
 @pytest.mark.parametrize("cfg", TM_CFGS)
