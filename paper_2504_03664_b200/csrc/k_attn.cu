@@ -725,7 +725,12 @@ int launch_attention_decode(const AttnArgs& a, cudaStream_t st) {
   const int pairs = a.b * a.n_heads / G;
   // enough CTAs for ~8 waves of resident blocks (9 per SM): the block scheduler then
   // balances the tail to within ~1/8 of the kernel; splits merge in a second kernel
-  const int target = a.num_sms * 72;
+  // Split positions only when (b, head) pairs cannot fill the GPU: measured on B200
+  // (profiles/r01/attn_splits) one split per pair wins from 512 pairs up (c5 166 -> 155 us,
+  // c3 56.5 -> 50.6, c2 15.0 -> 12.5: no partial writes, no merge launch); small batches
+  // (c7: b = 1, 8 KV-head pairs) still split.  PIPO_ATTN_WAVES = w: target w x 9 CTAs/SM.
+  static const int waves = getenv("PIPO_ATTN_WAVES") ? atoi(getenv("PIPO_ATTN_WAVES")) : -1;
+  const int target = waves < 0 ? a.num_sms * 2 : a.num_sms * 9 * waves;
   int n_splits = pairs >= target ? 1 : (target + pairs - 1) / pairs;
   n_splits = max(1, min(n_splits, (L + 63) / 64));
   const int per = (L + n_splits - 1) / n_splits;
