@@ -392,7 +392,10 @@ def run_pipo(args):
                     "bytes_per_unit": per_unit_bytes, "us_per_unit": per_unit_s * 1e6,
                     "tflops": kd["flops"] / kd["units"] / per_unit_s / 1e12,
                     "tflops_frac_of_fp16_peak": kd["flops"] / kd["units"] / per_unit_s / 1e12 / tc,
-                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy), bf16_tflops_sustained (fp16 same rate)"}
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy), bf16_tflops_sustained (fp16 same rate)",
+                    "note": ("host/disk tier: CUDA timing events on the compute stream wait ~25 us behind the copy "
+                             "engine's in-flight H2D command (DESIGN.md §11), so the event bracket over-counts; "
+                             "roofline_cupti has the kernel-only time") if c["weight_tier"] != 0 else None}
     line = None
     if rank == 0:
         line = {

@@ -56,6 +56,13 @@ for (s0, e0, n0), (s1, e1, n1) in zip(comp, comp[1:]):
         gaps.append(s1 - e0)
 out["_gap_before_gemm_tm_us"] = {"avg": float(np.mean(gaps)) if gaps else None,
                                 "p50": float(np.median(gaps)) if gaps else None, "n": len(gaps)}
+# gap statistics by (previous kernel -> next kernel) pair on the compute stream
+pairs = collections.defaultdict(list)
+short = lambda n: n.split("(")[0].replace("void pipo::", "").replace("pipo::", "")[:28]
+for (s0, e0, n0), (s1, e1, n1) in zip(comp, comp[1:]):
+    pairs[f"{short(n0)} -> {short(n1)}"].append(s1 - e0)
+out["_gaps_by_pair_us"] = {k: {"n": len(v), "avg": float(np.mean(v)), "p50": float(np.median(v))}
+                          for k, v in sorted(pairs.items(), key=lambda kv: -np.sum(kv[1]))[:12]}
 span = (kern[-1][1] - kern[0][0]) / 1e3 if kern else 0
 out["_span_ms"] = span
 print(json.dumps({"config": args.config, "tier": args.tier, "kernels": out}, indent=1))
