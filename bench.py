@@ -69,6 +69,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cupti", action="store_true", help="skip the torch.profiler kernel-duration pass")
+    ap.add_argument("--no-kprof", action="store_true",
+                    help="no per-kernel timing events (no kernel roofline); A/B of the event overhead")
     ap.add_argument("--no-timeline", action="store_true",
                     help="no per-phase span events (busy fractions unavailable); A/B of the event overhead")
     ap.add_argument("--disk-dir", default="/tmp/pipo_disk")
@@ -270,7 +272,7 @@ def run_pipo(args):
     torch.cuda.set_device(local)
     c = CONFIGS[args.config]
     s, b, P, G = c["shape"], c["b"], c["P"], c["G"]
-    steps_needed = args.warmup + args.steps * (1 if args.no_e2e else 2) + (0 if args.no_cupti else 2)
+    steps_needed = args.warmup + args.steps * (2 if args.no_e2e else 3) + (0 if args.no_cupti else 2)
     max_seq = P + max(G, steps_needed + 1)
     if args.weight_tier:
         c = {**c, "weight_tier": ["device", "host", "disk"].index(args.weight_tier)}
@@ -282,7 +284,8 @@ def run_pipo(args):
                            weight_tier=c["weight_tier"], kv_tier=c["kv_tier"], ring_layers=args.ring,
                            kv_fmt=pipo.PIPO_W_INT4_G64 if args.kv_fmt == "int4" else pipo.PIPO_W_FP16,
                            chunk_bytes=int(args.chunk_mb * (1 << 20)), disk_dir=disk_dir,
-                           flags=(0 if args.no_timeline else pipo.PIPO_F_TIMELINE) | pipo.PIPO_F_KPROF)
+                           flags=(0 if args.no_timeline else pipo.PIPO_F_TIMELINE) |
+                                 (0 if args.no_kprof else pipo.PIPO_F_KPROF))
     t_setup = time.perf_counter()
     pl = pipo.Pipeline(cfg)
     if args.shard_stream:
@@ -361,6 +364,25 @@ def run_pipo(args):
                "h2d_bytes_per_step": int(per_step_h2d), "d2h_bytes_per_step": int(b * 4),
                "note": "decode_step(host tokens) -> host next ids; h2d counts the streamed weights too"}
 
+    # Uninstrumented pass (same K steps, no timeline / per-kernel events): CUDA timing
+    # events on the compute stream wait behind the copy engine (~25 us each, DESIGN.md
+    # §11), which costs the small configs a few % of throughput; reported alongside.
+    uninstr = None
+    if rank == 0 or world > 1:
+        pipo.pipo_set_flags(pl.ctx, 0)
+        barrier()
+        e0.record(comp)
+        for _ in range(args.steps):
+            pipo.decode_step_dev(pl.ctx, tok_dev.data_ptr(), tok_dev.data_ptr())
+        e1.record(comp)
+        torch.cuda.synchronize(local)
+        barrier()
+        t_un = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+        pipo.pipo_set_flags(pl.ctx, pipo.PIPO_F_TIMELINE | pipo.PIPO_F_KPROF)
+        un_ms = t_un / args.steps * 1e3
+        uninstr = {"value": aggregate_throughput(b, world, args.steps, t_un), "ms_per_step": un_ms,
+                   "link_frac": None, "note": "same K steps with PIPO_F_TIMELINE / PIPO_F_KPROF off"}
+
     # CUPTI (torch.profiler) view of 2 extra untimed steps: true per-kernel GPU durations
     # with the copy stream running (context for the event-bracketed roofline above)
     cupti = None
@@ -372,6 +394,8 @@ def run_pipo(args):
     peaks = measured_peaks()
     layer_bytes = st["h2d_bytes"] / max(1, st["decode_steps"])
     link_floor_s = layer_bytes / (link_probe * 1e9)
+    if uninstr and uninstr["ms_per_step"] > 0 and layer_bytes > 0:
+        uninstr["link_frac"] = link_floor_s / (uninstr["ms_per_step"] / 1e3)
     kernels = {}
     for name, k in kst.items():
         if k["units"] and k["ms"] > 0:
@@ -420,6 +444,7 @@ def run_pipo(args):
             "roofline": roofline,
             "kernels": kernels,
             "roofline_cupti": cupti,
+            "uninstrumented": uninstr,
             "link_roofline": {"bound": "host-link", "bytes_per_step": int(layer_bytes),
                               "probe_gbs": link_probe, "achieved_gbs": layer_bytes / (ms / 1e3) / 1e9,
                               "frac": link_floor_s / (ms / 1e3), "copy_engine_gbs": st["h2d_gbs"]},

@@ -194,6 +194,12 @@ pipo_status decode_step_dev(pipo_ctx* ctx, const int32_t* tokens_dev, int32_t* n
 pipo_status pipeline_stats(pipo_ctx* ctx, pipo_stats* out);
 pipo_status pipeline_stats_reset(pipo_ctx* ctx);
 
+/* Change the PIPO_F_* instrumentation flags between calls (synchronises the device).
+ * Timing events on the compute stream are not free while the copy engine streams
+ * (~25 us each): PIPO_F_TIMELINE / PIPO_F_KPROF off gives the
+ * uninstrumented step. */
+pipo_status pipo_set_flags(pipo_ctx* ctx, uint32_t flags);
+
 /* Per-kernel-class timing (needs PIPO_F_KPROF): one unit = one linear layer / one
  * attention layer / one LM head; ms from CUDA events on the compute stream around
  * each unit; bytes / flops are the ALGORITHMIC counts. */

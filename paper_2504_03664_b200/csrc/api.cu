@@ -1047,6 +1047,16 @@ pipo_status pipeline_stats(pipo_ctx* ctx, pipo_stats* out) {
   return PIPO_OK;
 }
 
+pipo_status pipo_set_flags(pipo_ctx* ctx, uint32_t flags) {
+  CHECK_CTX();
+  CK(cudaSetDevice(ctx->cfg.device));
+  CK(cudaDeviceSynchronize());   // spans / kernel records in flight keep their events
+  ctx->timeline = (flags & PIPO_F_TIMELINE) != 0;
+  ctx->kprof = (flags & PIPO_F_KPROF) != 0;
+  ctx->cfg.flags = flags;
+  return PIPO_OK;
+}
+
 pipo_status pipeline_stats_reset(pipo_ctx* ctx) {
   CHECK_CTX();
   CK(cudaSetDevice(ctx->cfg.device));

@@ -121,6 +121,7 @@ _sig("decode_step", C.c_int, _P, _i32, _i32, _f)
 _sig("decode_step_dev", C.c_int, _P, _P, _P)
 _sig("pipeline_stats", C.c_int, _P, C.POINTER(pipo_stats))
 _sig("pipeline_stats_reset", C.c_int, _P)
+_sig("pipo_set_flags", C.c_int, _P, C.c_uint32)
 _sig("pipo_stream", _P, _P, C.c_int32)
 _sig("pipo_kernel_stats", C.c_int, _P, C.c_int32, C.POINTER(pipo_kstats))
 _sig("pipo_quantize_int4_g64", C.c_int, _f, C.c_int64, C.c_int64, _u8, _u16)
@@ -155,7 +156,7 @@ EXPORTED = ["pipo_last_error", "pipo_abi_version", "pipeline_init", "pipeline_de
             "pipo_load_synthetic", "prefill", "decode_step", "decode_step_dev", "pipeline_stats",
             "pipeline_stats_reset", "pipo_stream", "pipo_kernel_stats", "pipo_quantize_int4_g64", "pipo_quantize_int4_g64_gpu",
             "pipo_unpack_int4_g64", "pipo_linear", "pipo_bench_linear", "pipo_probe_bulk", "pipo_bench_attention", "pipo_attention_decode", "pipo_attention_prefill", "pipo_debug_capture", "pipo_probe_h2d",
-            "pipo_attention_gqa", "pipo_rope", "pipo_shard_range", "pipo_nccl_unique_id", "pipo_shard_stream_init",
+            "pipo_attention_gqa", "pipo_rope", "pipo_set_flags", "pipo_shard_range", "pipo_nccl_unique_id", "pipo_shard_stream_init",
             "pipo_ffn_hidden_dim", "pipo_memory_model", "pipo_choose_block_size", "pipo_choose_plan"]
 
 
@@ -382,6 +383,10 @@ def pipo_shard_stream_init(ctx, rank: int, world: int, uid: bytes):
     buf = np.frombuffer(uid, dtype=np.uint8).copy()
     assert buf.size == 128
     _check(_lib.pipo_shard_stream_init(ctx, rank, world, _ptr(buf, C.c_uint8)))
+
+
+def pipo_set_flags(ctx, flags: int):
+    _check(_lib.pipo_set_flags(ctx, flags))
 
 
 def pipo_debug_capture(ctx, out: np.ndarray | None):
