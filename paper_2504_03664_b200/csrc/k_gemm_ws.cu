@@ -447,48 +447,45 @@ __global__ void __launch_bounds__(256) ws_reduce_kernel(LinearArgs a, int n_rt, 
   }
 }
 
-// Stream-K reduce v2: one 128-thread block per (tile, 8-column group, weight tile) — only
+// Stream-K reduce v2: one 256-thread block per (tile, 4 columns), float4 partial loads — only
 // the tiles that exist (no early-exit blocks for CTA boundaries, no shared-memory
 // broadcast), one resident wave.  Same operands and order as ws_reduce_kernel
 // (0 + p_cf + p_cf+1 + ... in CTA order), so the two are bit-identical.
 template <int BN>
-__global__ void __launch_bounds__(128) ws_reduce2_kernel(LinearArgs a, int n_rt, int m_tiles, int G, int kbu) {
+__global__ void __launch_bounds__(256) ws_reduce2_kernel(LinearArgs a, int n_rt, int m_tiles, int G, int kbu) {
   ws::griddep_wait();
   ws::griddep_launch();
   const int n_ku = a.K / 64 / kbu, n_pairs = (n_rt + 1) >> 1;
   const int64_t U = (int64_t)n_pairs * m_tiles * n_ku;
   const int64_t tile = blockIdx.x;
-  const int t = blockIdx.z;
   const int pr = (int)(tile % n_pairs), mt = (int)(tile / n_pairs);
-  if (2 * pr + t >= n_rt) return;
   const int cf = ws::cta_of_unit(tile * n_ku, U, G), cl = ws::cta_of_unit((tile + 1) * n_ku - 1, U, G);
   if (cf == cl) return;                                   // owned whole: stored by the GEMM
   const bool cf_first = ws::u_begin(cf, U, G) / n_ku == tile;
-  const int row = threadIdx.x, c0 = blockIdx.y * 8;
-  const int n = (2 * pr + t) * 128 + row, m0 = mt * BN;
-  float acc[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+  // thread -> (column c, weight tile t, 4 consecutive rows): float4 partial loads
+  const int t = (threadIdx.x >> 5) & 1, row4 = (threadIdx.x & 31) * 4;
+  if (2 * pr + t >= n_rt) return;
+  const int c = blockIdx.y * 4 + (threadIdx.x >> 6);
+  const int n = (2 * pr + t) * 128 + row4, m = mt * BN + c;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int cb = cf; cb <= cl; cb += 4) {
-    float v[4][8];
+    float4 v[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int cc = cb + q;
       if (cc <= cl) {
         const int sl = 2 * cc + ((cc == cf && !cf_first) ? 1 : 0);
-        const float* src = a.ws + (int64_t)sl * (2 * BN * 128) + (t * BN + c0) * 128 + row;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) v[q][j] = __ldcg(src + j * 128);
+        v[q] = __ldcg(reinterpret_cast<const float4*>(a.ws + (int64_t)sl * (2 * BN * 128) + (t * BN + c) * 128 + row4));
       }
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-      if (cb + q <= cl)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] += v[q][j];
+      if (cb + q <= cl) { acc.x += v[q].x; acc.y += v[q].y; acc.z += v[q].z; acc.w += v[q].w; }
   }
-#pragma unroll
-  for (int j = 0; j < 8; ++j) epi_store(a.epi, m0 + c0 + j, n, acc[j]);
+  epi_store(a.epi, m, n, acc.x);
+  epi_store(a.epi, m, n + 1, acc.y);
+  epi_store(a.epi, m, n + 2, acc.z);
+  epi_store(a.epi, m, n + 3, acc.w);
 }
 
 // ---------------------------------------------------------------------------------
@@ -1096,8 +1093,8 @@ static int run_tm(const LinearArgs& a, cudaStream_t st) {
       dim3 rg((unsigned)(G - 1), BN / 8);
       launch_pdl(ws_reduce_kernel<BN>, rg, dim3(256), 0, st, a, n_rt, m_tiles, G, KBU, dbg);
     } else {
-      dim3 rg((unsigned)tiles, BN / 8, 2);
-      launch_pdl(ws_reduce2_kernel<BN>, rg, dim3(128), 0, st, a, n_rt, m_tiles, G, KBU);
+      dim3 rg((unsigned)tiles, BN / 4);   // (tile, 4 columns) x (2 weight tiles x 32 row quads)
+      launch_pdl(ws_reduce2_kernel<BN>, rg, dim3(256), 0, st, a, n_rt, m_tiles, G, KBU);
     }
   }
   return G > 1 ? 2 : 1;
