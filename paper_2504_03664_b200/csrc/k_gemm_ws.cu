@@ -1147,10 +1147,10 @@ template <int BN, int TILES, int NACC, int EPW, int KBU = 1>
 struct TpCfg {
   static constexpr int RAW_T = (int)kInt4BlockBytes;
   static constexpr int RAW = TILES * RAW_T * KBU;
-  static constexpr int NR = 12 / KBU;
+  static constexpr int NR = KBU == 1 ? 12 : 4;
   static constexpr int X_KB = BN * 128;                  // x of one k-block
   static constexpr int X_ST = KBU * X_KB;                // x stage
-  static constexpr int NX_MAX = (200 * 1024 - NR * RAW) / X_ST;
+  static constexpr int NX_MAX = ((KBU == 1 ? 200 : 210) * 1024 - NR * RAW) / X_ST;
   static constexpr int NX = NX_MAX > 8 ? 8 : NX_MAX;
   static constexpr int ACC_COLS = NACC * TILES * BN;
   static constexpr int A_COLS = TILES * 32 * KBU;
@@ -1454,6 +1454,8 @@ int launch_linear_tp(const LinearArgs& a, cudaStream_t st) {
     case 7: return (a.K / 64) % 2 ? run_tp<256, 1, 1, 8>(a, st) : run_tp<256, 1, 1, 8, 2>(a, st);   // 2-k-block units
     case 8: return (a.K / 64) % 2 ? run_tp<192, 1, 2, 8>(a, st) : run_tp<192, 1, 2, 8, 2>(a, st);
     case 9: return (a.K / 64) % 2 ? run_tp<128, 1, 2, 8>(a, st) : run_tp<128, 1, 2, 8, 2>(a, st);
+    case 10: return (a.K / 64) % 2 ? run_tp<224, 1, 2, 8>(a, st) : run_tp<224, 1, 1, 8, 2>(a, st);
+    case 11: return (a.K / 64) % 2 ? run_tp<192, 1, 2, 8>(a, st) : run_tp<192, 1, 1, 8, 2>(a, st);
     default: return run_tp<256, 1, 1, 8>(a, st);
   }
 }

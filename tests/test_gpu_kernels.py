@@ -103,7 +103,7 @@ def test_linear_tm_configs(env, cfg, M, N, K, monkeypatch):
     assert np.array_equal(y, pipo.pipo_linear(pl.ctx, 1, pipo.PATH_TM, x, w, bias))
 
 
-TP_CFGS = ["0", "1", "2", "3", "4", "5", "6", "7", "8", "9"]   # PIPO_TP_CFG: prefill tile configurations (k_gemm_ws.cu)
+TP_CFGS = ["0", "1", "2", "3", "4", "5", "6", "7", "8", "9", "10", "11"]   # PIPO_TP_CFG: prefill tile configurations (k_gemm_ws.cu)
 
 
 @pytest.mark.parametrize("cfg", TP_CFGS)
