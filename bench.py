@@ -366,7 +366,7 @@ def run_pipo(args):
 
     # Uninstrumented pass (same K steps, no timeline / per-kernel events): CUDA timing
     # events on the compute stream wait behind the copy engine (~25 us each, DESIGN.md
-    # §11), which costs the small configs a few % of throughput; reported alongside.
+    # §12), which costs the small configs a few % of throughput; reported alongside.
     uninstr = None
     if rank == 0 or world > 1:
         pipo.pipo_set_flags(pl.ctx, 0)
@@ -418,7 +418,7 @@ def run_pipo(args):
                     "tflops_frac_of_fp16_peak": kd["flops"] / kd["units"] / per_unit_s / 1e12 / tc,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy), bf16_tflops_sustained (fp16 same rate)",
                     "note": ("host/disk tier: CUDA timing events on the compute stream wait ~25 us behind the copy "
-                             "engine's in-flight H2D command (DESIGN.md §11), so the event bracket over-counts; "
+                             "engine's in-flight H2D command (DESIGN.md §12), so the event bracket over-counts; "
                              "roofline_cupti has the kernel-only time") if c["weight_tier"] != 0 else None}
     line = None
     if rank == 0:

@@ -196,7 +196,7 @@ pipo_status pipeline_stats_reset(pipo_ctx* ctx);
 
 /* Change the PIPO_F_* instrumentation flags between calls (synchronises the device).
  * Timing events on the compute stream are not free while the copy engine streams
- * (~25 us each, DESIGN.md §11): PIPO_F_TIMELINE / PIPO_F_KPROF off gives the
+ * (~25 us each, DESIGN.md §12): PIPO_F_TIMELINE / PIPO_F_KPROF off gives the
  * uninstrumented step. */
 pipo_status pipo_set_flags(pipo_ctx* ctx, uint32_t flags);
 
