@@ -1081,14 +1081,14 @@ static int run_tm(const LinearArgs& a, cudaStream_t st) {
   // 22 us) — clock64 stamps put ~30k cycles in the finisher's final-output stores at the
   // kernel tail (partial spin ~3k, bulk copy ~1.2k), so the separate reduce stays default.
   // The in-kernel fixup spins on other CTAs: it needs G <= #SMs, one CTA per SM.
-  static const int fix_env = getenv("PIPO_TM_FIXUP") ? atoi(getenv("PIPO_TM_FIXUP")) : 0;
+  const int fix_env = getenv("PIPO_TM_FIXUP") ? atoi(getenv("PIPO_TM_FIXUP")) : 0;   // read per launch (A/B tests)
   const int64_t tiles = (int64_t)n_pairs * m_tiles;
   const int fix = fix_env && G > 1 && G <= a.num_sms && tiles <= a.n_counters && !(dbg & 64) ? 1 : 0;
   launch_pdl(gemm_tm_kernel<BN, KBU, NACC, UW>, dim3(G), dim3(C::THREADS), C::SMEM, st, map, a, n_rt, m_tiles, G, dbg,
              fix);
   if ((dbg & 64) || fix) return 1;   // debug: main kernel only / fixup done in-kernel
   if (G > 1) {
-    static const int red_v = getenv("PIPO_REDUCE") ? atoi(getenv("PIPO_REDUCE")) : 2;   // 1 = the v1 reduce
+    const int red_v = getenv("PIPO_REDUCE") ? atoi(getenv("PIPO_REDUCE")) : 2;   // 1 = the v1 reduce
     if (red_v == 1 || (dbg & 128)) {
       dim3 rg((unsigned)(G - 1), BN / 8);
       launch_pdl(ws_reduce_kernel<BN>, rg, dim3(256), 0, st, a, n_rt, m_tiles, G, KBU, dbg);

@@ -103,6 +103,21 @@ def test_linear_tm_configs(env, cfg, M, N, K, monkeypatch):
     assert np.array_equal(y, pipo.pipo_linear(pl.ctx, 1, pipo.PATH_TM, x, w, bias))
 
 
+@pytest.mark.parametrize("M,N,K", [(64, 2304, 7168), (40, 200, 1024), (16, 1024, 8192)])
+@pytest.mark.parametrize("knob,val", [("PIPO_TM_FIXUP", "1"), ("PIPO_REDUCE", "1")])
+def test_linear_tm_fixup_variants_bit_identical(env, M, N, K, knob, val, monkeypatch):
+    """The stream-K fixup variants (in-kernel finisher; v1 reduce kernel) sum the same
+    partials in the same k order as the default reduce: bit-identical outputs."""
+    pipo, pl = env
+    rng = np.random.default_rng(M + N + K + len(knob))
+    x = rng.standard_normal((M, K)).astype(np.float16)
+    w = (rng.standard_normal((N, K)) * 0.02).astype(np.float16).astype(np.float32)
+    bias = (rng.uniform(-0.02, 0.02, N)).astype(np.float32)
+    base = pipo.pipo_linear(pl.ctx, 1, pipo.PATH_TM, x, w, bias)
+    monkeypatch.setenv(knob, val)
+    assert np.array_equal(base, pipo.pipo_linear(pl.ctx, 1, pipo.PATH_TM, x, w, bias))
+
+
 TP_CFGS = ["0", "1", "2", "3", "4", "5", "6", "7", "8", "9", "10", "11"]   # PIPO_TP_CFG: prefill tile configurations (k_gemm_ws.cu)
 
 
