@@ -307,6 +307,13 @@ def run_pipo(args):
     # batch shard: rank r owns sequences [r*b, (r+1)*b) of the global prompt batch
     lo, hi = shard_range(b * world, world, rank)
     prompt = synth.prompts(b * world, P, s.vocab)[lo:hi]
+    # TTFT: the first prefill of a fresh process also pays CUDA's lazy module loading
+    # for every kernel it touches; the warm prefill (a second one, new batch) is the
+    # serving number (the paper's latency table)
+    t0 = time.perf_counter()
+    nxt, _ = pl.prefill(prompt)
+    t_prefill_cold = time.perf_counter() - t0
+    pl.stats_reset()
     t0 = time.perf_counter()
     nxt, _ = pl.prefill(prompt)
     t_prefill = time.perf_counter() - t0
@@ -450,7 +457,8 @@ def run_pipo(args):
                               "frac": link_floor_s / (ms / 1e3), "copy_engine_gbs": st["h2d_gbs"]},
             "busy": {"union": st["union_busy"], "copy": st["copy_busy"], "kernel": st["kernel_busy"]},
             "prefill_kernels": prefill_kernels,
-            "setup": {"load_s": t_load, "prefill_s": t_prefill, "hbm_bytes": st["hbm_bytes"],
+            "setup": {"load_s": t_load, "prefill_s": t_prefill, "prefill_cold_s": t_prefill_cold,
+                      "hbm_bytes": st["hbm_bytes"],
                       "pinned_host_bytes": st["pinned_host_bytes"]},
             "peaks": {"hbm_gbs": peaks.get("hbm_gbs"), "bf16_tflops": peaks.get("bf16_tflops")},
         }
