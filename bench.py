@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--weight-tier", default=None, choices=["device", "host", "disk"],
                     help="override the config's weight tier (device = no streaming: isolates H2D interference)")
     ap.add_argument("--chunk-mb", type=float, default=0)
+    ap.add_argument("--prompt", type=int, default=0, help="override the config's prompt length P")
+    ap.add_argument("--batch", type=int, default=0, help="override the config's per-GPU batch b")
     ap.add_argument("--shard-stream", action="store_true",
                     help="NEXT-1: each rank streams 1/N of every layer over its host link and all-gathers the "
                          "rest over NVLink (NCCL); compute stays batch-sharded (host weight tier only)")
@@ -272,6 +274,10 @@ def run_pipo(args):
     torch.cuda.set_device(local)
     c = CONFIGS[args.config]
     s, b, P, G = c["shape"], c["b"], c["P"], c["G"]
+    if args.prompt:
+        P = args.prompt   # context-length sweeps (the paper's latency table)
+    if args.batch:
+        b = args.batch
     steps_needed = args.warmup + args.steps * (2 if args.no_e2e else 3) + (0 if args.no_cupti else 2)
     max_seq = P + max(G, steps_needed + 1)
     if args.weight_tier:
