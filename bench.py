@@ -64,6 +64,7 @@ def parse():
                     help="override the config's weight tier (device = no streaming: isolates H2D interference)")
     ap.add_argument("--chunk-mb", type=float, default=0)
     ap.add_argument("--prompt", type=int, default=0, help="override the config's prompt length P")
+    ap.add_argument("--kv-tier", default=None, choices=["device", "host"], help="override the config's KV tier")
     ap.add_argument("--batch", type=int, default=0, help="override the config's per-GPU batch b")
     ap.add_argument("--shard-stream", action="store_true",
                     help="NEXT-1: each rank streams 1/N of every layer over its host link and all-gathers the "
@@ -282,6 +283,8 @@ def run_pipo(args):
     max_seq = P + max(G, steps_needed + 1)
     if args.weight_tier:
         c = {**c, "weight_tier": ["device", "host", "disk"].index(args.weight_tier)}
+    if args.kv_tier:
+        c = {**c, "kv_tier": ["device", "host"].index(args.kv_tier)}
     disk_dir = f"{args.disk_dir}/rank{rank}" if c["weight_tier"] == 2 else None
     if disk_dir:
         os.makedirs(disk_dir, exist_ok=True)
