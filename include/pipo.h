@@ -87,7 +87,8 @@ typedef struct {
                             efficient (one layer resident). 0 -> 2    */
   int64_t chunk_bytes;   /* blockwise-transfer chunk; 0 -> whole segment */
   int32_t gemv_max_m;    /* rows M <= this use the CUDA-core int4 GEMV (PAPER.md:360
-                            "batch sizes less than 16"); larger M the tensor-core GEMM.
+                            "batch sizes less than 16") for matrices below 8 M weights;
+                            larger M or matrices the tensor-core GEMM (measured faster).
                             0 -> 15                                                  */
   int32_t disk_threads;  /* DISK tier reader threads; 0 -> 4        */
   const char* disk_dir;  /* DISK tier directory (copied at init)                      */

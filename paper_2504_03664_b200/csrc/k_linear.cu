@@ -327,13 +327,18 @@ int launch_linear(const LinearArgs& a, int path, int gemv_max_m, cudaStream_t st
   if (a.M <= 0 || a.N <= 0 || a.K <= 0 || a.K % 64 != 0) return -1;
   bool gemv = false;
   if (path == PATH_GEMV) gemv = true;
-  else if (path == PATH_AUTO) gemv = (a.wfmt == 1 && a.M <= gemv_max_m);
+  // M <= gemv_max_m: the CUDA-core GEMV ("batch sizes less than 16") — but
+  // only for small matrices: from 8 M weights up the tcgen05 stream-K kernel (BN = 16, rows
+  // >= M zero-filled by TMA) streams 1.5-2.6x faster even at M = 1 (c7: FC1 72 -> 27 us,
+  // profiles/r01/gemv_crossover; reading Q4 "re-tune the crossover by measurement")
+  else if (path == PATH_AUTO) gemv = (a.wfmt == 1 && a.M <= gemv_max_m && (int64_t)a.N * a.K < (8ll << 20));
   if (path == PATH_TP || (path == PATH_AUTO && !gemv && a.wfmt == 1 && a.M > 128)) return launch_linear_tp(a, st);
   if (path == PATH_TM || (path == PATH_AUTO && !gemv && a.wfmt == 1 && a.M <= 64)) return launch_linear_tm(a, st);
   if (path == PATH_WS || (path == PATH_AUTO && !gemv && a.wfmt == 1 && a.M <= 128)) return launch_linear_ws(a, st);
   if (path == PATH_TC || (path == PATH_AUTO && !gemv)) return launch_linear_tc(a, st);
   if (gemv) {
     if (a.wfmt != 1 || a.M > 16) return -1;
+    if (a.M == 1) return run_gemv<1>(a, st);
     if (a.M <= 4) return run_gemv<4>(a, st);
     if (a.M <= 8) return run_gemv<8>(a, st);
     return run_gemv<16>(a, st);
