@@ -1,6 +1,6 @@
 #!/bin/bash
 # Full sweep of every config with the current code + the c5 ncu evidence.
-O=gpurun_out/${TAG:-sweep3}; mkdir -p $O
+O=gpurun_out/${TAG:-sweep4}; mkdir -p $O
 for c in c5 c2 c1 c3 c6 c7; do
   timeout 1200 python bench.py --config $c --steps 10 --warmup 3 > $O/bench_$c.json 2> $O/bench_$c.err
 done
