@@ -397,7 +397,9 @@ def run_pipo(args):
         pipo.pipo_set_flags(pl.ctx, pipo.PIPO_F_TIMELINE | pipo.PIPO_F_KPROF)
         un_ms = t_un / args.steps * 1e3
         uninstr = {"value": aggregate_throughput(b, world, args.steps, t_un), "ms_per_step": un_ms,
-                   "link_frac": None, "note": "same K steps with PIPO_F_TIMELINE / PIPO_F_KPROF off (run after the timed and e2e passes, i.e. at later KV positions: host-KV configs move more bytes)"}
+                   "link_frac": None,
+                   "note": ("same K steps with PIPO_F_TIMELINE / PIPO_F_KPROF off (run after the timed and e2e "
+                            "passes, i.e. at later KV positions: host-KV configs move more bytes)")}
 
     # CUPTI (torch.profiler) view of 2 extra untimed steps: true per-kernel GPU durations
     # with the copy stream running (context for the event-bracketed roofline above)
