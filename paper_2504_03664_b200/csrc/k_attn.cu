@@ -159,34 +159,46 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnArgs a, int n_spli
 // runs its own online softmax over an interleaved subset of positions, 4 positions per
 // step (8 x 16-B loads in flight per lane); the NV = 4*RPW virtual warps of the CTA are
 // merged in fixed order, splits in a second kernel (deterministic).
-template <int HD>
+template <int HD, int G>
 __global__ void __launch_bounds__(128) attn_decode_v2_kernel(AttnArgs a, int n_splits, int pos_per_split) {
+  // G > 1 (GQA): as in attn_decode_kernel, one CTA per (KV head, b, split) serves the G
+  // query heads sharing the KV head; the lane-group layout needs log2(HD/8) shuffle steps
+  // per (head, position) instead of 5, which is what GQA's G-fold dot products need
   constexpr int LPR = HD / 8, RPW = 32 / LPR, NV = 4 * RPW;
-  __shared__ float sm_m[NV], sm_l[NV];
-  __shared__ float sm_acc[NV][HD];
-  const int head = blockIdx.x, bi = blockIdx.y, split = blockIdx.z;
+  __shared__ float sm_m[G][NV], sm_l[G][NV];
+  __shared__ float sm_acc[G][NV][HD];
+  pdl_wait();
+  const int bi = blockIdx.y, split = blockIdx.z;
+  const int head0 = G == 1 ? blockIdx.x : blockIdx.x * G;
+  const int kvh = G == 1 ? blockIdx.x / a.group : blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int sub = lane / LPR, sl = lane % LPR;            // row slot within the warp, lane within row
   const int vw = warp * RPW + sub;                          // virtual warp id 0..NV-1
   const int L = a.past + 1;
   const int lo = split * pos_per_split, hi = min(L, lo + pos_per_split);
-  float q[8];
-  {
-    const uint4 qr = *reinterpret_cast<const uint4*>(a.q + (int64_t)bi * a.d + head * HD + sl * 8);
+  float q[G][8];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const uint4 qr = *reinterpret_cast<const uint4*>(a.q + (int64_t)bi * a.d + (head0 + g) * HD + sl * 8);
     const __half2* qh = reinterpret_cast<const __half2*>(&qr);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const float2 f = __half22float2(qh[e]);
-      q[2 * e] = f.x * kLog2e;
-      q[2 * e + 1] = f.y * kLog2e;
+      q[g][2 * e] = f.x * kLog2e;
+      q[g][2 * e + 1] = f.y * kLog2e;
     }
   }
   const int64_t pstride = kv_pstride(a);
-  const __half* kbase = a.kc + (int64_t)bi * kv_bstride(a) + (head / a.group) * HD + sl * 8;
-  const __half* vbase = a.vc + (int64_t)bi * kv_bstride(a) + (head / a.group) * HD + sl * 8;
-  float m_run = -INFINITY, l_run = 0.f, acc[8];
+  const __half* kbase = a.kc + (int64_t)bi * kv_bstride(a) + kvh * HD + sl * 8;
+  const __half* vbase = a.vc + (int64_t)bi * kv_bstride(a) + kvh * HD + sl * 8;
+  float m_run[G], l_run[G], acc[G][8];
 #pragma unroll
-  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+  for (int g = 0; g < G; ++g) {
+    m_run[g] = -INFINITY;
+    l_run[g] = 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[g][e] = 0.f;
+  }
   constexpr int U = 4;
   // the trip count must be warp-uniform (full-mask shuffles): loop on the warp's first
   // position, each lane group masks its own positions past `hi`
@@ -199,62 +211,75 @@ __global__ void __launch_bounds__(128) attn_decode_v2_kernel(AttnArgs a, int n_s
       kr[u] = ld_nc_v4(kbase + p * pstride);
       vr[u] = ld_nc_v4(vbase + p * pstride);
     }
-    float s[U];
+    float s[G][U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const __half2* kh = reinterpret_cast<const __half2*>(&kr[u]);
-      float t = 0.f;
+      float2 kf[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 f = __half22float2(kh[e]);
-        t = fmaf(q[2 * e], f.x, t);
-        t = fmaf(q[2 * e + 1], f.y, t);
+      for (int e = 0; e < 4; ++e) kf[e] = __half22float2(kh[e]);
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        float t = 0.f;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          t = fmaf(q[g][2 * e], kf[e].x, t);
+          t = fmaf(q[g][2 * e + 1], kf[e].y, t);
+        }
+        s[g][u] = t;
       }
-      s[u] = t;
     }
 #pragma unroll
     for (int o = LPR / 2; o > 0; o >>= 1)
 #pragma unroll
-      for (int u = 0; u < U; ++u) s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
-    float mx = m_run;
+      for (int g = 0; g < G; ++g)
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (p0 + u >= hi) s[u] = -INFINITY;
-      mx = fmaxf(mx, s[u]);
-    }
-    const float corr = mx == -INFINITY ? 1.f : exp2f(m_run - mx);   // group may have no live position yet
-    l_run *= corr;
+        for (int u = 0; u < U; ++u) s[g][u] += __shfl_xor_sync(0xffffffffu, s[g][u], o);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] *= corr;
+    for (int g = 0; g < G; ++g) {
+      float mx = m_run[g];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const float pu = s[u] == -INFINITY ? 0.f : exp2f(s[u] - mx);
-      l_run += pu;
-      const __half2* vh = reinterpret_cast<const __half2*>(&vr[u]);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 f = __half22float2(vh[e]);
-        acc[2 * e] = fmaf(pu, f.x, acc[2 * e]);
-        acc[2 * e + 1] = fmaf(pu, f.y, acc[2 * e + 1]);
+      for (int u = 0; u < U; ++u) {
+        if (p0 + u >= hi) s[g][u] = -INFINITY;
+        mx = fmaxf(mx, s[g][u]);
       }
-    }
-    m_run = mx;
-  }
-  if (sl == 0) { sm_m[vw] = m_run; sm_l[vw] = l_run; }
+      const float corr = mx == -INFINITY ? 1.f : exp2f(m_run[g] - mx);   // group may have no live position yet
+      l_run[g] *= corr;
 #pragma unroll
-  for (int e = 0; e < 8; ++e) sm_acc[vw][sl * 8 + e] = acc[e];
+      for (int e = 0; e < 8; ++e) acc[g][e] *= corr;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float pu = s[g][u] == -INFINITY ? 0.f : exp2f(s[g][u] - mx);
+        l_run[g] += pu;
+        const __half2* vh = reinterpret_cast<const __half2*>(&vr[u]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __half22float2(vh[e]);
+          acc[g][2 * e] = fmaf(pu, f.x, acc[g][2 * e]);
+          acc[g][2 * e + 1] = fmaf(pu, f.y, acc[g][2 * e + 1]);
+        }
+      }
+      m_run[g] = mx;
+    }
+  }
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    if (sl == 0) { sm_m[g][vw] = m_run[g]; sm_l[g][vw] = l_run[g]; }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) sm_acc[g][vw][sl * 8 + e] = acc[g][e];
+  }
   __syncthreads();
-  if (threadIdx.x < HD) {
-    const int t = threadIdx.x;
+  for (int i = threadIdx.x; i < G * HD; i += 128) {
+    const int g = i / HD, t = i - g * HD, head = head0 + g;
     float M = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < NV; ++w) M = fmaxf(M, sm_m[w]);
+    for (int w = 0; w < NV; ++w) M = fmaxf(M, sm_m[g][w]);
     float l = 0.f, o = 0.f;
 #pragma unroll
     for (int w = 0; w < NV; ++w) {
-      const float f = sm_m[w] == -INFINITY ? 0.f : exp2f(sm_m[w] - M);
-      l += sm_l[w] * f;
-      o += sm_acc[w][t] * f;
+      const float f = sm_m[g][w] == -INFINITY ? 0.f : exp2f(sm_m[g][w] - M);
+      l += sm_l[g][w] * f;
+      o += sm_acc[g][w][t] * f;
     }
     if (n_splits == 1) {
       a.o[(int64_t)bi * a.d + head * HD + t] = __float2half_rn(o / l);
@@ -720,8 +745,13 @@ int launch_attention_decode(const AttnArgs& a, cudaStream_t st) {
   const int hd = a.d / a.n_heads;
   if (hd != 64 && hd != 128) return -1;
   const int L = a.past + 1;
-  // GQA: one CTA per KV head serves its whole query-head group (group sizes 2, 4, 8)
-  const int G = (a.group == 2 || a.group == 4 || a.group == 8) && !a.use_cuda_cores ? a.group : 1;
+  // GQA: one CTA per KV head serves its whole query-head group (group sizes 2, 4, 8).
+  // The lane-group kernel (v2, variant 1 / PIPO_ATTN_V2=1) is 16 % faster on c6's GQA
+  // attention (fewer shuffles per head) but the c6 step measured the same (the following
+  // linears timed slower; profiles/r01/gqa_v2), so the one-row-per-warp kernel stays default
+  const int G = (a.group == 2 || a.group == 4 || a.group == 8) ? a.group : 1;
+  const char* v2e = getenv("PIPO_ATTN_V2");
+  const bool v2 = a.use_cuda_cores || (v2e ? atoi(v2e) != 0 : false);
   const int pairs = a.b * a.n_heads / G;
   // enough CTAs for ~8 waves of resident blocks (9 per SM): the block scheduler then
   // balances the tail to within ~1/8 of the kernel; splits merge in a second kernel
@@ -737,7 +767,7 @@ int launch_attention_decode(const AttnArgs& a, cudaStream_t st) {
   n_splits = (L + per - 1) / per;
   if (n_splits > 1 && (int64_t)a.b * a.n_heads * n_splits * (hd + 2) > a.ws_floats) return -1;
   dim3 grid(a.n_heads / G, a.b, n_splits);
-  if (!a.use_cuda_cores) {   // one K/V row per warp: measured 0-5% ahead of v2 at c3-c5
+  if (!v2) {   // one K/V row per warp: measured 0-5% ahead of v2 at c3-c5 (MHA)
 #define PIPO_DECODE(HDV, GV) launch_pdl_k(attn_decode_kernel<HDV, GV>, grid, dim3(128), 0, st, a, n_splits, per)
     if (hd == 64) {
       if (G == 1) PIPO_DECODE(64, 1); else if (G == 2) PIPO_DECODE(64, 2); else if (G == 4) PIPO_DECODE(64, 4);
@@ -747,9 +777,16 @@ int launch_attention_decode(const AttnArgs& a, cudaStream_t st) {
       else PIPO_DECODE(128, 8);
     }
 #undef PIPO_DECODE
-  } else {                   // v2: lane groups with 16-B row loads (kept for A/B)
-    if (hd == 64) attn_decode_v2_kernel<64><<<grid, 128, 0, st>>>(a, n_splits, per);
-    else attn_decode_v2_kernel<128><<<grid, 128, 0, st>>>(a, n_splits, per);
+  } else {     // v2: lane groups with 16-B row loads
+#define PIPO_DECODE2(HDV, GV) launch_pdl_k(attn_decode_v2_kernel<HDV, GV>, grid, dim3(128), 0, st, a, n_splits, per)
+    if (hd == 64) {
+      if (G == 1) PIPO_DECODE2(64, 1); else if (G == 2) PIPO_DECODE2(64, 2); else if (G == 4) PIPO_DECODE2(64, 4);
+      else PIPO_DECODE2(64, 8);
+    } else {
+      if (G == 1) PIPO_DECODE2(128, 1); else if (G == 2) PIPO_DECODE2(128, 2); else if (G == 4) PIPO_DECODE2(128, 4);
+      else PIPO_DECODE2(128, 8);
+    }
+#undef PIPO_DECODE2
   }
   if (n_splits == 1) return 1;
   dim3 g2(a.n_heads, a.b);
