@@ -56,10 +56,12 @@ def test_rope_kernel_vs_oracle():
     assert np.array_equal(ko[:past], k[:past].astype(np.float32))      # older positions untouched
 
 
+@pytest.mark.parametrize("v2", ["0", "1"])
 @pytest.mark.parametrize("hd,H,Hkv,n,past", [(64, 8, 2, 1, 37), (128, 8, 4, 1, 300), (64, 8, 1, 1, 0),
-                                             (64, 8, 2, 70, 0), (128, 4, 2, 33, 12)])
-def test_gqa_attention_vs_oracle(hd, H, Hkv, n, past):
+                                             (64, 8, 2, 70, 0), (128, 4, 2, 33, 12), (128, 16, 2, 1, 100)])
+def test_gqa_attention_vs_oracle(hd, H, Hkv, n, past, v2, monkeypatch):
     pipo = pipo_mod()
+    monkeypatch.setenv("PIPO_ATTN_V2", v2)   # decode: one-row-per-warp (0) or lane-group (1) kernel
     rng = np.random.default_rng(hd + H + n + past)
     b = 3
     q = (rng.standard_normal((b, n, H * hd)) * hd ** -0.5).astype(np.float16)
