@@ -43,6 +43,9 @@ CONFIGS = {
     # NEXT-4: the paper's LLaMA3.1 family (§4.1)
     "c6": dict(shape=synth.LLAMA31_8B, b=64, P=512, G=32, weight_tier=1, kv_tier=0,
                desc="NEXT-4: LLaMA3.1-8B streamed int4 weights (GQA 32/8, SwiGLU 14336, RoPE llama3), b=64, P=512, gen 32"),
+    "c8": dict(shape=synth.LLAMA32_1B, b=1, P=512, G=32, weight_tier=1, kv_tier=0,
+               desc="NEXT-4: LLaMA3.2-1B streamed int4 weights, b=1, P=512, gen 32 (the paper's offloading-overhead "
+                    "table PAPER.md:727-742)"),
     "c7": dict(shape=synth.LLAMA31_8B, b=1, P=512, G=32, weight_tier=1, kv_tier=0,
                desc="NEXT-4: LLaMA3.1-8B streamed int4 weights, b=1, context 512, gen 32 (the paper's latency "
                     "table PAPER.md:697-713: TTFT + per-token decode latency)"),

@@ -234,6 +234,9 @@ class LlamaShape:
 
 
 LLAMA31_8B = LlamaShape(4096, 32, 32, 8, 14336)
+# [ext] Llama-3.2-1B config: rope factor 32 (the paper's offloading-overhead table, PAPER.md:727-742;
+# its tied LM head is drawn here as a separate tensor — throughput is unaffected)
+LLAMA32_1B = LlamaShape(2048, 16, 32, 8, 8192, rope_factor=32.0)
 
 
 def llama_layer_tensor_specs(s: LlamaShape):
