@@ -451,10 +451,11 @@ __global__ void __launch_bounds__(256) ws_reduce_kernel(LinearArgs a, int n_rt, 
 // the tiles that exist (no early-exit blocks for CTA boundaries, no shared-memory
 // broadcast), one resident wave.  Same operands and order as ws_reduce_kernel
 // (0 + p_cf + p_cf+1 + ... in CTA order), so the two are bit-identical.
-template <int BN>
-__global__ void __launch_bounds__(256) ws_reduce2_kernel(LinearArgs a, int n_rt, int m_tiles, int G, int kbu) {
+template <int BN, int CPT>
+__global__ void __launch_bounds__(256) ws_reduce2_kernel(LinearArgs a, int n_rt, int m_tiles, int G, int kbu,
+                                                          int late) {
   ws::griddep_wait();
-  ws::griddep_launch();
+  if (!late) ws::griddep_launch();   // late: no early trigger (implicit at block exit)
   const int n_ku = a.K / 64 / kbu, n_pairs = (n_rt + 1) >> 1;
   const int64_t U = (int64_t)n_pairs * m_tiles * n_ku;
   const int64_t tile = blockIdx.x;
@@ -462,30 +463,45 @@ __global__ void __launch_bounds__(256) ws_reduce2_kernel(LinearArgs a, int n_rt,
   const int cf = ws::cta_of_unit(tile * n_ku, U, G), cl = ws::cta_of_unit((tile + 1) * n_ku - 1, U, G);
   if (cf == cl) return;                                   // owned whole: stored by the GEMM
   const bool cf_first = ws::u_begin(cf, U, G) / n_ku == tile;
-  // thread -> (column c, weight tile t, 4 consecutive rows): float4 partial loads
+  // thread -> (CPT columns c, weight tile t, 4 consecutive rows): float4 partial loads.
+  // CPT > 1 puts CPT columns' loads in flight per thread and shrinks the grid to one
+  // resident wave for the wide matrices (c5 QKV / FC1: 1344 / 1792 blocks at CPT = 1).
   const int t = (threadIdx.x >> 5) & 1, row4 = (threadIdx.x & 31) * 4;
   if (2 * pr + t >= n_rt) return;
-  const int c = blockIdx.y * 4 + (threadIdx.x >> 6);
-  const int n = (2 * pr + t) * 128 + row4, m = mt * BN + c;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int n = (2 * pr + t) * 128 + row4;
+  float4 acc[CPT];
+#pragma unroll
+  for (int i = 0; i < CPT; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int cb = cf; cb <= cl; cb += 4) {
-    float4 v[4];
+    float4 v[4][CPT];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int cc = cb + q;
       if (cc <= cl) {
         const int sl = 2 * cc + ((cc == cf && !cf_first) ? 1 : 0);
-        v[q] = __ldcg(reinterpret_cast<const float4*>(a.ws + (int64_t)sl * (2 * BN * 128) + (t * BN + c) * 128 + row4));
+#pragma unroll
+        for (int i = 0; i < CPT; ++i) {
+          const int c = (blockIdx.y * CPT + i) * 4 + (threadIdx.x >> 6);
+          v[q][i] = __ldcg(reinterpret_cast<const float4*>(a.ws + (int64_t)sl * (2 * BN * 128) + (t * BN + c) * 128 + row4));
+        }
       }
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-      if (cb + q <= cl) { acc.x += v[q].x; acc.y += v[q].y; acc.z += v[q].z; acc.w += v[q].w; }
+      if (cb + q <= cl)
+#pragma unroll
+        for (int i = 0; i < CPT; ++i) {
+          acc[i].x += v[q][i].x; acc[i].y += v[q][i].y; acc[i].z += v[q][i].z; acc[i].w += v[q][i].w;
+        }
   }
-  epi_store(a.epi, m, n, acc.x);
-  epi_store(a.epi, m, n + 1, acc.y);
-  epi_store(a.epi, m, n + 2, acc.z);
-  epi_store(a.epi, m, n + 3, acc.w);
+#pragma unroll
+  for (int i = 0; i < CPT; ++i) {
+    const int m = mt * BN + (blockIdx.y * CPT + i) * 4 + (threadIdx.x >> 6);
+    epi_store(a.epi, m, n, acc[i].x);
+    epi_store(a.epi, m, n + 1, acc[i].y);
+    epi_store(a.epi, m, n + 2, acc[i].z);
+    epi_store(a.epi, m, n + 3, acc[i].w);
+  }
 }
 
 // ---------------------------------------------------------------------------------
@@ -1093,8 +1109,14 @@ static int run_tm(const LinearArgs& a, cudaStream_t st) {
       dim3 rg((unsigned)(G - 1), BN / 8);
       launch_pdl(ws_reduce_kernel<BN>, rg, dim3(256), 0, st, a, n_rt, m_tiles, G, KBU, dbg);
     } else {
-      dim3 rg((unsigned)tiles, BN / 4);   // (tile, 4 columns) x (2 weight tiles x 32 row quads)
-      launch_pdl(ws_reduce2_kernel<BN>, rg, dim3(256), 0, st, a, n_rt, m_tiles, G, KBU);
+      // (tile, 4*CPT columns) x (2 weight tiles x 32 row quads); PIPO_RED_CPT tunes CPT
+      const int cpt_env = getenv("PIPO_RED_CPT") ? atoi(getenv("PIPO_RED_CPT")) : 1;
+      const int cpt = (cpt_env == 2 || cpt_env == 4) && BN / 4 >= cpt_env ? cpt_env : 1;
+      dim3 rg((unsigned)tiles, BN / (4 * cpt));
+      const int late = getenv("PIPO_RED_LATE") ? atoi(getenv("PIPO_RED_LATE")) : 0;
+      if (cpt == 4) launch_pdl(ws_reduce2_kernel<BN, 4>, rg, dim3(256), 0, st, a, n_rt, m_tiles, G, KBU, late);
+      else if (cpt == 2) launch_pdl(ws_reduce2_kernel<BN, 2>, rg, dim3(256), 0, st, a, n_rt, m_tiles, G, KBU, late);
+      else launch_pdl(ws_reduce2_kernel<BN, 1>, rg, dim3(256), 0, st, a, n_rt, m_tiles, G, KBU, late);
     }
   }
   return G > 1 ? 2 : 1;

@@ -104,9 +104,11 @@ def test_linear_tm_configs(env, cfg, M, N, K, monkeypatch):
 
 
 @pytest.mark.parametrize("M,N,K", [(64, 2304, 7168), (40, 200, 1024), (16, 1024, 8192)])
-@pytest.mark.parametrize("knob,val", [("PIPO_TM_FIXUP", "1"), ("PIPO_REDUCE", "1")])
+@pytest.mark.parametrize("knob,val", [("PIPO_TM_FIXUP", "1"), ("PIPO_REDUCE", "1"), ("PIPO_RED_CPT", "2"),
+                                      ("PIPO_RED_CPT", "4")])
 def test_linear_tm_fixup_variants_bit_identical(env, M, N, K, knob, val, monkeypatch):
-    """The stream-K fixup variants (in-kernel finisher; v1 reduce kernel) sum the same
+    """The stream-K fixup variants (in-kernel finisher; v1 reduce kernel; reduce with 2 / 4
+    columns per thread) sum the same
     partials in the same k order as the default reduce: bit-identical outputs."""
     pipo, pl = env
     rng = np.random.default_rng(M + N + K + len(knob))

@@ -16,7 +16,8 @@ if os.environ.get("KBENCH_PATHS"):
 cases = [("c5_qkv", 64, 21504, 7168), ("c5_out", 64, 7168, 7168), ("c5_fc1", 64, 28672, 7168),
          ("c5_fc2", 64, 7168, 28672), ("c2_qkv", 16, 6144, 2048), ("c2_fc2", 16, 2048, 8192),
          ("c3_qkv", 32, 12288, 4096), ("pre_c2_qkv", 4096, 6144, 2048), ("c5_head", 64, 50272, 7168),
-         ("c6_head", 64, 128256, 4096), ("c7_qkv", 1, 6144, 4096), ("c7_fc1", 1, 28672, 4096),
+         ("c6_head", 64, 128256, 4096), ("c6_qkv", 64, 6144, 4096), ("c6_fc1", 64, 28672, 4096), ("c6_fc2", 64, 4096, 14336),
+         ("c7_qkv", 1, 6144, 4096), ("c7_fc1", 1, 28672, 4096),
          ("c7_fc2", 1, 4096, 14336), ("c1_fc1", 4, 3072, 768)]
 if len(sys.argv) > 1:
     cases = [c for c in cases if c[0] in sys.argv[1:]]
