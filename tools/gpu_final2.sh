@@ -1,0 +1,7 @@
+#!/bin/bash
+# end-of-session regression: full GPU suite, smoke, default bench (c5) and c6
+O=gpurun_out/${TAG:-final2}; mkdir -p $O
+timeout 1500 python -m pytest tests -m gpu -q > $O/gpu_tests.log 2>&1; echo rc=$? >> $O/gpu_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/smoke.log 2>&1; echo rc=$? >> $O/smoke.log
+timeout 900 python bench.py > $O/bench_c5.json 2> $O/e5
+timeout 600 python bench.py --config c6 --no-cpu-baseline > $O/bench_c6.json 2> $O/e6
