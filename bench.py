@@ -561,11 +561,13 @@ def ncu_traffic(cls, args):
         t = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")))
     except (OSError, ValueError):
         return None
-    want = t.get("applies_to", {})
-    if (want.get("config"), want.get("wfmt"), want.get("kv_fmt")) != (args.config, args.wfmt, args.kv_fmt):
-        return None
-    e = t.get(cls)
-    return None if e is None else e["traffic_bytes_per_unit"]
+    for ent in t.get("entries", [t]):   # one entry per captured workload
+        want = ent.get("applies_to", {})
+        if (want.get("config"), want.get("wfmt"), want.get("kv_fmt")) != (args.config, args.wfmt, args.kv_fmt):
+            continue
+        e = ent.get(cls)
+        return None if e is None else e["traffic_bytes_per_unit"]
+    return None
 
 
 def main():
