@@ -469,6 +469,147 @@ __global__ void __launch_bounds__(128) attn_decode_gqa_mma_kernel(AttnArgs a, in
   }
 }
 
+// Variant 2 with 32-position tiles (PIPO_GQA_TILE=32): q fragments straight from global
+// (rows 8-15 of the m16 tile are always zero since G <= 8), no Q staging, so three K/V
+// stages take 52 KB and 4 CTAs fit per SM (vs 2 with 64-position tiles).  Warp w takes
+// positions 8w .. 8w+7 of each tile: S is one m16n8 tile per k-step pair; P.V uses the
+// k = 0..7 half of m16n8k16 (the other half zero).
+template <int HD, int NS>
+__global__ void __launch_bounds__(128) attn_decode_gqa_mma32_kernel(AttnArgs a, int n_splits, int pos_per_split) {
+  constexpr int KP = HD + 8;
+  constexpr int NT_O = HD / 8;
+  constexpr int CH = HD / 8;
+  constexpr int T = 32;
+  extern __shared__ __align__(16) uint8_t smem_attn[];
+  __half* sK = reinterpret_cast<__half*>(smem_attn);           // [NS][T][KP]
+  __half* sV = sK + NS * T * KP;                               // [NS][T][KP]
+  float* sM = reinterpret_cast<float*>(sV + NS * T * KP);      // [4 warps][8 rows]
+  float* sL = sM + 32;
+  float* sO = reinterpret_cast<float*>(sK);                    // [4][8][HD], reuses sK after the loop
+  static_assert(4 * 8 * HD * 4 <= NS * T * KP * 2, "merge buffer fits in sK");
+  pdl_wait();
+  const int kvh = blockIdx.x, bi = blockIdx.y, split = blockIdx.z;
+  const int G = a.group;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int L = a.past + 1;
+  const int lo = split * pos_per_split, hi = min(L, lo + pos_per_split);
+  const int n_kv = (hi - lo + T - 1) / T;
+  const int64_t pstride = kv_pstride(a), bstride = kv_bstride(a);
+  auto load_kv = [&](int j, int buf) {
+    for (int c = tid; c < T * CH; c += 128) {
+      const int r = c / CH, ch = c % CH, p = lo + j * T + r;
+      const int64_t off = (int64_t)min(p, hi - 1) * pstride + (int64_t)bi * bstride + kvh * HD + ch * 8;
+      const int bytes = p < hi ? 16 : 0;
+      cp_async16(sK + (buf * T + r) * KP + ch * 8, a.kc + off, bytes);
+      cp_async16(sV + (buf * T + r) * KP + ch * 8, a.vc + off, bytes);
+    }
+  };
+#pragma unroll
+  for (int st = 0; st < NS - 1; ++st) {
+    if (st < n_kv) load_kv(st, st);
+    cp_async_commit();
+  }
+  // A fragments of q: row g (query head kvh*G + g) when g < G, rows 8-15 zero
+  uint32_t qf[HD / 16][2];
+  {
+    const __half* qrow = a.q + (int64_t)bi * a.d + (kvh * G + min(g, G - 1)) * HD;
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk) {
+      qf[kk][0] = g < G ? *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * tq) : 0u;
+      qf[kk][1] = g < G ? *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 8 + 2 * tq) : 0u;
+    }
+  }
+  float o[NT_O][4];
+#pragma unroll
+  for (int i = 0; i < NT_O; ++i)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) o[i][c] = 0.f;
+  float m_r = -INFINITY, l_r = 0.f;   // row g (rows g + 8 are padding)
+  for (int j = 0; j < n_kv; ++j) {
+    const int buf = j % NS;
+    if (j + NS - 1 < n_kv) load_kv(j + NS - 1, (j + NS - 1) % NS);
+    cp_async_commit();
+    cp_async_wait<NS - 1>();
+    __syncthreads();
+    float sc[4] = {0.f, 0.f, 0.f, 0.f};
+    const __half* kb = sK + (buf * T + warp * 8) * KP;
+#pragma unroll
+    for (int kk2 = 0; kk2 < HD / 32; ++kk2) {
+      uint32_t b0, b1, b2, b3;
+      ldmatrix_x4(b0, b1, b2, b3, kb + (lane & 7) * KP + kk2 * 32 + (lane >> 3) * 8);
+      const uint32_t a0[4] = {qf[2 * kk2][0], 0u, qf[2 * kk2][1], 0u};
+      const uint32_t a1[4] = {qf[2 * kk2 + 1][0], 0u, qf[2 * kk2 + 1][1], 0u};
+      mma_16816(sc, a0, b0, b1);
+      mma_16816(sc, a1, b2, b3);
+    }
+    float mx = m_r;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int p = lo + j * T + warp * 8 + 2 * tq + c;
+      sc[c] = p < hi ? sc[c] * kLog2e : -INFINITY;
+      mx = fmaxf(mx, sc[c]);
+    }
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    const float corr = mx == -INFINITY ? 1.f : exp2f(m_r - mx);
+    m_r = mx;
+    l_r *= corr;
+#pragma unroll
+    for (int i = 0; i < NT_O; ++i) { o[i][0] *= corr; o[i][1] *= corr; }
+    const float e0 = mx == -INFINITY ? 0.f : exp2f(sc[0] - mx);
+    const float e1 = mx == -INFINITY ? 0.f : exp2f(sc[1] - mx);
+    l_r += e0 + e1;
+    const __half2 p2 = __floats2half2_rn(e0, e1);
+    const uint32_t pf[4] = {*reinterpret_cast<const uint32_t*>(&p2), 0u, 0u, 0u};
+    const __half* vb = sV + (buf * T + warp * 8) * KP;
+#pragma unroll
+    for (int nt4 = 0; nt4 < HD / 32; ++nt4) {
+      uint32_t b0, b1, b2, b3;
+      const __half* ptr = vb + (lane & 7) * KP + nt4 * 32 + (lane >> 3) * 8;
+      asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                   : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
+                   : "r"(smem_u32(ptr)));
+      mma_16816(o[4 * nt4 + 0], pf, b0, 0u);
+      mma_16816(o[4 * nt4 + 1], pf, b1, 0u);
+      mma_16816(o[4 * nt4 + 2], pf, b2, 0u);
+      mma_16816(o[4 * nt4 + 3], pf, b3, 0u);
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+  l_r += __shfl_xor_sync(0xffffffffu, l_r, 1);
+  l_r += __shfl_xor_sync(0xffffffffu, l_r, 2);
+  __syncthreads();
+  if (tq == 0) { sM[warp * 8 + g] = m_r; sL[warp * 8 + g] = l_r; }
+#pragma unroll
+  for (int i = 0; i < NT_O; ++i) {
+    sO[(warp * 8 + g) * HD + i * 8 + 2 * tq] = o[i][0];
+    sO[(warp * 8 + g) * HD + i * 8 + 2 * tq + 1] = o[i][1];
+  }
+  __syncthreads();
+  for (int i = tid; i < G * HD; i += 128) {
+    const int r = i / HD, t = i - r * HD, head = kvh * G + r;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, sM[w * 8 + r]);
+    float l = 0.f, ov = 0.f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const float f = sM[w * 8 + r] == -INFINITY ? 0.f : exp2f(sM[w * 8 + r] - M);
+      l += sL[w * 8 + r] * f;
+      ov += sO[(w * 8 + r) * HD + t] * f;
+    }
+    if (n_splits == 1) {
+      a.o[(int64_t)bi * a.d + head * HD + t] = __float2half_rn(ov / l);
+    } else {
+      float* part = a.ws + ((int64_t)(bi * a.n_heads + head) * n_splits + split) * (HD + 2);
+      if (t == 0) { part[0] = M; part[1] = l; }
+      part[2 + t] = ov;
+    }
+  }
+}
+
 template <int HD>
 __global__ void attn_merge_kernel(AttnArgs a, int n_splits) {
   pdl_wait();
@@ -935,10 +1076,27 @@ static int launch_attention_decode_gqa_mma(const AttnArgs& a, int G, cudaStream_
     n_splits = pairs >= target ? 1 : (target + pairs - 1) / pairs;
   }
   n_splits = max(1, min(n_splits, (L + 63) / 64));
-  const int per = ((L + n_splits - 1) / n_splits + 63) / 64 * 64;   // whole 64-position tiles per split
+  // 32-position tiles, 3 stages, 4 CTAs/SM (attn_decode_gqa_mma32_kernel, default: c6
+  // attention 1.35 -> 1.24 ms/step); PIPO_GQA_TILE=64: 64-position tiles, PIPO_GQA_STAGES deep
+  const int tile = getenv("PIPO_GQA_TILE") && atoi(getenv("PIPO_GQA_TILE")) == 64 ? 64 : 32;
+  const int per = ((L + n_splits - 1) / n_splits + tile - 1) / tile * tile;   // whole tiles per split
   n_splits = (L + per - 1) / per;
   if (n_splits > 1 && (int64_t)a.b * a.n_heads * n_splits * (hd + 2) > a.ws_floats) return -1;
   dim3 grid(a.n_heads / G, a.b, n_splits);
+  if (tile == 32) {
+    const int smem32 = 2 * 3 * 32 * (hd + 8) * 2 + 2 * 32 * 4;
+#define PIPO_GQA32(HDV)                                                                                          \
+  do {                                                                                                           \
+    static bool set_ = false;                                                                                    \
+    if (!set_) {                                                                                                 \
+      cudaFuncSetAttribute(attn_decode_gqa_mma32_kernel<HDV, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem32); \
+      set_ = true;                                                                                               \
+    }                                                                                                            \
+    launch_pdl_k(attn_decode_gqa_mma32_kernel<HDV, 3>, grid, dim3(128), smem32, st, a, n_splits, per);           \
+  } while (0)
+    if (hd == 64) PIPO_GQA32(64); else PIPO_GQA32(128);
+#undef PIPO_GQA32
+  } else {
   const int smem = (16 * (hd + 8) + 2 * ns * 64 * (hd + 8)) * 2 + 2 * 64 * 4;
 #define PIPO_GQA_LAUNCH(HDV, NSV)                                                                               \
   do {                                                                                                          \
@@ -952,6 +1110,7 @@ static int launch_attention_decode_gqa_mma(const AttnArgs& a, int G, cudaStream_
   if (hd == 64) { if (ns == 3) PIPO_GQA_LAUNCH(64, 3); else PIPO_GQA_LAUNCH(64, 2); }
   else { if (ns == 3) PIPO_GQA_LAUNCH(128, 3); else PIPO_GQA_LAUNCH(128, 2); }
 #undef PIPO_GQA_LAUNCH
+  }
   if (n_splits == 1) return 1;
   dim3 g2(a.n_heads, a.b);
   if (hd == 64) launch_pdl_k(attn_merge_kernel<64>, g2, dim3(64), 0, st, a, n_splits);
