@@ -144,9 +144,10 @@ constexpr int APAD = 72;  // halves per smem row: 64 + 8 pad (conflict-free ldma
 template <int WT, int BN>
 struct GemmCfg {
   static constexpr int RAW = WT ? (int)kInt4BlockBytes : (int)kFp16BlockBytes;
-  static constexpr int RAW_STAGE = (RAW + 127) / 128 * 128;
+  // fp16 weights land straight in the padded ldmatrix layout (no staging copy, no A buffer)
+  static constexpr int RAW_STAGE = WT ? (RAW + 127) / 128 * 128 : 128 * APAD * 2;
   static constexpr int X_STAGE = BN * APAD * 2;
-  static constexpr int A_BYTES = 128 * APAD * 2;
+  static constexpr int A_BYTES = WT ? 128 * APAD * 2 : 0;
   static constexpr int SMEM = GEMM_STAGES * (RAW_STAGE + X_STAGE) + A_BYTES;
   static constexpr int NT = BN / 16;           // n8 tiles per warp
   static constexpr int NACC = 2 * NT * 4;
@@ -171,7 +172,12 @@ __global__ void __launch_bounds__(GEMM_THREADS) gemm_kernel(LinearArgs a, int kb
     const int s = i % GEMM_STAGES, kb = kb0 + i;
     const uint8_t* src = wbase + (int64_t)kb * C::RAW;
     uint8_t* dst = raw + s * C::RAW_STAGE;
-    for (int c = tid; c < C::RAW / 16; c += GEMM_THREADS) cp_async16(dst + c * 16, src + c * 16);
+    if constexpr (WT == 1) {
+      for (int c = tid; c < C::RAW / 16; c += GEMM_THREADS) cp_async16(dst + c * 16, src + c * 16);
+    } else {   // 128 rows x 8 chunks of 16 B -> padded rows of APAD halves
+      for (int c = tid; c < C::RAW / 16; c += GEMM_THREADS)
+        cp_async16(dst + ((c >> 3) * APAD + (c & 7) * 8) * 2, src + c * 16);
+    }
     __half* xd = xs + s * BN * APAD;
     for (int c = tid; c < BN * 8; c += GEMM_THREADS) {
       const int r = c >> 3, col = c & 7, m = m0 + r;
@@ -202,6 +208,7 @@ __global__ void __launch_bounds__(GEMM_THREADS) gemm_kernel(LinearArgs a, int kb
     cp_async_commit();
     const int s = i % GEMM_STAGES;
     const uint8_t* rs = raw + s * C::RAW_STAGE;
+    const __half* aS = WT ? as : reinterpret_cast<const __half*>(rs);
     if constexpr (WT == 1) {
       const int h = tid >> 7, r = tid & 127;
       const uint4 cw = *reinterpret_cast<const uint4*>(rs + (h * 128 + r) * 16);
@@ -216,14 +223,8 @@ __global__ void __launch_bounds__(GEMM_THREADS) gemm_kernel(LinearArgs a, int kb
       const uint4* src = reinterpret_cast<const uint4*>(o);
 #pragma unroll
       for (int q = 0; q < 4; ++q) dst[q] = src[q];
-    } else {
-      for (int c = tid; c < 1024; c += GEMM_THREADS) {
-        const int row = c >> 3, col = c & 7;
-        *reinterpret_cast<uint4*>(as + row * APAD + col * 8) =
-            *reinterpret_cast<const uint4*>(rs + (row * 64 + col * 8) * 2);
-      }
+      __syncthreads();
     }
-    __syncthreads();
     const __half* xsS = xs + s * BN * APAD;
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk) {
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(GEMM_THREADS) gemm_kernel(LinearArgs a, int kb
 #pragma unroll
       for (int mi = 0; mi < 2; ++mi)
         ldmatrix_x4(af[mi][0], af[mi][1], af[mi][2], af[mi][3],
-                    as + (wr * 32 + mi * 16 + (lane & 15)) * APAD + kk * 16 + (lane >> 4) * 8);
+                    aS + (wr * 32 + mi * 16 + (lane & 15)) * APAD + kk * 16 + (lane >> 4) * 8);
       if constexpr (C::NT == 1) {
         uint32_t b0, b1;
         ldmatrix_x2(b0, b1, xsS + (wc * (BN / 2) + (lane & 7)) * APAD + kk * 16 + ((lane >> 3) & 1) * 8);
