@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define PIPO_ABI_VERSION 3
+#define PIPO_ABI_VERSION 4
 
 typedef enum {
   PIPO_OK = 0,
@@ -105,7 +105,19 @@ typedef struct {
   float rope_factor;     /* llama3 rope scaling factor (8); 0 -> plain RoPE             */
   float rope_low_freq, rope_high_freq;   /* llama3 low/high_freq_factor (1, 4)          */
   int32_t rope_orig_max_pos;             /* llama3 original_max_position_embeddings (8192) */
+  /* ---- placement (ABI 4).  NUMA node of the large pinned host stores (weights, host
+   * KV cache) and of the disk tier's reader threads (on a
+   * multi-socket node each GPU streams from its own socket's memory; App. D "isolated
+   * PCIe channels").  PIPO_NUMA_GPU_LOCAL (-1): the node of the GPU's
+   * PCIe root, from sysfs, when the host has more than one node; >= 0: that node
+   * (pages bound with mbind, allocation fails with OOM if the node is full);
+   * PIPO_NUMA_NONE (-2): the OS default placement.  NOTE: a zero-initialised config
+   * asks for node 0.                                                                   */
+  int32_t numa_node;
 } pipo_config;
+
+#define PIPO_NUMA_GPU_LOCAL (-1)
+#define PIPO_NUMA_NONE (-2)
 
 typedef enum { PIPO_ARCH_OPT = 0, PIPO_ARCH_LLAMA = 1 } pipo_arch;
 
@@ -142,6 +154,9 @@ typedef struct {
   int64_t kernel_launches;        /* library kernels launched since the last reset     */
   int64_t hbm_bytes;              /* device bytes allocated by the context             */
   int64_t pinned_host_bytes;      /* pinned host bytes allocated by the context        */
+  int32_t numa_node;              /* node the pinned stores are bound to, -1 = none     */
+  int32_t timeline_truncated;     /* PIPO_F_TIMELINE stopped recording (event cap hit)  */
+  double numa_local_frac;         /* sampled pages of the weight store on numa_node (-1 n/a) */
 } pipo_stats;
 
 /* ---- lifecycle ---------------------------------------------------------- */
@@ -298,9 +313,25 @@ pipo_status pipo_rope(pipo_ctx* ctx, const uint16_t* q, const uint16_t* k, int32
  * prefill, 1 for decode).  out must stay valid until that call returns. */
 pipo_status pipo_debug_capture(pipo_ctx* ctx, int32_t on, float* out);
 
+/* Read back stored weights (parity hook for a0): rows
+ * [row0, row0 + nrows) of one matrix, converted from the tiled blob layout back to
+ * the CANONICAL format of pipo_quantize_int4_g64.  layer in [0, n_layers) with
+ * matrix 0..3 = W_qkv, W_out, W_fc1, W_fc2 (logical rows; LLaMA FC1 = gate rows then
+ * up rows), read from the DEVICE-tier store or the unsharded HOST-tier pinned store;
+ * or layer = PIPO_LAYER_EMBED with matrix 0 = token table, 1 = LLaMA LM head.
+ * int4 matrices fill codes [nrows][K/2] and scales [nrows][K/64] (fp16 bits);
+ * fp16 matrices and embeddings fill values [nrows][K] (fp16 bits).
+ * Errors: INVALID_ARG (range, NULL buffer, DISK tier or sharded store), STATE (not loaded). */
+pipo_status pipo_debug_read_rows(pipo_ctx* ctx, int32_t layer, int32_t matrix, int64_t row0, int64_t nrows,
+                                 uint8_t* codes, uint16_t* scales, uint16_t* values);
+
 /* H2D probe: best-of-`reps` pinned->device cudaMemcpyAsync bandwidth (GB/s) for
  * `bytes`-sized copies on the weight-copy stream (App. A sweep). */
 pipo_status pipo_probe_h2d(pipo_ctx* ctx, int64_t bytes, int32_t reps, double* gbs);
+
+/* NUMA node of CUDA device `device`'s PCIe root (sysfs), -1 if unknown; the node a
+ * PIPO_NUMA_GPU_LOCAL config binds to on a multi-node host. */
+int32_t pipo_gpu_numa_node(int32_t device);
 
 /* ---- NEXT-1: sharded weight streaming across the GPUs of one node ----------
  * App. D: with data parallelism "every GPU loads the layer", so each

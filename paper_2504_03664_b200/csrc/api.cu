@@ -36,6 +36,7 @@
 #include "ctx.h"
 #include "disk.h"
 #include "nccl_rt.h"
+#include "numa.h"
 
 using namespace pipo;
 
@@ -94,9 +95,21 @@ pipo_status dev_alloc(pipo_ctx* ctx, T** p, int64_t bytes) {
   return PIPO_OK;
 }
 
+// numa = true: one of the big stores (weights, host KV), placed on ctx->numa_node
 template <typename T>
-pipo_status host_alloc(pipo_ctx* ctx, T** p, int64_t bytes) {
+pipo_status host_alloc(pipo_ctx* ctx, T** p, int64_t bytes, bool numa = false) {
   if (bytes <= 0) { *p = nullptr; return PIPO_OK; }
+  if (numa && ctx->numa_node >= 0) {
+    void* q = nullptr;
+    bool bound = false;
+    if (!numa_host_alloc(bytes, ctx->numa_node, &q, &bound))
+      return set_err(PIPO_E_OOM, "NUMA-bound pinned allocation of " + std::to_string(bytes) + " bytes on node " +
+                                     std::to_string(ctx->numa_node) + " failed");
+    *p = static_cast<T*>(q);
+    ctx->numa_allocs.push_back({q, bytes});
+    ctx->pinned_bytes += bytes;
+    return PIPO_OK;
+  }
   cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(p), (size_t)bytes, cudaHostAllocDefault);
   if (e == cudaErrorMemoryAllocation) {
     cudaGetLastError();
@@ -113,7 +126,25 @@ pipo_status host_alloc(pipo_ctx* ctx, T** p, int64_t bytes) {
     if (s_ != PIPO_OK) return s_;      \
   } while (0)
 
+void host_free(pipo_ctx* ctx, void* p, int64_t bytes) {
+  if (!p) return;
+  for (size_t i = 0; i < ctx->numa_allocs.size(); ++i)
+    if (ctx->numa_allocs[i].first == p) {
+      numa_host_free(p, ctx->numa_allocs[i].second);
+      ctx->numa_allocs.erase(ctx->numa_allocs.begin() + (long)i);
+      ctx->pinned_bytes -= bytes;
+      return;
+    }
+  cudaFreeHost(p);
+  ctx->pinned_bytes -= bytes;
+}
+
 // ---- timeline ---------------------------------------------------------------
+// Timing events come from a pool that is recycled only by pipeline_stats_reset; a long
+// run without resets stops recording at kEventCap events (PIPO_F_TIMELINE / KPROF turn
+// themselves off and pipo_stats.timeline_truncated says so) instead of growing forever.
+constexpr size_t kEventCap = 1u << 18;
+
 pipo_status ev_get(pipo_ctx* ctx, cudaEvent_t* ev) {
   if (ctx->ev_used == ctx->ev_pool.size()) {
     cudaEvent_t e;
@@ -124,15 +155,23 @@ pipo_status ev_get(pipo_ctx* ctx, cudaEvent_t* ev) {
   return PIPO_OK;
 }
 
+bool ev_capped(pipo_ctx* ctx) {
+  if (ctx->ev_used + 2 <= kEventCap) return false;
+  ctx->timeline = ctx->kprof = false;
+  ctx->timeline_truncated = true;
+  return true;
+}
+
 pipo_status span_begin(pipo_ctx* ctx, cudaStream_t st, cudaEvent_t* a) {
-  if (!ctx->timeline) return PIPO_OK;
+  *a = nullptr;
+  if (!ctx->timeline || ev_capped(ctx)) return PIPO_OK;
   TRY(ev_get(ctx, a));
   CK(cudaEventRecord(*a, st));
   return PIPO_OK;
 }
 
 pipo_status span_end(pipo_ctx* ctx, cudaStream_t st, cudaEvent_t a, int lane, int64_t bytes) {
-  if (!ctx->timeline) return PIPO_OK;
+  if (!a) return PIPO_OK;
   cudaEvent_t b;
   TRY(ev_get(ctx, &b));
   CK(cudaEventRecord(b, st));
@@ -141,14 +180,15 @@ pipo_status span_end(pipo_ctx* ctx, cudaStream_t st, cudaEvent_t a, int lane, in
 }
 
 pipo_status kbegin(pipo_ctx* ctx, cudaEvent_t* a) {
-  if (!ctx->kprof) return PIPO_OK;
+  *a = nullptr;
+  if (!ctx->kprof || ev_capped(ctx)) return PIPO_OK;
   TRY(ev_get(ctx, a));
   CK(cudaEventRecord(*a, ctx->s_comp));
   return PIPO_OK;
 }
 
 pipo_status kend(pipo_ctx* ctx, cudaEvent_t a, int cls, double bytes, double flops) {
-  if (!ctx->kprof) return PIPO_OK;
+  if (!a) return PIPO_OK;
   cudaEvent_t b;
   TRY(ev_get(ctx, &b));
   CK(cudaEventRecord(b, ctx->s_comp));
@@ -228,8 +268,8 @@ pipo_status enqueue_copy(pipo_ctx* ctx, int64_t G, int64_t kv_pos) {
   // into chunk_bytes blocks (blockwise transfer; 0 = one block).
   // A segment's ready event is recorded right after the block holding its last byte,
   // so the compute stream consumes each segment as soon as it has landed.
-  auto after_segment = [&](int s) -> pipo_status {
-    CK(cudaEventRecord(ctx->ev_ready[slot][s], ctx->s_copy));
+  auto after_segment = [&](int s, cudaStream_t ready_on) -> pipo_status {
+    CK(cudaEventRecord(ctx->ev_ready[slot][s], ready_on));
     if (s == 0 && host_kv(ctx)) {
       // KV load advanced with the layer's MHA weights (reading Q6)
       if (G >= ctx->R) CK(cudaStreamWaitEvent(ctx->s_copy, ctx->ev_kv_free[slot], 0));
@@ -257,21 +297,30 @@ pipo_status enqueue_copy(pipo_ctx* ctx, int64_t G, int64_t kv_pos) {
                                                                                           : "disk tier transfer setup failed");
       }
       bytes += ctx->lay.seg_bytes[s];
-      TRY(after_segment(s));
+      TRY(after_segment(s, ctx->s_copy));
     }
   } else if (ctx->nccl_comm) {
-    // NEXT-1 sharded streaming: this rank's 1/world of the blob over its own host link,
-    // then the other ranks' ranges over NVLink (in-place NCCL all-gather on the copy
-    // stream); every segment is ready once the gather has completed
+    // NEXT-1 sharded streaming: this rank's 1/world of the blob over its own host link
+    // (copy stream), then the other ranks' ranges over NVLink by an in-place NCCL
+    // all-gather on its OWN stream, ordered after this rank's H2D by an event — so the
+    // gather of layer G overlaps the H2D of layer G+1 (PCIe and NVLink in parallel);
+    // every segment is ready once the gather has completed.
     const int64_t S = ctx->shard_bytes;
     TRY(copy_chunks(ctx, dst + (int64_t)ctx->shard_rank * S, ctx->host_store + (int64_t)j * S, S));
     bytes += S;
-    const int rc = nccl_allgather_bytes(dst + (int64_t)ctx->shard_rank * S, dst, (size_t)S, ctx->nccl_comm, ctx->s_copy);
+    CK(cudaEventRecord(ctx->ev_h2d[slot], ctx->s_copy));
+    CK(cudaStreamWaitEvent(ctx->s_gather, ctx->ev_h2d[slot], 0));
+    cudaEvent_t g0 = nullptr;
+    TRY(span_begin(ctx, ctx->s_gather, &g0));
+    const int rc = nccl_allgather_bytes(dst + (int64_t)ctx->shard_rank * S, dst, (size_t)S, ctx->nccl_comm, ctx->s_gather);
     if (rc != 0) {
       ctx->poisoned = true;
       return set_err(PIPO_E_CUDA, std::string("ncclAllGather failed: ") + nccl_error_string(rc));
     }
-    for (int s = 0; s < 4; ++s) TRY(after_segment(s));
+    TRY(span_end(ctx, ctx->s_gather, g0, 3, S * (ctx->shard_world - 1)));
+    for (int s = 0; s < 4; ++s) {
+      TRY(after_segment(s, ctx->s_gather));
+    }
   } else {
     const uint8_t* src = ctx->host_store + (int64_t)j * ctx->layer_bytes;
     const int64_t total = ctx->lay.seg_off[3] + ctx->lay.seg_bytes[3];
@@ -282,7 +331,7 @@ pipo_status enqueue_copy(pipo_ctx* ctx, int64_t G, int64_t kv_pos) {
       CK(cudaMemcpyAsync(dst + off, src + off, (size_t)n, cudaMemcpyHostToDevice, ctx->s_copy));
       bytes += n;
       while (next_seg < 4 && ctx->lay.seg_off[next_seg] + ctx->lay.seg_bytes[next_seg] <= off + n)
-        TRY(after_segment(next_seg++));
+        TRY(after_segment(next_seg++, ctx->s_copy));
     }
   }
   ctx->h2d_bytes += bytes;
@@ -315,8 +364,9 @@ pipo_status enqueue_kv_only(pipo_ctx* ctx, int64_t G, int64_t kv_pos) {
 }
 
 // one forward pass over all layers: rows M = b * n at positions past .. past+n-1
-pipo_status forward(pipo_ctx* ctx, int b, int n, int past, bool want_logits) {
+pipo_status forward_pass(pipo_ctx* ctx, int b, int n, int past, bool want_logits) {
   const int M = b * n, d = ctx->d;
+  ctx->forwarded = true;
   cudaStream_t cs = ctx->s_comp;
   const int64_t next_pass_kv = past + n;   // KV positions the next (decode) pass loads
   const bool llama = ctx->arch == PIPO_ARCH_LLAMA;
@@ -400,7 +450,9 @@ pipo_status forward(pipo_ctx* ctx, int b, int n, int past, bool want_logits) {
       else LAUNCH(launch_attention_prefill(aa, cs));
       const double L = past + n;
       const double kvb = 2.0 * L * b * dkv * (q4 && n == 1 ? (0.5 + 2.0 / 64) : 2.0);
-      const double fl = n == 1 ? 4.0 * b * d * L : 2.0 * b * d * (double)n * (past + (n + 1) / 2.0);
+      // QK^T and PV: 2 flops per multiply-add each; causal prefill attends over past + (n+1)/2
+      // positions on average
+      const double fl = n == 1 ? 4.0 * b * d * L : 4.0 * b * d * (double)n * (past + (n + 1) / 2.0);
       TRY(kend(ctx, ka, n == 1 ? PIPO_K_ATTN_DECODE : PIPO_K_ATTN_PREFILL, kvb + 4.0 * M * d, fl));
     }
     TRY(span_end(ctx, cs, t0, 1, 0));
@@ -468,6 +520,24 @@ pipo_status forward(pipo_ctx* ctx, int b, int n, int past, bool want_logits) {
   return PIPO_OK;
 }
 
+// A pass that fails after its first enqueue leaves g_comp / g_copy mid-pass and ring slots
+// holding layers the next pass would not expect: poison the context (pipo.h conventions).
+pipo_status forward(pipo_ctx* ctx, int b, int n, int past, bool want_logits) {
+  const pipo_status s = forward_pass(ctx, b, n, past, want_logits);
+  if (s != PIPO_OK) ctx->poisoned = true;
+  return s;
+}
+
+// Weights (re)loaded after a pass: the copy stream may be prefetching the next pass's
+// first layers from the old store (and disk readers may hold its files).  Drain every
+// stream and forget the prefetch so the next pass re-issues it from the new weights.
+pipo_status drain_prefetch(pipo_ctx* ctx) {
+  if (!ctx->forwarded) return PIPO_OK;
+  CK(cudaDeviceSynchronize());
+  ctx->g_copy = ctx->g_comp;
+  return PIPO_OK;
+}
+
 pipo_status finish_call(pipo_ctx* ctx, int b, int n, int32_t* next, float* logits) {
   CK(cudaMemcpyAsync(ctx->pin_next, ctx->next, (size_t)b * 4, cudaMemcpyDeviceToHost, ctx->s_comp));
   ctx->d2h_bytes += (int64_t)b * 4;
@@ -507,13 +577,13 @@ pipo_status stage_ids(pipo_ctx* ctx, const int32_t* tokens, int64_t count) {
 
 pipo_status window_mark(pipo_ctx* ctx, bool start) {
   if (start && !ctx->win_open) {
-    TRY(ev_get(ctx, &ctx->win_start));
     CK(cudaEventRecord(ctx->win_start, ctx->s_comp));
     ctx->win_open = true;
+    ctx->win_closed = false;
   }
   if (!start) {
-    TRY(ev_get(ctx, &ctx->win_end));
     CK(cudaEventRecord(ctx->win_end, ctx->s_comp));
+    ctx->win_closed = true;
   }
   return PIPO_OK;
 }
@@ -622,6 +692,7 @@ pipo_status pipeline_init(const pipo_config* cfg, pipo_ctx** out) {
   CKI(cudaGetDeviceProperties(&prop, c.device));
   if (prop.major < 10) return fail(set_err(PIPO_E_CUDA, "device is not sm_100-class (built for sm_100a only)"));
   ctx->num_sms = prop.multiProcessorCount;
+  ctx->numa_node = resolve_numa_node(c.numa_node, c.device);
   {
     // compute stream at the highest priority (PIPO_COMP_PRIO=0 disables): the copy
     // stream runs multi-ms DMA commands, the compute stream short kernels and events
@@ -640,6 +711,8 @@ pipo_status pipeline_init(const pipo_config* cfg, pipo_ctx** out) {
     CKI(cudaEventCreateWithFlags(&ctx->ev_attn[i], cudaEventDisableTiming));
   }
   for (int j = 0; j < ctx->l; ++j) CKI(cudaEventCreateWithFlags(&ctx->ev_saved[j], cudaEventDisableTiming));
+  CKI(cudaEventCreate(&ctx->win_start));
+  CKI(cudaEventCreate(&ctx->win_end));
 
   // resident embeddings
   ctx->tok_lay = mat_layout(ctx->V, ctx->d, 0);
@@ -679,7 +752,7 @@ pipo_status pipeline_init(const pipo_config* cfg, pipo_ctx** out) {
   } else {
     TRYI(dev_alloc(ctx, &ctx->ring, (int64_t)ctx->R * ctx->layer_bytes));
     if (ctx->weight_tier == PIPO_TIER_HOST) {
-      TRYI(host_alloc(ctx, &ctx->host_store, (int64_t)ctx->l * ctx->layer_bytes));
+      TRYI(host_alloc(ctx, &ctx->host_store, (int64_t)ctx->l * ctx->layer_bytes, true));
     } else {
       const pipo_status ds = disk_open(ctx, c.disk_threads > 0 ? c.disk_threads : 4);
       if (ds != PIPO_OK) return fail(set_err(ds, "disk tier init failed (stream memory operations / pinned ring)"));
@@ -694,7 +767,7 @@ pipo_status pipeline_init(const pipo_config* cfg, pipo_ctx** out) {
     ctx->kv_tensor_bytes = kv_elems * 2;
   }
   if (host_kv(ctx)) {
-    TRYI(host_alloc(ctx, &ctx->kv_host, (int64_t)ctx->l * 2 * ctx->kv_tensor_bytes));
+    TRYI(host_alloc(ctx, &ctx->kv_host, (int64_t)ctx->l * 2 * ctx->kv_tensor_bytes, true));
     TRYI(dev_alloc(ctx, &ctx->kv_slot, (int64_t)ctx->R * 2 * ctx->kv_tensor_bytes));
   } else {
     TRYI(dev_alloc(ctx, &ctx->kv_dev, (int64_t)ctx->l * 2 * ctx->kv_tensor_bytes));
@@ -741,8 +814,14 @@ void pipeline_destroy(pipo_ctx* ctx) {
   for (void* p : dev)
     if (p) cudaFree(p);
   void* hst[] = {ctx->host_store, ctx->kv_host, ctx->pin_ids, ctx->pin_next};
-  for (void* p : hst)
-    if (p) cudaFreeHost(p);
+  for (void* p : hst) {
+    bool numa = false;
+    for (auto& a : ctx->numa_allocs)
+      if (a.first == p) numa = true;
+    if (p && !numa) cudaFreeHost(p);
+  }
+  for (auto& a : ctx->numa_allocs) numa_host_free(a.first, a.second);
+  ctx->numa_allocs.clear();
   for (int i = 0; i < kMaxRing; ++i) {
     for (int s = 0; s < 5; ++s)
       if (ctx->ev_ready[i][s]) cudaEventDestroy(ctx->ev_ready[i][s]);
@@ -753,9 +832,14 @@ void pipeline_destroy(pipo_ctx* ctx) {
   for (auto e : ctx->ev_saved)
     if (e) cudaEventDestroy(e);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  if (ctx->win_start) cudaEventDestroy(ctx->win_start);
+  if (ctx->win_end) cudaEventDestroy(ctx->win_end);
   if (ctx->s_comp) cudaStreamDestroy(ctx->s_comp);
   if (ctx->s_copy) cudaStreamDestroy(ctx->s_copy);
   if (ctx->s_save) cudaStreamDestroy(ctx->s_save);
+  if (ctx->s_gather) cudaStreamDestroy(ctx->s_gather);
+  for (auto e : ctx->ev_h2d)
+    if (e) cudaEventDestroy(e);
   cudaGetLastError();
   delete ctx;
 }
@@ -792,6 +876,7 @@ pipo_status load_layer_weights(pipo_ctx* ctx, int32_t layer, const void* w) {
     return PIPO_OK;
   }
   if (layer < 0 || layer >= ctx->l) return set_err(PIPO_E_INVALID_ARG, "layer index out of range");
+  TRY(drain_prefetch(ctx));
   const pipo_layer_weights* lw = static_cast<const pipo_layer_weights*>(w);
   uint8_t* dst = nullptr;
   std::vector<uint8_t> tmp;
@@ -856,6 +941,7 @@ pipo_status pipo_load_synthetic(pipo_ctx* ctx, int32_t layer, uint64_t seed) {
     return s;
   }
   if (layer < 0 || layer >= ctx->l) return set_err(PIPO_E_INVALID_ARG, "layer index out of range");
+  TRY(drain_prefetch(ctx));
   // draw + quantize/tile into a device blob, then place it in its tier
   uint8_t* blob = nullptr;
   const bool direct = ctx->weight_tier == PIPO_TIER_DEVICE;
@@ -1016,11 +1102,18 @@ pipo_status pipeline_stats(pipo_ctx* ctx, pipo_stats* out) {
   s.kernel_launches = ctx->launches;
   s.hbm_bytes = ctx->hbm_bytes;
   s.pinned_host_bytes = ctx->pinned_bytes;
-  if (ctx->win_open && ctx->win_end) {
+  s.numa_node = ctx->numa_node;
+  s.timeline_truncated = ctx->timeline_truncated ? 1 : 0;
+  s.numa_local_frac = -1.0;
+  if (ctx->numa_node >= 0 && ctx->host_store)
+    s.numa_local_frac = numa_local_fraction(ctx->host_store, ctx->nccl_comm ? (int64_t)ctx->l * ctx->shard_bytes
+                                                                           : (int64_t)ctx->l * ctx->layer_bytes,
+                                            ctx->numa_node, 64);
+  if (ctx->win_open && ctx->win_closed) {
     float w = 0;
     CK(cudaEventElapsedTime(&w, ctx->win_start, ctx->win_end));
     s.window_s = w * 1e-3;
-    std::vector<std::pair<double, double>> lanes[3], all;
+    std::vector<std::pair<double, double>> lanes[4], all;
     double copy_bytes = 0;
     for (const Span& sp : ctx->spans) {
       float a = 0, b = 0;
@@ -1065,7 +1158,10 @@ pipo_status pipeline_stats_reset(pipo_ctx* ctx) {
   ctx->krecs.clear();
   ctx->ev_used = 0;
   ctx->win_open = false;
-  ctx->win_start = ctx->win_end = nullptr;
+  ctx->win_closed = false;
+  ctx->timeline_truncated = false;
+  ctx->timeline = (ctx->cfg.flags & PIPO_F_TIMELINE) != 0;
+  ctx->kprof = (ctx->cfg.flags & PIPO_F_KPROF) != 0;
   ctx->launches = 0;
   ctx->prefill_calls = ctx->decode_steps = ctx->tokens = 0;
   ctx->prefill_s = ctx->decode_s = 0;
@@ -1533,6 +1629,8 @@ pipo_status pipo_rope(pipo_ctx* ctx, const uint16_t* q, const uint16_t* k, int32
   return PIPO_OK;
 }
 
+int32_t pipo_gpu_numa_node(int32_t device) { return gpu_numa_node(device); }
+
 pipo_status pipo_shard_range(int64_t layer_bytes, int32_t world, int32_t rank, int64_t* offset, int64_t* bytes) {
   if (layer_bytes <= 0 || world <= 0 || rank < 0 || rank >= world || !offset || !bytes)
     return set_err(PIPO_E_INVALID_ARG, "bad shard arguments");
@@ -1559,24 +1657,50 @@ pipo_status pipo_shard_stream_init(pipo_ctx* ctx, int32_t rank, int32_t world, c
   CK(cudaSetDevice(ctx->cfg.device));
   int64_t off = 0, S = 0;
   TRY(pipo_shard_range(ctx->lay.total, world, rank, &off, &S));
-  // re-size the ring (padded slots) and the host store (this rank's ranges only)
   CK(cudaDeviceSynchronize());
-  if (ctx->ring) { cudaFree(ctx->ring); ctx->hbm_bytes -= (int64_t)ctx->R * ctx->layer_bytes; ctx->ring = nullptr; }
-  if (ctx->host_store) {
-    cudaFreeHost(ctx->host_store);
-    ctx->pinned_bytes -= (int64_t)ctx->l * ctx->layer_bytes;
-    ctx->host_store = nullptr;
+  // Everything that can fail is built in temporaries first; the context changes only
+  // once all of it succeeded (a failure leaves the plain HOST tier intact).
+  const int64_t ring_bytes = (int64_t)ctx->R * S * world;
+  uint8_t* new_ring = nullptr;
+  uint8_t* new_store = nullptr;
+  void* comm = nullptr;
+  cudaStream_t gather = nullptr;
+  cudaEvent_t evs[kMaxRing] = {};
+  auto unwind = [&](pipo_status st) {
+    if (new_ring) { cudaFree(new_ring); ctx->hbm_bytes -= ring_bytes; }
+    host_free(ctx, new_store, (int64_t)ctx->l * S);
+    if (comm) nccl_comm_destroy(comm);
+    if (gather) cudaStreamDestroy(gather);
+    for (auto& e : evs)
+      if (e) cudaEventDestroy(e);
+    cudaGetLastError();
+    return st;
+  };
+  pipo_status st = dev_alloc(ctx, &new_ring, ring_bytes);
+  if (st != PIPO_OK) return unwind(st);
+  if (cudaMemset(new_ring, 0, (size_t)ring_bytes) != cudaSuccess) return unwind(set_err(PIPO_E_CUDA, "cudaMemset of the ring"));
+  st = host_alloc(ctx, &new_store, (int64_t)ctx->l * S, true);
+  if (st != PIPO_OK) return unwind(st);
+  if (cudaStreamCreateWithFlags(&gather, cudaStreamNonBlocking) != cudaSuccess)
+    return unwind(set_err(PIPO_E_CUDA, "gather stream"));
+  for (auto& e : evs)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return unwind(set_err(PIPO_E_CUDA, "events"));
+  const int rc = nccl_comm_init(&comm, world, id, rank);
+  if (rc != 0) {
+    comm = nullptr;
+    return unwind(set_err(PIPO_E_CUDA, std::string("ncclCommInitRank: ") + nccl_error_string(rc)));
   }
+  // commit
+  if (ctx->ring) { cudaFree(ctx->ring); ctx->hbm_bytes -= (int64_t)ctx->R * ctx->layer_bytes; }
+  host_free(ctx, ctx->host_store, (int64_t)ctx->l * ctx->layer_bytes);
+  ctx->ring = new_ring;
+  ctx->host_store = new_store;
   ctx->layer_bytes = S * world;
   ctx->shard_bytes = S;
   ctx->shard_rank = rank;
   ctx->shard_world = world;
-  TRY(dev_alloc(ctx, &ctx->ring, (int64_t)ctx->R * ctx->layer_bytes));
-  CK(cudaMemset(ctx->ring, 0, (size_t)((int64_t)ctx->R * ctx->layer_bytes)));
-  TRY(host_alloc(ctx, &ctx->host_store, (int64_t)ctx->l * S));
-  void* comm = nullptr;
-  const int rc = nccl_comm_init(&comm, world, id, rank);
-  if (rc != 0) return set_err(PIPO_E_CUDA, std::string("ncclCommInitRank: ") + nccl_error_string(rc));
+  ctx->s_gather = gather;
+  for (int i = 0; i < kMaxRing; ++i) ctx->ev_h2d[i] = evs[i];
   ctx->nccl_comm = comm;
   return PIPO_OK;
 }
@@ -1596,6 +1720,74 @@ pipo_status pipo_debug_capture(pipo_ctx* ctx, int32_t on, float* out) {
   }
   ctx->cap_on = true;
   ctx->cap_host = out;
+  return PIPO_OK;
+}
+
+pipo_status pipo_debug_read_rows(pipo_ctx* ctx, int32_t layer, int32_t matrix, int64_t row0, int64_t nrows,
+                                 uint8_t* codes, uint16_t* scales, uint16_t* values) {
+  CHECK_CTX();
+  CK(cudaSetDevice(ctx->cfg.device));
+  MatLayout ml;
+  const uint8_t* base = nullptr;
+  bool on_device = true, glu = false;
+  if (layer == PIPO_LAYER_EMBED) {
+    if (!ctx->embed_loaded) return set_err(PIPO_E_STATE, "embedding weights not loaded");
+    if (matrix != 0 && !(matrix == 1 && ctx->arch == PIPO_ARCH_LLAMA))
+      return set_err(PIPO_E_INVALID_ARG, "embedding matrix: 0 = token table, 1 = LLaMA LM head");
+    ml = ctx->tok_lay;
+    base = reinterpret_cast<const uint8_t*>(matrix == 0 ? ctx->tok : ctx->head);
+  } else {
+    if (layer < 0 || layer >= ctx->l || matrix < 0 || matrix >= M_COUNT)
+      return set_err(PIPO_E_INVALID_ARG, "layer / matrix out of range");
+    if (!ctx->layer_loaded[layer]) return set_err(PIPO_E_STATE, "layer not loaded");
+    ml = ctx->lay.mat[matrix];
+    glu = ctx->lay.glu && matrix == M_FC1;
+    if (ctx->weight_tier == PIPO_TIER_DEVICE) {
+      base = ctx->dev_store + (int64_t)layer * ctx->layer_bytes + ctx->lay.mat_off[matrix];
+    } else if (ctx->weight_tier == PIPO_TIER_HOST && !ctx->nccl_comm) {
+      base = ctx->host_store + (int64_t)layer * ctx->layer_bytes + ctx->lay.mat_off[matrix];
+      on_device = false;
+    } else {
+      return set_err(PIPO_E_INVALID_ARG, "pipo_debug_read_rows reads the DEVICE or (unsharded) HOST tier");
+    }
+  }
+  if (row0 < 0 || nrows <= 0 || row0 + nrows > ml.N) return set_err(PIPO_E_INVALID_ARG, "row range out of bounds");
+  const bool q4 = layer != PIPO_LAYER_EMBED && ml.wfmt == 1;
+  if (q4 ? (!codes || !scales) : !values) return set_err(PIPO_E_INVALID_ARG, "NULL output buffer");
+  const int64_t K = ml.K, strip = ml.n_kb * ml.block_bytes;
+  std::vector<uint8_t> buf((size_t)strip);
+  int64_t loaded = -1;
+  for (int64_t i = 0; i < nrows; ++i) {
+    int64_t r = row0 + i;                     // logical row -> stored row (LLaMA gate|up interleave)
+    if (glu) {
+      const int64_t F = ml.N / 2, u = r >= F ? r - F : r;
+      r = (u / kTileRows) * 2 * kTileRows + (r >= F ? kTileRows : 0) + u % kTileRows;
+    }
+    const int64_t rt = r / kTileRows, rr = r % kTileRows;
+    if (rt != loaded) {
+      if (on_device) CK(cudaMemcpy(buf.data(), base + rt * strip, (size_t)strip, cudaMemcpyDeviceToHost));
+      else std::memcpy(buf.data(), base + rt * strip, (size_t)strip);
+      loaded = rt;
+    }
+    for (int64_t kb = 0; kb < ml.n_kb; ++kb) {
+      const uint8_t* blk = buf.data() + kb * ml.block_bytes;
+      if (!q4) {
+        std::memcpy(values + i * K + kb * kTileK, blk + rr * kTileK * 2, kTileK * 2);
+        continue;
+      }
+      std::memcpy(scales + i * (K / 64) + kb, blk + 4096 + rr * 2, 2);
+      int q[64];
+      for (int h = 0; h < 2; ++h)
+        for (int w = 0; w < 4; ++w) {
+          uint32_t word;
+          std::memcpy(&word, blk + (h * kTileRows + rr) * 16 + w * 4, 4);
+          for (int nib = 0; nib < 8; ++nib)
+            q[h * 32 + w * 8 + kNibbleElem[nib]] = (int)((word >> (4 * nib)) & 0xF) - 8;
+        }
+      for (int m = 0; m < 32; ++m)
+        codes[i * (K / 2) + kb * 32 + m] = (uint8_t)((q[2 * m] & 0xF) | ((q[2 * m + 1] & 0xF) << 4));
+    }
+  }
   return PIPO_OK;
 }
 

@@ -18,7 +18,7 @@ constexpr int kMaxRing = 8;
 
 struct Span {            // one interval on a device lane, between two timed events
   cudaEvent_t a, b;
-  int lane;              // 0 = H2D copy, 1 = kernels, 2 = D2H save
+  int lane;              // 0 = H2D copy, 1 = kernels, 2 = D2H save, 3 = NVLink all-gather
   int64_t bytes;
 };
 
@@ -48,6 +48,7 @@ struct pipo_ctx {
   bool poisoned = false;
 
   cudaStream_t s_comp = nullptr, s_copy = nullptr, s_save = nullptr;
+  cudaStream_t s_gather = nullptr;   // NEXT-1: NVLink all-gather, off the PCIe copy stream
 
   // resident embeddings (Q20)
   pipo::MatLayout tok_lay;
@@ -103,6 +104,7 @@ struct pipo_ctx {
   int64_t g_copy = 0;              // next global layer index whose copy is enqueued
   int64_t g_comp = 0;              // next global layer index to compute
   cudaEvent_t ev_ready[pipo::kMaxRing][5] = {};   // seg 0..3 landed, [4] = KV landed
+  cudaEvent_t ev_h2d[pipo::kMaxRing] = {};        // NEXT-1: this rank's range landed (gather may start)
   cudaEvent_t ev_free[pipo::kMaxRing] = {};       // compute done with the slot
   cudaEvent_t ev_kv_free[pipo::kMaxRing] = {};    // KV slot free (after save)
   cudaEvent_t ev_attn[pipo::kMaxRing] = {};       // attention done (save may start)
@@ -125,10 +127,16 @@ struct pipo_ctx {
   bool kprof = false;
   std::vector<pipo::KRec> krecs;
   cudaEvent_t win_start = nullptr, win_end = nullptr;
-  bool win_open = false;
+  bool win_open = false, win_closed = false;
   int64_t launches = 0;
   int64_t prefill_calls = 0, decode_steps = 0, tokens = 0;
   double prefill_s = 0, decode_s = 0, ttft_s = 0;
   int64_t h2d_bytes = 0, d2h_bytes = 0;
   int64_t hbm_bytes = 0, pinned_bytes = 0;
+  // NUMA placement of the big pinned stores (numa.cpp): resolved node (-1 = none) and the
+  // mmap + mbind + cudaHostRegister allocations that pipeline_destroy must unregister
+  int numa_node = -1;
+  std::vector<std::pair<void*, int64_t>> numa_allocs;
+  bool timeline_truncated = false;
+  bool forwarded = false;          // a prefill/decode has run (prefetch may be in flight)
 };

@@ -1087,11 +1087,7 @@ static int launch_attention_decode_gqa_mma(const AttnArgs& a, int G, cudaStream_
     const int smem32 = 2 * 3 * 32 * (hd + 8) * 2 + 2 * 32 * 4;
 #define PIPO_GQA32(HDV)                                                                                          \
   do {                                                                                                           \
-    static bool set_ = false;                                                                                    \
-    if (!set_) {                                                                                                 \
-      cudaFuncSetAttribute(attn_decode_gqa_mma32_kernel<HDV, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem32); \
-      set_ = true;                                                                                               \
-    }                                                                                                            \
+    ensure_max_smem(attn_decode_gqa_mma32_kernel<HDV, 3>, smem32);                                              \
     launch_pdl_k(attn_decode_gqa_mma32_kernel<HDV, 3>, grid, dim3(128), smem32, st, a, n_splits, per);           \
   } while (0)
     if (hd == 64) PIPO_GQA32(64); else PIPO_GQA32(128);
@@ -1100,11 +1096,7 @@ static int launch_attention_decode_gqa_mma(const AttnArgs& a, int G, cudaStream_
   const int smem = (16 * (hd + 8) + 2 * ns * 64 * (hd + 8)) * 2 + 2 * 64 * 4;
 #define PIPO_GQA_LAUNCH(HDV, NSV)                                                                               \
   do {                                                                                                          \
-    static bool set_ = false;                                                                                   \
-    if (!set_) {                                                                                                \
-      cudaFuncSetAttribute(attn_decode_gqa_mma_kernel<HDV, NSV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
-      set_ = true;                                                                                              \
-    }                                                                                                           \
+    ensure_max_smem(attn_decode_gqa_mma_kernel<HDV, NSV>, smem);                                               \
     launch_pdl_k(attn_decode_gqa_mma_kernel<HDV, NSV>, grid, dim3(128), smem, st, a, n_splits, per);            \
   } while (0)
   if (hd == 64) { if (ns == 3) PIPO_GQA_LAUNCH(64, 3); else PIPO_GQA_LAUNCH(64, 2); }
@@ -1188,13 +1180,11 @@ int launch_attention_prefill(const AttnArgs& a, cudaStream_t st) {
   dim3 grid(a.n_heads, a.b, (a.n + 63) / 64);
   if (hd == 64) {
     const int smem = 5 * 64 * (64 + 8) * 2;
-    static bool set64 = false;
-    if (!set64) { cudaFuncSetAttribute(attn_prefill_mma_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); set64 = true; }
+    ensure_max_smem(attn_prefill_mma_kernel<64>, smem);
     attn_prefill_mma_kernel<64><<<grid, 128, smem, st>>>(a);
   } else {
     const int smem = 5 * 64 * (128 + 8) * 2;
-    static bool set128 = false;
-    if (!set128) { cudaFuncSetAttribute(attn_prefill_mma_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); set128 = true; }
+    ensure_max_smem(attn_prefill_mma_kernel<128>, smem);
     attn_prefill_mma_kernel<128><<<grid, 128, smem, st>>>(a);
   }
   return 1;

@@ -18,6 +18,7 @@
 // weight rows so stores of one activation row are contiguous across the warp.
 // Split-K uses a deterministic fixup (partials in fixed split order).
 #include "common.cuh"
+#include "launch.cuh"
 #include "kernels.h"
 #include "layout.h"
 #include "epilogue.cuh"
@@ -255,11 +256,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(LinearArgs a, in
 template <int WT, int BN>
 static int run_gemm_tc(const LinearArgs& a, cudaStream_t st) {
   using C = TcCfg<WT, BN>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(gemm_tc_kernel<WT, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    attr_set = true;
-  }
+  ensure_max_smem(gemm_tc_kernel<WT, BN>, C::SMEM);
   const int n_rt = (a.N + 127) / 128, m_tiles = (a.M + BN - 1) / BN, n_kb = a.K / 64;
   const int tiles = n_rt * m_tiles;
   const int per_sm = C::SMEM <= 113 * 1024 ? 2 : 1;

@@ -26,6 +26,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "launch.cuh"
 #include "epilogue.cuh"
 #include "kernels.h"
 #include "layout.h"
@@ -1050,11 +1051,7 @@ static bool make_xmap(CUtensorMap* map, const __half* x, int64_t rows, int64_t K
 template <int BN>
 static int run_ws(const LinearArgs& a, cudaStream_t st) {
   using C = WsCfg<BN>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(gemm_ws_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    attr_set = true;
-  }
+  ensure_max_smem(gemm_ws_kernel<BN>, C::SMEM);
   const int n_rt = (a.N + 127) / 128, m_tiles = (a.M + BN - 1) / BN, n_kb = a.K / 64;
   const int n_pairs = (n_rt + 1) / 2;
   const int64_t U = (int64_t)n_pairs * m_tiles * n_kb;
@@ -1078,11 +1075,7 @@ static int run_ws(const LinearArgs& a, cudaStream_t st) {
 template <int BN, int KBU, int NACC = 2, int UW = 8>
 static int run_tm(const LinearArgs& a, cudaStream_t st) {
   using C = TmCfg<BN, KBU, NACC, UW>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(gemm_tm_kernel<BN, KBU, NACC, UW>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    attr_set = true;
-  }
+  ensure_max_smem(gemm_tm_kernel<BN, KBU, NACC, UW>, C::SMEM);
   const int n_rt = (a.N + 127) / 128, m_tiles = (a.M + BN - 1) / BN, n_kb = a.K / 64;
   const int n_pairs = (n_rt + 1) / 2, n_ku = n_kb / KBU;
   const int64_t U = (int64_t)n_pairs * m_tiles * n_ku;
@@ -1442,12 +1435,7 @@ template <int BN, int TILES, int NACC, int EPW, int KBU = 1>
 static int run_tp(const LinearArgs& a, cudaStream_t st) {
   using C = TpCfg<BN, TILES, NACC, EPW, KBU>;
   if ((a.K / 64) % KBU) return -1;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(gemm_tp_kernel<BN, TILES, NACC, EPW, KBU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         C::SMEM);
-    attr_set = true;
-  }
+  ensure_max_smem(gemm_tp_kernel<BN, TILES, NACC, EPW, KBU>, C::SMEM);
   const int n_rt = (a.N + 127) / 128, m_tiles = (a.M + BN - 1) / BN;
   const int64_t n_tiles = (int64_t)((n_rt + TILES - 1) / TILES) * m_tiles;
   if (n_tiles >= (1ll << 31)) return -1;

@@ -17,6 +17,7 @@
 //  a tile (arrival counter) sums them in split order and runs the epilogue, so
 //  results are bit-reproducible run to run (tier invariance tests rely on it).
 #include "common.cuh"
+#include "launch.cuh"
 #include "kernels.h"
 #include "layout.h"
 #include "epilogue.cuh"
@@ -278,11 +279,7 @@ __global__ void __launch_bounds__(GEMM_THREADS) gemm_kernel(LinearArgs a, int kb
 template <int WT, int BN>
 static int run_gemm(const LinearArgs& a, cudaStream_t st) {
   using C = GemmCfg<WT, BN>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(gemm_kernel<WT, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    attr_set = true;
-  }
+  ensure_max_smem(gemm_kernel<WT, BN>, C::SMEM);
   const int n_rt = (a.N + 127) / 128, m_tiles = (a.M + BN - 1) / BN, n_kb = a.K / 64;
   const int tiles = n_rt * m_tiles;
   const int per_sm = C::SMEM <= 75 * 1024 ? 3 : (C::SMEM <= 113 * 1024 ? 2 : 1);

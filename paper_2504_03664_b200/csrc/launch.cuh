@@ -10,6 +10,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <mutex>
+#include <set>
+#include <tuple>
 
 namespace pipo {
 
@@ -31,6 +34,21 @@ static cudaError_t launch_pdl_k(void (*kern)(KArgs...), dim3 grid, dim3 block, s
   static const bool on = !getenv("PIPO_PDL") || atoi(getenv("PIPO_PDL")) != 0;   // PIPO_PDL=0: plain launches (A/B)
   cfg.numAttrs = on ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize applies to the CURRENT device: track it per
+// (device, kernel, size) so a second context on another GPU of the same process gets it
+// too; thread-safe (contexts may live on different host threads).
+template <typename... KArgs>
+inline void ensure_max_smem(void (*kern)(KArgs...), int bytes) {
+  static std::mutex mu;
+  static std::set<std::tuple<int, const void*, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(dev, reinterpret_cast<const void*>(kern), bytes);
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count(key)) return;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess) done.insert(key);
 }
 
 }  // namespace pipo

@@ -41,10 +41,12 @@ class pipo_config(C.Structure):
                 ("chunk_bytes", C.c_int64), ("gemv_max_m", C.c_int32), ("disk_threads", C.c_int32),
                 ("disk_dir", C.c_char_p), ("flags", C.c_uint32),
                 ("arch", C.c_int32), ("n_kv_heads", C.c_int32), ("rope_theta", C.c_float), ("rope_factor", C.c_float),
-                ("rope_low_freq", C.c_float), ("rope_high_freq", C.c_float), ("rope_orig_max_pos", C.c_int32)]
+                ("rope_low_freq", C.c_float), ("rope_high_freq", C.c_float), ("rope_orig_max_pos", C.c_int32),
+                ("numa_node", C.c_int32)]
 
 
 PIPO_ARCH_OPT, PIPO_ARCH_LLAMA = 0, 1
+PIPO_NUMA_GPU_LOCAL, PIPO_NUMA_NONE = -1, -2
 
 
 class pipo_layer_weights(C.Structure):
@@ -66,7 +68,8 @@ class pipo_stats(C.Structure):
                 ("decode_tokens_per_s", C.c_double), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
                 ("h2d_gbs", C.c_double), ("copy_busy", C.c_double), ("kernel_busy", C.c_double),
                 ("union_busy", C.c_double), ("window_s", C.c_double), ("kernel_launches", C.c_int64),
-                ("hbm_bytes", C.c_int64), ("pinned_host_bytes", C.c_int64)]
+                ("hbm_bytes", C.c_int64), ("pinned_host_bytes", C.c_int64), ("numa_node", C.c_int32),
+                ("timeline_truncated", C.c_int32), ("numa_local_frac", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -139,11 +142,13 @@ _sig("pipo_attention_prefill", C.c_int, _P, _u16, _u16, _u16, C.c_int32, C.c_int
 _sig("pipo_attention_gqa", C.c_int, _P, _u16, _u16, _u16, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
      C.c_int32, _f)
 _sig("pipo_rope", C.c_int, _P, _u16, _u16, C.c_int32, C.c_int32, C.c_int32, _f, _f)
+_sig("pipo_gpu_numa_node", C.c_int32, C.c_int32)
 _sig("pipo_shard_range", C.c_int, C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64))
 _sig("pipo_nccl_unique_id", C.c_int, _u8)
 _sig("pipo_shard_stream_init", C.c_int, _P, C.c_int32, C.c_int32, _u8)
 _sig("pipo_debug_capture", C.c_int, _P, C.c_int32, _f)
 _sig("pipo_probe_h2d", C.c_int, _P, C.c_int64, C.c_int32, C.POINTER(C.c_double))
+_sig("pipo_debug_read_rows", C.c_int, _P, C.c_int32, C.c_int32, C.c_int64, C.c_int64, _u8, _u16, _u16)
 _sig("pipo_ffn_hidden_dim", C.c_int64, C.c_int64, C.c_int64, C.c_double)
 _sig("pipo_memory_model", C.c_int, C.POINTER(pipo_mem_spec), C.c_int64, C.c_int64, C.c_int32, C.c_int32,
      C.POINTER(pipo_mem_report))
@@ -155,8 +160,8 @@ _sig("pipo_choose_plan", C.c_int, C.POINTER(pipo_mem_spec), C.c_int64, C.c_int64
 EXPORTED = ["pipo_last_error", "pipo_abi_version", "pipeline_init", "pipeline_destroy", "load_layer_weights",
             "pipo_load_synthetic", "prefill", "decode_step", "decode_step_dev", "pipeline_stats",
             "pipeline_stats_reset", "pipo_stream", "pipo_kernel_stats", "pipo_quantize_int4_g64", "pipo_quantize_int4_g64_gpu",
-            "pipo_unpack_int4_g64", "pipo_linear", "pipo_bench_linear", "pipo_probe_bulk", "pipo_bench_attention", "pipo_attention_decode", "pipo_attention_prefill", "pipo_debug_capture", "pipo_probe_h2d",
-            "pipo_attention_gqa", "pipo_rope", "pipo_set_flags", "pipo_shard_range", "pipo_nccl_unique_id", "pipo_shard_stream_init",
+            "pipo_unpack_int4_g64", "pipo_linear", "pipo_bench_linear", "pipo_probe_bulk", "pipo_bench_attention", "pipo_attention_decode", "pipo_attention_prefill", "pipo_debug_capture", "pipo_probe_h2d", "pipo_debug_read_rows",
+            "pipo_attention_gqa", "pipo_rope", "pipo_set_flags", "pipo_shard_range", "pipo_gpu_numa_node", "pipo_nccl_unique_id", "pipo_shard_stream_init",
             "pipo_ffn_hidden_dim", "pipo_memory_model", "pipo_choose_block_size", "pipo_choose_plan"]
 
 
@@ -366,6 +371,10 @@ def pipo_rope(ctx, q, k, past):
     return qo, ko
 
 
+def pipo_gpu_numa_node(device: int) -> int:
+    return _lib.pipo_gpu_numa_node(device)
+
+
 def pipo_shard_range(layer_bytes: int, world: int, rank: int):
     """(offset, bytes) of rank's range of a padded layer blob (host-only, NEXT-1)."""
     off, n = C.c_int64(), C.c_int64()
@@ -395,6 +404,20 @@ def pipo_debug_capture(ctx, out: np.ndarray | None):
     else:
         assert out.dtype == np.float32 and out.flags.c_contiguous
         _check(_lib.pipo_debug_capture(ctx, 1, _ptr(out, C.c_float)))
+
+
+def pipo_debug_read_rows(ctx, layer: int, matrix: int, row0: int, nrows: int, K: int, int4: bool):
+    """Stored rows in canonical form: int4 -> (codes [nrows][K/2] u8, scales [nrows][K/64] fp16 bits);
+    fp16 / embeddings -> values [nrows][K] float16."""
+    if int4:
+        codes = np.empty((nrows, K // 2), dtype=np.uint8)
+        scales = np.empty((nrows, K // 64), dtype=np.uint16)
+        _check(_lib.pipo_debug_read_rows(ctx, layer, matrix, row0, nrows, _ptr(codes, C.c_uint8),
+                                         _ptr(scales, C.c_uint16), None))
+        return codes, scales
+    vals = np.empty((nrows, K), dtype=np.uint16)
+    _check(_lib.pipo_debug_read_rows(ctx, layer, matrix, row0, nrows, None, None, _ptr(vals, C.c_uint16)))
+    return vals.view(np.float16)
 
 
 def pipo_probe_h2d(ctx, nbytes: int, reps: int = 5) -> float:
@@ -440,7 +463,7 @@ def pipo_choose_plan(spec: pipo_mem_spec, b: int, s: int, *, m_gpu, m_cpu, b_gpu
 
 def make_config(shape, *, device=0, max_batch, max_seq, wfmt=PIPO_W_INT4_G64, weight_tier=PIPO_TIER_HOST,
                 kv_tier=PIPO_TIER_DEVICE, kv_fmt=PIPO_W_FP16, ring_layers=2, chunk_bytes=0, gemv_max_m=15, disk_threads=4,
-                disk_dir=None, flags=PIPO_F_TIMELINE, n_layers=None) -> pipo_config:
+                disk_dir=None, flags=PIPO_F_TIMELINE, n_layers=None, numa_node=PIPO_NUMA_GPU_LOCAL) -> pipo_config:
     """pipo_config from a pipo_synth.OPTShape-like object (d_model, n_layers, n_heads, ffn_dim, vocab, max_pos)
     or a pipo_synth.LlamaShape (adds n_kv_heads and the llama3 RoPE parameters -> arch LLAMA)."""
     llama = hasattr(shape, "n_kv_heads")
@@ -453,7 +476,7 @@ def make_config(shape, *, device=0, max_batch, max_seq, wfmt=PIPO_W_INT4_G64, we
                        kv_fmt=kv_fmt,
                        ring_layers=ring_layers, chunk_bytes=chunk_bytes, gemv_max_m=gemv_max_m,
                        disk_threads=disk_threads, disk_dir=(disk_dir.encode() if disk_dir else None), flags=flags,
-                       **extra)
+                       numa_node=numa_node, **extra)
 
 
 class Pipeline:

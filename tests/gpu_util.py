@@ -32,30 +32,89 @@ def load_masters(pl, emb, layers):
         pl.load_layer_weights(j, m)
 
 
+def check_greedy_ids(ids_g, lg_g, lg_r, where=""):
+    """Reading Q11: the GPU's greedy ids against the oracle's, row by row.
+
+    Row r is DECIDED when the oracle's top-1 minus top-2 margin exceeds
+    2 * delta_r, delta_r = max_v |g_rv - r_rv| (this row's largest logit error): then
+    g_top1 >= r_top1 - delta_r > r_top2 + delta_r >= g_v for every other v, so the
+    argmax of the GPU logits IS the oracle's argmax — equality is a theorem, and
+    it is asserted exactly.  Undecided rows (a near tie within the row's error)
+    must still pick a token whose oracle logit is within 2 * delta_r of the max.
+    `ids_g` are the ids the GPU's own argmax kernel returned (not recomputed here).
+    Returns the number of undecided rows."""
+    from oracle import opt
+    lg_g = np.asarray(lg_g, np.float64)
+    lg_r = np.asarray(lg_r, np.float64)
+    ids_g = np.asarray(ids_g)
+    ids_r = opt.greedy(lg_r)
+    delta = np.abs(lg_g - lg_r).max(axis=-1)
+    srt = np.sort(lg_r, axis=-1)
+    margin = srt[:, -1] - srt[:, -2]
+    decided = margin > 2 * delta
+    assert np.array_equal(ids_g[decided], ids_r[decided]), f"{where}: greedy id mismatch on a decided row"
+    rows = np.arange(len(ids_g))
+    assert np.all(lg_r[rows, ids_g] >= srt[:, -1] - 2 * delta), f"{where}: invalid near-tie choice"
+    return int((~decided).sum())
+
+
+# SURVEY.md §8(c) Q11: "near-ties must be <= 2 % and reported"
+NEAR_TIE_CAP = 0.02
+
+
 def teacher_forced(pl, ref, prompt, gen, tol=2e-2, capture_layers=False):
     """Run prefill + (gen-1) decode steps on both sides, feeding BOTH the oracle's
-    greedy token (reading Q11).  Returns per-step (rel err, ids_match_where_decided,
-    n_near_ties).  Asserts the 2e-2 bound on logits."""
+    greedy token (reading Q11).  Asserts the 2e-2 bound on logits and, per row, the
+    greedy-id rule of check_greedy_ids (on the ids the GPU's argmax returned).
+    Returns per-step (rel err, n_undecided)."""
     from oracle import opt
     out = []
-    lg_g = pl.prefill(prompt, want_logits=True)[1]
+    nxt, lg_g = pl.prefill(prompt, want_logits=True)
     lg_r = ref.prefill(prompt)
     for step in range(gen):
         err = rel_inf(lg_g, lg_r)
         assert err < tol, f"step {step}: logits rel err {err}"
-        ids_r = opt.greedy(lg_r)
-        ids_g = np.argmax(lg_g, axis=-1)
-        delta = np.abs(lg_g - lg_r).max()
-        srt = np.sort(lg_r, axis=-1)
-        margin = srt[:, -1] - srt[:, -2]
-        decided = margin >= 4 * delta
-        assert np.array_equal(ids_g[decided], ids_r[decided]), f"step {step}: greedy id mismatch"
-        # near ties: the GPU's choice must still be a valid argmax within the error bound
-        rows = np.arange(len(ids_g))
-        assert np.all(lg_r[rows, ids_g] >= srt[:, -1] - 2 * delta), f"step {step}: invalid near-tie choice"
-        out.append((err, int((~decided).sum())))
+        out.append((err, check_greedy_ids(nxt, lg_g, lg_r, f"step {step}")))
         if step == gen - 1:
             break
-        lg_g = pl.decode_step(ids_r, want_logits=True)[1]
+        ids_r = opt.greedy(lg_r)
+        nxt, lg_g = pl.decode_step(ids_r, want_logits=True)
         lg_r = ref.decode(ids_r)
     return out
+
+
+def free_running(pl, ref, prompt, gen, rows=None, tol=2e-2):
+    """Free-running greedy generation on both sides: the GPU feeds back its own ids,
+    the oracle (`ref`, covering the sequences `rows` of the GPU batch, all by default)
+    its own.  While a sequence's ids agree its two trajectories have identical inputs,
+    so its logits must be within `tol` and every decided step's id equal
+    (check_greedy_ids).  A sequence may leave the comparison only at an UNDECIDED step
+    where the two picks differ.  Returns (ids_gpu [b, gen], ids_ref [len(rows), gen],
+    n_undecided, n_diverged)."""
+    from oracle import opt
+    rows = np.arange(prompt.shape[0]) if rows is None else np.asarray(rows)
+    live = np.ones(len(rows), bool)
+    nxt, lg_g = pl.prefill(prompt, want_logits=True)
+    lg_r = ref.prefill(prompt[rows])
+    ids_g, ids_r, n_und = [nxt], [opt.greedy(lg_r)], 0
+    for step in range(gen):
+        g, r = lg_g[rows][live], lg_r[live]
+        if live.any():
+            assert rel_inf(g, r) < tol, f"step {step}: logits rel err {rel_inf(g, r)}"
+            n_und += check_greedy_ids(ids_g[-1][rows][live], g, r, f"free-running step {step}")
+        live &= ids_g[-1][rows] == ids_r[-1]
+        if step == gen - 1:
+            break
+        nxt, lg_g = pl.decode_step(ids_g[-1], want_logits=True)
+        lg_r = ref.decode(ids_r[-1])
+        ids_g.append(nxt)
+        ids_r.append(opt.greedy(lg_r))
+    return np.stack(ids_g, 1), np.stack(ids_r, 1), n_und, int((~live).sum())
+
+
+def assert_near_ties(res, rows_per_step):
+    """The Q11 cap over a whole teacher-forced run: undecided rows <= 2 % of all rows."""
+    n = sum(u for _, u in res)
+    total = rows_per_step * len(res)
+    print(f"undecided {n}/{total} rows; rel err per step:", [f"{e:.2e}" for e, _ in res])
+    assert n <= NEAR_TIE_CAP * total, f"{n} of {total} greedy positions undecided (> {NEAR_TIE_CAP:.0%})"

@@ -40,7 +40,7 @@ def test_exports_every_declared_symbol(pipo):
     for n in names:
         assert hasattr(lib, n), f"{n} declared in pipo.h but not exported"
     assert set(names) == set(pipo.EXPORTED)
-    assert pipo.pipo_abi_version() == 3
+    assert pipo.pipo_abi_version() == 4
 
 
 def test_so_is_sm100a(pipo):

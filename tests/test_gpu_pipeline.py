@@ -15,7 +15,7 @@ import pytest
 
 import pipo_synth as synth
 from oracle import opt
-from tests.gpu_util import load_masters, pipo_mod, rel_inf, teacher_forced
+from tests.gpu_util import assert_near_ties, free_running, load_masters, pipo_mod, rel_inf, teacher_forced
 
 pytestmark = pytest.mark.gpu
 
@@ -59,28 +59,31 @@ def test_c1_vs_oracle_layer_outputs_and_logits(c1_masters):
             tok = opt.greedy(rl)
 
 
-def test_c1_free_running_greedy_ids(c1_masters):
-    """Free-running greedy generation: ids equal to the oracle's (fixture seed chosen
-    with decided margins, reading Q11)."""
+# Reading Q11: "the committed fixture seed is also chosen so that free-running greedy
+# ids match exactly".  At the default prompt seed (3664) two c1 oracle steps have
+# top-2 margins of 1.7e-3 and 2.2e-3 (logits up to 3.0), i.e. ties within fp16
+# arithmetic; 3667 is the first seed >= 3664 whose 32 oracle steps all have margins
+# > 0.02 (min 0.040), so every step is decided and exact equality is a theorem.
+C1_FREE_SEED = 3667
+
+
+@pytest.mark.parametrize("seed", [C1_FREE_SEED, synth.PROMPT_SEED])
+def test_c1_free_running_greedy_ids(c1_masters, seed):
+    """Free-running greedy generation (each side feeds back its own ids).  At the
+    fixture seed every step must be decided and all 4 x 8 ids equal; at the default
+    seed decided steps must agree and a sequence may only diverge at a near tie."""
     pipo = pipo_mod()
     emb, layers = c1_masters
     b, P, G = 4, 32, 8
-    prompt = synth.prompts(b, P, C1.vocab)
-    ids_ref, logits_ref = opt.generate(_oracle(C1, emb, layers, "int4", P + G), prompt, G)
+    prompt = synth.prompts(b, P, C1.vocab, seed=seed)
     cfg = pipo.make_config(C1, max_batch=b, max_seq=P + G, weight_tier=pipo.PIPO_TIER_HOST)
     with pipo.Pipeline(cfg) as pl:
         load_masters(pl, emb, layers)
-        nxt, _ = pl.prefill(prompt)
-        ids = [nxt]
-        for _ in range(G - 1):
-            nxt, _ = pl.decode_step(nxt)
-            ids.append(nxt)
-    ids = np.stack(ids, 1)
-    margins = [np.sort(l, -1)[:, -1] - np.sort(l, -1)[:, -2] for l in logits_ref]
-    if min(m.min() for m in margins) > 1e-3:
-        assert np.array_equal(ids, ids_ref)
-    else:
-        assert (ids == ids_ref).mean() >= 0.98
+        ids_g, ids_r, n_und, n_div = free_running(pl, _oracle(C1, emb, layers, "int4", P + G), prompt, G)
+    print(f"seed {seed}: undecided {n_und}, diverged {n_div}")
+    if seed == C1_FREE_SEED:
+        assert n_und == 0 and n_div == 0
+        assert np.array_equal(ids_g, ids_r)
 
 
 def _run(pipo, shape, cfg_kw, loader, prompt, G, want_logits=True):
@@ -131,10 +134,10 @@ def test_tier_and_ring_invariance_bit_identical(variant):
 
 
 @pytest.mark.parametrize("shape,b,P,G,wfmt", [
-    (synth.OPTShape(d_model=1024, n_layers=3, n_heads=16, ffn_dim=4096, vocab=2048, max_pos=256), 16, 48, 4, "int4"),
-    (synth.OPTShape(d_model=1024, n_layers=2, n_heads=8, ffn_dim=4096, vocab=2048, max_pos=256), 20, 33, 4, "int4"),
-    (synth.OPTShape(d_model=512, n_layers=2, n_heads=8, ffn_dim=2048, vocab=1500, max_pos=256), 6, 40, 4, "fp16"),
-    (synth.OPTShape(d_model=512, n_layers=2, n_heads=4, ffn_dim=2048, vocab=1500, max_pos=256), 17, 24, 3, "fp16"),
+    (synth.OPTShape(d_model=1024, n_layers=3, n_heads=16, ffn_dim=4096, vocab=2048, max_pos=256), 16, 48, 8, "int4"),
+    (synth.OPTShape(d_model=1024, n_layers=2, n_heads=8, ffn_dim=4096, vocab=2048, max_pos=256), 20, 33, 8, "int4"),
+    (synth.OPTShape(d_model=512, n_layers=2, n_heads=8, ffn_dim=2048, vocab=1500, max_pos=256), 6, 40, 8, "fp16"),
+    (synth.OPTShape(d_model=512, n_layers=2, n_heads=4, ffn_dim=2048, vocab=1500, max_pos=256), 17, 24, 8, "fp16"),
 ])
 def test_model_vs_oracle(shape, b, P, G, wfmt):
     pipo = pipo_mod()
@@ -146,9 +149,9 @@ def test_model_vs_oracle(shape, b, P, G, wfmt):
     with pipo.Pipeline(cfg) as pl:
         load_masters(pl, emb, layers)
         res = teacher_forced(pl, ref, synth.prompts(b, P, shape.vocab), G)
-    # undecided positions (oracle margin < 4 x max|dlogit|) are reported, not failed:
-    # teacher_forced() already checked that the GPU's pick is a valid near-argmax there
-    print("near-ties per step:", [n for _, n in res], "rel err:", [f"{e:.2e}" for e, _ in res])
+    # every decided row's id is asserted equal inside teacher_forced(); the undecided
+    # (near-tie) rows are capped at 2 % of all rows and reported
+    assert_near_ties(res, b)
 
 
 def test_api_errors():
@@ -272,3 +275,36 @@ def test_int4_kv_tiers_bit_identical():
     fp, _ = _run(pipo, SMALL, dict(weight_tier=0), syn, prompt, 5)
     assert np.array_equal(fp[0], ref[0])          # prefill attends over fresh fp16 K/V: identical
     assert not np.array_equal(fp[1:], ref[1:])    # decode reads the int4 cache
+
+
+@pytest.mark.parametrize("kv_tier", [0, 1])
+def test_int4_kv_decode_reads_own_row_quantized(kv_tier):
+    """Reading Q17b on the GPU: on the hand-built model of tests/q17b_model.py the two
+    readings of an int4 KV decode step differ by 0.063 per element; the pipeline's
+    layer output must match reading A (own row read back from the int4 cache) to
+    fp16 accuracy and be far from reading B (own row in full precision)."""
+    from tests import q17b_model as qm
+    pipo = pipo_mod()
+    emb, layers = qm.masters()
+    b = 2
+    ref_a = opt.OracleOPT.from_masters(1, emb, layers, "int4", 4, kv_int4=True)
+    ref_b = opt.OracleOPT.from_masters(1, emb, layers, "int4", 4, kv_int4=True)
+    ref_a.prefill(qm.prompt(b))
+    ref_a.decode(qm.decode_tokens(b))
+    ref_b.prefill(qm.prompt(b))
+    ref_b.kv_int4 = False                 # decode: own row fresh, old rows from the int4 cache
+    ref_b.decode(qm.decode_tokens(b))
+    want_a, want_b = ref_a.capture[0][:, 0], ref_b.capture[0][:, 0]
+    cfg = pipo.make_config(qm.SHAPE, max_batch=b, max_seq=4, weight_tier=pipo.PIPO_TIER_HOST, kv_tier=kv_tier,
+                           kv_fmt=pipo.PIPO_W_INT4_G64)
+    with pipo.Pipeline(cfg) as pl:
+        load_masters(pl, emb, layers)
+        pl.prefill(qm.prompt(b))
+        cap = np.zeros((1, b, 1, qm.SHAPE.d_model), np.float32)
+        pipo.pipo_debug_capture(pl.ctx, cap)
+        pl.decode_step(qm.decode_tokens(b))
+    got = cap[0][:, 0].astype(np.float64)
+    err_a = np.abs(got - want_a)[:, 1:].max()
+    gap = np.abs(want_a - want_b)[:, 1:].min()
+    assert gap > 0.05 and err_a < 5e-3, (err_a, gap)
+    assert np.abs(got - want_b)[:, 1:].min() > 0.04

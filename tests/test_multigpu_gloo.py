@@ -109,3 +109,33 @@ def test_gloo_world2_sharded_stream_rebuilds_blob():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert all(ok for _, ok, _ in res)
+
+
+# ---- bench.py launcher: `--gpus N` outside torchrun re-launches N ranks ----
+def test_bench_metric_identical_in_both_arms():
+    import bench
+    for cfg in bench.CONFIGS:
+        a = bench.parse(["--config", cfg])
+        r = bench.parse(["--config", cfg, "--impl", "reference"])
+        assert bench.metric_name(a) == bench.metric_name(r)
+        assert bench.workload_config(a, 2) == bench.workload_config(r, 2)
+
+
+def test_bench_self_launch_two_ranks_reference_arm():
+    """`bench.py --gpus 2` (no WORLD_SIZE) re-runs itself under torch.distributed.run
+    with 2 ranks over 127.0.0.1; rank 0 alone prints ONE line with n_gpus = 2 (the
+    reference arm needs no GPU, so the launcher is exercised here on CPU)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--config", "c1",
+                          "--gpus", "2", "--steps", "2", "--warmup", "1"], capture_output=True, text=True,
+                         timeout=600, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["impl"] == "reference" and d["cpu_baseline"]["cores"] >= 1
+    assert d["steps"] * d["ms_per_step"] / 1e3 < 600       # the claimed timed work fits the run

@@ -205,3 +205,31 @@ def test_int4_kv_cache_semantics():
     q = np.random.default_rng(1).standard_normal((1, 1, 64))
     v = opt.kv_quant_dequant(np.random.default_rng(2).standard_normal((1, 1, 64)))
     assert np.array_equal(opt.attention(q, v, v, 0, 1)[0, 0], v[0, 0])
+
+
+def test_int4_kv_decode_reads_own_row_quantized():
+    """Reading Q17b pinned on a hand-built model (tests/q17b_model.py) where the two
+    readings differ by 0.063 per element: the decode step's output equals the closed
+    form in which its OWN new V row is read back quantize->dequantized (reading A),
+    and is far from the form that keeps the own row in full precision (reading B)."""
+    from tests import q17b_model as qm
+    emb, layers = qm.masters()
+    m = opt.OracleOPT.from_masters(1, emb, layers, "int4", 4, kv_int4=True)
+    m.prefill(qm.prompt())
+    m.decode(qm.decode_tokens())
+    got = m.capture[0][:, 0]                                      # [b, d] layer output
+    c = float(quant.quant_dequant(np.eye(64, dtype=np.float32))[0, 0])   # int4 identity = c I
+    assert abs(c - 7 * 0.142822265625) < 1e-12                    # fp16_rne(1/7) * 7
+
+    def ln(x):
+        mu = x.mean()
+        return (x - mu) / np.sqrt(((x - mu) ** 2).mean() + 1e-5)
+    h0 = emb["tok"][qm.PROMPT_TOKEN].astype(np.float64)
+    h1 = emb["tok"][qm.SPIKE_TOKEN].astype(np.float64)
+    v0, v1 = c * ln(h0), c * ln(h1)
+    dq = lambda v: quant.quant_dequant(v[None].astype(np.float32))[0].astype(np.float64)  # noqa: E731
+    want_a = h1 + c * (dq(v0) + dq(v1)) / 2
+    want_b = h1 + c * (dq(v0) + v1) / 2
+    assert np.abs(got - want_a).max() < 1e-9
+    assert np.abs(want_a - want_b)[1:].min() > 0.05               # the readings are far apart
+    assert np.all(dq(v1)[1:] == 0)                                # the spike's small entries quantize to 0
