@@ -756,7 +756,7 @@ def run_pipo(args):
     pl.close()
 
     # ---- NEXT-1 variant at N > 1: sharded streaming timed in the same run ----
-    if world > 1 and not args.no_variants and not args.shard_stream and c["weight_tier"] == 1:
+    if world > 1 and not shared_gpu and not args.no_variants and not args.shard_stream and c["weight_tier"] == 1:
         try:
             pv, t_load_v = make_pipeline(True)
             nv, _ = pv.prefill(prompt)

@@ -66,6 +66,14 @@ typedef enum { PIPO_TIER_DEVICE = 0, PIPO_TIER_HOST = 1, PIPO_TIER_DISK = 2 } pi
 /* flags */
 #define PIPO_F_TIMELINE 1u  /* record per-segment CUDA events for busy fractions (default on) */
 #define PIPO_F_KPROF 2u     /* time every kernel unit with CUDA events (pipo_kernel_stats) */
+/* NEXT-3 automatic configuration (§3.5, Eq. (1)): pipeline_init ignores
+ * weight_tier, kv_tier, ring_layers, chunk_bytes and gemv_max_m and takes them from
+ * pipo_choose_plan on this machine — M_GPU = free device memory (capped by hbm_budget),
+ * M_CPU = MemAvailable, B_GPU and the block size from a pinned H2D probe (App. A),
+ * B_SSD = B_GPU / 10 (not probed) — for b = max_batch, s = max_seq.  Weights on CPU put the
+ * KV cache on CPU too (Eq. (1) tests W + C < M_CPU); the DISK tier needs disk_dir (else
+ * PIPO_E_INFEASIBLE).  pipo_get_plan returns what was applied. */
+#define PIPO_F_AUTO_PLAN 4u
 
 typedef struct {
   int32_t device;        /* CUDA ordinal */
@@ -114,6 +122,8 @@ typedef struct {
    * PIPO_NUMA_NONE (-2): the OS default placement.  NOTE: a zero-initialised config
    * asks for node 0.                                                                   */
   int32_t numa_node;
+  /* device-memory budget for PIPO_F_AUTO_PLAN (M_GPU of Eq. (1)); 0 = free memory       */
+  int64_t hbm_budget;
 } pipo_config;
 
 #define PIPO_NUMA_GPU_LOCAL (-1)
@@ -402,6 +412,10 @@ typedef struct {
   double m_peak;              /* M (prefill with preloading)                 */
   double m_peak_no_preload;   /* prefill peak of the memory-efficient pipeline            */
 } pipo_plan;
+
+/* The plan pipeline_init applied under PIPO_F_AUTO_PLAN (STATE if the context was not
+ * configured automatically). */
+pipo_status pipo_get_plan(pipo_ctx* ctx, pipo_plan* out);
 
 /* Smallest probed block size whose min-over-edges throughput (h2d, and disk when
  * disk_bps != NULL) is within 5 % of the best (App. A, reading Q26); -1 if n < 1. */

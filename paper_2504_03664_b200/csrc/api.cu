@@ -408,11 +408,9 @@ pipo_status forward_pass(pipo_ctx* ctx, int b, int n, int past, bool want_logits
     if (host_kv(ctx) && n == 1 && ctx->kv_load_past[slot] != past)
       return set_err(PIPO_E_STATE, "internal: KV prefetch range mismatch");
     cudaEvent_t t0;
-    // SynchronizeLoadTask granularity: per segment (the paper's tasks, default for the
-    // memory-efficient ring R = 1) or per layer (R >= 2: one wait on the layer's last
-    // segment — same-stream events are ordered — so the compute stream wakes once per
-    // layer instead of before every linear; the copy stream is still R-1 layers ahead)
-    const bool seg_wait = ctx->layer_wait ? false : true;
+    // SynchronizeLoadTask granularity: per segment (the paper's tasks): each phase waits
+    // for its own segment's event right before its first kernel
+    const bool seg_wait = true;
     if (streamed(ctx)) CK(cudaStreamWaitEvent(cs, ctx->ev_ready[slot][seg_wait ? 0 : 3], 0));
     if (host_kv(ctx)) CK(cudaStreamWaitEvent(cs, ctx->ev_ready[slot][4], 0));
     TRY(span_begin(ctx, cs, &t0));
@@ -604,6 +602,68 @@ double union_len(std::vector<std::pair<double, double>>& v) {
   return tot;
 }
 
+// NEXT-3: Eq. (1) on this machine.  The memory model is the paper's
+// (App. B) for b = max_batch, s = max_seq; the hardware numbers are measured here.
+pipo_status apply_auto_plan(pipo_ctx* ctx) {
+  const pipo_config& c = ctx->cfg;
+  pipo_mem_spec sp{};
+  sp.n_layers = ctx->l; sp.d_model = ctx->d; sp.vocab = ctx->V; sp.n_heads = ctx->H; sp.n_kv_heads = ctx->Hkv;
+  sp.ffn_hidden = ctx->F; sp.mlp_mats = ctx->arch == PIPO_ARCH_LLAMA ? 3 : 2;
+  sp.p_weight = ctx->wfmt == PIPO_W_INT4_G64 ? 17.0 / 32.0 : 2.0;
+  sp.p_act = 2.0;
+  size_t free_b = 0, total_b = 0;
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  double m_gpu = (double)free_b;
+  if (c.hbm_budget > 0) m_gpu = std::min(m_gpu, (double)c.hbm_budget);
+  double m_cpu = 0;
+  if (FILE* f = fopen("/proc/meminfo", "r")) {
+    char key[64];
+    long long kb = 0;
+    while (fscanf(f, "%63s %lld kB\n", key, &kb) == 2)
+      if (!strcmp(key, "MemAvailable:")) { m_cpu = (double)kb * 1024.0; break; }
+    fclose(f);
+  }
+  if (m_cpu <= 0) m_cpu = 1;
+  // App. A: pinned H2D probe over block sizes on the copy stream (best of 3 each)
+  const int64_t sizes[4] = {4ll << 20, 16ll << 20, 32ll << 20, 64ll << 20};
+  double bps[4] = {0, 0, 0, 0};
+  uint8_t *hsrc = nullptr, *ddst = nullptr;
+  TRY(host_alloc(ctx, &hsrc, sizes[3]));
+  pipo_status st = dev_alloc(ctx, &ddst, sizes[3]);
+  if (st != PIPO_OK) { host_free(ctx, hsrc, sizes[3]); return st; }
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  for (int i = 0; i < 4; ++i)
+    for (int r = 0; r < 4; ++r) {
+      CK(cudaEventRecord(e0, ctx->s_copy));
+      CK(cudaMemcpyAsync(ddst, hsrc, (size_t)sizes[i], cudaMemcpyHostToDevice, ctx->s_copy));
+      CK(cudaEventRecord(e1, ctx->s_copy));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      if (r > 0) bps[i] = std::max(bps[i], sizes[i] / (ms * 1e-3));
+    }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  host_free(ctx, hsrc, sizes[3]);
+  cudaFree(ddst);
+  ctx->hbm_bytes -= sizes[3];
+  pipo_hw_spec hw{m_gpu, m_cpu, bps[3], bps[3] / 10.0};
+  pipo_plan plan{};
+  TRY(pipo_choose_plan(&sp, ctx->max_b, ctx->max_s, &hw, sizes, bps, nullptr, 4, &plan));
+  if (plan.weight_tier == PIPO_TIER_DISK && ctx->disk_dir.empty())
+    return set_err(PIPO_E_INFEASIBLE, "Eq. (1) puts the weights on disk (W + C >= M_CPU) but cfg.disk_dir is empty");
+  ctx->weight_tier = plan.weight_tier;
+  ctx->kv_tier = plan.weight_tier == PIPO_TIER_DEVICE ? PIPO_TIER_DEVICE : PIPO_TIER_HOST;
+  ctx->R = std::min(plan.ring_layers, ctx->l);
+  ctx->chunk = plan.block_bytes;
+  ctx->gemv_max_m = plan.gemv_max_m;
+  ctx->auto_plan = true;
+  ctx->plan = plan;
+  return PIPO_OK;
+}
+
 }  // namespace
 
 pipo_status pipo::set_last_error(pipo_status s, const char* msg) { return set_err(s, msg); }
@@ -655,12 +715,7 @@ pipo_status pipeline_init(const pipo_config* cfg, pipo_ctx** out) {
   ctx->weight_tier = c.weight_tier; ctx->kv_tier = c.kv_tier; ctx->kv_fmt = c.kv_fmt;
   ctx->R = c.ring_layers > 0 ? c.ring_layers : 2;
   ctx->R = std::min({ctx->R, kMaxRing, ctx->l});
-  if (host_kv(ctx) && ctx->R < 2 && ctx->l >= 2) ctx->R = 2;
   ctx->chunk = c.chunk_bytes;
-  {
-    const char* lw = getenv("PIPO_LAYER_WAIT");   // 1 = per-layer wait (R >= 2), 0 = per segment
-    ctx->layer_wait = (lw ? atoi(lw) : 0) && ctx->R >= 2;
-  }
   ctx->gemv_max_m = c.gemv_max_m > 0 ? std::min(c.gemv_max_m, 16) : 15;
   ctx->timeline = (c.flags & PIPO_F_TIMELINE) != 0;
   ctx->kprof = (c.flags & PIPO_F_KPROF) != 0;
@@ -694,13 +749,11 @@ pipo_status pipeline_init(const pipo_config* cfg, pipo_ctx** out) {
   ctx->num_sms = prop.multiProcessorCount;
   ctx->numa_node = resolve_numa_node(c.numa_node, c.device);
   {
-    // compute stream at the highest priority (PIPO_COMP_PRIO=0 disables): the copy
-    // stream runs multi-ms DMA commands, the compute stream short kernels and events
+    // compute stream at the highest priority: the copy stream runs multi-ms DMA commands,
+    // the compute stream short kernels and events
     int lo = 0, hi = 0;
     CKI(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    const char* pe = getenv("PIPO_COMP_PRIO");
-    const bool prio = pe ? atoi(pe) != 0 : true;
-    CKI(cudaStreamCreateWithPriority(&ctx->s_comp, cudaStreamNonBlocking, prio ? hi : lo));
+    CKI(cudaStreamCreateWithPriority(&ctx->s_comp, cudaStreamNonBlocking, hi));
   }
   CKI(cudaStreamCreateWithFlags(&ctx->s_copy, cudaStreamNonBlocking));
   CKI(cudaStreamCreateWithFlags(&ctx->s_save, cudaStreamNonBlocking));
@@ -711,6 +764,7 @@ pipo_status pipeline_init(const pipo_config* cfg, pipo_ctx** out) {
     CKI(cudaEventCreateWithFlags(&ctx->ev_attn[i], cudaEventDisableTiming));
   }
   for (int j = 0; j < ctx->l; ++j) CKI(cudaEventCreateWithFlags(&ctx->ev_saved[j], cudaEventDisableTiming));
+  if (c.flags & PIPO_F_AUTO_PLAN) TRYI(apply_auto_plan(ctx));
   CKI(cudaEventCreate(&ctx->win_start));
   CKI(cudaEventCreate(&ctx->win_end));
 
@@ -747,6 +801,8 @@ pipo_status pipeline_init(const pipo_config* cfg, pipo_ctx** out) {
     CKI(cudaMemcpy(ctx->rope_inv, inv.data(), inv.size() * 4, cudaMemcpyHostToDevice));
   }
   // weights
+  if (ctx->weight_tier == PIPO_TIER_DISK && ctx->disk_dir.empty())
+    return fail(set_err(PIPO_E_INVALID_ARG, "disk tier needs disk_dir"));
   if (ctx->weight_tier == PIPO_TIER_DEVICE) {
     TRYI(dev_alloc(ctx, &ctx->dev_store, (int64_t)ctx->l * ctx->layer_bytes));
   } else {
@@ -1347,26 +1403,6 @@ pipo_status pipo_bench_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, int32_t
   CK(cudaEventSynchronize(e1));
   float ms = 0;
   CK(cudaEventElapsedTime(&ms, e0, e1));
-  // PIPO_BENCH_IDLE_US > 0: time each launch alone after the GPU sat idle that long
-  // (the pipeline's situation when the link is the bottleneck), average of iters
-  const int idle_us = getenv("PIPO_BENCH_IDLE_US") ? atoi(getenv("PIPO_BENCH_IDLE_US")) : 0;
-  if (idle_us > 0) {
-    double tot = 0;
-    for (int i = 0; i < iters; ++i) {
-      la.w = wcopy(i + 1);
-      CK(cudaStreamSynchronize(st));
-      const auto t_end = std::chrono::steady_clock::now() + std::chrono::microseconds(idle_us);
-      while (std::chrono::steady_clock::now() < t_end) {}
-      CK(cudaEventRecord(e0, st));
-      LAUNCH(launch_linear(la, path, ctx->gemv_max_m, st));
-      CK(cudaEventRecord(e1, st));
-      CK(cudaEventSynchronize(e1));
-      float m1 = 0;
-      CK(cudaEventElapsedTime(&m1, e0, e1));
-      tot += m1;
-    }
-    ms = (float)tot;
-  }
   cudaEventDestroy(e0); cudaEventDestroy(e1);
   if (getenv("PIPO_WS_DEBUG") && (atoi(getenv("PIPO_WS_DEBUG")) & 128) && path == 5) {
     // globaltimer stamps of the last launch: 9 entry, 10 after setup, 11 MMA done,
@@ -1375,12 +1411,13 @@ pipo_status pipo_bench_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, int32_t
     CK(cudaMemcpy(ts.data(), ctx->ws + (15ll << 20), ts.size() * 8, cudaMemcpyDeviceToHost));
     uint64_t t0 = ~0ull;
     for (int c = 0; c < 148; ++c) if (ts[c * 16 + 9]) t0 = std::min(t0, ts[c * 16 + 9]);
-    const char* nm[6] = {"entry", "setup", "mma_end", "epi_end", "exit", "fixup_end"};
-    for (int k = 9; k <= 14; ++k) {
+    const char* nm[8] = {"entry", "setup", "mma_end", "epi_end", "syncd", "dealloc", "tail_end", "tail1"};
+    for (int k = 3; k <= 15; ++k) {
+      if (k == 8) continue;
       std::vector<double> v;
       for (int c = 0; c < 148; ++c) if (ts[c * 16 + k] >= t0 && ts[c * 16 + k] - t0 < 10000000ull) v.push_back((ts[c * 16 + k] - t0) * 1e-3);
       std::sort(v.begin(), v.end());
-      if (!v.empty()) fprintf(stderr, "tm-stamp %-8s min %7.2f med %7.2f max %7.2f us (n=%zu)\n", nm[k - 9], v.front(), v[v.size() / 2], v.back(), v.size());
+      if (!v.empty()) fprintf(stderr, "tm-stamp %-8s min %7.2f med %7.2f max %7.2f us (n=%zu)\n", k == 7 ? "tail0" : k == 3 ? "w0_wait" : k == 4 ? "w0_loop" : k == 5 ? "w1_wait" : k == 6 ? "w1_loop" : nm[k - 9], v.front(), v[v.size() / 2], v.back(), v.size());
     }
     {   // same-CTA ordering check: exit (after the final __syncthreads) minus MMA / epilogue end
       double lo = 1e30, hi = -1e30, lo2 = 1e30;
@@ -1394,11 +1431,6 @@ pipo_status pipo_bench_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, int32_t
       double fx = 0, bm = 0;
       for (int c = 0; c < 148; ++c) { fx += (double)ts[c * 16] / 148; bm += (double)(int64_t)ts[c * 16 + 1] / 148; }
       fprintf(stderr, "tm-clk fixup %.0f cycles, barrier-after-MMA-end %.0f cycles (avg over CTAs)\n", fx, bm);
-      for (int c = 0; c < 148; ++c)
-        if (ts[c * 16 + 6] && ts[c * 16 + 6] < 1000)
-          fprintf(stderr, "tm-fin cta %d: n_fin %llu spin %llu copy %llu process %llu cycles\n", c,
-                  (unsigned long long)ts[c * 16 + 6], (unsigned long long)ts[c * 16 + 3],
-                  (unsigned long long)ts[c * 16 + 4], (unsigned long long)ts[c * 16 + 5]);
     }
     fprintf(stderr, "reduce first start %.2f last end %.2f us\n", (double)(int64_t)(ts[148 * 16] - t0) * 1e-3, (double)(int64_t)(ts[148 * 16 + 1] - t0) * 1e-3);
   } else if (getenv("PIPO_WS_DEBUG") && (atoi(getenv("PIPO_WS_DEBUG")) & 32) && path == 5) {
@@ -1630,6 +1662,14 @@ pipo_status pipo_rope(pipo_ctx* ctx, const uint16_t* q, const uint16_t* k, int32
 }
 
 int32_t pipo_gpu_numa_node(int32_t device) { return gpu_numa_node(device); }
+
+pipo_status pipo_get_plan(pipo_ctx* ctx, pipo_plan* out) {
+  CHECK_CTX();
+  if (!out) return set_err(PIPO_E_INVALID_ARG, "out is NULL");
+  if (!ctx->auto_plan) return set_err(PIPO_E_STATE, "context was not configured by PIPO_F_AUTO_PLAN");
+  *out = ctx->plan;
+  return PIPO_OK;
+}
 
 pipo_status pipo_shard_range(int64_t layer_bytes, int32_t world, int32_t rank, int64_t* offset, int64_t* bytes) {
   if (layer_bytes <= 0 || world <= 0 || rank < 0 || rank >= world || !offset || !bytes)

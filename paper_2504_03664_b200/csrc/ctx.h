@@ -41,7 +41,6 @@ struct pipo_ctx {
   float* rope_inv = nullptr;       // LLaMA: device [hd/2] inverse frequencies (llama3 rule)
   int weight_tier = 1, kv_tier = 0, R = 2, gemv_max_m = 15;
   int64_t chunk = 0;
-  bool layer_wait = false;         // compute waits once per layer (see forward())
   pipo::LayerLayout lay;
   int64_t layer_bytes = 0;
   int num_sms = 148;
@@ -139,4 +138,6 @@ struct pipo_ctx {
   std::vector<std::pair<void*, int64_t>> numa_allocs;
   bool timeline_truncated = false;
   bool forwarded = false;          // a prefill/decode has run (prefetch may be in flight)
+  bool auto_plan = false;          // PIPO_F_AUTO_PLAN: the fields below came from Eq. (1)
+  pipo_plan plan{};
 };

@@ -294,186 +294,13 @@ __global__ void __launch_bounds__(128) attn_decode_v2_kernel(AttnArgs a, int n_s
 // GQA decode on tensor cores (variant 2): CTA = (KV head, sequence,
 // split).  The G <= 8 query heads of the KV head are the 16-row M dimension of
 // mma.sync m16n8k16 (rows >= G zero-filled, never stored), so each K/V row is read once
-// for the whole group and the G dot products cost no shuffles.  K/V tiles of 64
-// positions are double-buffered with cp.async by all 128 threads; warp w takes
-// positions 16w .. 16w+15 of every tile (S = 16 x 16, one k-step of P.V = 16 x HD) with
-// its own online softmax (fp32, log2 domain, P rounded to fp16 as in the prefill
-// kernel); the 4 warps merge in fixed order through shared memory; splits merge in
-// attn_merge_kernel.
-template <int HD, int NS>
-__global__ void __launch_bounds__(128) attn_decode_gqa_mma_kernel(AttnArgs a, int n_splits, int pos_per_split) {
-  constexpr int KP = HD + 8;      // padded smem row (halves): conflict-free ldmatrix
-  constexpr int NT_O = HD / 8;
-  constexpr int CH = HD / 8;      // 16-B chunks per row
-  extern __shared__ __align__(16) uint8_t smem_attn[];
-  __half* sQ = reinterpret_cast<__half*>(smem_attn);          // [16][KP]
-  __half* sK = sQ + 16 * KP;                                   // [NS][64][KP]
-  __half* sV = sK + NS * 64 * KP;                              // [NS][64][KP]
-  float* sM = reinterpret_cast<float*>(sV + NS * 64 * KP);     // [4 warps][16 rows]
-  float* sL = sM + 64;                                         // [4][16]
-  float* sO = reinterpret_cast<float*>(sK);                    // [4][16][HD], reuses sK after the loop
-  static_assert(4 * 16 * HD * 4 <= NS * 64 * KP * 2, "merge buffer fits in sK");
-  pdl_wait();
-  const int kvh = blockIdx.x, bi = blockIdx.y, split = blockIdx.z;
-  const int G = a.group;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, tq = lane & 3;
-  const int L = a.past + 1;
-  const int lo = split * pos_per_split, hi = min(L, lo + pos_per_split);
-  const int n_kv = (hi - lo + 63) / 64;
-  const int64_t pstride = kv_pstride(a), bstride = kv_bstride(a);
-  for (int c = tid; c < 16 * CH; c += 128) {
-    const int r = c / CH, ch = c % CH;
-    const __half* src = a.q + (int64_t)bi * a.d + (kvh * G + min(r, G - 1)) * HD + ch * 8;
-    cp_async16(sQ + r * KP + ch * 8, src, r < G ? 16 : 0);
-  }
-  auto load_kv = [&](int j, int buf) {
-    for (int c = tid; c < 64 * CH; c += 128) {
-      const int r = c / CH, ch = c % CH, p = lo + j * 64 + r;
-      const int64_t off = (int64_t)min(p, hi - 1) * pstride + (int64_t)bi * bstride + kvh * HD + ch * 8;
-      const int bytes = p < hi ? 16 : 0;
-      cp_async16(sK + (buf * 64 + r) * KP + ch * 8, a.kc + off, bytes);
-      cp_async16(sV + (buf * 64 + r) * KP + ch * 8, a.vc + off, bytes);
-    }
-  };
-#pragma unroll
-  for (int st = 0; st < NS - 1; ++st) {   // NS - 1 tiles in flight ahead of the consumer
-    if (st < n_kv) load_kv(st, st);
-    cp_async_commit();
-  }
-
-  float o[NT_O][4];
-#pragma unroll
-  for (int i = 0; i < NT_O; ++i)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) o[i][c] = 0.f;
-  float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f};
-  uint32_t qf[HD / 16][4];
-  for (int j = 0; j < n_kv; ++j) {
-    const int buf = j % NS;
-    if (j + NS - 1 < n_kv) load_kv(j + NS - 1, (j + NS - 1) % NS);
-    cp_async_commit();
-    cp_async_wait<NS - 1>();
-    __syncthreads();
-    if (j == 0) {
-#pragma unroll
-      for (int kk = 0; kk < HD / 16; ++kk)
-        ldmatrix_x4(qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3], sQ + (lane & 15) * KP + kk * 16 + (lane >> 4) * 8);
-    }
-    // S = Q K^T for this warp's 16 positions of the tile
-    float sc[2][4];
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) sc[i][c] = 0.f;
-    const __half* kb = sK + (buf * 64 + warp * 16) * KP;
-#pragma unroll
-    for (int kk = 0; kk < HD / 16; ++kk) {
-      uint32_t b0, b1, b2, b3;
-      ldmatrix_x4(b0, b1, b2, b3, kb + ((lane & 7) + ((lane >> 4) << 3)) * KP + kk * 16 + ((lane >> 3) & 1) * 8);
-      mma_16816(sc[0], qf[kk], b0, b1);
-      mma_16816(sc[1], qf[kk], b2, b3);
-    }
-    // mask (positions >= hi) + online softmax (log2 domain)
-    float mx[2] = {m_r[0], m_r[1]};
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int p = lo + j * 64 + warp * 16 + i * 8 + 2 * tq + (c & 1);
-        sc[i][c] = p < hi ? sc[i][c] * kLog2e : -INFINITY;
-        mx[c >> 1] = fmaxf(mx[c >> 1], sc[i][c]);
-      }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 1));
-      mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 2));
-    }
-    float corr[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      corr[h] = mx[h] == -INFINITY ? 1.f : exp2f(m_r[h] - mx[h]);
-      m_r[h] = mx[h];
-      l_r[h] *= corr[h];
-    }
-#pragma unroll
-    for (int i = 0; i < NT_O; ++i) {
-      o[i][0] *= corr[0]; o[i][1] *= corr[0];
-      o[i][2] *= corr[1]; o[i][3] *= corr[1];
-    }
-    uint32_t pf[4];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      float e[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const float mm = m_r[c >> 1];
-        e[c] = mm == -INFINITY ? 0.f : exp2f(sc[i][c] - mm);
-        l_r[c >> 1] += e[c];
-      }
-      const __half2 lo2 = __floats2half2_rn(e[0], e[1]), hi2 = __floats2half2_rn(e[2], e[3]);
-      pf[2 * i] = *reinterpret_cast<const uint32_t*>(&lo2);
-      pf[2 * i + 1] = *reinterpret_cast<const uint32_t*>(&hi2);
-    }
-    // O += P V (one k-step: this warp's 16 positions)
-    const __half* vb = sV + (buf * 64 + warp * 16) * KP;
-#pragma unroll
-    for (int nt2 = 0; nt2 < HD / 16; ++nt2) {
-      uint32_t b0, b1, b2, b3;
-      const __half* ptr = vb + ((lane & 7) + ((lane >> 3) & 1) * 8) * KP + nt2 * 16 + (lane >> 4) * 8;
-      asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
-                   : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
-                   : "r"(smem_u32(ptr)));
-      mma_16816(o[2 * nt2], pf, b0, b1);
-      mma_16816(o[2 * nt2 + 1], pf, b2, b3);
-    }
-    __syncthreads();
-  }
-  cp_async_wait<0>();
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    l_r[h] += __shfl_xor_sync(0xffffffffu, l_r[h], 1);
-    l_r[h] += __shfl_xor_sync(0xffffffffu, l_r[h], 2);
-  }
-  __syncthreads();   // every warp is done with sK: it becomes the merge buffer
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int r = g + h * 8;
-    if (tq == 0) { sM[warp * 16 + r] = m_r[h]; sL[warp * 16 + r] = l_r[h]; }
-#pragma unroll
-    for (int i = 0; i < NT_O; ++i) {
-      sO[(warp * 16 + r) * HD + i * 8 + 2 * tq] = o[i][2 * h];
-      sO[(warp * 16 + r) * HD + i * 8 + 2 * tq + 1] = o[i][2 * h + 1];
-    }
-  }
-  __syncthreads();
-  for (int i = tid; i < G * HD; i += 128) {
-    const int r = i / HD, t = i - r * HD, head = kvh * G + r;
-    float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) M = fmaxf(M, sM[w * 16 + r]);
-    float l = 0.f, ov = 0.f;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const float f = sM[w * 16 + r] == -INFINITY ? 0.f : exp2f(sM[w * 16 + r] - M);
-      l += sL[w * 16 + r] * f;
-      ov += sO[(w * 16 + r) * HD + t] * f;
-    }
-    if (n_splits == 1) {
-      a.o[(int64_t)bi * a.d + head * HD + t] = __float2half_rn(ov / l);
-    } else {
-      float* part = a.ws + ((int64_t)(bi * a.n_heads + head) * n_splits + split) * (HD + 2);
-      if (t == 0) { part[0] = M; part[1] = l; }
-      part[2 + t] = ov;
-    }
-  }
-}
-
-// Variant 2 with 32-position tiles (PIPO_GQA_TILE=32): q fragments straight from global
-// (rows 8-15 of the m16 tile are always zero since G <= 8), no Q staging, so three K/V
-// stages take 52 KB and 4 CTAs fit per SM (vs 2 with 64-position tiles).  Warp w takes
-// positions 8w .. 8w+7 of each tile: S is one m16n8 tile per k-step pair; P.V uses the
-// k = 0..7 half of m16n8k16 (the other half zero).
+// for the whole group and the G dot products cost no shuffles.  32-position K/V tiles in
+// a 3-stage cp.async ring; q fragments straight from global (rows 8-15 of the m16 tile
+// are always zero since G <= 8), no Q staging, so three K/V stages take 52 KB and 4 CTAs
+// fit per SM.  Warp w takes positions 8w .. 8w+7 of each tile: S is one m16n8 tile per
+// k-step pair; P.V uses the k = 0..7 half of m16n8k16 (the other half zero), online
+// softmax in fp32 (log2 domain, P rounded to fp16 as in the prefill kernel); the 4 warps
+// merge in fixed order through shared memory; splits merge in attn_merge_kernel.
 template <int HD, int NS>
 __global__ void __launch_bounds__(128) attn_decode_gqa_mma32_kernel(AttnArgs a, int n_splits, int pos_per_split) {
   constexpr int KP = HD + 8;
@@ -1060,49 +887,30 @@ int launch_attention_decode_q4(const AttnArgs& a, cudaStream_t st) {
   return 2;
 }
 
-// variant 2: the tensor-core GQA kernel (default for group sizes 2/4/8).  Splits:
-// PIPO_GQA_SPLITS (read per launch) or the rule below.
+// The tensor-core GQA kernel (default for group sizes 2/4/8): 32-position K/V tiles in a
+// 3-stage cp.async ring, 4 CTAs/SM.  Measured alternatives (64-position tiles with 2 or 3
+// stages, forced position splits: profiles/r01/gqa_tc) were slower and are not built.
 static int launch_attention_decode_gqa_mma(const AttnArgs& a, int G, cudaStream_t st) {
   const int hd = a.d / a.n_heads;
   const int L = a.past + 1;
   const int pairs = a.b * (a.n_heads / G);
-  // PIPO_GQA_STAGES: K/V tile ring depth (3, default: 109 KB, 2 CTAs/SM; 2: 74.5 KB, 3 CTAs/SM)
-  const int ns = getenv("PIPO_GQA_STAGES") && atoi(getenv("PIPO_GQA_STAGES")) == 2 ? 2 : 3;
-  const char* se = getenv("PIPO_GQA_SPLITS");
-  int n_splits = se ? atoi(se) : 0;
-  if (n_splits <= 0) {   // split positions only when the (b, KV head) pairs cannot cover the SMs:
-    // the merge launch costs more than the tail wave (c6: 512 pairs, 1.33 vs 1.62 ms/step)
-    const int target = a.num_sms;
-    n_splits = pairs >= target ? 1 : (target + pairs - 1) / pairs;
-  }
+  // split positions only when the (b, KV head) pairs cannot cover the SMs: the merge
+  // launch costs more than the tail wave (c6: 512 pairs, 1.33 vs 1.62 ms/step)
+  int n_splits = pairs >= a.num_sms ? 1 : (a.num_sms + pairs - 1) / pairs;
   n_splits = max(1, min(n_splits, (L + 63) / 64));
-  // 32-position tiles, 3 stages, 4 CTAs/SM (attn_decode_gqa_mma32_kernel, default: c6
-  // attention 1.35 -> 1.24 ms/step); PIPO_GQA_TILE=64: 64-position tiles, PIPO_GQA_STAGES deep
-  const int tile = getenv("PIPO_GQA_TILE") && atoi(getenv("PIPO_GQA_TILE")) == 64 ? 64 : 32;
+  constexpr int tile = 32;
   const int per = ((L + n_splits - 1) / n_splits + tile - 1) / tile * tile;   // whole tiles per split
   n_splits = (L + per - 1) / per;
   if (n_splits > 1 && (int64_t)a.b * a.n_heads * n_splits * (hd + 2) > a.ws_floats) return -1;
   dim3 grid(a.n_heads / G, a.b, n_splits);
-  if (tile == 32) {
-    const int smem32 = 2 * 3 * 32 * (hd + 8) * 2 + 2 * 32 * 4;
+  const int smem32 = 2 * 3 * 32 * (hd + 8) * 2 + 2 * 32 * 4;
 #define PIPO_GQA32(HDV)                                                                                          \
   do {                                                                                                           \
     ensure_max_smem(attn_decode_gqa_mma32_kernel<HDV, 3>, smem32);                                              \
     launch_pdl_k(attn_decode_gqa_mma32_kernel<HDV, 3>, grid, dim3(128), smem32, st, a, n_splits, per);           \
   } while (0)
-    if (hd == 64) PIPO_GQA32(64); else PIPO_GQA32(128);
+  if (hd == 64) PIPO_GQA32(64); else PIPO_GQA32(128);
 #undef PIPO_GQA32
-  } else {
-  const int smem = (16 * (hd + 8) + 2 * ns * 64 * (hd + 8)) * 2 + 2 * 64 * 4;
-#define PIPO_GQA_LAUNCH(HDV, NSV)                                                                               \
-  do {                                                                                                          \
-    ensure_max_smem(attn_decode_gqa_mma_kernel<HDV, NSV>, smem);                                               \
-    launch_pdl_k(attn_decode_gqa_mma_kernel<HDV, NSV>, grid, dim3(128), smem, st, a, n_splits, per);            \
-  } while (0)
-  if (hd == 64) { if (ns == 3) PIPO_GQA_LAUNCH(64, 3); else PIPO_GQA_LAUNCH(64, 2); }
-  else { if (ns == 3) PIPO_GQA_LAUNCH(128, 3); else PIPO_GQA_LAUNCH(128, 2); }
-#undef PIPO_GQA_LAUNCH
-  }
   if (n_splits == 1) return 1;
   dim3 g2(a.n_heads, a.b);
   if (hd == 64) launch_pdl_k(attn_merge_kernel<64>, g2, dim3(64), 0, st, a, n_splits);
@@ -1119,10 +927,11 @@ int launch_attention_decode(const AttnArgs& a, cudaStream_t st) {
   // attention (fewer shuffles per head) but the c6 step measured the same (the following
   // linears timed slower; profiles/r01/gqa_v2), so the one-row-per-warp kernel stays default
   const int G = (a.group == 2 || a.group == 4 || a.group == 8) ? a.group : 1;
-  const char* v2e = getenv("PIPO_ATTN_V2");
-  // variant: 0 one-row-per-warp, 1 lane groups (CUDA cores), 2 tensor cores (GQA default:
-  // c6 attention 1.98 -> 1.33 ms/step, c7 0.435 -> 0.36; profiles/r01/gqa_tc)
-  const int var = a.use_cuda_cores ? 1 : (v2e ? atoi(v2e) : (G > 1 ? 2 : 0));
+  // variant: 0 one-row-per-warp (MHA default), 1 lane groups (CUDA cores; AttnArgs
+  // use_cuda_cores = 1 through the pipo_attention_decode hook), 2 tensor cores (GQA default:
+  // c6 attention 1.98 -> 1.33 ms/step, c7 0.435 -> 0.36; profiles/r01/gqa_tc); 3 forces the
+  // one-row-per-warp kernel for a GQA group (test hook)
+  const int var = a.use_cuda_cores == 1 ? 1 : a.use_cuda_cores == 3 ? 0 : (G > 1 ? 2 : 0);
   if (var == 2) return launch_attention_decode_gqa_mma(a, G, st);
   const bool v2 = var == 1;
   const int pairs = a.b * a.n_heads / G;
@@ -1131,9 +940,8 @@ int launch_attention_decode(const AttnArgs& a, cudaStream_t st) {
   // Split positions only when (b, head) pairs cannot fill the GPU: measured on B200
   // (profiles/r01/attn_splits) one split per pair wins from 512 pairs up (c5 166 -> 155 us,
   // c3 56.5 -> 50.6, c2 15.0 -> 12.5: no partial writes, no merge launch); small batches
-  // (c7: b = 1, 8 KV-head pairs) still split.  PIPO_ATTN_WAVES = w: target w x 9 CTAs/SM.
-  static const int waves = getenv("PIPO_ATTN_WAVES") ? atoi(getenv("PIPO_ATTN_WAVES")) : -1;
-  const int target = waves < 0 ? a.num_sms * 2 : a.num_sms * 9 * waves;
+  // (c7: b = 1, 8 KV-head pairs) still split.
+  const int target = a.num_sms * 2;
   int n_splits = pairs >= target ? 1 : (target + pairs - 1) / pairs;
   n_splits = max(1, min(n_splits, (L + 63) / 64));
   const int per = (L + n_splits - 1) / n_splits;

@@ -515,11 +515,9 @@ __global__ void __launch_bounds__(256) ws_reduce2_kernel(LinearArgs a, int n_rt,
 // the x producer.
 // One unit = 2 weight tiles (256 rows) x KBU k-blocks: the per-unit synchronisation
 // (mbarrier waits, tcgen05.commit, producer bookkeeping) is amortised over 8*KBU MMAs.
-// NACC accumulator buffers (2: the epilogue of one tile overlaps the next tile's MMAs;
-// 1: more TMEM for the A ring).  UW unpack warps: 8 (warp -> tile x lane quarter, all
-// KBU k-blocks) or 16 (warp -> tile x lane quarter x k-block (KBU = 2) or 32-code half
-// (KBU = 1)), i.e. twice the warps to hide the dequant latency chain.
-template <int BN, int KBU, int NACC = 2, int UW = 8>
+// NACC = 2 accumulator buffers (the epilogue of one tile overlaps the next tile's MMAs);
+// 8 unpack warps (warp -> tile x lane quarter, all KBU k-blocks), software-pipelined.
+template <int BN, int KBU, int NACC = 2, int UW = 98>
 struct TmCfg {
   static constexpr int RAW_T = KBU * (int)kInt4BlockBytes;     // one tile's blocks (contiguous)
   static constexpr int RAW = 2 * RAW_T;
@@ -530,20 +528,15 @@ struct TmCfg {
   static constexpr int ACC_COLS = NACC * 2 * BN;                // NACC buffers x 2 tiles
   static constexpr int A_COLS = 2 * 32 * KBU;                   // per A stage (2 tiles x KBU x 32 cols)
   static constexpr int NA = (512 - ACC_COLS) / A_COLS < 8 ? (512 - ACC_COLS) / A_COLS : 8;
-  // UW = 8: 8 unpack warps; 16: 16 warps splitting each unit's k-blocks; 88: two groups of
-  // 8 warps taking alternate units (each warp's serial per-unit barrier/TMEM latency chain
-  // runs at half the unit rate)
-  static constexpr int UWW = (UW == 88 || UW == 98) ? 8 : UW;   // unpack warps per unit
-  static constexpr int UG = UW == 88 ? 2 : 1;                    // unit-interleaved groups
-  static constexpr bool PIPE = UW == 98;                         // 8 warps, software-pipelined
-  static constexpr int E0 = 2 + UWW * UG;                        // first epilogue warp
+  static constexpr int UWW = 8;                                  // software-pipelined unpack warps
+  static constexpr int E0 = 2 + UWW;                             // first epilogue warp
   static constexpr int XW = E0 + 4;                              // x producer warp
   static constexpr int THREADS = (XW + 1) * 32;
   static constexpr int SMEM = 1024 + NX * X_TILE + NR * RAW + 1024;   // + mbarriers (<= 70) and TMEM slot
   static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
   static_assert(NA >= 2, "TMEM budget");
-  static_assert(UW == 8 || UW == 16 || UW == 88 || UW == 98, "unpack warps");
+  static_assert(UW == 98, "software-pipelined unpack (8 warps) is the one built configuration");
   static_assert((2 * NR + 2 * NX + 2 * NA + 2 + NACC + 1) * 8 + 4 <= 1024, "barrier area");
 };
 
@@ -580,27 +573,9 @@ __device__ __forceinline__ uint64_t clk() {
   return t;
 }
 
-// In-kernel stream-K fixup ("finisher" scheme, fix = 1).  A shared tile t is split
-// over CTAs cf..cl.  cf (the CTA holding t's first unit) processes t's head as the LAST
-// segment of its range; every other contributor holds t's tail as the FIRST segment of
-// its range (or its whole range), so their partials are written early — each CTA writes
-// at most one partial, to its own ws slot, then releases arrive[t].  cf keeps its own
-// part in TMEM: when its accumulator is ready it waits for arrive[t] == n - 1, adds the
-// partials of cf+1 .. cl in that order to its accumulator and runs the fused epilogue.
-// The sum is acc_cf + p_cf+1 + ... + p_cl — the same operands in the same order as the
-// separate ws_reduce_kernel (0 + p_cf + ...), so both modes are bit-identical and
-// deterministic.  Spinning is safe: grid <= #SMs with one CTA per SM (all co-resident),
-// and contributors never wait on anything.
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
 template <int BN, int KBU, int NACC, int UW>
 __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
-    gemm_tm_kernel(const __grid_constant__ CUtensorMap xmap, LinearArgs a, int n_rt, int m_tiles, int G, int dbg,
-                   int fix) {
+    gemm_tm_kernel(const __grid_constant__ CUtensorMap xmap, LinearArgs a, int n_rt, int m_tiles, int G, int dbg) {
   using C = TmCfg<BN, KBU, NACC, UW>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -616,8 +591,7 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
   uint64_t* a_empty = a_full + C::NA;
   uint64_t* acc_full = a_empty + C::NA;
   uint64_t* acc_empty = acc_full + 2;
-  uint64_t* fin_bar = acc_empty + NACC;                     // fixup: partials landed in smem
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin_bar + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + NACC);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n_kb = a.K / 64, n_ku = n_kb / KBU;
@@ -640,7 +614,6 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
     for (int i = 0; i < C::NX; ++i) { ws::mbar_init(&x_full[i], 1); ws::mbar_init(&x_empty[i], 1); }
     for (int i = 0; i < C::NA; ++i) { ws::mbar_init(&a_full[i], C::UWW); ws::mbar_init(&a_empty[i], 1); }
     for (int i = 0; i < NACC; ++i) { ws::mbar_init(&acc_full[i], 1); ws::mbar_init(&acc_empty[i], 4); }
-    ws::mbar_init(fin_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&xmap) : "memory");
   }
@@ -771,16 +744,12 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
     if (lane == 0 && ts) ts[2] = clk();
   } else if (warp < C::E0) {
     // ---------------- unpack + scale straight into TMEM ----------------
-    // a warp may only touch its TMEM lane quarter (warp % 4).  UW = 8: warp -> (tile,
-    // quarter), all KBU k-blocks; UW = 16: warp -> (tile, quarter) and one k-block
-    // (KBU = 2) or one 32-code half (KBU = 1).
-    constexpr int UWW = C::UWW;
-    const int grp = (warp - 2) / UWW;                 // unit group (UW = 88: alternate units)
-    const int g = ((warp - 2) % UWW) >> 2, q = warp & 3;
-    const int t = UWW == 8 ? g : (g >> 1), sub = UWW == 8 ? 0 : (g & 1);
+    // a warp may only touch its TMEM lane quarter (warp % 4): warp -> (tile, quarter),
+    // all KBU k-blocks of the unit.
+    const int t = (warp - 2) >> 2, q = warp & 3;
     const int r = q * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    if constexpr (C::PIPE) {
+    {
       // software-pipelined: unit u+1's raw wait + shared loads + ring release are issued
       // while unit u's TMEM stores drain (before tcgen05.wait::st), so the per-unit
       // barrier/latency chain overlaps the store completion
@@ -820,65 +789,12 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
         __syncwarp();
         if (lane == 0) ws::mbar_arrive(&a_full[sa]);
       }
-    } else
-    for (int64_t u = u0 + grp; u < u1; u += C::UG) {
-      const int64_t iu = u - u0;
-      const int s = (int)(iu % C::NR), sa = (int)(iu % C::NA);
-      const uint32_t ph_r = (uint32_t)((iu / C::NR) & 1), ph_a = (uint32_t)(((iu / C::NA) & 1) ^ 1);
-      TWAIT(0, &raw_full[s], ph_r);
-      constexpr int NK = UWW == 8 ? KBU : (KBU == 2 ? 1 : 1);
-      uint4 cw[NK][2];
-      __half2 s2[NK];
-#pragma unroll
-      for (int kk = 0; kk < NK; ++kk) {
-        const int k = UWW == 8 ? kk : (KBU == 2 ? sub : 0);
-        const uint8_t* rs = raw + s * C::RAW + t * C::RAW_T + k * kInt4BlockBytes;
-        if (UWW == 8 || KBU == 2) {
-          cw[kk][0] = *reinterpret_cast<const uint4*>(rs + r * 16);
-          cw[kk][1] = *reinterpret_cast<const uint4*>(rs + (128 + r) * 16);
-        } else {
-          cw[kk][0] = *reinterpret_cast<const uint4*>(rs + (sub * 128 + r) * 16);
-        }
-        s2[kk] = __half2half2(*reinterpret_cast<const __half*>(rs + 4096 + r * 2));
-      }
-      __syncwarp();
-      if (lane == 0) ws::mbar_arrive(&raw_empty[s]);
-      TWAIT(1, &a_empty[sa], ph_a);
-      ws::tc_after();
-#pragma unroll
-      for (int kk = 0; kk < NK; ++kk) {
-        const int k = UWW == 8 ? kk : (KBU == 2 ? sub : 0);
-        if (UWW == 8 || KBU == 2) {
-          uint32_t o[32];
-          const uint32_t w[8] = {cw[kk][0].x, cw[kk][0].y, cw[kk][0].z, cw[kk][0].w,
-                                 cw[kk][1].x, cw[kk][1].y, cw[kk][1].z, cw[kk][1].w};
-          if (dbg & 4) {   // debug: skip the dequant arithmetic
-#pragma unroll
-            for (int ch = 0; ch < 8; ++ch) o[4 * ch] = o[4 * ch + 1] = o[4 * ch + 2] = o[4 * ch + 3] = w[ch];
-          } else {
-#pragma unroll
-            for (int ch = 0; ch < 8; ++ch) dequant8(w[ch], s2[kk], reinterpret_cast<__half2*>(o + ch * 4));
-          }
-          if (!(dbg & 1)) tmem_st32(a_base + sa * C::A_COLS + k * 64 + t * 32 + lane_off, o);   // debug: skip
-        } else {
-          uint32_t o[16];
-          const uint32_t w[4] = {cw[kk][0].x, cw[kk][0].y, cw[kk][0].z, cw[kk][0].w};
-#pragma unroll
-          for (int ch = 0; ch < 4; ++ch) dequant8(w[ch], s2[kk], reinterpret_cast<__half2*>(o + ch * 4));
-          if (!(dbg & 1)) tmem_st16(a_base + sa * C::A_COLS + t * 32 + sub * 16 + lane_off, o);
-        }
-      }
-      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-      ws::tc_before();
-      __syncwarp();
-      if (lane == 0) ws::mbar_arrive(&a_full[sa]);
     }
   } else {
     // ---------------- epilogue ----------------
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     int seg = 0;
-    uint32_t fin_phase = 0;
     int64_t u = u0;
     const int64_t first_tile_mine = u0 / n_ku;
     while (u < u1) {
@@ -903,75 +819,9 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
         }
       }
       ws::tc_after();
-      // fix = 1: a segment starting at the tile's first unit belongs to cf (finisher);
-      // a partial segment starting mid-tile is a contributor (writes ws slot blockIdx.x)
-      const bool finisher = fix && !full && u == tile * n_ku;
-      if (finisher) {
-        // all of this CTA's MMAs are done, so the raw-weight ring is idle: land the other
-        // contributors' partials there with bulk copies (2 per batch), add them to the
-        // TMEM accumulator in contributor order (k order), epilogue after the last batch
-        const int n_fin = ws::cta_of_unit((tile + 1) * n_ku - 1, U, G) - (int)blockIdx.x;
-        const uint32_t pbytes = (uint32_t)(ntile * BN * 128 * 4);
-        const uint64_t f0 = clk();
-        uint64_t f1 = 0, f2 = 0;
-        if (warp == C::E0 && lane == 0) {
-          if (!(dbg & 512))   // debug: no wait (wrong results; timing only)
-            while (ld_acquire(&a.counters[tile]) < n_fin) __nanosleep(32);
-          a.counters[tile] = 0;                                 // every contributor has arrived
-          asm volatile("fence.proxy.async.global;\n" ::: "memory");
-        }
-        __syncwarp();   // reconverge before the .aligned tcgen05 / bar.sync instructions
-        constexpr int NB = (C::NR * C::RAW) / (2 * BN * 128 * 4) < 2 ? 1 : 2;
-        for (int b0 = (dbg & 1024) ? n_fin : 1; b0 <= n_fin; b0 += NB) {   // debug 1024: one batch only
-          const int nb = min(NB, n_fin - b0 + 1);
-          const bool last = b0 + nb > n_fin;
-          if (warp == C::E0 && lane == 0) {
-            ws::mbar_expect_tx(fin_bar, pbytes * nb);
-            for (int k = 0; k < nb; ++k)
-              ws::bulk_g2s(raw + k * pbytes, a.ws + (int64_t)((int)blockIdx.x + b0 + k) * (2 * BN * 128), pbytes,
-                           fin_bar);
-          }
-          __syncwarp();
-          if (!f1) f1 = clk();
-          ws::mbar_wait(fin_bar, fin_phase);
-          fin_phase ^= 1;
-          if (!f2) f2 = clk();
-          const float* land = reinterpret_cast<const float*>(raw);
-          for (int tt = 0; tt < ntile; ++tt) {
-            const uint32_t t_row = tmem + ab * (2 * BN) + tt * BN + ((uint32_t)(quarter * 32) << 16);
-            const int n = (2 * pr + tt) * 128 + row;
-            for (int c0 = 0; c0 < BN; c0 += 16) {
-              float v[16];
-              if (dbg & 16384) {
-#pragma unroll
-                for (int j = 0; j < 16; ++j) v[j] = 0.f;
-              } else {
-                ws::tmem_ld16(t_row + c0, v);
-              }
-              if (!(dbg & 8192))
-                for (int k = 0; k < nb; ++k)
-#pragma unroll
-                  for (int j = 0; j < 16; ++j) v[j] += land[k * (pbytes / 4) + (tt * BN + c0 + j) * 128 + row];
-              if (last) {
-                if (!(dbg & 4096))
-#pragma unroll
-                  for (int j = 0; j < 16; ++j) epi_store(a.epi, m0 + c0 + j, n, v[j]);
-              } else {
-                uint32_t w[16];
-#pragma unroll
-                for (int j = 0; j < 16; ++j) w[j] = __float_as_uint(v[j]);
-                tmem_st16(t_row + c0, w);
-                asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-              }
-            }
-          }
-          ws::named_bar(1, 128);   // the landing buffer is free for the next batch
-        }
-        if (ts && warp == C::E0 && lane == 0) { ts[3] = f1 - f0; ts[4] = f2 - f1; ts[5] = clk() - f2; ts[6] = n_fin; }
-      }
-      const int slot = fix ? (int)blockIdx.x : 2 * (int)blockIdx.x + (tile == first_tile_mine ? 0 : 1);
+      const int slot = 2 * (int)blockIdx.x + (tile == first_tile_mine ? 0 : 1);
       float* part = a.ws + (int64_t)slot * (2 * BN * 128);
-      for (int tt = 0; tt < ntile && !finisher; ++tt) {
+      for (int tt = 0; tt < ntile; ++tt) {
         const uint32_t t_row = tmem + ab * (2 * BN) + tt * BN + ((uint32_t)(quarter * 32) << 16);
         const int n = (2 * pr + tt) * 128 + row;
         for (int c0 = 0; c0 < BN; c0 += 16) {
@@ -987,12 +837,6 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
         }
       }
       ws::tc_before();
-      if (fix && !full && !finisher) {   // contributor: release the partial
-        if (!(dbg & 2048)) __threadfence();   // debug: no fence
-        ws::named_bar(1, 128);
-        if (warp == C::E0 && lane == 0) atomicAdd(&a.counters[tile], 1);
-        __syncwarp();
-      }
       __syncwarp();
       if (lane == 0) ws::mbar_arrive(&acc_empty[ab]);
       u = seg_end;
@@ -1084,59 +928,31 @@ static int run_tm(const LinearArgs& a, cudaStream_t st) {
   CUtensorMap map;
   if (!make_xmap(&map, a.x, a.M, a.K, BN)) return -1;
   static const int dbg = getenv("PIPO_WS_DEBUG") ? atoi(getenv("PIPO_WS_DEBUG")) : 0;
-  // stream-K fixup as a separate ws_reduce_kernel launch (default, 0) or inside the GEMM
-  // by the tile's first CTA (PIPO_TM_FIXUP=1, the "finisher" scheme above).  Measured on
-  // B200 (profiles/r01/fixup/): the finisher is SLOWER (c5 QKV 52 vs 40 us, out-proj 41 vs
-  // 22 us) — clock64 stamps put ~30k cycles in the finisher's final-output stores at the
-  // kernel tail (partial spin ~3k, bulk copy ~1.2k), so the separate reduce stays default.
-  // The in-kernel fixup spins on other CTAs: it needs G <= #SMs, one CTA per SM.
-  const int fix_env = getenv("PIPO_TM_FIXUP") ? atoi(getenv("PIPO_TM_FIXUP")) : 0;   // read per launch (A/B tests)
-  const int64_t tiles = (int64_t)n_pairs * m_tiles;
-  const int fix = fix_env && G > 1 && G <= a.num_sms && tiles <= a.n_counters && !(dbg & 64) ? 1 : 0;
-  launch_pdl(gemm_tm_kernel<BN, KBU, NACC, UW>, dim3(G), dim3(C::THREADS), C::SMEM, st, map, a, n_rt, m_tiles, G, dbg,
-             fix);
-  if ((dbg & 64) || fix) return 1;   // debug: main kernel only / fixup done in-kernel
+  // Stream-K fixup as a separate launch (ws_reduce2_kernel, PDL).  Three in-kernel
+  // alternatives were built and measured SLOWER on B200 (profiles/r02/tm_fixup/, DESIGN.md
+  // §6): the tile's first CTA finishing from TMEM, the last-arriving contributor summing all
+  // partials, and a tail phase where the sharing CTAs reduce their tiles together (+4-5 us
+  // on every c5 linear).
+  launch_pdl(gemm_tm_kernel<BN, KBU, NACC, UW>, dim3(G), dim3(C::THREADS), C::SMEM, st, map, a, n_rt, m_tiles, G, dbg);
+  if (dbg & 64) return 1;   // debug: main kernel only
   if (G > 1) {
-    const int red_v = getenv("PIPO_REDUCE") ? atoi(getenv("PIPO_REDUCE")) : 2;   // 1 = the v1 reduce
-    if (red_v == 1 || (dbg & 128)) {
-      dim3 rg((unsigned)(G - 1), BN / 8);
-      launch_pdl(ws_reduce_kernel<BN>, rg, dim3(256), 0, st, a, n_rt, m_tiles, G, KBU, dbg);
-    } else {
-      // (tile, 4*CPT columns) x (2 weight tiles x 32 row quads); PIPO_RED_CPT tunes CPT
-      const int cpt_env = getenv("PIPO_RED_CPT") ? atoi(getenv("PIPO_RED_CPT")) : 1;
-      const int cpt = (cpt_env == 2 || cpt_env == 4) && BN / 4 >= cpt_env ? cpt_env : 1;
-      dim3 rg((unsigned)tiles, BN / (4 * cpt));
-      const int late = getenv("PIPO_RED_LATE") ? atoi(getenv("PIPO_RED_LATE")) : 0;
-      if (cpt == 4) launch_pdl(ws_reduce2_kernel<BN, 4>, rg, dim3(256), 0, st, a, n_rt, m_tiles, G, KBU, late);
-      else if (cpt == 2) launch_pdl(ws_reduce2_kernel<BN, 2>, rg, dim3(256), 0, st, a, n_rt, m_tiles, G, KBU, late);
-      else launch_pdl(ws_reduce2_kernel<BN, 1>, rg, dim3(256), 0, st, a, n_rt, m_tiles, G, KBU, late);
-    }
+    // (tile, 4 columns) x (2 weight tiles x 32 row quads)
+    dim3 rg((unsigned)((int64_t)n_pairs * m_tiles), BN / 4);
+    launch_pdl(ws_reduce2_kernel<BN, 1>, rg, dim3(256), 0, st, a, n_rt, m_tiles, G, KBU, 0);
   }
   return G > 1 ? 2 : 1;
 }
 
 int launch_linear_tm(const LinearArgs& a, cudaStream_t st) {
+  // 8 software-pipelined unpack warps (unit u+1's raw wait / shared loads overlap unit u's
+  // TMEM store drain), two accumulators, 2-k-block units when K/64 is even.  The other
+  // configurations measured on B200 (one accumulator, 16 or 2 x 8 unpack warps, 1-k-block
+  // units with 4-6 A stages: profiles/r01/tm_pipe, profiles/r02/tm_fixup) were slower.
   if (a.wfmt != 1) return -1;
   const bool even = (a.K / 64) % 2 == 0;
-  const char* env = getenv("PIPO_TM_CFG");   // tuning hook: (NACC, unpack warps) variants
-  const int cfg = env ? atoi(env) : 6;      // 6: software-pipelined unpack (3-5 % faster at c5)
-  if (a.M <= 16)
-    return cfg == 6 ? (even ? run_tm<16, 2, 2, 98>(a, st) : run_tm<16, 1, 2, 98>(a, st))
-                    : (even ? run_tm<16, 2>(a, st) : run_tm<16, 1>(a, st));
-  if (a.M <= 32)
-    return cfg == 6 ? (even ? run_tm<32, 2, 2, 98>(a, st) : run_tm<32, 1, 2, 98>(a, st))
-                    : (even ? run_tm<32, 2>(a, st) : run_tm<32, 1>(a, st));
-  if (a.M <= 64) {
-    switch (cfg) {
-      case 1: return even ? run_tm<64, 2, 1, 8>(a, st) : run_tm<64, 1, 1, 8>(a, st);
-      case 2: return even ? run_tm<64, 2, 2, 16>(a, st) : run_tm<64, 1, 2, 16>(a, st);
-      case 3: return even ? run_tm<64, 2, 1, 16>(a, st) : run_tm<64, 1, 1, 16>(a, st);
-      case 4: return run_tm<64, 1, 2, 16>(a, st);
-      case 5: return even ? run_tm<64, 2, 2, 88>(a, st) : run_tm<64, 1, 2, 88>(a, st);
-      case 6: return even ? run_tm<64, 2, 2, 98>(a, st) : run_tm<64, 1, 2, 98>(a, st);
-      default: return even ? run_tm<64, 2>(a, st) : run_tm<64, 1>(a, st);
-    }
-  }
+  if (a.M <= 16) return even ? run_tm<16, 2, 2, 98>(a, st) : run_tm<16, 1, 2, 98>(a, st);
+  if (a.M <= 32) return even ? run_tm<32, 2, 2, 98>(a, st) : run_tm<32, 1, 2, 98>(a, st);
+  if (a.M <= 64) return even ? run_tm<64, 2, 2, 98>(a, st) : run_tm<64, 1, 2, 98>(a, st);
   return -1;
 }
 
@@ -1448,26 +1264,11 @@ static int run_tp(const LinearArgs& a, cudaStream_t st) {
 
 int launch_linear_tp(const LinearArgs& a, cudaStream_t st) {
   if (a.wfmt != 1) return -1;
-  const char* env = getenv("PIPO_TP_CFG");   // tuning / test hook: tile configuration
-  // measured at the OPT prefill shapes (tools/tpbench.py, profiles/r01/prefill_nacc2):
-  // 224-token tiles with two accumulators (the epilogue of one tile overlaps the next
-  // tile's MMAs) win except for the long-K down-projection (K >= 4N: fewer, longer
-  // tiles, where 256-token tiles with one accumulator are 4 % faster)
-  const int cfg = env ? atoi(env) : (a.K >= 4 * a.N ? 0 : 5);
-  switch (cfg) {
-    case 1: return run_tp<96, 2, 2, 4>(a, st);
-    case 2: return run_tp<128, 2, 1, 8>(a, st);
-    case 3: return run_tp<128, 1, 2, 4>(a, st);
-    case 4: return run_tp<128, 2, 1, 4>(a, st);
-    case 5: return run_tp<224, 1, 2, 8>(a, st);   // two accumulators: epilogue overlaps the next tile
-    case 6: return run_tp<192, 1, 2, 8>(a, st);
-    case 7: return (a.K / 64) % 2 ? run_tp<256, 1, 1, 8>(a, st) : run_tp<256, 1, 1, 8, 2>(a, st);   // 2-k-block units
-    case 8: return (a.K / 64) % 2 ? run_tp<192, 1, 2, 8>(a, st) : run_tp<192, 1, 2, 8, 2>(a, st);
-    case 9: return (a.K / 64) % 2 ? run_tp<128, 1, 2, 8>(a, st) : run_tp<128, 1, 2, 8, 2>(a, st);
-    case 10: return (a.K / 64) % 2 ? run_tp<224, 1, 2, 8>(a, st) : run_tp<224, 1, 1, 8, 2>(a, st);
-    case 11: return (a.K / 64) % 2 ? run_tp<192, 1, 2, 8>(a, st) : run_tp<192, 1, 1, 8, 2>(a, st);
-    default: return run_tp<256, 1, 1, 8>(a, st);
-  }
+  // measured at the OPT prefill shapes (tools/tpbench.py, profiles/r01/prefill_nacc2, twelve
+  // tile configurations): 224-token tiles with two accumulators (the epilogue of one tile
+  // overlaps the next tile's MMAs) win except for the long-K down-projection (K >= 4N:
+  // fewer, longer tiles, where 256-token tiles with one accumulator are 4 % faster)
+  return a.K >= 4 * a.N ? run_tp<256, 1, 1, 8>(a, st) : run_tp<224, 1, 2, 8>(a, st);
 }
 
 int launch_linear_ws(const LinearArgs& a, cudaStream_t st) {

@@ -23,6 +23,7 @@ PIPO_W_FP16, PIPO_W_INT4_G64 = 0, 1
 PIPO_TIER_DEVICE, PIPO_TIER_HOST, PIPO_TIER_DISK = 0, 1, 2
 PIPO_F_TIMELINE = 1
 PIPO_F_KPROF = 2
+PIPO_F_AUTO_PLAN = 4
 K_CLASSES = ["linear_decode", "attn_decode", "lm_head", "linear_prefill", "attn_prefill", "misc"]
 PIPO_LAYER_EMBED = -1
 PATH_AUTO, PATH_GEMV, PATH_GEMM, PATH_TC, PATH_WS, PATH_TM, PATH_TP = 0, 1, 2, 3, 4, 5, 6
@@ -42,7 +43,7 @@ class pipo_config(C.Structure):
                 ("disk_dir", C.c_char_p), ("flags", C.c_uint32),
                 ("arch", C.c_int32), ("n_kv_heads", C.c_int32), ("rope_theta", C.c_float), ("rope_factor", C.c_float),
                 ("rope_low_freq", C.c_float), ("rope_high_freq", C.c_float), ("rope_orig_max_pos", C.c_int32),
-                ("numa_node", C.c_int32)]
+                ("numa_node", C.c_int32), ("hbm_budget", C.c_int64)]
 
 
 PIPO_ARCH_OPT, PIPO_ARCH_LLAMA = 0, 1
@@ -154,6 +155,7 @@ _sig("pipo_memory_model", C.c_int, C.POINTER(pipo_mem_spec), C.c_int64, C.c_int6
      C.POINTER(pipo_mem_report))
 _sig("pipo_choose_block_size", C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_double), C.POINTER(C.c_double),
      C.c_int32)
+_sig("pipo_get_plan", C.c_int, _P, C.POINTER(pipo_plan))
 _sig("pipo_choose_plan", C.c_int, C.POINTER(pipo_mem_spec), C.c_int64, C.c_int64, C.POINTER(pipo_hw_spec),
      C.POINTER(C.c_int64), C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int32, C.POINTER(pipo_plan))
 
@@ -162,7 +164,7 @@ EXPORTED = ["pipo_last_error", "pipo_abi_version", "pipeline_init", "pipeline_de
             "pipeline_stats_reset", "pipo_stream", "pipo_kernel_stats", "pipo_quantize_int4_g64", "pipo_quantize_int4_g64_gpu",
             "pipo_unpack_int4_g64", "pipo_linear", "pipo_bench_linear", "pipo_probe_bulk", "pipo_bench_attention", "pipo_attention_decode", "pipo_attention_prefill", "pipo_debug_capture", "pipo_probe_h2d", "pipo_debug_read_rows",
             "pipo_attention_gqa", "pipo_rope", "pipo_set_flags", "pipo_shard_range", "pipo_gpu_numa_node", "pipo_nccl_unique_id", "pipo_shard_stream_init",
-            "pipo_ffn_hidden_dim", "pipo_memory_model", "pipo_choose_block_size", "pipo_choose_plan"]
+            "pipo_ffn_hidden_dim", "pipo_memory_model", "pipo_choose_block_size", "pipo_choose_plan", "pipo_get_plan"]
 
 
 class PipoError(RuntimeError):
@@ -461,9 +463,16 @@ def pipo_choose_plan(spec: pipo_mem_spec, b: int, s: int, *, m_gpu, m_cpu, b_gpu
     return out.as_dict()
 
 
+def pipo_get_plan(ctx) -> dict:
+    out = pipo_plan()
+    _check(_lib.pipo_get_plan(ctx, C.byref(out)))
+    return out.as_dict()
+
+
 def make_config(shape, *, device=0, max_batch, max_seq, wfmt=PIPO_W_INT4_G64, weight_tier=PIPO_TIER_HOST,
                 kv_tier=PIPO_TIER_DEVICE, kv_fmt=PIPO_W_FP16, ring_layers=2, chunk_bytes=0, gemv_max_m=15, disk_threads=4,
-                disk_dir=None, flags=PIPO_F_TIMELINE, n_layers=None, numa_node=PIPO_NUMA_GPU_LOCAL) -> pipo_config:
+                disk_dir=None, flags=PIPO_F_TIMELINE, n_layers=None, numa_node=PIPO_NUMA_GPU_LOCAL,
+                hbm_budget=0) -> pipo_config:
     """pipo_config from a pipo_synth.OPTShape-like object (d_model, n_layers, n_heads, ffn_dim, vocab, max_pos)
     or a pipo_synth.LlamaShape (adds n_kv_heads and the llama3 RoPE parameters -> arch LLAMA)."""
     llama = hasattr(shape, "n_kv_heads")
@@ -476,7 +485,7 @@ def make_config(shape, *, device=0, max_batch, max_seq, wfmt=PIPO_W_INT4_G64, we
                        kv_fmt=kv_fmt,
                        ring_layers=ring_layers, chunk_bytes=chunk_bytes, gemv_max_m=gemv_max_m,
                        disk_threads=disk_threads, disk_dir=(disk_dir.encode() if disk_dir else None), flags=flags,
-                       numa_node=numa_node, **extra)
+                       numa_node=numa_node, hbm_budget=hbm_budget, **extra)
 
 
 class Pipeline:

@@ -56,13 +56,13 @@ def test_rope_kernel_vs_oracle():
     assert np.array_equal(ko[:past], k[:past].astype(np.float32))      # older positions untouched
 
 
-@pytest.mark.parametrize("v2,tile", [("0", "32"), ("1", "32"), ("2", "32"), ("2", "64")])
 @pytest.mark.parametrize("hd,H,Hkv,n,past", [(64, 8, 2, 1, 37), (128, 8, 4, 1, 300), (64, 8, 1, 1, 0),
-                                             (64, 8, 2, 70, 0), (128, 4, 2, 33, 12), (128, 16, 2, 1, 100)])
-def test_gqa_attention_vs_oracle(hd, H, Hkv, n, past, v2, tile, monkeypatch):
+                                             (64, 8, 2, 70, 0), (128, 4, 2, 33, 12), (128, 16, 2, 1, 100),
+                                             (128, 32, 8, 1, 527), (64, 16, 4, 1, 5)])
+def test_gqa_attention_vs_oracle(hd, H, Hkv, n, past):
+    """GQA attention (decode: the tensor-core kernel, position splits + merge when the
+    (b, KV head) pairs do not cover the SMs; prefill: the causal kernel)."""
     pipo = pipo_mod()
-    monkeypatch.setenv("PIPO_ATTN_V2", v2)   # decode: one-row-per-warp (0), lane-group (1), tensor-core (2)
-    monkeypatch.setenv("PIPO_GQA_TILE", tile)   # tensor-core kernel: 32- or 64-position K/V tiles
     rng = np.random.default_rng(hd + H + n + past)
     b = 3
     q = (rng.standard_normal((b, n, H * hd)) * hd ** -0.5).astype(np.float16)
@@ -121,20 +121,6 @@ def test_llama_tiny_vs_oracle(tiny, wfmt, b):
     pipo = pipo_mod()
     emb, layers = tiny
     _teacher_forced(pipo, TINY, emb, layers, wfmt, b, 20, 5)
-
-
-@pytest.mark.parametrize("var,splits,tile", [("2", "0", "32"), ("2", "1", "32"), ("2", "3", "32"), ("2", "0", "64"),
-                                             ("2", "3", "64"), ("0", "0", "32"), ("1", "0", "32")])
-def test_llama_tiny_attention_variants_vs_oracle(tiny, var, splits, tile, monkeypatch):
-    """Each GQA decode kernel in the whole model: tensor cores (variant 2, the default for
-    G > 1) with the default, no and forced position splits (+ merge kernel); the
-    CUDA-core kernels (0, 1)."""
-    pipo = pipo_mod()
-    monkeypatch.setenv("PIPO_ATTN_V2", var)
-    monkeypatch.setenv("PIPO_GQA_SPLITS", splits)
-    monkeypatch.setenv("PIPO_GQA_TILE", tile)
-    emb, layers = tiny
-    _teacher_forced(pipo, TINY, emb, layers, "int4", 24, 70, 5)
 
 
 def test_llama_hd128_vs_oracle():
