@@ -95,6 +95,9 @@ def parse(argv=None):
     ap.add_argument("--shard-stream", action="store_true",
                     help="NEXT-1 as the primary mode: each rank streams 1/N of every layer over its host link and "
                          "all-gathers the rest over NVLink (NCCL); compute stays batch-sharded (host tier only)")
+    ap.add_argument("--shard-transport", default="p2p", choices=["p2p", "nccl"],
+                    help="sharded streaming's gather: peer copies out of the peers' HBM rings through CUDA IPC "
+                         "(p2p, the library's own transport) or an NCCL all-gather")
     ap.add_argument("--no-variants", action="store_true", help="N > 1: skip the sharded-streaming variant pass")
     ap.add_argument("--allow-shared-gpu", action="store_true",
                     help="let N ranks share fewer GPUs (launcher test only; gloo plumbing)")
@@ -140,8 +143,8 @@ def workload_config(args, world: int) -> dict:
             "seq_len": c["P"], "gen": c["G"], "n_layers": s.n_layers, "d_model": s.d_model,
             "wfmt": args.wfmt, "kv_fmt": args.kv_fmt,
             "weight_tier": TIERS[c["weight_tier"]], "kv_tier": ["device", "host"][c["kv_tier"]],
-            "parallelism": (f"batch-shard x{world} + sharded streaming (1/{world} of each layer over PCIe, NCCL "
-                            f"all-gather over NVLink)") if args.shard_stream
+            "parallelism": (f"batch-shard x{world} + sharded streaming (1/{world} of each layer over PCIe, the rest "
+                            f"gathered over NVLink, {args.shard_transport})") if args.shard_stream
             else f"batch-shard x{world} (no hot-path collective)",
             "l2": "inputs larger than L2 (every step streams all layer weights through HBM)"}
 
@@ -573,6 +576,13 @@ def run_pipo(args):
         os.makedirs(disk_dir, exist_ok=True)
     flags = (0 if args.no_timeline else pipo.PIPO_F_TIMELINE) | (0 if args.no_kprof else pipo.PIPO_F_KPROF)
 
+    def gather_list(x):
+        if world == 1:
+            return [x]
+        out = [None] * world
+        dist.all_gather_object(out, x)
+        return out
+
     def make_pipeline(shard: bool):
         cfg = pipo.make_config(s, device=local, max_batch=b, max_seq=max_seq,
                                wfmt=pipo.PIPO_W_INT4_G64 if args.wfmt == "int4" else pipo.PIPO_W_FP16,
@@ -582,7 +592,10 @@ def run_pipo(args):
                                chunk_bytes=int(args.chunk_mb * (1 << 20)), disk_dir=disk_dir, flags=flags)
         t0 = time.perf_counter()
         pl = pipo.Pipeline(cfg)
-        if shard:
+        if shard and args.shard_transport == "p2p":
+            h = pipo.pipo_shard_p2p_export(pl.ctx, rank, world)
+            pipo.pipo_shard_p2p_init(pl.ctx, gather_list(h))
+        elif shard:
             uid = pipo.pipo_nccl_unique_id() if rank == 0 else bytes(128)
             if world > 1:
                 t = torch.tensor(list(uid), dtype=torch.uint8, device="cpu" if shared_gpu else f"cuda:{local}")
@@ -599,13 +612,6 @@ def run_pipo(args):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(local)
-
-    def gather_list(x):
-        if world == 1:
-            return [x]
-        out = [None] * world
-        dist.all_gather_object(out, x)
-        return out
 
     pl, t_load = make_pipeline(args.shard_stream)
     link_probe = pipo.pipo_probe_h2d(pl.ctx, 256 << 20, 5)
@@ -756,7 +762,8 @@ def run_pipo(args):
     pl.close()
 
     # ---- NEXT-1 variant at N > 1: sharded streaming timed in the same run ----
-    if world > 1 and not shared_gpu and not args.no_variants and not args.shard_stream and c["weight_tier"] == 1:
+    if world > 1 and not args.no_variants and not args.shard_stream and c["weight_tier"] == 1 and \
+            (args.shard_transport == "p2p" or not shared_gpu):   # NCCL refuses two ranks on one GPU
         try:
             pv, t_load_v = make_pipeline(True)
             nv, _ = pv.prefill(prompt)
@@ -784,8 +791,11 @@ def run_pipo(args):
                     "per_rank_link_bytes_per_step": int(per_rank_link),
                     "link_frac": per_rank_link / (link_probe * 1e9) / (t_v / args.steps),
                     "union_busy": sv["union_busy"], "load_s": t_load_v,
-                    "how": "each rank streams 1/N of every layer over its own PCIe link; NCCL all-gather over "
-                           "NVLink on its own stream (ring 3); compute batch-sharded as the main line"}}
+                    "transport": args.shard_transport,
+                    "how": "each rank streams 1/N of every layer over its own PCIe link; the other ranges come from "
+                           "the peers' HBM rings over NVLink on a gather stream (p2p: copy-engine pulls through CUDA "
+                           "IPC ordered by flags in peer memory; nccl: all-gather), ring 3; compute batch-sharded as "
+                           "the main line"}}
         except Exception as e:  # noqa: BLE001  (report the variant's failure, keep the main line)
             if rank == 0:
                 line["variants"] = {"shard_stream": {"error": str(e)[:300]}}

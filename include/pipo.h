@@ -367,6 +367,22 @@ pipo_status pipo_nccl_unique_id(uint8_t id[128]);
  * already loaded), OOM, CUDA (NCCL missing or failing). */
 pipo_status pipo_shard_stream_init(pipo_ctx* ctx, int32_t rank, int32_t world, const uint8_t id[128]);
 
+/* Peer transport for sharded streaming (no NCCL): the gather is the copy engines pulling
+ * each peer's range straight out of the peer's HBM ring slot over NVLink (CUDA IPC
+ * mappings), ordered by flags in peer memory (a 1-thread wait kernel before, a release
+ * store after — the same ordering protocol on one box whatever the GPU count; two
+ * processes may even share one GPU, which is how the N-rank path is tested on 1 GPU).
+ * Every rank: (1) pipo_shard_p2p_export -> a PIPO_SHARD_HANDLE_BYTES blob (allocates the
+ * padded ring + this rank's host store, nothing switched yet); the caller all-gathers the
+ * blobs in rank order (any host collective); (2) pipo_shard_p2p_init with all of them
+ * (opens the peers' rings; on success the context streams sharded, on failure it is
+ * unchanged).  Before any weights are loaded; HOST tier; world <= 8.
+ * Errors: INVALID_ARG (rank/world/tier, blob of another world), STATE (weights loaded,
+ * already sharded, init without export), OOM, CUDA (IPC / peer access failure). */
+#define PIPO_SHARD_HANDLE_BYTES 128
+pipo_status pipo_shard_p2p_export(pipo_ctx* ctx, int32_t rank, int32_t world, uint8_t handle[PIPO_SHARD_HANDLE_BYTES]);
+pipo_status pipo_shard_p2p_init(pipo_ctx* ctx, const uint8_t* handles);
+
 /* ---- automatic configuration (NEXT-3): memory model + Eq. (1) ---------------
  * Host-only pure functions (no context, no GPU).  The paper states them for
  * LLaMA3.1 (§3.5, App. B); readings Q23-Q27 in

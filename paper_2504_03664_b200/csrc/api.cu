@@ -224,6 +224,7 @@ const __half* vec_ptr(const pipo_ctx* c, const uint8_t* blob, int v) {
 }
 
 bool streamed(const pipo_ctx* c) { return c->weight_tier != PIPO_TIER_DEVICE; }
+bool sharded(const pipo_ctx* c) { return c->shard_mode != 0; }   // NEXT-1: rank keeps 1/world of each blob
 bool host_kv(const pipo_ctx* c) { return c->kv_tier == PIPO_TIER_HOST; }
 
 uint8_t* kv_region(pipo_ctx* c, int layer, int which, int64_t G) {
@@ -299,7 +300,46 @@ pipo_status enqueue_copy(pipo_ctx* ctx, int64_t G, int64_t kv_pos) {
       bytes += ctx->lay.seg_bytes[s];
       TRY(after_segment(s, ctx->s_copy));
     }
-  } else if (ctx->nccl_comm) {
+  } else if (ctx->shard_mode == 2) {
+    // NEXT-1 sharded streaming, peer transport: this rank's 1/world over its own host
+    // link (copy stream), then the copy engines pull every peer's range of the same layer
+    // straight out of the peer's ring slot over NVLink (gather stream).  Flags in peer
+    // memory order it across processes: a peer's range is read only after that peer
+    // posted the layer; this rank's slot is overwritten only after every peer copied its
+    // range of the layer the slot held (R layers earlier).
+    const int64_t S = ctx->shard_bytes;
+    const int W = ctx->shard_world, me = ctx->shard_rank;
+    if (G >= ctx->R) {
+      P2PFlags war{};
+      for (int p = 0; p < W; ++p)
+        if (p != me) war.addr[war.n++] = ctx->own_flags + 1 + p;
+      LAUNCH(launch_p2p_wait(war, (int)(G - ctx->R + 1), ctx->s_copy));
+    }
+    TRY(copy_chunks(ctx, dst + (int64_t)me * S, ctx->host_store + (int64_t)j * S, S));
+    bytes += S;
+    P2PFlags post{};
+    post.addr[post.n++] = ctx->own_flags;
+    LAUNCH(launch_p2p_signal(post, (int)(G + 1), ctx->s_copy));
+    CK(cudaEventRecord(ctx->ev_h2d[slot], ctx->s_copy));
+    CK(cudaStreamWaitEvent(ctx->s_gather, ctx->ev_h2d[slot], 0));   // (also orders after ev_free)
+    cudaEvent_t g0 = nullptr;
+    TRY(span_begin(ctx, ctx->s_gather, &g0));
+    P2PFlags ready{}, done{};
+    for (int p = 0; p < W; ++p)
+      if (p != me) {
+        const int* pf = reinterpret_cast<const int*>(ctx->peer_ring[p] + (int64_t)ctx->R * ctx->layer_bytes);
+        ready.addr[ready.n++] = const_cast<int*>(pf);
+        done.addr[done.n++] = const_cast<int*>(pf) + 1 + me;
+      }
+    LAUNCH(launch_p2p_wait(ready, (int)(G + 1), ctx->s_gather));
+    for (int p = 0; p < W; ++p)
+      if (p != me)
+        CK(cudaMemcpyAsync(dst + (int64_t)p * S, ctx->peer_ring[p] + (int64_t)slot * ctx->layer_bytes + (int64_t)p * S,
+                           (size_t)S, cudaMemcpyDeviceToDevice, ctx->s_gather));
+    LAUNCH(launch_p2p_signal(done, (int)(G + 1), ctx->s_gather));
+    TRY(span_end(ctx, ctx->s_gather, g0, 3, S * (W - 1)));
+    for (int s = 0; s < 4; ++s) TRY(after_segment(s, ctx->s_gather));
+  } else if (ctx->shard_mode == 1) {
     // NEXT-1 sharded streaming: this rank's 1/world of the blob over its own host link
     // (copy stream), then the other ranks' ranges over NVLink by an in-place NCCL
     // all-gather on its OWN stream, ordered after this rank's H2D by an event — so the
@@ -863,6 +903,10 @@ void pipeline_destroy(pipo_ctx* ctx) {
   cudaGetLastError();
   if (ctx->disk) disk_close(ctx);
   if (ctx->nccl_comm) nccl_comm_destroy(ctx->nccl_comm);
+  for (auto& p : ctx->peer_ring)
+    if (p) cudaIpcCloseMemHandle(p);
+  if (ctx->pend_ring) cudaFree(ctx->pend_ring);
+  if (ctx->pend_store) host_free(ctx, ctx->pend_store, (int64_t)ctx->l * ctx->pend_S);
   if (ctx->head == ctx->tok) ctx->head = nullptr;
   void* dev[] = {ctx->tok, ctx->head, ctx->gu, ctx->rope_inv, ctx->pos, ctx->lnf_g, ctx->lnf_b, ctx->dev_store, ctx->ring, ctx->kv_dev, ctx->kv_slot, ctx->kv_stage,
                  ctx->h, ctx->xa, ctx->q, ctx->u, ctx->logits, ctx->ids, ctx->next, ctx->ws, ctx->counters,
@@ -936,7 +980,7 @@ pipo_status load_layer_weights(pipo_ctx* ctx, int32_t layer, const void* w) {
   const pipo_layer_weights* lw = static_cast<const pipo_layer_weights*>(w);
   uint8_t* dst = nullptr;
   std::vector<uint8_t> tmp;
-  if (ctx->weight_tier == PIPO_TIER_HOST && !ctx->nccl_comm) {
+  if (ctx->weight_tier == PIPO_TIER_HOST && !sharded(ctx)) {
     dst = ctx->host_store + (int64_t)layer * ctx->layer_bytes;
   } else {
     tmp.resize((size_t)ctx->layer_bytes);
@@ -944,7 +988,7 @@ pipo_status load_layer_weights(pipo_ctx* ctx, int32_t layer, const void* w) {
   }
   if (!build_layer_blob(lw, ctx->lay, ctx->wfmt, dst))
     return set_err(PIPO_E_INVALID_ARG, "non-finite weight, NULL tensor or fp16-overflowing group scale");
-  if (ctx->nccl_comm)   // sharded streaming: keep only this rank's range (padding is zero)
+  if (sharded(ctx))   // sharded streaming: keep only this rank's range (padding is zero)
     std::memcpy(ctx->host_store + (int64_t)layer * ctx->shard_bytes, dst + (int64_t)ctx->shard_rank * ctx->shard_bytes,
                 (size_t)ctx->shard_bytes);
   if (ctx->weight_tier == PIPO_TIER_DEVICE)
@@ -1050,7 +1094,7 @@ pipo_status pipo_load_synthetic(pipo_ctx* ctx, int32_t layer, uint64_t seed) {
     }
   }
   if (s == PIPO_OK && !direct) {
-    if (ctx->nccl_comm) {   // sharded streaming: this rank's range only
+    if (sharded(ctx)) {   // sharded streaming: this rank's range only
       CK(cudaMemcpyAsync(ctx->host_store + (int64_t)layer * ctx->shard_bytes,
                          blob + (int64_t)ctx->shard_rank * ctx->shard_bytes, (size_t)ctx->shard_bytes,
                          cudaMemcpyDeviceToHost, st));
@@ -1162,7 +1206,7 @@ pipo_status pipeline_stats(pipo_ctx* ctx, pipo_stats* out) {
   s.timeline_truncated = ctx->timeline_truncated ? 1 : 0;
   s.numa_local_frac = -1.0;
   if (ctx->numa_node >= 0 && ctx->host_store)
-    s.numa_local_frac = numa_local_fraction(ctx->host_store, ctx->nccl_comm ? (int64_t)ctx->l * ctx->shard_bytes
+    s.numa_local_frac = numa_local_fraction(ctx->host_store, sharded(ctx) ? (int64_t)ctx->l * ctx->shard_bytes
                                                                            : (int64_t)ctx->l * ctx->layer_bytes,
                                             ctx->numa_node, 64);
   if (ctx->win_open && ctx->win_closed) {
@@ -1691,7 +1735,7 @@ pipo_status pipo_shard_stream_init(pipo_ctx* ctx, int32_t rank, int32_t world, c
   CHECK_CTX();
   if (!id || world <= 0 || rank < 0 || rank >= world) return set_err(PIPO_E_INVALID_ARG, "bad rank/world");
   if (ctx->weight_tier != PIPO_TIER_HOST) return set_err(PIPO_E_INVALID_ARG, "sharded streaming needs the HOST tier");
-  if (ctx->nccl_comm) return set_err(PIPO_E_STATE, "sharded streaming already initialised");
+  if (sharded(ctx)) return set_err(PIPO_E_STATE, "sharded streaming already initialised");
   for (int j = 0; j < ctx->l; ++j)
     if (ctx->layer_loaded[j]) return set_err(PIPO_E_STATE, "call pipo_shard_stream_init before loading weights");
   CK(cudaSetDevice(ctx->cfg.device));
@@ -1742,6 +1786,99 @@ pipo_status pipo_shard_stream_init(pipo_ctx* ctx, int32_t rank, int32_t world, c
   ctx->s_gather = gather;
   for (int i = 0; i < kMaxRing; ++i) ctx->ev_h2d[i] = evs[i];
   ctx->nccl_comm = comm;
+  ctx->shard_mode = 1;
+  return PIPO_OK;
+}
+
+pipo_status pipo_shard_p2p_export(pipo_ctx* ctx, int32_t rank, int32_t world, uint8_t handle[PIPO_SHARD_HANDLE_BYTES]) {
+  CHECK_CTX();
+  if (!handle || world <= 0 || world > 8 || rank < 0 || rank >= world)
+    return set_err(PIPO_E_INVALID_ARG, "bad rank/world (world <= 8)");
+  if (ctx->weight_tier != PIPO_TIER_HOST) return set_err(PIPO_E_INVALID_ARG, "sharded streaming needs the HOST tier");
+  if (sharded(ctx)) return set_err(PIPO_E_STATE, "sharded streaming already initialised");
+  for (int j = 0; j < ctx->l; ++j)
+    if (ctx->layer_loaded[j]) return set_err(PIPO_E_STATE, "export before loading weights");
+  CK(cudaSetDevice(ctx->cfg.device));
+  if (ctx->pend_ring) { cudaFree(ctx->pend_ring); ctx->hbm_bytes -= ctx->pend_ring_bytes; ctx->pend_ring = nullptr; }
+  if (ctx->pend_store) { host_free(ctx, ctx->pend_store, (int64_t)ctx->l * ctx->pend_S); ctx->pend_store = nullptr; }
+  int64_t off = 0, S = 0;
+  TRY(pipo_shard_range(ctx->lay.total, world, rank, &off, &S));
+  const int64_t ring_bytes = (int64_t)ctx->R * S * world + 4096;   // + the flags page
+  TRY(dev_alloc(ctx, &ctx->pend_ring, ring_bytes));
+  ctx->pend_ring_bytes = ring_bytes;
+  CK(cudaMemset(ctx->pend_ring, 0, (size_t)ring_bytes));
+  TRY(host_alloc(ctx, &ctx->pend_store, (int64_t)ctx->l * S, true));
+  ctx->pend_S = S;
+  ctx->pend_rank = rank;
+  ctx->pend_world = world;
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, ctx->pend_ring));
+  std::memset(handle, 0, PIPO_SHARD_HANDLE_BYTES);
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  std::memcpy(handle, &h, 64);
+  const int64_t meta[4] = {(int64_t)rank, (int64_t)world, ring_bytes, (int64_t)ctx->R};
+  std::memcpy(handle + 64, meta, sizeof meta);
+  return PIPO_OK;
+}
+
+pipo_status pipo_shard_p2p_init(pipo_ctx* ctx, const uint8_t* handles) {
+  CHECK_CTX();
+  if (!handles) return set_err(PIPO_E_INVALID_ARG, "handles is NULL");
+  if (!ctx->pend_ring) return set_err(PIPO_E_STATE, "pipo_shard_p2p_export first");
+  if (sharded(ctx)) return set_err(PIPO_E_STATE, "sharded streaming already initialised");
+  CK(cudaSetDevice(ctx->cfg.device));
+  const int W = ctx->pend_world, me = ctx->pend_rank;
+  for (int p = 0; p < W; ++p) {
+    int64_t meta[4];
+    std::memcpy(meta, handles + (size_t)p * PIPO_SHARD_HANDLE_BYTES + 64, sizeof meta);
+    if (meta[0] != p || meta[1] != W || meta[2] != ctx->pend_ring_bytes || meta[3] != ctx->R)
+      return set_err(PIPO_E_INVALID_ARG, "handle " + std::to_string(p) + " is not rank " + std::to_string(p) +
+                                             " of this sharded configuration");
+  }
+  cudaStream_t gather = nullptr;
+  cudaEvent_t evs[kMaxRing] = {};
+  uint8_t* opened[8] = {};
+  auto unwind = [&](pipo_status st) {
+    for (auto& o : opened)
+      if (o) cudaIpcCloseMemHandle(o);
+    if (gather) cudaStreamDestroy(gather);
+    for (auto& e : evs)
+      if (e) cudaEventDestroy(e);
+    cudaGetLastError();
+    return st;
+  };
+  for (int p = 0; p < W; ++p) {
+    if (p == me) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handles + (size_t)p * PIPO_SHARD_HANDLE_BYTES, 64);
+    void* ptr = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess)
+      return unwind(set_err(PIPO_E_CUDA, std::string("cudaIpcOpenMemHandle of rank ") + std::to_string(p) + ": " +
+                                             cudaGetErrorString(e)));
+    opened[p] = static_cast<uint8_t*>(ptr);
+  }
+  if (cudaStreamCreateWithFlags(&gather, cudaStreamNonBlocking) != cudaSuccess)
+    return unwind(set_err(PIPO_E_CUDA, "gather stream"));
+  for (auto& e : evs)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return unwind(set_err(PIPO_E_CUDA, "events"));
+  // commit
+  CK(cudaDeviceSynchronize());
+  if (ctx->ring) { cudaFree(ctx->ring); ctx->hbm_bytes -= (int64_t)ctx->R * ctx->layer_bytes; }
+  host_free(ctx, ctx->host_store, (int64_t)ctx->l * ctx->layer_bytes);
+  ctx->ring = ctx->pend_ring;
+  ctx->host_store = ctx->pend_store;
+  ctx->pend_ring = nullptr;
+  ctx->pend_store = nullptr;
+  ctx->shard_bytes = ctx->pend_S;
+  ctx->layer_bytes = ctx->pend_S * W;
+  ctx->shard_rank = me;
+  ctx->shard_world = W;
+  ctx->own_flags = reinterpret_cast<int*>(ctx->ring + (int64_t)ctx->R * ctx->layer_bytes);
+  for (int p = 0; p < W; ++p) ctx->peer_ring[p] = opened[p];
+  ctx->s_gather = gather;
+  for (int i = 0; i < kMaxRing; ++i) ctx->ev_h2d[i] = evs[i];
+  ctx->shard_mode = 2;
   return PIPO_OK;
 }
 
@@ -1784,7 +1921,7 @@ pipo_status pipo_debug_read_rows(pipo_ctx* ctx, int32_t layer, int32_t matrix, i
     glu = ctx->lay.glu && matrix == M_FC1;
     if (ctx->weight_tier == PIPO_TIER_DEVICE) {
       base = ctx->dev_store + (int64_t)layer * ctx->layer_bytes + ctx->lay.mat_off[matrix];
-    } else if (ctx->weight_tier == PIPO_TIER_HOST && !ctx->nccl_comm) {
+    } else if (ctx->weight_tier == PIPO_TIER_HOST && !sharded(ctx)) {
       base = ctx->host_store + (int64_t)layer * ctx->layer_bytes + ctx->lay.mat_off[matrix];
       on_device = false;
     } else {

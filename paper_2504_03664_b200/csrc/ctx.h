@@ -68,6 +68,16 @@ struct pipo_ctx {
   int shard_rank = 0, shard_world = 1;
   int64_t shard_bytes = 0;         // per-rank range; host_store holds l * shard_bytes
   void* nccl_comm = nullptr;       // ncclComm_t
+  int shard_mode = 0;              // 0 plain, 1 NCCL all-gather, 2 peer copies (CUDA IPC)
+  // peer transport: pending allocations between export and init, then the peers' rings
+  // (IPC mappings; the flags live in the last 4 KiB of every ring allocation:
+  // [0] = layers this rank has landed, [1 + p] = layers of this rank's ring peer p copied)
+  uint8_t* pend_ring = nullptr;
+  uint8_t* pend_store = nullptr;
+  int64_t pend_ring_bytes = 0, pend_S = 0;
+  int pend_rank = -1, pend_world = 0;
+  uint8_t* peer_ring[8] = {};
+  int* own_flags = nullptr;
   pipo::DiskTier* disk = nullptr;
 
   // KV cache: position-major [pos][b][d] per (layer, K/V)

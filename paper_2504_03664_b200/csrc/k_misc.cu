@@ -331,3 +331,44 @@ int launch_f16_to_f32(const __half* src, float* dst, int64_t n, cudaStream_t st)
 }
 
 }  // namespace pipo
+
+namespace pipo {
+
+// ---- NEXT-1 peer transport: cross-process flags in peer (CUDA IPC) memory ----------
+// One thread per flag: spin until *addr >= target (acquire at system scope: the flag
+// lives in another process's — possibly another GPU's — memory, written after that
+// process's copy engine filled the data it guards).
+__global__ void p2p_wait_kernel(P2PFlags f, int target) {
+  const int i = threadIdx.x;
+  if (i >= f.n) return;
+  const int* p = f.addr[i];
+  int v;
+  while (true) {
+    asm volatile("ld.acquire.sys.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    if (v >= target) break;
+    __nanosleep(256);
+  }
+}
+
+// One thread per flag: publish `value` (release at system scope, after everything the
+// stream ordered before this kernel — the copies it signals — has completed).
+__global__ void p2p_signal_kernel(P2PFlags f, int value) {
+  const int i = threadIdx.x;
+  if (i >= f.n) return;
+  __threadfence_system();
+  asm volatile("st.release.sys.global.b32 [%0], %1;\n" ::"l"(f.addr[i]), "r"(value) : "memory");
+}
+
+int launch_p2p_wait(const P2PFlags& f, int target, cudaStream_t st) {
+  if (f.n <= 0) return 0;
+  p2p_wait_kernel<<<1, 32, 0, st>>>(f, target);
+  return 1;
+}
+
+int launch_p2p_signal(const P2PFlags& f, int value, cudaStream_t st) {
+  if (f.n <= 0) return 0;
+  p2p_signal_kernel<<<1, 32, 0, st>>>(f, value);
+  return 1;
+}
+
+}  // namespace pipo

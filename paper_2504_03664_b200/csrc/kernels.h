@@ -126,4 +126,12 @@ int launch_synth(float* out, int64_t start, int64_t count, uint64_t key, int kin
 uint64_t synth_key(uint64_t seed, uint32_t slot, uint32_t tid);
 float synth_scale(int kind, double param);
 
+// NEXT-1 peer transport (k_misc.cu): flags in peer memory, <= 8 per launch
+struct P2PFlags {
+  int* addr[8];
+  int n;
+};
+int launch_p2p_wait(const P2PFlags& f, int target, cudaStream_t st);     // all *addr >= target
+int launch_p2p_signal(const P2PFlags& f, int value, cudaStream_t st);    // all *addr = value
+
 }  // namespace pipo

@@ -147,6 +147,8 @@ _sig("pipo_gpu_numa_node", C.c_int32, C.c_int32)
 _sig("pipo_shard_range", C.c_int, C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64))
 _sig("pipo_nccl_unique_id", C.c_int, _u8)
 _sig("pipo_shard_stream_init", C.c_int, _P, C.c_int32, C.c_int32, _u8)
+_sig("pipo_shard_p2p_export", C.c_int, _P, C.c_int32, C.c_int32, _u8)
+_sig("pipo_shard_p2p_init", C.c_int, _P, _u8)
 _sig("pipo_debug_capture", C.c_int, _P, C.c_int32, _f)
 _sig("pipo_probe_h2d", C.c_int, _P, C.c_int64, C.c_int32, C.POINTER(C.c_double))
 _sig("pipo_debug_read_rows", C.c_int, _P, C.c_int32, C.c_int32, C.c_int64, C.c_int64, _u8, _u16, _u16)
@@ -163,7 +165,7 @@ EXPORTED = ["pipo_last_error", "pipo_abi_version", "pipeline_init", "pipeline_de
             "pipo_load_synthetic", "prefill", "decode_step", "decode_step_dev", "pipeline_stats",
             "pipeline_stats_reset", "pipo_stream", "pipo_kernel_stats", "pipo_quantize_int4_g64", "pipo_quantize_int4_g64_gpu",
             "pipo_unpack_int4_g64", "pipo_linear", "pipo_bench_linear", "pipo_probe_bulk", "pipo_bench_attention", "pipo_attention_decode", "pipo_attention_prefill", "pipo_debug_capture", "pipo_probe_h2d", "pipo_debug_read_rows",
-            "pipo_attention_gqa", "pipo_rope", "pipo_set_flags", "pipo_shard_range", "pipo_gpu_numa_node", "pipo_nccl_unique_id", "pipo_shard_stream_init",
+            "pipo_attention_gqa", "pipo_rope", "pipo_set_flags", "pipo_shard_range", "pipo_gpu_numa_node", "pipo_nccl_unique_id", "pipo_shard_stream_init", "pipo_shard_p2p_export", "pipo_shard_p2p_init",
             "pipo_ffn_hidden_dim", "pipo_memory_model", "pipo_choose_block_size", "pipo_choose_plan", "pipo_get_plan"]
 
 
@@ -394,6 +396,22 @@ def pipo_shard_stream_init(ctx, rank: int, world: int, uid: bytes):
     buf = np.frombuffer(uid, dtype=np.uint8).copy()
     assert buf.size == 128
     _check(_lib.pipo_shard_stream_init(ctx, rank, world, _ptr(buf, C.c_uint8)))
+
+
+PIPO_SHARD_HANDLE_BYTES = 128
+
+
+def pipo_shard_p2p_export(ctx, rank: int, world: int) -> bytes:
+    buf = np.zeros(PIPO_SHARD_HANDLE_BYTES, dtype=np.uint8)
+    _check(_lib.pipo_shard_p2p_export(ctx, rank, world, _ptr(buf, C.c_uint8)))
+    return buf.tobytes()
+
+
+def pipo_shard_p2p_init(ctx, handles: list):
+    """handles: every rank's export blob, in rank order."""
+    buf = np.frombuffer(b"".join(handles), dtype=np.uint8).copy()
+    assert buf.size == PIPO_SHARD_HANDLE_BYTES * len(handles)
+    _check(_lib.pipo_shard_p2p_init(ctx, _ptr(buf, C.c_uint8)))
 
 
 def pipo_set_flags(ctx, flags: int):
