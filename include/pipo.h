@@ -263,7 +263,9 @@ pipo_status pipo_unpack_int4_g64(pipo_ctx* ctx, const uint8_t* codes, const uint
  * 2 = mma.sync GEMM (legacy baseline), 3 = tcgen05/TMEM GEMM (synchronous pipeline),
  * 4 = warp-specialized stream-K tcgen05 GEMM (int4, A in shared memory),
  * 5 = same with A in TMEM (int4, M <= 64), 6 = prefill tcgen05 GEMM with A in TMEM
- * (int4, any M; static persistent tile schedule). */
+ * (int4, any M; static persistent tile schedule), 7 = streaming fp16-weight tcgen05 GEMM
+ * (fp16, M <= 64: TMA-fed, warp-specialized; the fp16 decode linears), 8 = the same kernel
+ * as the LM head (a13) runs it. */
 pipo_status pipo_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, const uint16_t* x,
                         const float* w, const float* bias, int32_t M, int32_t N, int32_t K,
                         float* y);

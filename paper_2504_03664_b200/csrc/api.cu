@@ -551,7 +551,8 @@ pipo_status forward_pass(pipo_ctx* ctx, int b, int n, int past, bool want_logits
   la.x = ctx->xa; la.w = reinterpret_cast<const uint8_t*>(ctx->head); la.wfmt = 0; la.M = b; la.N = ctx->V; la.K = d;
   la.epi = EpiParams{};
   la.epi.kind = EPI_F32; la.epi.M = b; la.epi.N = ctx->V; la.epi.y = ctx->logits; la.epi.ldy = ctx->V;
-  TRY(run_linear(ctx, la, PATH_GEMM, PIPO_K_HEAD));
+  // LM head: the streaming tcgen05 kernel for b <= 64, else the tile GEMM
+  TRY(run_linear(ctx, la, b <= 64 ? PATH_HEAD : PATH_TC, PIPO_K_HEAD));
   LAUNCH(launch_argmax(ctx->logits, b, ctx->V, ctx->V, ctx->next, cs));
   TRY(span_end(ctx, cs, t0, 1, 0));
   (void)want_logits;
@@ -1351,7 +1352,7 @@ pipo_status pipo_unpack_int4_g64(pipo_ctx* ctx, const uint8_t* codes, const uint
 pipo_status pipo_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, const uint16_t* x, const float* w,
                         const float* bias, int32_t M, int32_t N, int32_t K, float* y) {
   CHECK_CTX();
-  if (!x || !w || !y || M <= 0 || N <= 0 || K <= 0 || K % 64 || (wfmt != 0 && wfmt != 1) || path < 0 || path > 6)
+  if (!x || !w || !y || M <= 0 || N <= 0 || K <= 0 || K % 64 || (wfmt != 0 && wfmt != 1) || path < 0 || path > 8)
     return set_err(PIPO_E_INVALID_ARG, "bad linear arguments");
   CK(cudaSetDevice(ctx->cfg.device));
   const MatLayout ml = mat_layout(N, K, wfmt);
@@ -1392,7 +1393,7 @@ pipo_status pipo_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, const uint16_
 pipo_status pipo_bench_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, int32_t M, int32_t N, int32_t K,
                               int32_t iters, double* us) {
   CHECK_CTX();
-  if (!us || M <= 0 || N <= 0 || K <= 0 || K % 64 || iters <= 0 || (wfmt != 0 && wfmt != 1) || path < 0 || path > 6)
+  if (!us || M <= 0 || N <= 0 || K <= 0 || K % 64 || iters <= 0 || (wfmt != 0 && wfmt != 1) || path < 0 || path > 8)
     return set_err(PIPO_E_INVALID_ARG, "bad bench arguments");
   CK(cudaSetDevice(ctx->cfg.device));
   const MatLayout ml = mat_layout(N, K, wfmt);

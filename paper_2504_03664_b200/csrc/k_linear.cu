@@ -330,6 +330,8 @@ int launch_linear(const LinearArgs& a, int path, int gemv_max_m, cudaStream_t st
   // >= M zero-filled by TMA) streams 1.5-2.6x faster even at M = 1 (c7: FC1 72 -> 27 us,
   // profiles/r01/gemv_crossover; reading Q4 "re-tune the crossover by measurement")
   else if (path == PATH_AUTO) gemv = (a.wfmt == 1 && a.M <= gemv_max_m && (int64_t)a.N * a.K < (8ll << 20));
+  if (path == PATH_HEAD) return launch_linear_stream_f16(a, true, st);
+  if (path == PATH_STREAM || (path == PATH_AUTO && a.wfmt == 0 && a.M <= 64)) return launch_linear_stream_f16(a, false, st);
   if (path == PATH_TP || (path == PATH_AUTO && !gemv && a.wfmt == 1 && a.M > 128)) return launch_linear_tp(a, st);
   if (path == PATH_TM || (path == PATH_AUTO && !gemv && a.wfmt == 1 && a.M <= 64)) return launch_linear_tm(a, st);
   if (path == PATH_WS || (path == PATH_AUTO && !gemv && a.wfmt == 1 && a.M <= 128)) return launch_linear_ws(a, st);

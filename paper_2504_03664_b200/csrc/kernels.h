@@ -47,7 +47,12 @@ struct LinearArgs {
   int num_sms = 148;
 };
 
-enum LinearPath { PATH_AUTO = 0, PATH_GEMV = 1, PATH_GEMM = 2, PATH_TC = 3, PATH_WS = 4, PATH_TM = 5, PATH_TP = 6 };
+enum LinearPath { PATH_AUTO = 0, PATH_GEMV = 1, PATH_GEMM = 2, PATH_TC = 3, PATH_WS = 4, PATH_TM = 5, PATH_TP = 6,
+                  PATH_STREAM = 7, PATH_HEAD = 8 };
+
+// streaming fp16-weight tcgen05 GEMM, M <= 64 (k_head.cu): the LM head (lm_head = true,
+// PATH_HEAD) and the fp16 decode linears (PATH_STREAM)
+int launch_linear_stream_f16(const LinearArgs& a, bool lm_head, cudaStream_t st);
 
 // warp-specialized stream-K tcgen05 GEMM with A in TMEM, int4 weights, M <= 64
 int launch_linear_tm(const LinearArgs& a, cudaStream_t st);

@@ -26,7 +26,7 @@ PIPO_F_KPROF = 2
 PIPO_F_AUTO_PLAN = 4
 K_CLASSES = ["linear_decode", "attn_decode", "lm_head", "linear_prefill", "attn_prefill", "misc"]
 PIPO_LAYER_EMBED = -1
-PATH_AUTO, PATH_GEMV, PATH_GEMM, PATH_TC, PATH_WS, PATH_TM, PATH_TP = 0, 1, 2, 3, 4, 5, 6
+PATH_AUTO, PATH_GEMV, PATH_GEMM, PATH_TC, PATH_WS, PATH_TM, PATH_TP, PATH_STREAM, PATH_HEAD = 0, 1, 2, 3, 4, 5, 6, 7, 8
 
 _f = C.POINTER(C.c_float)
 _u8 = C.POINTER(C.c_uint8)

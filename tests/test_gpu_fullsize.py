@@ -29,16 +29,17 @@ def env():
     pl.close()
 
 
-def _sampled_linear_check(pipo, pl, M, N, K, path, seed, n_rows=384, m_rows=None, tol=2e-3):
+def _sampled_linear_check(pipo, pl, M, N, K, path, seed, n_rows=384, m_rows=None, tol=2e-3, wfmt=1):
     rng = np.random.default_rng(seed)
     x = rng.standard_normal((M, K), dtype=np.float32).astype(np.float16)
     w = (rng.standard_normal((N, K), dtype=np.float32) * np.float32(0.02)).astype(np.float16).astype(np.float32)
     bias = rng.uniform(-0.02, 0.02, N).astype(np.float32)
-    y = pipo.pipo_linear(pl.ctx, 1, path, x, w, bias)
+    y = pipo.pipo_linear(pl.ctx, wfmt, path, x, w, bias)
     rows = np.sort(rng.choice(N, n_rows, replace=False))
     rows[0], rows[-1] = 0, N - 1                              # first and last (ragged) tile
     ms = np.arange(M) if m_rows is None else np.sort(rng.choice(M, m_rows, replace=False))
-    wh = quant.quant_dequant(np.ascontiguousarray(w[rows])).astype(np.float64)
+    wsel = np.ascontiguousarray(w[rows])
+    wh = (quant.quant_dequant(wsel) if wfmt == 1 else wsel).astype(np.float64)
     ref = x[ms].astype(np.float64) @ wh.T + bias[rows].astype(np.float16).astype(np.float64)
     err = rel_inf(y[np.ix_(ms, rows)], ref)
     assert err < 2e-2 and err < tol, (M, N, K, err)
@@ -50,6 +51,15 @@ def _sampled_linear_check(pipo, pl, M, N, K, path, seed, n_rows=384, m_rows=None
 def test_decode_linear_fullsize(env, name, N, K):
     pipo, pl = env
     _sampled_linear_check(pipo, pl, 64, N, K, pipo.PATH_AUTO, N + K)
+
+
+@pytest.mark.parametrize("name,M,N,K", [("c5_head", 64, 50272, 7168), ("c6_head", 64, 128256, 4096),
+                                        ("c7_head", 1, 128256, 4096)])
+def test_lm_head_fullsize(env, name, M, N, K):
+    """The LM head (a13) at the c5 / c6 / c7 shapes through the streaming fp16 tcgen05
+    kernel the pipeline launches (PATH_HEAD), sampled vocabulary rows against fp64."""
+    pipo, pl = env
+    _sampled_linear_check(pipo, pl, M, N, K, pipo.PATH_HEAD, N + 1, wfmt=0, tol=1e-4)
 
 
 def test_decode_linear_fullsize_b1_gemv(env):

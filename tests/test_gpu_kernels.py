@@ -75,7 +75,7 @@ def test_linear_vs_oracle(env, M, N, K, wfmt):
     ref = _ref_linear(x, w, bias, wfmt)
     paths = [pipo.PATH_TC, pipo.PATH_GEMM] + ([pipo.PATH_GEMV] if wfmt == 1 and M <= 16 else []) + \
         ([pipo.PATH_WS] if wfmt == 1 and M <= 128 else []) + ([pipo.PATH_TM] if wfmt == 1 and M <= 64 else []) + \
-        ([pipo.PATH_TP] if wfmt == 1 else [])
+        ([pipo.PATH_TP] if wfmt == 1 else []) + ([pipo.PATH_STREAM, pipo.PATH_HEAD] if wfmt == 0 and M <= 64 else [])
     for path in paths:
         y = pipo.pipo_linear(pl.ctx, wfmt, path, x, w, bias)
         err = rel_inf(y, ref)
@@ -204,3 +204,30 @@ def test_attention_prefill_vs_oracle(env, b, n, past, d, H, cuda_cores):
     assert rel_inf(o, ref) < 2e-2
     # P is rounded to fp16 before P.V on the tensor-core path
     assert rel_inf(o, ref) < (5e-3 if cuda_cores else 1e-2)
+
+
+@pytest.mark.parametrize("path", ["stream", "head"])
+@pytest.mark.parametrize("M", [1, 16, 33, 64])
+def test_linear_fp16_stream_exact(env, path, M):
+    """The streaming fp16 tcgen05 GEMM (LM head a13 / fp16 decode linears): x = 0 gives the
+    bias exactly, one-hot rows give the fp16 weight column exactly (one fp32 rounding of
+    w + b), power-of-two scaling is exact; ragged N (last 128-row tile partly padding) and
+    M below the tile width (TMA zero-fill)."""
+    pipo, pl = env
+    p = pipo.PATH_STREAM if path == "stream" else pipo.PATH_HEAD
+    rng = np.random.default_rng(M + 3)
+    N, K = 300, 320
+    w = (rng.standard_normal((N, K)) * 0.02).astype(np.float16).astype(np.float32)
+    bias = rng.uniform(-0.02, 0.02, N).astype(np.float16).astype(np.float32)
+    y0 = pipo.pipo_linear(pl.ctx, 0, p, np.zeros((M, K), np.float16), w, bias)
+    assert np.array_equal(y0, np.broadcast_to(bias, (M, N)))
+    x = np.zeros((M, K), np.float16)
+    ks = (np.arange(M) * 37) % K
+    x[np.arange(M), ks] = 1
+    y = pipo.pipo_linear(pl.ctx, 0, p, x, w, bias)
+    assert np.array_equal(y, (w[:, ks].T + bias).astype(np.float32))
+    x = rng.standard_normal((M, K)).astype(np.float16)
+    y1 = pipo.pipo_linear(pl.ctx, 0, p, x, w, None)
+    y2 = pipo.pipo_linear(pl.ctx, 0, p, (x.astype(np.float32) * 4).astype(np.float16), w, None)
+    assert np.array_equal(y2, y1 * 4)
+    assert rel_inf(y1, x.astype(np.float64) @ w.astype(np.float64).T) < 1e-4
