@@ -265,7 +265,9 @@ pipo_status pipo_unpack_int4_g64(pipo_ctx* ctx, const uint8_t* codes, const uint
  * 5 = same with A in TMEM (int4, M <= 64), 6 = prefill tcgen05 GEMM with A in TMEM
  * (int4, any M; static persistent tile schedule), 7 = streaming fp16-weight tcgen05 GEMM
  * (fp16, M <= 64: TMA-fed, warp-specialized; the fp16 decode linears), 8 = the same kernel
- * as the LM head (a13) runs it. */
+ * as the LM head (a13) runs it, 9 = int4 tcgen05 GEMM on SM pairs (cta_group::2, A in
+ * TMEM, stream-K with the fixup inside the kernel; M <= 64: the decode linears).
+ * A path that cannot run the shape returns PIPO_E_INVALID_ARG. */
 pipo_status pipo_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, const uint16_t* x,
                         const float* w, const float* bias, int32_t M, int32_t N, int32_t K,
                         float* y);
@@ -280,8 +282,10 @@ pipo_status pipo_bench_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, int32_t
                               int32_t iters, double* us);
 
 /* Measurement aid: HBM -> shared-memory streaming with cp.async.bulk, one CTA per
- * SM, `stages`-deep mbarrier ring of `chunk`-byte requests; GB/s in *gbs. */
-pipo_status pipo_probe_bulk(pipo_ctx* ctx, int32_t chunk, int32_t stages, double* gbs);
+ * SM, `stages`-deep mbarrier ring of `chunk`-byte requests, each CTA alternating its
+ * requests over `streams` contiguous regions (as a CTA that consumes several weight
+ * row-tiles at once); GB/s in *gbs. */
+pipo_status pipo_probe_bulk(pipo_ctx* ctx, int32_t chunk, int32_t stages, int32_t streams, double* gbs);
 
 /* Kernel micro-benchmark: decode attention over device-resident synthetic q/K/V
  * (b sequences, L positions, d = n_heads * head_dim), average microseconds per launch. */

@@ -1352,7 +1352,7 @@ pipo_status pipo_unpack_int4_g64(pipo_ctx* ctx, const uint8_t* codes, const uint
 pipo_status pipo_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, const uint16_t* x, const float* w,
                         const float* bias, int32_t M, int32_t N, int32_t K, float* y) {
   CHECK_CTX();
-  if (!x || !w || !y || M <= 0 || N <= 0 || K <= 0 || K % 64 || (wfmt != 0 && wfmt != 1) || path < 0 || path > 8)
+  if (!x || !w || !y || M <= 0 || N <= 0 || K <= 0 || K % 64 || (wfmt != 0 && wfmt != 1) || path < 0 || path > 9)
     return set_err(PIPO_E_INVALID_ARG, "bad linear arguments");
   CK(cudaSetDevice(ctx->cfg.device));
   const MatLayout ml = mat_layout(N, K, wfmt);
@@ -1393,7 +1393,7 @@ pipo_status pipo_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, const uint16_
 pipo_status pipo_bench_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, int32_t M, int32_t N, int32_t K,
                               int32_t iters, double* us) {
   CHECK_CTX();
-  if (!us || M <= 0 || N <= 0 || K <= 0 || K % 64 || iters <= 0 || (wfmt != 0 && wfmt != 1) || path < 0 || path > 8)
+  if (!us || M <= 0 || N <= 0 || K <= 0 || K % 64 || iters <= 0 || (wfmt != 0 && wfmt != 1) || path < 0 || path > 9)
     return set_err(PIPO_E_INVALID_ARG, "bad bench arguments");
   CK(cudaSetDevice(ctx->cfg.device));
   const MatLayout ml = mat_layout(N, K, wfmt);
@@ -1426,7 +1426,7 @@ pipo_status pipo_bench_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, int32_t
       CK(cudaMemcpyAsync(wcopies + (int64_t)c * ml.bytes, dw, ml.bytes, cudaMemcpyDeviceToDevice, st));
   }
   auto wcopy = [&](int i) { const int c = i % n_copies; return c == 0 ? dw : wcopies + (int64_t)(c - 1) * ml.bytes; };
-  if (getenv("PIPO_WS_DEBUG")) CK(cudaMemsetAsync(ctx->ws + (15ll << 20), 0, 148 * 16 * 8, st));
+  if (getenv("PIPO_WS_DEBUG")) CK(cudaMemsetAsync(ctx->ws + (15ll << 20), 0, 2 * 148 * 16 * 8, st));
   for (int i = 0; i < n_copies; ++i) {   // warm-up (touches every copy once)
     la.w = wcopy(i);
     LAUNCH(launch_linear(la, path, ctx->gemv_max_m, st));
@@ -1478,6 +1478,35 @@ pipo_status pipo_bench_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, int32_t
       fprintf(stderr, "tm-clk fixup %.0f cycles, barrier-after-MMA-end %.0f cycles (avg over CTAs)\n", fx, bm);
     }
     fprintf(stderr, "reduce first start %.2f last end %.2f us\n", (double)(int64_t)(ts[148 * 16] - t0) * 1e-3, (double)(int64_t)(ts[148 * 16 + 1] - t0) * 1e-3);
+  } else if (getenv("PIPO_WS_DEBUG") && (atoi(getenv("PIPO_WS_DEBUG")) & 128) && path == 9) {
+    // pair kernel stamps of the last launch (k_gemm_pair.cu): relative to the first entry
+    std::vector<uint64_t> ts(148 * 16);
+    CK(cudaMemcpy(ts.data(), ctx->ws + (15ll << 20), ts.size() * 8, cudaMemcpyDeviceToHost));
+    uint64_t t0 = ~0ull;
+    for (int c = 0; c < 148; ++c) if (ts[c * 16]) t0 = std::min(t0, ts[c * 16]);
+    const char* nm[13] = {"entry", "setup", "prod_end", "mma_end", "unpk_end", "last_acc", "flags_ok", "epi_end",
+                          "exit", "first_raw", "units", "lastkind", "seg0_epi"};
+    for (int k = 0; k < 13; ++k) {
+      std::vector<double> v;
+      for (int c = 0; c < 148; ++c) {
+        if (k == 10 || k == 11) { v.push_back((double)ts[c * 16 + k]); continue; }
+        if (ts[c * 16 + k] >= t0 && ts[c * 16 + k] - t0 < 10000000ull) v.push_back((ts[c * 16 + k] - t0) * 1e-3);
+      }
+      std::sort(v.begin(), v.end());
+      if (!v.empty()) fprintf(stderr, "pair-stamp %-9s min %8.2f med %8.2f max %8.2f (n=%zu)\n", nm[k], v.front(), v[v.size() / 2], v.back(), v.size());
+    }
+    std::vector<uint64_t> wc(148 * 16);
+    CK(cudaMemcpy(wc.data(), ctx->ws + (15ll << 20) + 148 * 16 * 2, wc.size() * 8, cudaMemcpyDeviceToHost));
+    const char* wn[13] = {"prod slot_empty", "prod total", "mma a_full", "mma acc_empty", "mma total",
+                          "unpk slot_full", "unpk a_empty", "unpk wait_st", "unpk total", "xld x_empty", "xld wait_group",
+                          "xld total", "unpk x_full"};
+    fprintf(stderr, "pair-waits (kcycles, avg over CTAs that ran the role):");
+    for (int k = 0; k < 13; ++k) {
+      double sum = 0; int n = 0;
+      for (int c = 0; c < 148; ++c) if (wc[c * 16 + k]) { sum += wc[c * 16 + k]; ++n; }
+      fprintf(stderr, " | %s %.1f", wn[k], n ? sum / n / 1e3 : 0.0);
+    }
+    fprintf(stderr, "\n");
   } else if (getenv("PIPO_WS_DEBUG") && (atoi(getenv("PIPO_WS_DEBUG")) & 32) && path == 5) {
     std::vector<uint64_t> wt(148 * 16);
     CK(cudaMemcpy(wt.data(), ctx->ws + (15ll << 20), wt.size() * 8, cudaMemcpyDeviceToHost));
@@ -1505,24 +1534,24 @@ pipo_status pipo_bench_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, int32_t
   return PIPO_OK;
 }
 
-pipo_status pipo_probe_bulk(pipo_ctx* ctx, int32_t chunk, int32_t stages, double* gbs) {
+pipo_status pipo_probe_bulk(pipo_ctx* ctx, int32_t chunk, int32_t stages, int32_t streams, double* gbs) {
   CHECK_CTX();
-  if (!gbs || chunk <= 0 || chunk % 16 || stages <= 0) return set_err(PIPO_E_INVALID_ARG, "bad probe arguments");
+  if (!gbs || chunk <= 0 || chunk % 16 || stages <= 0 || streams <= 0) return set_err(PIPO_E_INVALID_ARG, "bad probe arguments");
   CK(cudaSetDevice(ctx->cfg.device));
   const int ctas = ctx->num_sms;
-  const int64_t per = (int64_t)(512ll << 20) / ctas / chunk * chunk;
+  const int64_t per = (int64_t)(512ll << 20) / ctas / (chunk * (int64_t)streams) * chunk * streams;
   uint8_t* buf = nullptr;
   uint32_t* sink = nullptr;
   TRY(dev_alloc(ctx, &buf, per * ctas));
   TRY(dev_alloc(ctx, &sink, 4));
   cudaStream_t st = ctx->s_comp;
   CK(cudaMemsetAsync(buf, 1, (size_t)(per * ctas), st));
-  LAUNCH(launch_bulk_probe(buf, per, chunk, stages, ctas, sink, st));
+  LAUNCH(launch_bulk_probe(buf, per, chunk, stages, streams, ctas, sink, st));
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   CK(cudaEventRecord(e0, st));
-  for (int i = 0; i < 5; ++i) LAUNCH(launch_bulk_probe(buf, per, chunk, stages, ctas, sink, st));
+  for (int i = 0; i < 5; ++i) LAUNCH(launch_bulk_probe(buf, per, chunk, stages, streams, ctas, sink, st));
   CK(cudaEventRecord(e1, st));
   CK(cudaEventSynchronize(e1));
   float ms = 0;

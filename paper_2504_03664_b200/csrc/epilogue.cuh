@@ -29,4 +29,60 @@ __device__ __forceinline__ void epi_store(const EpiParams& e, int m, int n, floa
   }
 }
 
+// The same epilogue for 16 consecutive rows m0..m0+15 of one output column n (one
+// accumulator chunk read from TMEM): the bias is loaded once and, for the residual add,
+// all 16 old values are loaded before any store — epi_store's per-element load/store
+// pairs may alias, so the compiler serialises them (one memory round trip per element).
+__device__ __forceinline__ void epi_store16(const EpiParams& e, int m0, int n, const float* acc) {
+  if (n >= e.N) return;
+  const float b = e.bias ? __half2float(e.bias[n]) : 0.f;
+  float v[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = acc[i] + b;
+  switch (e.kind) {
+    case EPI_RESID: {
+      float old[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) old[i] = m0 + i < e.M ? e.h[(int64_t)(m0 + i) * e.N + n] : 0.f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (m0 + i < e.M) e.h[(int64_t)(m0 + i) * e.N + n] = old[i] + v[i];
+      break;
+    }
+    case EPI_QKV: {
+      const float qs = e.qscale;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int m = m0 + i;
+        if (m >= e.M) break;
+        if (n < e.d) {
+          e.q[(int64_t)m * e.d + n] = __float2half_rn(v[i] * qs);
+        } else {
+          const int bi = m / e.n_tok, t = m - bi * e.n_tok;
+          const int dkv = e.dkv ? e.dkv : e.d;
+          const int64_t off = e.kv_rowmajor ? (int64_t)m * 2 * dkv : ((int64_t)(e.past + t) * e.kv_b + bi) * dkv;
+          if (n < e.d + dkv) e.kc[off + n - e.d] = __float2half_rn(v[i]);
+          else e.vc[off + n - e.d - dkv] = __float2half_rn(v[i]);
+        }
+      }
+      break;
+    }
+    case EPI_RELU:
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (m0 + i < e.M) e.u[(int64_t)(m0 + i) * e.N + n] = __float2half_rn(fmaxf(v[i], 0.f));
+      break;
+    case EPI_HALF:
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (m0 + i < e.M) e.u[(int64_t)(m0 + i) * e.N + n] = __float2half_rn(v[i]);
+      break;
+    default:
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (m0 + i < e.M) e.y[(int64_t)(m0 + i) * e.ldy + n] = v[i];
+      break;
+  }
+}
+
 }  // namespace pipo

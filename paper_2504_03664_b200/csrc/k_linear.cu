@@ -333,6 +333,9 @@ int launch_linear(const LinearArgs& a, int path, int gemv_max_m, cudaStream_t st
   if (path == PATH_HEAD) return launch_linear_stream_f16(a, true, st);
   if (path == PATH_STREAM || (path == PATH_AUTO && a.wfmt == 0 && a.M <= 64)) return launch_linear_stream_f16(a, false, st);
   if (path == PATH_TP || (path == PATH_AUTO && !gemv && a.wfmt == 1 && a.M > 128)) return launch_linear_tp(a, st);
+  // PATH_PAIR (k_gemm_pair.cu, cta_group::2 + in-kernel fixup) is correct but measured
+  // slower than the TM kernel on every decode shape: selectable, not chosen.
+  if (path == PATH_PAIR) return launch_linear_pair(a, st);
   if (path == PATH_TM || (path == PATH_AUTO && !gemv && a.wfmt == 1 && a.M <= 64)) return launch_linear_tm(a, st);
   if (path == PATH_WS || (path == PATH_AUTO && !gemv && a.wfmt == 1 && a.M <= 128)) return launch_linear_ws(a, st);
   if (path == PATH_TC || (path == PATH_AUTO && !gemv)) return launch_linear_tc(a, st);

@@ -7,7 +7,7 @@
 namespace pipo {
 
 __global__ void __launch_bounds__(128, 1) bulk_probe_kernel(const uint8_t* src, int64_t bytes_per_cta, int chunk,
-                                                          int stages, uint32_t* sink) {
+                                                          int stages, int streams, uint32_t* sink) {
   extern __shared__ __align__(128) uint8_t sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + (size_t)stages * chunk);
   uint64_t* empty = full + stages;
@@ -33,7 +33,10 @@ __global__ void __launch_bounds__(128, 1) bulk_probe_kernel(const uint8_t* src, 
                    : "memory");
       asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
                        smem_u32(sm + (size_t)s * chunk)),
-                   "l"(base + (int64_t)i * chunk), "r"(chunk), "r"(smem_u32(&full[s]))
+                   // request i: stream i % streams (each stream one contiguous 1/streams of the
+                   // CTA's region), like a CTA that consumes several weight row-tiles at once
+                   "l"(base + (int64_t)(i % streams) * (bytes_per_cta / streams) + (int64_t)(i / streams) * chunk),
+                   "r"(chunk), "r"(smem_u32(&full[s]))
                    : "memory");
     }
   } else if (warp == 1 && (tid & 31) == 0) {
@@ -48,12 +51,12 @@ __global__ void __launch_bounds__(128, 1) bulk_probe_kernel(const uint8_t* src, 
   if (acc == 0xFFFFFFFFu) *sink = acc;
 }
 
-int launch_bulk_probe(const uint8_t* src, int64_t bytes_per_cta, int chunk, int stages, int ctas, uint32_t* sink,
-                      cudaStream_t st) {
+int launch_bulk_probe(const uint8_t* src, int64_t bytes_per_cta, int chunk, int stages, int streams, int ctas,
+                      uint32_t* sink, cudaStream_t st) {
   const int smem = stages * chunk + 2 * stages * 8 + 64;
   if (smem > 227 * 1024) return -1;
   cudaFuncSetAttribute(bulk_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  bulk_probe_kernel<<<ctas, 128, smem, st>>>(src, bytes_per_cta, chunk, stages, sink);
+  bulk_probe_kernel<<<ctas, 128, smem, st>>>(src, bytes_per_cta, chunk, stages, streams, sink);
   return 1;
 }
 

@@ -48,7 +48,7 @@ struct LinearArgs {
 };
 
 enum LinearPath { PATH_AUTO = 0, PATH_GEMV = 1, PATH_GEMM = 2, PATH_TC = 3, PATH_WS = 4, PATH_TM = 5, PATH_TP = 6,
-                  PATH_STREAM = 7, PATH_HEAD = 8 };
+                  PATH_STREAM = 7, PATH_HEAD = 8, PATH_PAIR = 9 };
 
 // streaming fp16-weight tcgen05 GEMM, M <= 64 (k_head.cu): the LM head (lm_head = true,
 // PATH_HEAD) and the fp16 decode linears (PATH_STREAM)
@@ -56,6 +56,8 @@ int launch_linear_stream_f16(const LinearArgs& a, bool lm_head, cudaStream_t st)
 
 // warp-specialized stream-K tcgen05 GEMM with A in TMEM, int4 weights, M <= 64
 int launch_linear_tm(const LinearArgs& a, cudaStream_t st);
+// the same on SM pairs (cta_group::2) with the stream-K fixup in-kernel (k_gemm_pair.cu), M <= 64
+int launch_linear_pair(const LinearArgs& a, cudaStream_t st);
 int launch_linear_tp(const LinearArgs& a, cudaStream_t st);
 
 // warp-specialized stream-K tcgen05 GEMM, int4 weights (k_gemm_ws.cu)
@@ -122,7 +124,7 @@ int launch_f32_to_f16(const float* src, __half* dst, int64_t n, cudaStream_t st)
 int launch_f16_to_f32(const __half* src, float* dst, int64_t n, cudaStream_t st);
 
 // measurement aid: bulk-copy streaming probe (k_probe.cu)
-int launch_bulk_probe(const uint8_t* src, int64_t bytes_per_cta, int chunk, int stages, int ctas, uint32_t* sink,
+int launch_bulk_probe(const uint8_t* src, int64_t bytes_per_cta, int chunk, int stages, int streams, int ctas, uint32_t* sink,
                       cudaStream_t st);
 
 // synthetic generator (pipo_synth mirror; input generation, not the method)

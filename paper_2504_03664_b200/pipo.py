@@ -26,7 +26,7 @@ PIPO_F_KPROF = 2
 PIPO_F_AUTO_PLAN = 4
 K_CLASSES = ["linear_decode", "attn_decode", "lm_head", "linear_prefill", "attn_prefill", "misc"]
 PIPO_LAYER_EMBED = -1
-PATH_AUTO, PATH_GEMV, PATH_GEMM, PATH_TC, PATH_WS, PATH_TM, PATH_TP, PATH_STREAM, PATH_HEAD = 0, 1, 2, 3, 4, 5, 6, 7, 8
+PATH_AUTO, PATH_GEMV, PATH_GEMM, PATH_TC, PATH_WS, PATH_TM, PATH_TP, PATH_STREAM, PATH_HEAD, PATH_PAIR = 0, 1, 2, 3, 4, 5, 6, 7, 8, 9
 
 _f = C.POINTER(C.c_float)
 _u8 = C.POINTER(C.c_uint8)
@@ -134,7 +134,7 @@ _sig("pipo_unpack_int4_g64", C.c_int, _P, _u8, _u16, C.c_int64, C.c_int64, _u16)
 _sig("pipo_linear", C.c_int, _P, C.c_int32, C.c_int32, _u16, _f, _f, C.c_int32, C.c_int32, C.c_int32, _f)
 _sig("pipo_bench_linear", C.c_int, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
      C.POINTER(C.c_double))
-_sig("pipo_probe_bulk", C.c_int, _P, C.c_int32, C.c_int32, C.POINTER(C.c_double))
+_sig("pipo_probe_bulk", C.c_int, _P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_double))
 _sig("pipo_bench_attention", C.c_int, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
      C.POINTER(C.c_double))
 _sig("pipo_attention_decode", C.c_int, _P, _u16, _u16, _u16, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _f)
@@ -316,9 +316,9 @@ def pipo_bench_linear(ctx, wfmt, path, M, N, K, iters=20) -> float:
     return us.value
 
 
-def pipo_probe_bulk(ctx, chunk: int, stages: int) -> float:
+def pipo_probe_bulk(ctx, chunk: int, stages: int, streams: int = 1) -> float:
     g = C.c_double()
-    _check(_lib.pipo_probe_bulk(ctx, chunk, stages, C.byref(g)))
+    _check(_lib.pipo_probe_bulk(ctx, chunk, stages, streams, C.byref(g)))
     return g.value
 
 

@@ -74,7 +74,7 @@ def test_linear_vs_oracle(env, M, N, K, wfmt):
     bias = (rng.uniform(-0.02, 0.02, N)).astype(np.float32)
     ref = _ref_linear(x, w, bias, wfmt)
     paths = [pipo.PATH_TC, pipo.PATH_GEMM] + ([pipo.PATH_GEMV] if wfmt == 1 and M <= 16 else []) + \
-        ([pipo.PATH_WS] if wfmt == 1 and M <= 128 else []) + ([pipo.PATH_TM] if wfmt == 1 and M <= 64 else []) + \
+        ([pipo.PATH_WS] if wfmt == 1 and M <= 128 else []) + ([pipo.PATH_TM, pipo.PATH_PAIR] if wfmt == 1 and M <= 64 else []) + \
         ([pipo.PATH_TP] if wfmt == 1 else []) + ([pipo.PATH_STREAM, pipo.PATH_HEAD] if wfmt == 0 and M <= 64 else [])
     for path in paths:
         y = pipo.pipo_linear(pl.ctx, wfmt, path, x, w, bias)
@@ -85,19 +85,24 @@ def test_linear_vs_oracle(env, M, N, K, wfmt):
 
 
 @pytest.mark.parametrize("M,N,K", [(64, 512, 2048), (40, 200, 1024), (33, 384, 320), (64, 2304, 7168),
-                                   (16, 1024, 8192), (64, 384, 4160)])
-def test_linear_tm_stream_k_deterministic(env, M, N, K):
-    """The decode GEMM (stream-K over CTAs, partials summed in k order by the reduce
-    kernel) within the bar and bit-reproducible run to run (the tier-invariance tests
-    rely on it); K/64 odd (4160) takes the 1-k-block units."""
+                                   (16, 1024, 8192), (64, 384, 4160), (1, 1664, 4096), (8, 7168, 28672),
+                                   (64, 5376, 7168), (31, 896, 1088)])
+@pytest.mark.parametrize("path", ["tm", "pair"])
+def test_linear_tm_stream_k_deterministic(env, M, N, K, path):
+    """The decode GEMMs (stream-K over CTAs / SM pairs; partials summed in k order by the
+    reduce kernel (tm) or by the finishing pair inside the kernel (pair)) within the bar
+    and bit-reproducible run to run (the tier-invariance tests rely on it); K/64 odd
+    (4160) takes the tm kernel's 1-k-block units; N not a multiple of 512 leaves the pair
+    kernel's last quad of row-tiles partly empty."""
     pipo, pl = env
+    p = pipo.PATH_TM if path == "tm" else pipo.PATH_PAIR
     rng = np.random.default_rng(M * 3 + N + K)
     x = rng.standard_normal((M, K)).astype(np.float16)
     w = (rng.standard_normal((N, K)) * 0.02).astype(np.float16).astype(np.float32)
     bias = (rng.uniform(-0.02, 0.02, N)).astype(np.float32)
-    y = pipo.pipo_linear(pl.ctx, 1, pipo.PATH_TM, x, w, bias)
+    y = pipo.pipo_linear(pl.ctx, 1, p, x, w, bias)
     assert rel_inf(y, _ref_linear(x, w, bias, 1)) < 2e-3
-    assert np.array_equal(y, pipo.pipo_linear(pl.ctx, 1, pipo.PATH_TM, x, w, bias))
+    assert np.array_equal(y, pipo.pipo_linear(pl.ctx, 1, p, x, w, bias))
 
 
 @pytest.mark.parametrize("M,N,K", [(1, 128, 64), (97, 384, 320), (300, 640, 512), (1000, 1152, 256),
@@ -124,11 +129,11 @@ def test_linear_prefill_configs(env, M, N, K):
     assert np.array_equal(yo, (col[:, ks].T + b16).astype(np.float32))
 
 
-@pytest.mark.parametrize("path", ["gemv", "gemm", "tc", "ws", "tm", "tp"])
+@pytest.mark.parametrize("path", ["gemv", "gemm", "tc", "ws", "tm", "tp", "pair"])
 def test_linear_special_cases_exact(env, path):
     pipo, pl = env
     p = {"gemv": pipo.PATH_GEMV, "gemm": pipo.PATH_GEMM, "tc": pipo.PATH_TC, "ws": pipo.PATH_WS, "tm": pipo.PATH_TM,
-         "tp": pipo.PATH_TP}[path]
+         "tp": pipo.PATH_TP, "pair": pipo.PATH_PAIR}[path]
     rng = np.random.default_rng(5)
     N, K = 200, 256
     w = (rng.standard_normal((N, K)) * 0.02).astype(np.float16).astype(np.float32)

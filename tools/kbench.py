@@ -9,7 +9,7 @@ from paper_2504_03664_b200 import pipo  # noqa: E402
 shape = synth.OPTShape(256, 1, 4, 512, vocab=512, max_pos=64)
 pl = pipo.Pipeline(pipo.make_config(shape, max_batch=4, max_seq=16, weight_tier=pipo.PIPO_TIER_DEVICE))
 paths = {"gemm_mma": pipo.PATH_GEMM, "tc_v1": pipo.PATH_TC, "ws": pipo.PATH_WS, "tm": pipo.PATH_TM,
-         "gemv": pipo.PATH_GEMV, "head": pipo.PATH_HEAD}
+         "gemv": pipo.PATH_GEMV, "head": pipo.PATH_HEAD, "pair": pipo.PATH_PAIR}
 import os
 if os.environ.get("KBENCH_PATHS"):
     paths = {k: v for k, v in paths.items() if k in os.environ["KBENCH_PATHS"].split(",")}
