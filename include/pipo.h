@@ -341,6 +341,24 @@ pipo_status pipo_debug_capture(pipo_ctx* ctx, int32_t on, float* out);
 pipo_status pipo_debug_read_rows(pipo_ctx* ctx, int32_t layer, int32_t matrix, int64_t row0, int64_t nrows,
                                  uint8_t* codes, uint16_t* scales, uint16_t* values);
 
+/* Test hooks for the method's invariance under timing and for transfer integrity
+ * ("chunk checksums equal the host blob", "injected
+ * delays do not change the tokens").  pipo_debug_inject: copy_delay_us > 0 enqueues a
+ * busy wait of that length on the weight-copy stream before every layer's transfer
+ * (a slow host link); compute_delay_us > 0 one on the compute stream before every
+ * layer's kernels (slow compute); ring_checksum != 0 computes, as each layer lands in
+ * its HBM ring slot, the position-weighted 64-bit checksum
+ *     C = sum_i w_i * (2i + 1)  mod 2^64,  w_i = little-endian 64-bit words of the slot,
+ * kept per layer (last transfer wins).  Synchronises the device; values 0 turn it off.
+ * pipo_debug_ring_checksums: the per-layer checksums, out[n_layers] (STATE if never
+ * enabled).  pipo_debug_read_blob: copies layer `layer`'s merged blob (layout.h) from
+ * the unsharded HOST-tier pinned store, `bytes` must equal pipo_layer_blob_bytes.
+ * Errors: INVALID_ARG (negative delay, range, NULL, other tiers). */
+pipo_status pipo_debug_inject(pipo_ctx* ctx, int32_t copy_delay_us, int32_t compute_delay_us, int32_t ring_checksum);
+pipo_status pipo_debug_ring_checksums(pipo_ctx* ctx, uint64_t* out);
+pipo_status pipo_debug_read_blob(pipo_ctx* ctx, int32_t layer, uint8_t* out, int64_t bytes);
+pipo_status pipo_layer_blob_bytes(pipo_ctx* ctx, int64_t* bytes);
+
 /* H2D probe: best-of-`reps` pinned->device cudaMemcpyAsync bandwidth (GB/s) for
  * `bytes`-sized copies on the weight-copy stream (App. A sweep). */
 pipo_status pipo_probe_h2d(pipo_ctx* ctx, int64_t bytes, int32_t reps, double* gbs);

@@ -261,6 +261,7 @@ pipo_status copy_chunks(pipo_ctx* ctx, void* dst, const void* src, int64_t bytes
 pipo_status enqueue_copy(pipo_ctx* ctx, int64_t G, int64_t kv_pos) {
   const int j = (int)(G % ctx->l), slot = (int)(G % ctx->R);
   if (G >= ctx->R) CK(cudaStreamWaitEvent(ctx->s_copy, ctx->ev_free[slot], 0));
+  LAUNCH(launch_spin(ctx->dbg_copy_delay_ns, ctx->s_copy));   // test hook: a slow host link
   cudaEvent_t t0 = nullptr;
   TRY(span_begin(ctx, ctx->s_copy, &t0));
   uint8_t* dst = ctx->ring + (int64_t)slot * ctx->layer_bytes;
@@ -270,6 +271,8 @@ pipo_status enqueue_copy(pipo_ctx* ctx, int64_t G, int64_t kv_pos) {
   // A segment's ready event is recorded right after the block holding its last byte,
   // so the compute stream consumes each segment as soon as it has landed.
   auto after_segment = [&](int s, cudaStream_t ready_on) -> pipo_status {
+    if (s == 3 && ctx->dbg_ring_sum)   // test hook: checksum of the layer as it landed in HBM
+      LAUNCH(launch_ring_sum(dst, ctx->layer_bytes, ctx->ring_sums + j, ready_on));
     CK(cudaEventRecord(ctx->ev_ready[slot][s], ready_on));
     if (s == 0 && host_kv(ctx)) {
       // KV load advanced with the layer's MHA weights (reading Q6)
@@ -453,6 +456,7 @@ pipo_status forward_pass(pipo_ctx* ctx, int b, int n, int past, bool want_logits
     const bool seg_wait = true;
     if (streamed(ctx)) CK(cudaStreamWaitEvent(cs, ctx->ev_ready[slot][seg_wait ? 0 : 3], 0));
     if (host_kv(ctx)) CK(cudaStreamWaitEvent(cs, ctx->ev_ready[slot][4], 0));
+    LAUNCH(launch_spin(ctx->dbg_comp_delay_ns, cs));   // test hook: slow compute
     TRY(span_begin(ctx, cs, &t0));
     LAUNCH(launch_layernorm(ctx->h, d, M, d, vec_ptr(ctx, blob, V_LN1_G), vec_ptr(ctx, blob, V_LN1_B), ctx->xa, cs));
     la.x = ctx->xa; la.w = blob + ctx->lay.mat_off[M_QKV]; la.wfmt = ctx->wfmt; la.N = d + 2 * dkv; la.K = d;
@@ -911,7 +915,7 @@ void pipeline_destroy(pipo_ctx* ctx) {
   if (ctx->head == ctx->tok) ctx->head = nullptr;
   void* dev[] = {ctx->tok, ctx->head, ctx->gu, ctx->rope_inv, ctx->pos, ctx->lnf_g, ctx->lnf_b, ctx->dev_store, ctx->ring, ctx->kv_dev, ctx->kv_slot, ctx->kv_stage,
                  ctx->h, ctx->xa, ctx->q, ctx->u, ctx->logits, ctx->ids, ctx->next, ctx->ws, ctx->counters,
-                 ctx->quant_bad, ctx->cap_dev};
+                 ctx->quant_bad, ctx->cap_dev, ctx->ring_sums};
   for (void* p : dev)
     if (p) cudaFree(p);
   void* hst[] = {ctx->host_store, ctx->kv_host, ctx->pin_ids, ctx->pin_next};
@@ -1927,6 +1931,50 @@ pipo_status pipo_debug_capture(pipo_ctx* ctx, int32_t on, float* out) {
   }
   ctx->cap_on = true;
   ctx->cap_host = out;
+  return PIPO_OK;
+}
+
+pipo_status pipo_debug_inject(pipo_ctx* ctx, int32_t copy_delay_us, int32_t compute_delay_us, int32_t ring_checksum) {
+  CHECK_CTX();
+  if (copy_delay_us < 0 || compute_delay_us < 0) return set_err(PIPO_E_INVALID_ARG, "negative delay");
+  CK(cudaSetDevice(ctx->cfg.device));
+  if (ring_checksum && !ctx->ring_sums) {
+    TRY(dev_alloc(ctx, &ctx->ring_sums, (int64_t)ctx->l * 8));
+    CK(cudaMemset(ctx->ring_sums, 0, (size_t)ctx->l * 8));
+  }
+  CK(cudaDeviceSynchronize());
+  ctx->dbg_copy_delay_ns = (int64_t)copy_delay_us * 1000;
+  ctx->dbg_comp_delay_ns = (int64_t)compute_delay_us * 1000;
+  ctx->dbg_ring_sum = ring_checksum != 0;
+  return PIPO_OK;
+}
+
+pipo_status pipo_debug_ring_checksums(pipo_ctx* ctx, uint64_t* out) {
+  CHECK_CTX();
+  if (!out) return set_err(PIPO_E_INVALID_ARG, "NULL output");
+  if (!ctx->ring_sums) return set_err(PIPO_E_STATE, "ring checksums were not enabled (pipo_debug_inject)");
+  CK(cudaSetDevice(ctx->cfg.device));
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(out, ctx->ring_sums, (size_t)ctx->l * 8, cudaMemcpyDeviceToHost));
+  return PIPO_OK;
+}
+
+pipo_status pipo_debug_read_blob(pipo_ctx* ctx, int32_t layer, uint8_t* out, int64_t bytes) {
+  CHECK_CTX();
+  if (!out || layer < 0 || layer >= ctx->l || bytes != ctx->layer_bytes)
+    return set_err(PIPO_E_INVALID_ARG, "layer out of range or bytes != layer blob size");
+  if (ctx->disk || ctx->shard_mode || !ctx->host_store)
+    return set_err(PIPO_E_INVALID_ARG, "pipo_debug_read_blob reads the unsharded HOST-tier pinned store");
+  CK(cudaSetDevice(ctx->cfg.device));
+  CK(cudaDeviceSynchronize());
+  std::memcpy(out, ctx->host_store + (int64_t)layer * ctx->layer_bytes, (size_t)bytes);
+  return PIPO_OK;
+}
+
+pipo_status pipo_layer_blob_bytes(pipo_ctx* ctx, int64_t* bytes) {
+  CHECK_CTX();
+  if (!bytes) return set_err(PIPO_E_INVALID_ARG, "NULL output");
+  *bytes = ctx->layer_bytes;
   return PIPO_OK;
 }
 

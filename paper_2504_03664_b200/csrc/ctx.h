@@ -147,6 +147,10 @@ struct pipo_ctx {
   int numa_node = -1;
   std::vector<std::pair<void*, int64_t>> numa_allocs;
   bool timeline_truncated = false;
+  // test hooks (pipo_debug_inject): injected delays, ring checksums per layer
+  int64_t dbg_copy_delay_ns = 0, dbg_comp_delay_ns = 0;
+  bool dbg_ring_sum = false;
+  uint64_t* ring_sums = nullptr;   // device [l]
   bool forwarded = false;          // a prefill/decode has run (prefetch may be in flight)
   bool auto_plan = false;          // PIPO_F_AUTO_PLAN: the fields below came from Eq. (1)
   pipo_plan plan{};

@@ -29,6 +29,29 @@ __device__ __forceinline__ void epi_store(const EpiParams& e, int m, int n, floa
   }
 }
 
+// The epilogue for 4 consecutive output features n..n+3 of one row m (the stream-K reduce
+// kernel's float4 partial sums): the residual add loads the four old values together
+// (epi_store's load/store pairs may alias, so the compiler would serialise them).
+__device__ __forceinline__ void epi_store4(const EpiParams& e, int m, int n, float4 acc) {
+  if (e.kind == EPI_RESID && m < e.M && n + 3 < e.N) {
+    float* hp = e.h + (int64_t)m * e.N + n;
+    float b[4] = {0.f, 0.f, 0.f, 0.f};
+    if (e.bias)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) b[i] = __half2float(e.bias[n + i]);
+    const float o0 = hp[0], o1 = hp[1], o2 = hp[2], o3 = hp[3];
+    hp[0] = o0 + (acc.x + b[0]);
+    hp[1] = o1 + (acc.y + b[1]);
+    hp[2] = o2 + (acc.z + b[2]);
+    hp[3] = o3 + (acc.w + b[3]);
+    return;
+  }
+  epi_store(e, m, n, acc.x);
+  epi_store(e, m, n + 1, acc.y);
+  epi_store(e, m, n + 2, acc.z);
+  epi_store(e, m, n + 3, acc.w);
+}
+
 // The same epilogue for 16 consecutive rows m0..m0+15 of one output column n (one
 // accumulator chunk read from TMEM): the bias is loaded once and, for the residual add,
 // all 16 old values are loaded before any store — epi_store's per-element load/store

@@ -357,8 +357,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
           float v[16];
           ws::tmem_ld16(t_row + c0, v);
           if (full) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) epi_store(a.epi, m0 + c0 + j, n, v[j]);
+            epi_store16(a.epi, m0 + c0, n, v);
           } else {
 #pragma unroll
             for (int j = 0; j < 16; ++j) __stcg(part + (t * BN + c0 + j) * 128 + row, v[j]);
@@ -498,10 +497,7 @@ __global__ void __launch_bounds__(256) ws_reduce2_kernel(LinearArgs a, int n_rt,
 #pragma unroll
   for (int i = 0; i < CPT; ++i) {
     const int m = mt * BN + (blockIdx.y * CPT + i) * 4 + (threadIdx.x >> 6);
-    epi_store(a.epi, m, n, acc[i].x);
-    epi_store(a.epi, m, n + 1, acc[i].y);
-    epi_store(a.epi, m, n + 2, acc[i].z);
-    epi_store(a.epi, m, n + 3, acc[i].w);
+    epi_store4(a.epi, m, n, acc[i]);
   }
 }
 
@@ -828,8 +824,7 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
           float v[16];
           ws::tmem_ld16(t_row + c0, v);
           if (full) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) epi_store(a.epi, m0 + c0 + j, n, v[j]);
+            epi_store16(a.epi, m0 + c0, n, v);
           } else {
 #pragma unroll
             for (int j = 0; j < 16; ++j) __stcg(part + (tt * BN + c0 + j) * 128 + row, v[j]);
@@ -1231,8 +1226,7 @@ __global__ void __launch_bounds__(TpCfg<BN, TILES, NACC, EPW, KBU>::THREADS, 1)
           if (m0 + c0 >= a.M) break;
           float v[16];
           ws::tmem_ld16(t_row + c0, v);
-#pragma unroll
-          for (int j = 0; j < 16; ++j) epi_store(a.epi, m0 + c0 + j, n, v[j]);
+          epi_store16(a.epi, m0 + c0, n, v);
         }
       }
       ws::tc_before();

@@ -365,6 +365,43 @@ int launch_p2p_wait(const P2PFlags& f, int target, cudaStream_t st) {
   return 1;
 }
 
+// ---- test hooks ------------------------------------------------
+// A one-thread busy wait of `ns` nanoseconds on a stream: injected delays in the host
+// tier (copy stream) or in the compute stream; the results must not change.
+__global__ void spin_kernel(int64_t ns) {
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while ((int64_t)(t - t0) < ns);
+}
+
+// Position-weighted 64-bit checksum of a byte range (multiple of 8 bytes), added into *out
+// (zeroed by the caller): sum_i w_i * (2i + 1) mod 2^64 over its little-endian 64-bit words.
+__global__ void ring_sum_kernel(const uint64_t* w, int64_t n_words, unsigned long long* out) {
+  uint64_t acc = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_words; i += (int64_t)gridDim.x * blockDim.x)
+    acc += w[i] * (uint64_t)(2 * i + 1);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, (unsigned long long)acc);
+}
+
+int launch_spin(int64_t ns, cudaStream_t st) {
+  if (ns <= 0) return 0;
+  spin_kernel<<<1, 1, 0, st>>>(ns);
+  return 1;
+}
+
+int launch_ring_sum(const uint8_t* p, int64_t bytes, uint64_t* out, cudaStream_t st) {
+  if (bytes % 8) return -1;
+  if (cudaMemsetAsync(out, 0, 8, st) != cudaSuccess) return -1;
+  ring_sum_kernel<<<148, 256, 0, st>>>(reinterpret_cast<const uint64_t*>(p), bytes / 8,
+                                       reinterpret_cast<unsigned long long*>(out));
+  return 1;
+}
+
 int launch_p2p_signal(const P2PFlags& f, int value, cudaStream_t st) {
   if (f.n <= 0) return 0;
   p2p_signal_kernel<<<1, 32, 0, st>>>(f, value);

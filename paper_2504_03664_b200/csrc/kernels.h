@@ -139,6 +139,9 @@ struct P2PFlags {
   int n;
 };
 int launch_p2p_wait(const P2PFlags& f, int target, cudaStream_t st);     // all *addr >= target
-int launch_p2p_signal(const P2PFlags& f, int value, cudaStream_t st);    // all *addr = value
+int launch_p2p_signal(const P2PFlags& f, int value, cudaStream_t st);
+// test hooks: a busy wait of ns nanoseconds; position-weighted 64-bit checksum of a range
+int launch_spin(int64_t ns, cudaStream_t st);
+int launch_ring_sum(const uint8_t* p, int64_t bytes, uint64_t* out, cudaStream_t st);    // all *addr = value
 
 }  // namespace pipo

@@ -126,6 +126,10 @@ _sig("decode_step_dev", C.c_int, _P, _P, _P)
 _sig("pipeline_stats", C.c_int, _P, C.POINTER(pipo_stats))
 _sig("pipeline_stats_reset", C.c_int, _P)
 _sig("pipo_set_flags", C.c_int, _P, C.c_uint32)
+_sig("pipo_debug_inject", C.c_int, _P, C.c_int32, C.c_int32, C.c_int32)
+_sig("pipo_debug_ring_checksums", C.c_int, _P, C.POINTER(C.c_uint64))
+_sig("pipo_debug_read_blob", C.c_int, _P, C.c_int32, C.POINTER(C.c_uint8), C.c_int64)
+_sig("pipo_layer_blob_bytes", C.c_int, _P, C.POINTER(C.c_int64))
 _sig("pipo_stream", _P, _P, C.c_int32)
 _sig("pipo_kernel_stats", C.c_int, _P, C.c_int32, C.POINTER(pipo_kstats))
 _sig("pipo_quantize_int4_g64", C.c_int, _f, C.c_int64, C.c_int64, _u8, _u16)
@@ -165,7 +169,8 @@ EXPORTED = ["pipo_last_error", "pipo_abi_version", "pipeline_init", "pipeline_de
             "pipo_load_synthetic", "prefill", "decode_step", "decode_step_dev", "pipeline_stats",
             "pipeline_stats_reset", "pipo_stream", "pipo_kernel_stats", "pipo_quantize_int4_g64", "pipo_quantize_int4_g64_gpu",
             "pipo_unpack_int4_g64", "pipo_linear", "pipo_bench_linear", "pipo_probe_bulk", "pipo_bench_attention", "pipo_attention_decode", "pipo_attention_prefill", "pipo_debug_capture", "pipo_probe_h2d", "pipo_debug_read_rows",
-            "pipo_attention_gqa", "pipo_rope", "pipo_set_flags", "pipo_shard_range", "pipo_gpu_numa_node", "pipo_nccl_unique_id", "pipo_shard_stream_init", "pipo_shard_p2p_export", "pipo_shard_p2p_init",
+            "pipo_attention_gqa", "pipo_rope", "pipo_set_flags", "pipo_debug_inject", "pipo_debug_ring_checksums",
+            "pipo_debug_read_blob", "pipo_layer_blob_bytes", "pipo_shard_range", "pipo_gpu_numa_node", "pipo_nccl_unique_id", "pipo_shard_stream_init", "pipo_shard_p2p_export", "pipo_shard_p2p_init",
             "pipo_ffn_hidden_dim", "pipo_memory_model", "pipo_choose_block_size", "pipo_choose_plan", "pipo_get_plan"]
 
 
@@ -416,6 +421,24 @@ def pipo_shard_p2p_init(ctx, handles: list):
 
 def pipo_set_flags(ctx, flags: int):
     _check(_lib.pipo_set_flags(ctx, flags))
+
+
+def pipo_debug_inject(ctx, copy_delay_us: int = 0, compute_delay_us: int = 0, ring_checksum: bool = False):
+    _check(_lib.pipo_debug_inject(ctx, copy_delay_us, compute_delay_us, 1 if ring_checksum else 0))
+
+
+def pipo_debug_ring_checksums(ctx, n_layers: int) -> np.ndarray:
+    out = np.zeros(n_layers, np.uint64)
+    _check(_lib.pipo_debug_ring_checksums(ctx, out.ctypes.data_as(C.POINTER(C.c_uint64))))
+    return out
+
+
+def pipo_debug_read_blob(ctx, layer: int) -> np.ndarray:
+    n = C.c_int64()
+    _check(_lib.pipo_layer_blob_bytes(ctx, C.byref(n)))
+    out = np.zeros(n.value, np.uint8)
+    _check(_lib.pipo_debug_read_blob(ctx, layer, out.ctypes.data_as(C.POINTER(C.c_uint8)), n.value))
+    return out
 
 
 def pipo_debug_capture(ctx, out: np.ndarray | None):

@@ -86,12 +86,14 @@ def test_c1_free_running_greedy_ids(c1_masters, seed):
         assert np.array_equal(ids_g, ids_r)
 
 
-def _run(pipo, shape, cfg_kw, loader, prompt, G, want_logits=True):
+def _run(pipo, shape, cfg_kw, loader, prompt, G, want_logits=True, hook=None):
     b, P = prompt.shape
     cfg = pipo.make_config(shape, max_batch=b, max_seq=P + G, **cfg_kw)
     out = []
     with pipo.Pipeline(cfg) as pl:
         loader(pl)
+        if hook is not None:
+            hook(pl)
         nxt, lg = pl.prefill(prompt, want_logits=want_logits)
         out.append(lg)
         for _ in range(G - 1):
@@ -202,6 +204,57 @@ def test_stats_busy_and_launches():
         assert 0 < st[k] <= 1.0 + 1e-6, (k, st[k])
     assert st["union_busy"] >= max(st["copy_busy"], st["kernel_busy"]) - 1e-9
     assert st["h2d_bytes"] > 0 and st["window_s"] > 0
+
+
+@pytest.mark.parametrize("copy_us,comp_us,variant", [
+    (400, 0, dict(weight_tier=1, ring_layers=2)), (0, 400, dict(weight_tier=1, ring_layers=2)),
+    (300, 300, dict(weight_tier=1, ring_layers=1)), (250, 0, dict(weight_tier=1, ring_layers=3, chunk_bytes=1 << 16)),
+    (300, 100, dict(weight_tier=1, ring_layers=2, kv_tier=1)), (0, 300, dict(weight_tier=0, kv_tier=1))])
+def test_injected_delays_bit_identical(copy_us, comp_us, variant):
+    """The method's invariance under timing (reading Q9): a slow host
+    link (a busy wait before every layer's transfer on the copy stream) or slow compute
+    (one before every layer's kernels) changes only when things happen, never the
+    logits — the events order every consumer after its producer."""
+    pipo = pipo_mod()
+    prompt = synth.prompts(3, 20, SMALL.vocab)
+    def syn(pl):
+        pl.load_synthetic(pipo.PIPO_LAYER_EMBED, 11)
+        for j in range(SMALL.n_layers):
+            pl.load_synthetic(j, 11)
+    ref, _ = _run(pipo, SMALL, dict(weight_tier=pipo.PIPO_TIER_DEVICE), syn, prompt, 5)
+    got, _ = _run(pipo, SMALL, variant, syn, prompt, 5,
+                  hook=lambda pl: pipo.pipo_debug_inject(pl.ctx, copy_us, comp_us))
+    assert np.array_equal(got, ref)
+
+
+def _ring_checksum(blob):
+    """SPEC.md:324's chunk checksum as pipo.h defines it: sum_i w_i * (2i + 1) mod 2^64
+    over the blob's little-endian 64-bit words."""
+    w = blob.view("<u8")
+    return int(np.sum(w * (2 * np.arange(w.size, dtype=np.uint64) + 1), dtype=np.uint64))
+
+
+@pytest.mark.parametrize("variant", [dict(ring_layers=2), dict(ring_layers=1, chunk_bytes=1 << 16),
+                                     dict(ring_layers=3, chunk_bytes=(1 << 20) + 4096), dict(ring_layers=2, kv_tier=1)])
+def test_ring_checksums_equal_host_blob(variant):
+    """Every layer lands in its HBM ring slot byte for byte as the pinned host store
+    holds it, for whole-blob and chunked transfers and all ring depths —
+    checked by the GPU's checksum of the slot against numpy's of the host blob."""
+    pipo = pipo_mod()
+    prompt = synth.prompts(3, 20, SMALL.vocab)
+    cfg = pipo.make_config(SMALL, max_batch=3, max_seq=25, weight_tier=pipo.PIPO_TIER_HOST, **variant)
+    with pipo.Pipeline(cfg) as pl:
+        pl.load_synthetic(pipo.PIPO_LAYER_EMBED, 11)
+        for j in range(SMALL.n_layers):
+            pl.load_synthetic(j, 11)
+        pipo.pipo_debug_inject(pl.ctx, 0, 0, True)
+        nxt, _ = pl.prefill(prompt)
+        for _ in range(3):
+            nxt, _ = pl.decode_step(nxt)
+        got = pipo.pipo_debug_ring_checksums(pl.ctx, SMALL.n_layers)
+        want = [_ring_checksum(pipo.pipo_debug_read_blob(pl.ctx, j)) for j in range(SMALL.n_layers)]
+    assert [int(x) for x in got] == want
+    assert len(set(want)) == SMALL.n_layers          # the layers differ (the check is not vacuous)
 
 
 @pytest.mark.parametrize("env_kw", [{}, {"PIPO_DISK_DELAY_US": "300"}])
