@@ -288,9 +288,12 @@ pipo_status pipo_bench_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, int32_t
 pipo_status pipo_probe_bulk(pipo_ctx* ctx, int32_t chunk, int32_t stages, int32_t streams, double* gbs);
 
 /* Kernel micro-benchmark: decode attention over device-resident synthetic q/K/V
- * (b sequences, L positions, d = n_heads * head_dim), average microseconds per launch. */
-pipo_status pipo_bench_attention(pipo_ctx* ctx, int32_t b, int32_t L, int32_t d, int32_t n_heads, int32_t variant,
-                                 int32_t iters, double* us);
+ * (b sequences, L positions, d = n_heads * head_dim, n_kv_heads K/V heads: 0 = n_heads,
+ * i.e. MHA; GQA otherwise), average microseconds per launch.  Launches rotate over
+ * copies of K/V totalling >= 384 MB so that every launch reads its KV from HBM.
+ * variant: as AttnArgs::use_cuda_cores (0 automatic). */
+pipo_status pipo_bench_attention(pipo_ctx* ctx, int32_t b, int32_t L, int32_t d, int32_t n_heads, int32_t n_kv_heads,
+                                 int32_t variant, int32_t iters, double* us);
 
 /* Decode attention kernel: q [b][d] fp16 bits (pre-scaled), k/v [L][b][d] fp16
  * bits (position-major) -> o [b][d] fp32.  n_heads | d.  variant: 0 = production

@@ -1567,18 +1567,24 @@ pipo_status pipo_probe_bulk(pipo_ctx* ctx, int32_t chunk, int32_t stages, int32_
   return PIPO_OK;
 }
 
-pipo_status pipo_bench_attention(pipo_ctx* ctx, int32_t b, int32_t L, int32_t d, int32_t n_heads, int32_t variant,
-                                 int32_t iters, double* us) {
+pipo_status pipo_bench_attention(pipo_ctx* ctx, int32_t b, int32_t L, int32_t d, int32_t n_heads, int32_t n_kv_heads,
+                                 int32_t variant, int32_t iters, double* us) {
   CHECK_CTX();
-  if (!us || b <= 0 || L <= 0 || d <= 0 || n_heads <= 0 || d % n_heads || iters <= 0)
+  if (n_kv_heads == 0) n_kv_heads = n_heads;
+  if (!us || b <= 0 || L <= 0 || d <= 0 || n_heads <= 0 || d % n_heads || iters <= 0 || n_kv_heads < 0 ||
+      n_heads % n_kv_heads)
     return set_err(PIPO_E_INVALID_ARG, "bad bench arguments");
   CK(cudaSetDevice(ctx->cfg.device));
-  const int64_t nq = (int64_t)b * d, nkv = (int64_t)L * b * d;
+  const int dkv = d / n_heads * n_kv_heads;
+  const int64_t nq = (int64_t)b * d, nkv = (int64_t)L * b * dkv;
+  // cold-HBM timing as in the pipeline (every layer's KV is fresh): launches rotate over
+  // copies of K/V totalling >= 384 MB (more than the 126 MB L2)
+  const int copies = (int)std::max<int64_t>(1, std::min<int64_t>(8, ((384ll << 20) + 4 * nkv - 1) / (4 * nkv)));
   __half *dq = nullptr, *dk = nullptr, *dv = nullptr, *dout = nullptr;
   float* tmp = nullptr;
   TRY(dev_alloc(ctx, &dq, nq * 2));
-  TRY(dev_alloc(ctx, &dk, nkv * 2));
-  TRY(dev_alloc(ctx, &dv, nkv * 2));
+  TRY(dev_alloc(ctx, &dk, nkv * 2 * copies));
+  TRY(dev_alloc(ctx, &dv, nkv * 2 * copies));
   TRY(dev_alloc(ctx, &dout, nq * 2));
   TRY(dev_alloc(ctx, &tmp, std::min<int64_t>(nkv, 64ll << 20) * 4));
   cudaStream_t st = ctx->s_comp;
@@ -1592,23 +1598,34 @@ pipo_status pipo_bench_attention(pipo_ctx* ctx, int32_t b, int32_t L, int32_t d,
       LAUNCH(launch_f32_to_f16(tmp, dst + off, c, st));
     }
   }
+  for (int c = 1; c < copies; ++c) {
+    CK(cudaMemcpyAsync(dk + c * nkv, dk, (size_t)nkv * 2, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(dv + c * nkv, dv, (size_t)nkv * 2, cudaMemcpyDeviceToDevice, st));
+  }
   AttnArgs aa;
   aa.q = dq; aa.kc = dk; aa.vc = dv; aa.o = dout; aa.b = b; aa.n = 1; aa.past = L - 1; aa.d = d;
   aa.n_heads = n_heads; aa.kv_b = b; aa.ws = ctx->ws; aa.ws_floats = ctx->ws_floats; aa.num_sms = ctx->num_sms;
+  aa.dkv = dkv; aa.group = n_heads / n_kv_heads;
   aa.use_cuda_cores = variant;
-  LAUNCH(launch_attention_decode(aa, st));
+  for (int c = 0; c < copies; ++c) {
+    aa.kc = dk + c * nkv; aa.vc = dv + c * nkv;
+    LAUNCH(launch_attention_decode(aa, st));
+  }
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   CK(cudaEventRecord(e0, st));
-  for (int i = 0; i < iters; ++i) LAUNCH(launch_attention_decode(aa, st));
+  for (int i = 0; i < iters; ++i) {
+    aa.kc = dk + (i % copies) * nkv; aa.vc = dv + (i % copies) * nkv;
+    LAUNCH(launch_attention_decode(aa, st));
+  }
   CK(cudaEventRecord(e1, st));
   CK(cudaEventSynchronize(e1));
   float ms = 0;
   CK(cudaEventElapsedTime(&ms, e0, e1));
   cudaEventDestroy(e0); cudaEventDestroy(e1);
   cudaFree(dq); cudaFree(dk); cudaFree(dv); cudaFree(dout); cudaFree(tmp);
-  ctx->hbm_bytes -= nq * 4 + nkv * 4 + std::min<int64_t>(nkv, 64ll << 20) * 4;
+  ctx->hbm_bytes -= nq * 4 + nkv * 4 * copies + std::min<int64_t>(nkv, 64ll << 20) * 4;
   *us = ms * 1e3 / iters;
   return PIPO_OK;
 }

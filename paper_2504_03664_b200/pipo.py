@@ -139,7 +139,7 @@ _sig("pipo_linear", C.c_int, _P, C.c_int32, C.c_int32, _u16, _f, _f, C.c_int32, 
 _sig("pipo_bench_linear", C.c_int, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
      C.POINTER(C.c_double))
 _sig("pipo_probe_bulk", C.c_int, _P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_double))
-_sig("pipo_bench_attention", C.c_int, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+_sig("pipo_bench_attention", C.c_int, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
      C.POINTER(C.c_double))
 _sig("pipo_attention_decode", C.c_int, _P, _u16, _u16, _u16, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _f)
 _sig("pipo_attention_prefill", C.c_int, _P, _u16, _u16, _u16, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
@@ -327,9 +327,9 @@ def pipo_probe_bulk(ctx, chunk: int, stages: int, streams: int = 1) -> float:
     return g.value
 
 
-def pipo_bench_attention(ctx, b, L, d, n_heads, variant=0, iters=10) -> float:
+def pipo_bench_attention(ctx, b, L, d, n_heads, variant=0, iters=10, n_kv_heads=0) -> float:
     us = C.c_double()
-    _check(_lib.pipo_bench_attention(ctx, b, L, d, n_heads, variant, iters, C.byref(us)))
+    _check(_lib.pipo_bench_attention(ctx, b, L, d, n_heads, n_kv_heads, variant, iters, C.byref(us)))
     return us.value
 
 
