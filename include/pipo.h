@@ -281,6 +281,13 @@ pipo_status pipo_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, const uint16_
 pipo_status pipo_bench_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, int32_t M, int32_t N, int32_t K,
                               int32_t iters, double* us);
 
+/* Kernel micro-benchmark: causal prefill attention (past = 0) over device-resident
+ * synthetic q [b][n][d], K/V [n][b][d_kv] (n_kv_heads: 0 = MHA), average microseconds
+ * per launch; variant as AttnArgs::use_cuda_cores (0 tcgen05 where it applies, 1 CUDA
+ * cores, 2 mma.sync). */
+pipo_status pipo_bench_attention_prefill(pipo_ctx* ctx, int32_t b, int32_t n, int32_t d, int32_t n_heads,
+                                         int32_t n_kv_heads, int32_t variant, int32_t iters, double* us);
+
 /* Measurement aid: HBM -> shared-memory streaming with cp.async.bulk, one CTA per
  * SM, `stages`-deep mbarrier ring of `chunk`-byte requests, each CTA alternating its
  * requests over `streams` contiguous regions (as a CTA that consumes several weight

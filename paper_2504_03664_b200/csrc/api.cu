@@ -1630,6 +1630,64 @@ pipo_status pipo_bench_attention(pipo_ctx* ctx, int32_t b, int32_t L, int32_t d,
   return PIPO_OK;
 }
 
+pipo_status pipo_bench_attention_prefill(pipo_ctx* ctx, int32_t b, int32_t n, int32_t d, int32_t n_heads,
+                                         int32_t n_kv_heads, int32_t variant, int32_t iters, double* us) {
+  CHECK_CTX();
+  if (n_kv_heads == 0) n_kv_heads = n_heads;
+  if (!us || b <= 0 || n <= 0 || d <= 0 || n_heads <= 0 || d % n_heads || iters <= 0 || n_kv_heads < 0 ||
+      n_heads % n_kv_heads)
+    return set_err(PIPO_E_INVALID_ARG, "bad bench arguments");
+  CK(cudaSetDevice(ctx->cfg.device));
+  const int dkv = d / n_heads * n_kv_heads;
+  const int64_t nq = (int64_t)b * n * d, nkv = (int64_t)n * b * dkv;
+  __half *dq = nullptr, *dk = nullptr, *dv = nullptr, *dout = nullptr;
+  float* tmp = nullptr;
+  TRY(dev_alloc(ctx, &dq, nq * 2));
+  TRY(dev_alloc(ctx, &dk, nkv * 2));
+  TRY(dev_alloc(ctx, &dv, nkv * 2));
+  TRY(dev_alloc(ctx, &dout, nq * 2));
+  TRY(dev_alloc(ctx, &tmp, std::min<int64_t>(std::max(nq, nkv), 64ll << 20) * 4));
+  cudaStream_t st = ctx->s_comp;
+  const int64_t chunk = std::min<int64_t>(std::max(nq, nkv), 64ll << 20);
+  for (int w = 0; w < 3; ++w) {
+    __half* dst = w == 0 ? dq : (w == 1 ? dk : dv);
+    const int64_t cnt = w == 0 ? nq : nkv;
+    for (int64_t off = 0; off < cnt; off += chunk) {
+      const int64_t c = std::min(chunk, cnt - off);
+      LAUNCH(launch_synth(tmp, off, c, synth_key(9, 8, w), 0, synth_scale(0, w == 0 ? 0.1 : 1.0), st));
+      LAUNCH(launch_f32_to_f16(tmp, dst + off, c, st));
+    }
+  }
+  AttnArgs aa;
+  aa.q = dq; aa.kc = dk; aa.vc = dv; aa.o = dout; aa.b = b; aa.n = n; aa.past = 0; aa.d = d;
+  aa.n_heads = n_heads; aa.kv_b = b; aa.ws = ctx->ws; aa.ws_floats = ctx->ws_floats; aa.num_sms = ctx->num_sms;
+  aa.dkv = dkv; aa.group = n_heads / n_kv_heads;
+  aa.use_cuda_cores = variant;
+  LAUNCH(launch_attention_prefill(aa, st));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, st));
+  for (int i = 0; i < iters; ++i) LAUNCH(launch_attention_prefill(aa, st));
+  CK(cudaEventRecord(e1, st));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0); cudaEventDestroy(e1);
+  if (getenv("PIPO_WS_DEBUG") && (atoi(getenv("PIPO_WS_DEBUG")) & 128) && variant == 0) {
+    std::vector<uint64_t> c(148 * 8);
+    CK(cudaMemcpy(c.data(), ctx->ws + (15ll << 20), c.size() * 8, cudaMemcpyDeviceToHost));
+    double t[6] = {0};
+    for (int i = 0; i < 148; ++i) for (int k = 0; k < 6; ++k) t[k] += (double)c[i * 8 + k];
+    fprintf(stderr, "attn-tc per item (cycles, warp 2): wait S %.0f | pass1 (max) %.0f | pass2 (exp, P) %.0f | wait O %.0f | epilogue %.0f  (%.0f items)\n",
+            t[0] / t[5], t[1] / t[5], t[2] / t[5], t[3] / t[5], t[4] / t[5], t[5]);
+  }
+  cudaFree(dq); cudaFree(dk); cudaFree(dv); cudaFree(dout); cudaFree(tmp);
+  ctx->hbm_bytes -= nq * 4 + nkv * 4 + chunk * 4;
+  *us = ms * 1e3 / iters;
+  return PIPO_OK;
+}
+
 pipo_status pipo_attention_decode(pipo_ctx* ctx, const uint16_t* q, const uint16_t* k, const uint16_t* v, int32_t b,
                                   int32_t L, int32_t d, int32_t n_heads, int32_t variant, float* o) {
   CHECK_CTX();

@@ -13,6 +13,7 @@
 // and reductions in flight), online softmax in fp32; warps merge in fixed order;
 // splits merge in fixed order in a second kernel (log-sum-exp weights).
 #include <float.h>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "launch.cuh"
@@ -979,7 +980,13 @@ int launch_attention_decode(const AttnArgs& a, cudaStream_t st) {
 int launch_attention_prefill(const AttnArgs& a, cudaStream_t st) {
   const int hd = a.d / a.n_heads;
   if (hd != 64 && hd != 128) return -1;
-  if (a.use_cuda_cores) {   // the v1 CUDA-core kernel, kept as a cross-check
+  // use_cuda_cores: 0 tcgen05 kernel where it applies (k_attn_tc.cu: causal key range
+  // <= 512), else mma.sync; 2 forces the mma.sync kernel; 1 the CUDA-core kernel
+  if (a.use_cuda_cores == 0) {
+    const int r = launch_attention_prefill_tc(a, st);
+    if (r >= 0) return r;
+  }
+  if (a.use_cuda_cores == 1) {   // the v1 CUDA-core kernel, kept as a cross-check
     dim3 grid(a.n_heads, a.b, (a.n + 31) / 32);
     if (hd == 64) attn_prefill_kernel<64><<<grid, 256, 0, st>>>(a);
     else attn_prefill_kernel<128><<<grid, 256, 0, st>>>(a);

@@ -91,6 +91,7 @@ struct AttnArgs {
 };
 int launch_attention_decode(const AttnArgs& a, cudaStream_t st);
 int launch_attention_prefill(const AttnArgs& a, cudaStream_t st);
+int launch_attention_prefill_tc(const AttnArgs& a, cudaStream_t st);   // tcgen05, key range <= 512 (else -1)
 
 // int4 KV: quantize the fresh fp16 K/V rows (staging [b*n][2d]) into the cache at
 // positions past..past+n-1 (codes [pos][kv_b][d/2], fast nibble order; scales fp16)

@@ -127,6 +127,8 @@ _sig("pipeline_stats", C.c_int, _P, C.POINTER(pipo_stats))
 _sig("pipeline_stats_reset", C.c_int, _P)
 _sig("pipo_set_flags", C.c_int, _P, C.c_uint32)
 _sig("pipo_debug_inject", C.c_int, _P, C.c_int32, C.c_int32, C.c_int32)
+_sig("pipo_bench_attention_prefill", C.c_int, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+     C.c_int32, C.POINTER(C.c_double))
 _sig("pipo_debug_ring_checksums", C.c_int, _P, C.POINTER(C.c_uint64))
 _sig("pipo_debug_read_blob", C.c_int, _P, C.c_int32, C.POINTER(C.c_uint8), C.c_int64)
 _sig("pipo_layer_blob_bytes", C.c_int, _P, C.POINTER(C.c_int64))
@@ -169,7 +171,7 @@ EXPORTED = ["pipo_last_error", "pipo_abi_version", "pipeline_init", "pipeline_de
             "pipo_load_synthetic", "prefill", "decode_step", "decode_step_dev", "pipeline_stats",
             "pipeline_stats_reset", "pipo_stream", "pipo_kernel_stats", "pipo_quantize_int4_g64", "pipo_quantize_int4_g64_gpu",
             "pipo_unpack_int4_g64", "pipo_linear", "pipo_bench_linear", "pipo_probe_bulk", "pipo_bench_attention", "pipo_attention_decode", "pipo_attention_prefill", "pipo_debug_capture", "pipo_probe_h2d", "pipo_debug_read_rows",
-            "pipo_attention_gqa", "pipo_rope", "pipo_set_flags", "pipo_debug_inject", "pipo_debug_ring_checksums",
+            "pipo_attention_gqa", "pipo_rope", "pipo_set_flags", "pipo_debug_inject", "pipo_debug_ring_checksums", "pipo_bench_attention_prefill",
             "pipo_debug_read_blob", "pipo_layer_blob_bytes", "pipo_shard_range", "pipo_gpu_numa_node", "pipo_nccl_unique_id", "pipo_shard_stream_init", "pipo_shard_p2p_export", "pipo_shard_p2p_init",
             "pipo_ffn_hidden_dim", "pipo_memory_model", "pipo_choose_block_size", "pipo_choose_plan", "pipo_get_plan"]
 
@@ -421,6 +423,12 @@ def pipo_shard_p2p_init(ctx, handles: list):
 
 def pipo_set_flags(ctx, flags: int):
     _check(_lib.pipo_set_flags(ctx, flags))
+
+
+def pipo_bench_attention_prefill(ctx, b, n, d, n_heads, variant=0, iters=5, n_kv_heads=0) -> float:
+    us = C.c_double()
+    _check(_lib.pipo_bench_attention_prefill(ctx, b, n, d, n_heads, n_kv_heads, variant, iters, C.byref(us)))
+    return us.value
 
 
 def pipo_debug_inject(ctx, copy_delay_us: int = 0, compute_delay_us: int = 0, ring_checksum: bool = False):

@@ -194,10 +194,15 @@ def test_attention_special_cases_exact(env):
 
 
 @pytest.mark.parametrize("b,n,past,d,H", [(1, 5, 0, 128, 2), (2, 64, 0, 256, 2), (2, 100, 0, 512, 4),
-                                          (3, 33, 7, 256, 4), (1, 130, 70, 1024, 8), (2, 512, 0, 512, 4)])
-@pytest.mark.parametrize("cuda_cores", [False, True])
-def test_attention_prefill_vs_oracle(env, b, n, past, d, H, cuda_cores):
+                                          (3, 33, 7, 256, 4), (1, 130, 70, 1024, 8), (2, 512, 0, 512, 4),
+                                          (2, 300, 200, 512, 4), (1, 384, 0, 256, 2), (2, 129, 0, 256, 4)])
+@pytest.mark.parametrize("kernel", ["tcgen05", "cuda_cores", "mma_sync"])
+def test_attention_prefill_vs_oracle(env, b, n, past, d, H, kernel):
+    """Causal prefill attention against the fp64 definition: the tcgen05 kernel (key
+    ranges <= 512; longer ones fall back), the legacy mma.sync kernel and the CUDA-core
+    reference; ragged q-tiles (n = 5, 33, 100, 129, 130, 300) and past > 0."""
     pipo, pl = env
+    cuda_cores = {"tcgen05": 0, "cuda_cores": 1, "mma_sync": 2}[kernel]
     rng = np.random.default_rng(n * 100 + past + d)
     q = (rng.standard_normal((b, n, d)) * (d // H) ** -0.5).astype(np.float16)
     L = past + n
@@ -209,6 +214,28 @@ def test_attention_prefill_vs_oracle(env, b, n, past, d, H, cuda_cores):
     assert rel_inf(o, ref) < 2e-2
     # P is rounded to fp16 before P.V on the tensor-core path
     assert rel_inf(o, ref) < (5e-3 if cuda_cores else 1e-2)
+
+
+@pytest.mark.parametrize("hd", [64, 128])
+def test_attention_prefill_tc_rescale_paths(env, hd):
+    """The tcgen05 kernel's online softmax rescales O only when a key block's max exceeds
+    the reference max by more than 2^8: keys growing along the positions force it for
+    some query rows of a warp and not for others (the warp-collective TMEM rescale must
+    then run with alpha = 1 on the rest), across 4 key blocks; checked against fp64."""
+    pipo, pl = env
+    rng = np.random.default_rng(hd)
+    b, n, H = 2, 512, 2
+    d = H * hd
+    q = rng.standard_normal((b, n, d))
+    q *= np.where(np.arange(n) % 3 == 0, 2.0, 0.25)[None, :, None]            # rows with / without rescales
+    k = rng.standard_normal((n, b, d)) * (1.0 + np.arange(n) / 48.0)[:, None, None]
+    q = (q * hd ** -0.5).astype(np.float16)
+    k = k.astype(np.float16)
+    v = rng.standard_normal((n, b, d)).astype(np.float16)
+    ref = opt.attention(q.astype(np.float64), k.astype(np.float64).transpose(1, 0, 2),
+                        v.astype(np.float64).transpose(1, 0, 2), 0, H)
+    o = pipo.pipo_attention_prefill(pl.ctx, q, k, v, 0, H, 0)
+    assert rel_inf(o, ref) < 1e-2
 
 
 @pytest.mark.parametrize("path", ["stream", "head"])
