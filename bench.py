@@ -203,38 +203,6 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def disk_probe(directory: str, threads: int = 4, chunk: int = 32 << 20) -> float:
-    """Raw O_DIRECT read bandwidth (GB/s) of the layer blob files with `threads`
-    concurrent readers and `chunk`-byte requests (App. A / Fig. 6 analogue,
-    PAPER.md:446-464, 580-581).  Python preadv: a lower bound of what the library's
-    reader pool reaches, reported as context, not as the disk roofline's denominator."""
-    import mmap
-    from concurrent.futures import ThreadPoolExecutor
-    files = sorted(os.path.join(directory, f) for f in os.listdir(directory) if f.endswith(".pipo"))
-    jobs = []
-    for f in files:
-        size = os.path.getsize(f)
-        jobs += [(f, off, min(chunk, size - off)) for off in range(0, size, chunk)]
-    bufs = [mmap.mmap(-1, chunk) for _ in range(threads)]
-    flag = getattr(os, "O_DIRECT", 0)
-
-    def work(t):
-        buf, total = bufs[t], 0
-        for f, off, n in jobs[t::threads]:
-            fd = os.open(f, os.O_RDONLY | flag)
-            try:
-                n4 = (n + 4095) // 4096 * 4096
-                total += os.preadv(fd, [memoryview(buf)[:n4]], off)
-            finally:
-                os.close(fd)
-        return total
-
-    t0 = time.perf_counter()
-    with ThreadPoolExecutor(threads) as ex:
-        total = sum(ex.map(work, range(threads)))
-    return total / (time.perf_counter() - t0) / 1e9
-
-
 def measured_peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -801,10 +769,15 @@ def run_pipo(args):
                 line["variants"] = {"shard_stream": {"error": str(e)[:300]}}
 
     if rank == 0 and disk_dir:
-        dgbs = disk_probe(disk_dir, threads=4)
-        line["disk_roofline"] = {"bound": "disk", "python_preadv_probe_gbs": dgbs,
-                                 "achieved_gbs": layer_bytes / (ms / 1e3) / 1e9,
-                                 "note": "the Python probe is weaker than the library's reader pool; context only"}
+        # the library's probe: the reader pool's read path (4 threads, O_DIRECT, the tier's
+        # 32 MiB or --chunk-mb chunks) without the GPU handshake, over the same layer files
+        chunk = int(args.chunk_mb * (1 << 20)) if args.chunk_mb else 32 << 20
+        chunk = max(4096, chunk // 4096 * 4096)
+        dgbs, _ = pipo.pipo_probe_disk(disk_dir, s.n_layers, 4, chunk)
+        ach = layer_bytes / (ms / 1e3) / 1e9
+        line["disk_roofline"] = {"bound": "disk", "probe_gbs": dgbs, "achieved_gbs": ach, "frac": ach / dgbs,
+                                 "probe": "pipo_probe_disk: 4 reader threads, O_DIRECT, %d MiB chunks, all %d "
+                                          "layer files once, no GPU handshake" % (chunk >> 20, s.n_layers)}
     if rank == 0:
         try:
             mem_cpu = int(open("/proc/meminfo").read().split("MemTotal:")[1].split()[0]) * 1024

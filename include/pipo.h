@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define PIPO_ABI_VERSION 4
+#define PIPO_ABI_VERSION 5
 
 typedef enum {
   PIPO_OK = 0,
@@ -322,10 +322,12 @@ pipo_status pipo_attention_prefill(pipo_ctx* ctx, const uint16_t* q, const uint1
  * past..past+n-1; k/v [past+n][b][n_kv_heads*head_dim] position-major; query head j
  * reads KV head j / (n_heads / n_kv_heads).  n == 1 runs the decode kernel, n > 1 the
  * causal prefill kernel.  o [b][n][n_heads*head_dim] fp32.  n_kv_heads | n_heads,
- * head_dim in {64, 128}. */
+ * head_dim in {64, 128}.  variant (decode): 0 the production choice; 3 the CUDA-core
+ * one-row-per-warp kernel; 5 / 6 the tensor-core kernel forced to 4 / 2 warps (test and
+ * measurement hooks). */
 pipo_status pipo_attention_gqa(pipo_ctx* ctx, const uint16_t* q, const uint16_t* k, const uint16_t* v, int32_t b,
                                int32_t n, int32_t past, int32_t n_heads, int32_t n_kv_heads, int32_t head_dim,
-                               float* o);
+                               int32_t variant, float* o);
 
 /* RoPE kernel of a LLaMA context (its n_heads, n_kv_heads, head_dim, llama3 frequencies):
  * q [b][n][n_heads*hd] fp16 bits at positions past..past+n-1 and k [past+n][b][n_kv_heads*hd]
@@ -372,6 +374,18 @@ pipo_status pipo_layer_blob_bytes(pipo_ctx* ctx, int64_t* bytes);
 /* H2D probe: best-of-`reps` pinned->device cudaMemcpyAsync bandwidth (GB/s) for
  * `bytes`-sized copies on the weight-copy stream (App. A sweep). */
 pipo_status pipo_probe_h2d(pipo_ctx* ctx, int64_t bytes, int32_t reps, double* gbs);
+
+/* Disk probe (the DISK tier's roofline denominator; the tier is
+ * PAPER.md:285-303 §3.3): reads the payload of the n_layers blob files
+ * dir/layer_<i>.pipo (as written by the DISK tier: 4 KiB header + payload) with the
+ * reader pool's method — `threads` threads, O_DIRECT preads of `chunk` bytes (a 4 KiB
+ * multiple) into per-thread aligned buffers, no GPU handshake — and returns payload
+ * GB/s over wall time.  checksum (optional, NULL to skip; it costs CPU time) receives
+ * sum over files and payload bytes of (offset + 1) * byte mod 2^64.  No CUDA calls.
+ * Errors: PIPO_E_INVALID_ARG, PIPO_E_IO (missing file, short read), PIPO_E_FORMAT (bad
+ * header), PIPO_E_OOM. */
+pipo_status pipo_probe_disk(const char* dir, int32_t n_layers, int32_t threads, int64_t chunk, double* gbs,
+                            uint64_t* checksum);
 
 /* NUMA node of CUDA device `device`'s PCIe root (sysfs), -1 if unknown; the node a
  * PIPO_NUMA_GPU_LOCAL config binds to on a multi-node host. */

@@ -1753,7 +1753,7 @@ pipo_status pipo_attention_prefill(pipo_ctx* ctx, const uint16_t* q, const uint1
 
 pipo_status pipo_attention_gqa(pipo_ctx* ctx, const uint16_t* q, const uint16_t* k, const uint16_t* v, int32_t b,
                                int32_t n, int32_t past, int32_t n_heads, int32_t n_kv_heads, int32_t head_dim,
-                               float* o) {
+                               int32_t variant, float* o) {
   CHECK_CTX();
   if (!q || !k || !v || !o || b <= 0 || n <= 0 || past < 0 || n_heads <= 0 || n_kv_heads <= 0 ||
       n_heads % n_kv_heads || (head_dim != 64 && head_dim != 128))
@@ -1776,6 +1776,7 @@ pipo_status pipo_attention_gqa(pipo_ctx* ctx, const uint16_t* q, const uint16_t*
   aa.q = dq; aa.kc = dk; aa.vc = dv; aa.o = dout; aa.b = b; aa.n = n; aa.past = past; aa.d = d;
   aa.n_heads = n_heads; aa.kv_b = b; aa.dkv = dkv; aa.group = n_heads / n_kv_heads;
   aa.ws = ctx->ws; aa.ws_floats = ctx->ws_floats; aa.num_sms = ctx->num_sms;
+  aa.use_cuda_cores = variant;
   if (n == 1) LAUNCH(launch_attention_decode(aa, st));
   else LAUNCH(launch_attention_prefill(aa, st));
   LAUNCH(launch_f16_to_f32(dout, df, nq, st));

@@ -16,6 +16,7 @@
 #include <sys/stat.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
@@ -23,7 +24,9 @@
 #include <cstring>
 #include <deque>
 #include <mutex>
+#include <string>
 #include <thread>
+#include <vector>
 
 #include "disk.h"
 
@@ -248,3 +251,83 @@ pipo_status disk_enqueue_segment(pipo_ctx* ctx, int layer, int seg, uint8_t* dst
 int disk_io_error(pipo_ctx* ctx) { return ctx->disk ? ctx->disk->io_error.load() : 0; }
 
 }  // namespace pipo
+
+// ---------------------------------------------------------------------------------
+// Disk roofline probe (the disk tier's denominator).  The same read
+// path as the reader pool above — one file per layer, O_DIRECT, fixed-size chunks
+// handed to `threads` reader threads, each pread into its own aligned buffer — minus
+// the GPU handshake, so it bounds what the tier can reach.  No CUDA calls: it runs
+// without a GPU.
+extern "C" pipo_status pipo_probe_disk(const char* dir, int32_t n_layers, int32_t threads, int64_t chunk, double* gbs,
+                                       uint64_t* checksum) {
+  using namespace pipo;
+  if (!dir || n_layers <= 0 || threads <= 0 || threads > 64 || chunk < 4096 || chunk % 4096 || !gbs)
+    return PIPO_E_INVALID_ARG;
+  struct PReq {
+    int fd;
+    int64_t off, len, valid;   // file offset, bytes requested (4 KiB multiple), payload bytes in it
+    int64_t pos;               // payload offset of the chunk (checksum weights)
+  };
+  std::vector<int> fds;
+  std::vector<PReq> reqs;
+  int64_t total = 0;
+  auto close_all = [&] {
+    for (int fd : fds) close(fd);
+  };
+  void* hbuf = nullptr;
+  if (posix_memalign(&hbuf, 4096, sizeof(BlobFileHeader)) != 0) return PIPO_E_OOM;
+  for (int l = 0; l < n_layers; ++l) {
+    const std::string path = blob_path(dir, l);
+    int fd = open(path.c_str(), O_RDONLY | O_DIRECT);
+    if (fd < 0) fd = open(path.c_str(), O_RDONLY);
+    if (fd < 0) { free(hbuf); close_all(); return PIPO_E_IO; }
+    fds.push_back(fd);
+    BlobFileHeader hd;
+    if (pread(fd, hbuf, sizeof hd, 0) != (ssize_t)sizeof hd) { free(hbuf); close_all(); return PIPO_E_IO; }
+    std::memcpy(&hd, hbuf, sizeof hd);
+    if (std::memcmp(hd.magic, "PIPOBLB1", 8) != 0 || hd.version != 1 || hd.layer != (uint32_t)l) {
+      free(hbuf); close_all(); return PIPO_E_FORMAT;
+    }
+    const int64_t pb = (int64_t)hd.payload_bytes;
+    for (int64_t off = 0; off < pb; off += chunk) {
+      const int64_t v = std::min(chunk, pb - off);
+      reqs.push_back(PReq{fd, (int64_t)sizeof(BlobFileHeader) + off, (v + 4095) / 4096 * 4096, v, off});
+    }
+    total += pb;
+  }
+  free(hbuf);
+  std::atomic<size_t> next{0};
+  std::atomic<int> err{0};
+  std::atomic<uint64_t> sum{0};
+  auto reader = [&] {
+    void* p = nullptr;
+    if (posix_memalign(&p, 4096, (size_t)chunk) != 0) { err = 1; return; }
+    uint8_t* buf = static_cast<uint8_t*>(p);
+    uint64_t local = 0;
+    for (size_t i = next.fetch_add(1); i < reqs.size() && !err; i = next.fetch_add(1)) {
+      const PReq& r = reqs[i];
+      int64_t done = 0;
+      while (done < r.len) {
+        const ssize_t n = pread(r.fd, buf + done, (size_t)(r.len - done), r.off + done);
+        if (n < 0) { err = 1; break; }
+        if (n == 0) break;   // end of file (the last request is rounded up to 4 KiB)
+        done += n;
+      }
+      if (done < r.valid) err = 1;
+      if (checksum)   // position-weighted: sum_j (pos + j + 1) * byte_j mod 2^64
+        for (int64_t j = 0; j < r.valid; ++j) local += (uint64_t)(r.pos + j + 1) * buf[j];
+    }
+    sum += local;
+    free(p);
+  };
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<std::thread> th;
+  for (int i = 0; i < threads; ++i) th.emplace_back(reader);
+  for (auto& t : th) t.join();
+  const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  close_all();
+  if (err) return PIPO_E_IO;
+  *gbs = s > 0 ? (double)total / s / 1e9 : 0.0;
+  if (checksum) *checksum = sum.load();
+  return PIPO_OK;
+}

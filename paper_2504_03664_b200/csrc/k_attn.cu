@@ -292,40 +292,48 @@ __global__ void __launch_bounds__(128) attn_decode_v2_kernel(AttnArgs a, int n_s
   }
 }
 
-// GQA decode on tensor cores (variant 2): CTA = (KV head, sequence,
-// split).  The G <= 8 query heads of the KV head are the 16-row M dimension of
-// mma.sync m16n8k16 (rows >= G zero-filled, never stored), so each K/V row is read once
-// for the whole group and the G dot products cost no shuffles.  32-position K/V tiles in
-// a 3-stage cp.async ring; q fragments straight from global (rows 8-15 of the m16 tile
-// are always zero since G <= 8), no Q staging, so three K/V stages take 52 KB and 4 CTAs
-// fit per SM.  Warp w takes positions 8w .. 8w+7 of each tile: S is one m16n8 tile per
-// k-step pair; P.V uses the k = 0..7 half of m16n8k16 (the other half zero), online
-// softmax in fp32 (log2 domain, P rounded to fp16 as in the prefill kernel); the 4 warps
-// merge in fixed order through shared memory; splits merge in attn_merge_kernel.
-template <int HD, int NS>
-__global__ void __launch_bounds__(128) attn_decode_gqa_mma32_kernel(AttnArgs a, int n_splits, int pos_per_split) {
+// GQA decode on tensor cores, transposed (S^T = K q^T, O^T = V^T P^T): the
+// positions are the 16-row M dimension and the G <= 8 query heads of the KV head the
+// n = 8 dimension of mma.sync m16n8k16, so no M rows are padding: per 16 positions a warp
+// issues HD/16 mma for the scores and HD/16 for P.V (round 1's kernel with the heads on M:
+// HD/8 and HD/4 per 8 positions, half of each on zero rows; 4-7 % slower, removed).  K tiles are the A operand as stored
+// (ldmatrix), V^T is ldmatrix.trans of the stored V tile, q^T sits in registers as the B
+// operand (rows >= G zero), and the score accumulator becomes P^T's B fragment with one
+// movmatrix.trans per 8 x 8 half.  Per-head softmax (fp32, log2 domain, P rounded to
+// fp16) reduces over the 8 lanes that share a head column.  NW warps per CTA, each 16
+// positions of a 16*NW-position tile, NS-stage cp.async ring; warps merge in fixed order
+// through shared memory, splits in attn_merge_kernel.
+__device__ __forceinline__ uint32_t movmatrix_t(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;\n" : "=r"(y) : "r"(x));
+  return y;
+}
+
+template <int HD, int NW, int NS>
+__global__ void __launch_bounds__(NW * 32) attn_decode_gqa_st_kernel(AttnArgs a, int n_splits, int pos_per_split) {
   constexpr int KP = HD + 8;
-  constexpr int NT_O = HD / 8;
   constexpr int CH = HD / 8;
-  constexpr int T = 32;
+  constexpr int T = 16 * NW;
+  constexpr int NTH = NW * 32;
+  constexpr int MT = HD / 16;
   extern __shared__ __align__(16) uint8_t smem_attn[];
   __half* sK = reinterpret_cast<__half*>(smem_attn);           // [NS][T][KP]
   __half* sV = sK + NS * T * KP;                               // [NS][T][KP]
-  float* sM = reinterpret_cast<float*>(sV + NS * T * KP);      // [4 warps][8 rows]
-  float* sL = sM + 32;
-  float* sO = reinterpret_cast<float*>(sK);                    // [4][8][HD], reuses sK after the loop
-  static_assert(4 * 8 * HD * 4 <= NS * T * KP * 2, "merge buffer fits in sK");
+  float* sM = reinterpret_cast<float*>(sV + NS * T * KP);      // [NW][8 heads]
+  float* sL = sM + NW * 8;
+  float* sO = reinterpret_cast<float*>(sK);                    // [NW][8][HD], reuses sK after the loop
+  static_assert(NW * 8 * HD * 4 <= NS * T * KP * 2, "merge buffer fits in sK");
   pdl_wait();
   const int kvh = blockIdx.x, bi = blockIdx.y, split = blockIdx.z;
   const int G = a.group;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, tq = lane & 3;
+  const int g = lane >> 2, tq = lane & 3, mi = lane >> 3, r8 = lane & 7;
   const int L = a.past + 1;
   const int lo = split * pos_per_split, hi = min(L, lo + pos_per_split);
   const int n_kv = (hi - lo + T - 1) / T;
   const int64_t pstride = kv_pstride(a), bstride = kv_bstride(a);
   auto load_kv = [&](int j, int buf) {
-    for (int c = tid; c < T * CH; c += 128) {
+    for (int c = tid; c < T * CH; c += NTH) {
       const int r = c / CH, ch = c % CH, p = lo + j * T + r;
       const int64_t off = (int64_t)min(p, hi - 1) * pstride + (int64_t)bi * bstride + kvh * HD + ch * 8;
       const int bytes = p < hi ? 16 : 0;
@@ -338,92 +346,106 @@ __global__ void __launch_bounds__(128) attn_decode_gqa_mma32_kernel(AttnArgs a, 
     if (st < n_kv) load_kv(st, st);
     cp_async_commit();
   }
-  // A fragments of q: row g (query head kvh*G + g) when g < G, rows 8-15 zero
-  uint32_t qf[HD / 16][2];
+  // B fragments of q^T: column g = query head kvh*G + g when g < G, else zero
+  uint32_t qf[MT][2];
   {
     const __half* qrow = a.q + (int64_t)bi * a.d + (kvh * G + min(g, G - 1)) * HD;
 #pragma unroll
-    for (int kk = 0; kk < HD / 16; ++kk) {
+    for (int kk = 0; kk < MT; ++kk) {
       qf[kk][0] = g < G ? *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * tq) : 0u;
       qf[kk][1] = g < G ? *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 8 + 2 * tq) : 0u;
     }
   }
-  float o[NT_O][4];
+  float o[MT][4];   // O^T: rows hd 16i+g (+8), columns heads 2tq, 2tq+1
 #pragma unroll
-  for (int i = 0; i < NT_O; ++i)
+  for (int i = 0; i < MT; ++i)
 #pragma unroll
     for (int c = 0; c < 4; ++c) o[i][c] = 0.f;
-  float m_r = -INFINITY, l_r = 0.f;   // row g (rows g + 8 are padding)
+  float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f};   // heads 2tq, 2tq+1 (l: my positions)
   for (int j = 0; j < n_kv; ++j) {
     const int buf = j % NS;
     if (j + NS - 1 < n_kv) load_kv(j + NS - 1, (j + NS - 1) % NS);
     cp_async_commit();
     cp_async_wait<NS - 1>();
     __syncthreads();
-    float sc[4] = {0.f, 0.f, 0.f, 0.f};
-    const __half* kb = sK + (buf * T + warp * 8) * KP;
+    // S^T (16 positions x 8 heads): two accumulators halve the dependent mma chain
+    float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
+    const __half* kb = sK + (buf * T + warp * 16) * KP;
 #pragma unroll
-    for (int kk2 = 0; kk2 < HD / 32; ++kk2) {
-      uint32_t b0, b1, b2, b3;
-      ldmatrix_x4(b0, b1, b2, b3, kb + (lane & 7) * KP + kk2 * 32 + (lane >> 3) * 8);
-      const uint32_t a0[4] = {qf[2 * kk2][0], 0u, qf[2 * kk2][1], 0u};
-      const uint32_t a1[4] = {qf[2 * kk2 + 1][0], 0u, qf[2 * kk2 + 1][1], 0u};
-      mma_16816(sc, a0, b0, b1);
-      mma_16816(sc, a1, b2, b3);
+    for (int kk = 0; kk < MT; ++kk) {
+      uint32_t af[4];
+      ldmatrix_x4(af[0], af[1], af[2], af[3], kb + ((mi & 1) * 8 + r8) * KP + kk * 16 + (mi >> 1) * 8);
+      mma_16816(kk & 1 ? s1 : s0, af, qf[kk][0], qf[kk][1]);
     }
-    float mx = m_r;
+    const int p0 = lo + j * T + warp * 16 + g;
+    float sc[4];
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const int p = lo + j * T + warp * 8 + 2 * tq + c;
-      sc[c] = p < hi ? sc[c] * kLog2e : -INFINITY;
-      mx = fmaxf(mx, sc[c]);
+    for (int c = 0; c < 4; ++c) sc[c] = (p0 + (c >> 1) * 8) < hi ? (s0[c] + s1[c]) * kLog2e : -INFINITY;
+    float mx[2], corr[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float m = fmaxf(m_r[h], fmaxf(sc[h], sc[h + 2]));
+      m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
+      m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
+      m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
+      mx[h] = m;
+      corr[h] = m == -INFINITY ? 1.f : exp2f(m_r[h] - m);
+      m_r[h] = m;
+      l_r[h] *= corr[h];
     }
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-    const float corr = mx == -INFINITY ? 1.f : exp2f(m_r - mx);
-    m_r = mx;
-    l_r *= corr;
+    float e[4];
 #pragma unroll
-    for (int i = 0; i < NT_O; ++i) { o[i][0] *= corr; o[i][1] *= corr; }
-    const float e0 = mx == -INFINITY ? 0.f : exp2f(sc[0] - mx);
-    const float e1 = mx == -INFINITY ? 0.f : exp2f(sc[1] - mx);
-    l_r += e0 + e1;
-    const __half2 p2 = __floats2half2_rn(e0, e1);
-    const uint32_t pf[4] = {*reinterpret_cast<const uint32_t*>(&p2), 0u, 0u, 0u};
-    const __half* vb = sV + (buf * T + warp * 8) * KP;
+    for (int c = 0; c < 4; ++c) e[c] = mx[c & 1] == -INFINITY ? 0.f : exp2f(sc[c] - mx[c & 1]);
+    l_r[0] += e[0] + e[2];
+    l_r[1] += e[1] + e[3];
 #pragma unroll
-    for (int nt4 = 0; nt4 < HD / 32; ++nt4) {
-      uint32_t b0, b1, b2, b3;
-      const __half* ptr = vb + (lane & 7) * KP + nt4 * 32 + (lane >> 3) * 8;
+    for (int i = 0; i < MT; ++i) {
+      o[i][0] *= corr[0]; o[i][1] *= corr[1]; o[i][2] *= corr[0]; o[i][3] *= corr[1];
+    }
+    __half2 top = __floats2half2_rn(e[0], e[1]), bot = __floats2half2_rn(e[2], e[3]);
+    const uint32_t pb0 = movmatrix_t(*reinterpret_cast<uint32_t*>(&top));   // P^T rows 2tq.. (positions 0-7)
+    const uint32_t pb1 = movmatrix_t(*reinterpret_cast<uint32_t*>(&bot));   // positions 8-15
+    const __half* vb = sV + (buf * T + warp * 16) * KP;
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      uint32_t af[4];
+      const __half* ptr = vb + ((mi >> 1) * 8 + r8) * KP + i * 16 + (mi & 1) * 8;
       asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
-                   : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
+                   : "=r"(af[0]), "=r"(af[1]), "=r"(af[2]), "=r"(af[3])
                    : "r"(smem_u32(ptr)));
-      mma_16816(o[4 * nt4 + 0], pf, b0, 0u);
-      mma_16816(o[4 * nt4 + 1], pf, b1, 0u);
-      mma_16816(o[4 * nt4 + 2], pf, b2, 0u);
-      mma_16816(o[4 * nt4 + 3], pf, b3, 0u);
+      mma_16816(o[i], af, pb0, pb1);
     }
     __syncthreads();
   }
   cp_async_wait<0>();
-  l_r += __shfl_xor_sync(0xffffffffu, l_r, 1);
-  l_r += __shfl_xor_sync(0xffffffffu, l_r, 2);
-  __syncthreads();
-  if (tq == 0) { sM[warp * 8 + g] = m_r; sL[warp * 8 + g] = l_r; }
 #pragma unroll
-  for (int i = 0; i < NT_O; ++i) {
-    sO[(warp * 8 + g) * HD + i * 8 + 2 * tq] = o[i][0];
-    sO[(warp * 8 + g) * HD + i * 8 + 2 * tq + 1] = o[i][1];
+  for (int h = 0; h < 2; ++h) {
+    l_r[h] += __shfl_xor_sync(0xffffffffu, l_r[h], 4);
+    l_r[h] += __shfl_xor_sync(0xffffffffu, l_r[h], 8);
+    l_r[h] += __shfl_xor_sync(0xffffffffu, l_r[h], 16);
   }
   __syncthreads();
-  for (int i = tid; i < G * HD; i += 128) {
+  if (g == 0) {
+    sM[warp * 8 + 2 * tq] = m_r[0]; sM[warp * 8 + 2 * tq + 1] = m_r[1];
+    sL[warp * 8 + 2 * tq] = l_r[0]; sL[warp * 8 + 2 * tq + 1] = l_r[1];
+  }
+  if (2 * tq < G) {
+    float* o0 = sO + (warp * 8 + 2 * tq) * HD;
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      o0[16 * i + g] = o[i][0]; o0[HD + 16 * i + g] = o[i][1];
+      o0[16 * i + g + 8] = o[i][2]; o0[HD + 16 * i + g + 8] = o[i][3];
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < G * HD; i += NTH) {
     const int r = i / HD, t = i - r * HD, head = kvh * G + r;
     float M = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) M = fmaxf(M, sM[w * 8 + r]);
+    for (int w = 0; w < NW; ++w) M = fmaxf(M, sM[w * 8 + r]);
     float l = 0.f, ov = 0.f;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
+    for (int w = 0; w < NW; ++w) {
       const float f = sM[w * 8 + r] == -INFINITY ? 0.f : exp2f(sM[w * 8 + r] - M);
       l += sL[w * 8 + r] * f;
       ov += sO[(w * 8 + r) * HD + t] * f;
@@ -891,27 +913,42 @@ int launch_attention_decode_q4(const AttnArgs& a, cudaStream_t st) {
 // The tensor-core GQA kernel (default for group sizes 2/4/8): 32-position K/V tiles in a
 // 3-stage cp.async ring, 4 CTAs/SM.  Measured alternatives (64-position tiles with 2 or 3
 // stages, forced position splits: profiles/r01/gqa_tc) were slower and are not built.
-static int launch_attention_decode_gqa_mma(const AttnArgs& a, int G, cudaStream_t st) {
+// The transposed tensor-core GQA kernel (default for group sizes 2/4/8).  4 warps x 16
+// positions per 64-position tile when the grid fits one wave at its occupancy (3 stages:
+// 104 KB at hd 128, 55 KB at hd 64), else 2 warps x 16 (52 / 28 KB, 4+ CTAs per SM): on
+// B200 (profiles/r02/attn_gqa_st/) 4 warps win at c8 / c7 / long contexts, 2 warps at c6
+// (512 CTAs would need 1.7 waves at 2 CTAs per SM).  Measured and not built: L2 prefetch
+// of the tiles past the ring (+14-70 %), 4 stages of 32 positions (+20 %).
+template <int HD, int NW>
+static void launch_gqa_st(const AttnArgs& a, dim3 grid, int n_splits, int per, cudaStream_t st) {
+  constexpr int smem = 2 * 3 * 16 * NW * (HD + 8) * 2 + 2 * NW * 8 * 4;
+  ensure_max_smem(attn_decode_gqa_st_kernel<HD, NW, 3>, smem);
+  launch_pdl_k(attn_decode_gqa_st_kernel<HD, NW, 3>, grid, dim3(NW * 32), smem, st, a, n_splits, per);
+}
+
+static int launch_attention_decode_gqa_mma(const AttnArgs& a, int G, int var, cudaStream_t st) {
   const int hd = a.d / a.n_heads;
   const int L = a.past + 1;
   const int pairs = a.b * (a.n_heads / G);
   // split positions only when the (b, KV head) pairs cannot cover the SMs: the merge
   // launch costs more than the tail wave (c6: 512 pairs, 1.33 vs 1.62 ms/step)
-  int n_splits = pairs >= a.num_sms ? 1 : (a.num_sms + pairs - 1) / pairs;
-  n_splits = max(1, min(n_splits, (L + 63) / 64));
-  constexpr int tile = 32;
-  const int per = ((L + n_splits - 1) / n_splits + tile - 1) / tile * tile;   // whole tiles per split
-  n_splits = (L + per - 1) / per;
+  int n_splits0 = pairs >= a.num_sms ? 1 : (a.num_sms + pairs - 1) / pairs;
+  n_splits0 = max(1, min(n_splits0, (L + 63) / 64));
+  auto splits_for = [&](int tile, int* per) {
+    *per = ((L + n_splits0 - 1) / n_splits0 + tile - 1) / tile * tile;   // whole tiles per split
+    return (L + *per - 1) / *per;
+  };
+  int per4 = 0, per2 = 0;
+  const int ns4 = splits_for(64, &per4), ns2 = splits_for(32, &per2);
+  const int smem4 = 2 * 3 * 64 * (hd + 8) * 2 + 2 * 4 * 8 * 4;
+  const int64_t fit4 = (int64_t)a.num_sms * ((228 << 10) / (smem4 + 1024));
+  // variant 5 forces 4 warps, 6 forces 2 (test and measurement hooks)
+  const bool four = var == 5 || (var != 6 && (int64_t)pairs * ns4 <= fit4);
+  const int n_splits = four ? ns4 : ns2, per = four ? per4 : per2;
   if (n_splits > 1 && (int64_t)a.b * a.n_heads * n_splits * (hd + 2) > a.ws_floats) return -1;
   dim3 grid(a.n_heads / G, a.b, n_splits);
-  const int smem32 = 2 * 3 * 32 * (hd + 8) * 2 + 2 * 32 * 4;
-#define PIPO_GQA32(HDV)                                                                                          \
-  do {                                                                                                           \
-    ensure_max_smem(attn_decode_gqa_mma32_kernel<HDV, 3>, smem32);                                              \
-    launch_pdl_k(attn_decode_gqa_mma32_kernel<HDV, 3>, grid, dim3(128), smem32, st, a, n_splits, per);           \
-  } while (0)
-  if (hd == 64) PIPO_GQA32(64); else PIPO_GQA32(128);
-#undef PIPO_GQA32
+  if (hd == 64) { if (four) launch_gqa_st<64, 4>(a, grid, n_splits, per, st); else launch_gqa_st<64, 2>(a, grid, n_splits, per, st); }
+  else { if (four) launch_gqa_st<128, 4>(a, grid, n_splits, per, st); else launch_gqa_st<128, 2>(a, grid, n_splits, per, st); }
   if (n_splits == 1) return 1;
   dim3 g2(a.n_heads, a.b);
   if (hd == 64) launch_pdl_k(attn_merge_kernel<64>, g2, dim3(64), 0, st, a, n_splits);
@@ -931,9 +968,11 @@ int launch_attention_decode(const AttnArgs& a, cudaStream_t st) {
   // variant: 0 one-row-per-warp (MHA default), 1 lane groups (CUDA cores; AttnArgs
   // use_cuda_cores = 1 through the pipo_attention_decode hook), 2 tensor cores (GQA default:
   // c6 attention 1.98 -> 1.33 ms/step, c7 0.435 -> 0.36; profiles/r01/gqa_tc); 3 forces the
-  // one-row-per-warp kernel for a GQA group (test hook)
-  const int var = a.use_cuda_cores == 1 ? 1 : a.use_cuda_cores == 3 ? 0 : (G > 1 ? 2 : 0);
-  if (var == 2) return launch_attention_decode_gqa_mma(a, G, st);
+  // one-row-per-warp kernel for a GQA group (test hook); 5 / 6 force the 4- / 2-warp
+  // tensor-core GQA kernel (launch_attention_decode_gqa_mma)
+  const int uc = a.use_cuda_cores;
+  const int var = uc == 1 ? 1 : uc == 3 ? 0 : G == 1 ? 0 : (uc == 5 || uc == 6) ? uc : 2;
+  if (var >= 2) return launch_attention_decode_gqa_mma(a, G, var, st);
   const bool v2 = var == 1;
   const int pairs = a.b * a.n_heads / G;
   // enough CTAs for ~8 waves of resident blocks (9 per SM): the block scheduler then

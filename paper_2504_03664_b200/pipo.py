@@ -147,9 +147,11 @@ _sig("pipo_attention_decode", C.c_int, _P, _u16, _u16, _u16, C.c_int32, C.c_int3
 _sig("pipo_attention_prefill", C.c_int, _P, _u16, _u16, _u16, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
      C.c_int32, C.c_int32, _f)
 _sig("pipo_attention_gqa", C.c_int, _P, _u16, _u16, _u16, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
-     C.c_int32, _f)
+     C.c_int32, C.c_int32, _f)
 _sig("pipo_rope", C.c_int, _P, _u16, _u16, C.c_int32, C.c_int32, C.c_int32, _f, _f)
 _sig("pipo_gpu_numa_node", C.c_int32, C.c_int32)
+_sig("pipo_probe_disk", C.c_int, C.c_char_p, C.c_int32, C.c_int32, C.c_int64, C.POINTER(C.c_double),
+     C.POINTER(C.c_uint64))
 _sig("pipo_shard_range", C.c_int, C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64))
 _sig("pipo_nccl_unique_id", C.c_int, _u8)
 _sig("pipo_shard_stream_init", C.c_int, _P, C.c_int32, C.c_int32, _u8)
@@ -173,7 +175,7 @@ EXPORTED = ["pipo_last_error", "pipo_abi_version", "pipeline_init", "pipeline_de
             "pipo_unpack_int4_g64", "pipo_linear", "pipo_bench_linear", "pipo_probe_bulk", "pipo_bench_attention", "pipo_attention_decode", "pipo_attention_prefill", "pipo_debug_capture", "pipo_probe_h2d", "pipo_debug_read_rows",
             "pipo_attention_gqa", "pipo_rope", "pipo_set_flags", "pipo_debug_inject", "pipo_debug_ring_checksums", "pipo_bench_attention_prefill",
             "pipo_debug_read_blob", "pipo_layer_blob_bytes", "pipo_shard_range", "pipo_gpu_numa_node", "pipo_nccl_unique_id", "pipo_shard_stream_init", "pipo_shard_p2p_export", "pipo_shard_p2p_init",
-            "pipo_ffn_hidden_dim", "pipo_memory_model", "pipo_choose_block_size", "pipo_choose_plan", "pipo_get_plan"]
+            "pipo_ffn_hidden_dim", "pipo_probe_disk", "pipo_memory_model", "pipo_choose_block_size", "pipo_choose_plan", "pipo_get_plan"]
 
 
 class PipoError(RuntimeError):
@@ -358,7 +360,7 @@ def pipo_attention_prefill(ctx, q, k, v, past, n_heads, cuda_cores=False):
     return o
 
 
-def pipo_attention_gqa(ctx, q, k, v, past, n_heads, n_kv_heads):
+def pipo_attention_gqa(ctx, q, k, v, past, n_heads, n_kv_heads, variant=0):
     """q [b][n][h*hd], k/v [past+n][b][h_kv*hd] (fp16 values) -> o [b][n][h*hd] fp32."""
     q = _c(np.asarray(q, dtype=np.float16).view(np.uint16), np.uint16)
     k = _c(np.asarray(k, dtype=np.float16).view(np.uint16), np.uint16)
@@ -366,7 +368,7 @@ def pipo_attention_gqa(ctx, q, k, v, past, n_heads, n_kv_heads):
     b, n, d = q.shape
     o = np.empty((b, n, d), dtype=np.float32)
     _check(_lib.pipo_attention_gqa(ctx, _ptr(q, C.c_uint16), _ptr(k, C.c_uint16), _ptr(v, C.c_uint16), b, n, past,
-                                   n_heads, n_kv_heads, d // n_heads, _ptr(o, C.c_float)))
+                                   n_heads, n_kv_heads, d // n_heads, variant, _ptr(o, C.c_float)))
     return o
 
 
@@ -475,6 +477,16 @@ def pipo_probe_h2d(ctx, nbytes: int, reps: int = 5) -> float:
     g = C.c_double()
     _check(_lib.pipo_probe_h2d(ctx, nbytes, reps, C.byref(g)))
     return g.value
+
+
+def pipo_probe_disk(directory: str, n_layers: int, threads: int = 4, chunk: int = 32 << 20,
+                    checksum: bool = False):
+    """Disk-tier roofline probe (no GPU): (GB/s, checksum or None)."""
+    g = C.c_double()
+    cs = C.c_uint64()
+    _check(_lib.pipo_probe_disk(str(directory).encode(), n_layers, threads, chunk, C.byref(g),
+                                C.byref(cs) if checksum else None))
+    return g.value, (cs.value if checksum else None)
 
 
 def mem_spec(*, l, d, V, h, h_kv, d_h, mlp_mats=3, p_weight=2.0, p_act=2.0) -> pipo_mem_spec:

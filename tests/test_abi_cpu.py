@@ -40,7 +40,7 @@ def test_exports_every_declared_symbol(pipo):
     for n in names:
         assert hasattr(lib, n), f"{n} declared in pipo.h but not exported"
     assert set(names) == set(pipo.EXPORTED)
-    assert pipo.pipo_abi_version() == 4
+    assert pipo.pipo_abi_version() == 5
 
 
 def test_so_is_sm100a(pipo):
@@ -80,3 +80,44 @@ def test_host_quantizer_domain_errors(pipo):
         pipo.pipo_quantize_int4_g64(np.full((1, 64), np.nan, dtype=np.float32))
     with pytest.raises(pipo.PipoError):
         pipo.pipo_quantize_int4_g64(np.full((1, 64), 1e6, dtype=np.float32))
+
+
+def _write_blob_file(directory, layer, payload, magic=b"PIPOBLB1"):
+    hdr = bytearray(4096)
+    hdr[0:8] = magic
+    hdr[8:12] = (1).to_bytes(4, "little")
+    hdr[12:16] = layer.to_bytes(4, "little")
+    hdr[16:24] = len(payload).to_bytes(8, "little")
+    with open(os.path.join(directory, f"layer_{layer}.pipo"), "wb") as f:
+        f.write(bytes(hdr) + payload.tobytes())
+
+
+def test_disk_probe_reads_every_payload_byte(pipo, tmp_path):
+    """The disk-tier roofline probe (pipo_probe_disk) reads exactly the
+    payload of each layer file — ragged sizes, chunks smaller and larger than a file, more
+    threads than chunks — checked by the position-weighted checksum computed here."""
+    rng = np.random.default_rng(5)
+    sizes = [10000, 8192, 123457, 1]
+    want = 0
+    for l, n in enumerate(sizes):
+        b = rng.integers(0, 256, n, dtype=np.uint8)
+        _write_blob_file(tmp_path, l, b)
+        want += int((np.arange(1, n + 1, dtype=np.uint64) * b.astype(np.uint64)).sum(dtype=np.uint64))
+    want %= 1 << 64
+    for threads, chunk in [(1, 4096), (4, 8192), (8, 1 << 20)]:
+        gbs, cs = pipo.pipo_probe_disk(str(tmp_path), len(sizes), threads, chunk, checksum=True)
+        assert cs == want and gbs > 0
+    gbs, cs = pipo.pipo_probe_disk(str(tmp_path), 2, 2, 4096)   # first two files only, no checksum
+    assert cs is None and gbs > 0
+
+
+def test_disk_probe_errors(pipo, tmp_path):
+    _write_blob_file(tmp_path, 0, np.zeros(100, np.uint8))
+    _write_blob_file(tmp_path, 1, np.zeros(100, np.uint8), magic=b"NOTABLOB")
+    with pytest.raises(pipo.PipoError):                         # bad header
+        pipo.pipo_probe_disk(str(tmp_path), 2, 1, 4096)
+    with pytest.raises(pipo.PipoError):                         # missing file
+        pipo.pipo_probe_disk(str(tmp_path / "none"), 1, 1, 4096)
+    with pytest.raises(pipo.PipoError):                         # chunk not a 4 KiB multiple
+        pipo.pipo_probe_disk(str(tmp_path), 1, 1, 5000)
+    assert pipo.pipo_probe_disk(str(tmp_path), 1, 1, 4096)[0] > 0

@@ -58,10 +58,15 @@ def test_rope_kernel_vs_oracle():
 
 @pytest.mark.parametrize("hd,H,Hkv,n,past", [(64, 8, 2, 1, 37), (128, 8, 4, 1, 300), (64, 8, 1, 1, 0),
                                              (64, 8, 2, 70, 0), (128, 4, 2, 33, 12), (128, 16, 2, 1, 100),
-                                             (128, 32, 8, 1, 527), (64, 16, 4, 1, 5)])
-def test_gqa_attention_vs_oracle(hd, H, Hkv, n, past):
-    """GQA attention (decode: the tensor-core kernel, position splits + merge when the
-    (b, KV head) pairs do not cover the SMs; prefill: the causal kernel)."""
+                                             (128, 32, 8, 1, 527), (64, 16, 4, 1, 5), (128, 64, 8, 1, 1039),
+                                             (64, 32, 4, 1, 33), (128, 16, 8, 1, 16)])
+@pytest.mark.parametrize("variant", [0, 5, 6])
+def test_gqa_attention_vs_oracle(hd, H, Hkv, n, past, variant):
+    """GQA attention (decode: the tensor-core kernel — variant 0 the production choice, 5 / 6
+    forced to 4 / 2 warps — position splits + merge when the (b, KV head) pairs do not cover the
+    SMs, ragged last tiles; prefill: the causal kernel)."""
+    if n > 1 and variant:
+        pytest.skip("variants select decode kernels")
     pipo = pipo_mod()
     rng = np.random.default_rng(hd + H + n + past)
     b = 3
@@ -70,7 +75,7 @@ def test_gqa_attention_vs_oracle(hd, H, Hkv, n, past):
     v = rng.standard_normal((past + n, b, Hkv * hd)).astype(np.float16)
     cfg = pipo.make_config(TINY, max_batch=4, max_seq=16, weight_tier=pipo.PIPO_TIER_DEVICE)
     with pipo.Pipeline(cfg) as pl:
-        o = pipo.pipo_attention_gqa(pl.ctx, q, k, v, past, H, Hkv)
+        o = pipo.pipo_attention_gqa(pl.ctx, q, k, v, past, H, Hkv, variant)
     ref = llama.attention_gqa(q.astype(np.float64), k.astype(np.float64).transpose(1, 0, 2),
                               v.astype(np.float64).transpose(1, 0, 2), past, H, Hkv)
     assert rel_inf(o, ref) < 5e-3

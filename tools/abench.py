@@ -15,7 +15,7 @@ if len(sys.argv) > 1:
 for name, b, L, d, H, Hkv in cases:
     row = {}
     dkv = d // H * (Hkv or H)
-    for v in ([0, 1] if not Hkv else [0, 1, 3]):
+    for v in ([0, 1] if not Hkv else [0, 5, 6, 3]):
         us = pipo.pipo_bench_attention(pl.ctx, b, L, d, H, v, 20, Hkv)
         row[f"var{v}"] = (round(us, 2), round(2 * L * b * dkv * 2 / us / 1e3, 1))
     print(name, "us, GB/s:", row, flush=True)
