@@ -403,8 +403,8 @@ _CLASS_KERNELS = {"linear_decode": ("gemm_tm_kernel", "gemm_ws_kernel", "gemv_in
 
 def cupti_kernel_times(pl, tok_dev, steps, timed_steps, kst, profile: bool):
     """Kernel-only GPU time per unit of each class from a CUPTI trace (torch.profiler)
-    of `steps` extra decode steps run right after the timed region (all of a class's
-    kernels summed, e.g. a GEMM and its stream-K reduce).  Units and algorithmic bytes
+    of `steps` extra decode steps run right after the timed region (a class's kernels
+    as the union of their intervals, e.g. a GEMM and its overlapping stream-K reduce).  Units and algorithmic bytes
     per unit come from the event-timed region (`timed_steps` steps).  Every rank runs
     the steps (the sharded variant has a collective); only `profile` ranks trace."""
     import torch
@@ -421,17 +421,34 @@ def cupti_kernel_times(pl, tok_dev, steps, timed_steps, kst, profile: bool):
             torch.cuda.synchronize()
     except Exception as e:  # noqa: BLE001  (profiler unavailable: report, do not fail the bench)
         return {"error": str(e)[:200]}
-    tot = {c: 0.0 for c in _CLASS_KERNELS}
+    # per class, the UNION of its kernels' intervals: a GEMM and its stream-K reduce
+    # overlap under programmatic dependent launch, and summing their durations would count
+    # the overlap twice
+    iv = {c: [] for c in _CLASS_KERNELS}
     names = {}
     for e in prof.events():
         if e.device_type != torch.autograd.DeviceType.CUDA:
             continue
         for c, pats in _CLASS_KERNELS.items():
             if any(n in e.name for n in pats):
-                tot[c] += (e.time_range.end - e.time_range.start) * 1e-6
+                iv[c].append((e.time_range.start, e.time_range.end))
                 names.setdefault(c, set()).add(e.name.split("(")[0].split("<")[0])
                 break
-    out = {"source": f"torch.profiler CUDA activity (CUPTI), {steps} untimed steps right after the timed region"}
+    tot = {}
+    for c, lst in iv.items():
+        t, cur_s, cur_e = 0.0, None, None
+        for a, b in sorted(lst):
+            if cur_e is None or a > cur_e:
+                if cur_e is not None:
+                    t += cur_e - cur_s
+                cur_s, cur_e = a, b
+            else:
+                cur_e = max(cur_e, b)
+        if cur_e is not None:
+            t += cur_e - cur_s
+        tot[c] = t * 1e-6
+    out = {"source": f"torch.profiler CUDA activity (CUPTI), {steps} untimed steps right after the timed region; "
+                     "per class the union of its kernels' intervals"}
     for c, t in tot.items():
         k = kst.get(c)
         if not k or not k["units"] or t <= 0:

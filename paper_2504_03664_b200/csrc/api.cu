@@ -1514,11 +1514,11 @@ pipo_status pipo_bench_linear(pipo_ctx* ctx, int32_t wfmt, int32_t path, int32_t
   } else if (getenv("PIPO_WS_DEBUG") && (atoi(getenv("PIPO_WS_DEBUG")) & 32) && path == 5) {
     std::vector<uint64_t> wt(148 * 16);
     CK(cudaMemcpy(wt.data(), ctx->ws + (15ll << 20), wt.size() * 8, cudaMemcpyDeviceToHost));
-    double avg[9] = {0};
+    double avg[11] = {0};
     for (int c = 0; c < 148; ++c)
-      for (int k = 0; k < 9; ++k) avg[k] += wt[c * 16 + k] / 148.0;
-    fprintf(stderr, "tm-waits(kcycles): prod raw_empty %.1f | mma a_full %.1f x_full %.1f | unpack raw_full %.1f a_empty %.1f | xprod x_empty %.1f | total %.1f\n",
-            avg[0] / 1e3, avg[2] / 1e3, avg[3] / 1e3, avg[4] / 1e3, avg[5] / 1e3, avg[6] / 1e3, avg[8] / 1e3);
+      for (int k = 0; k < 11; ++k) avg[k] += wt[c * 16 + k] / 148.0;
+    fprintf(stderr, "tm-waits(kcycles): prod raw_empty %.1f | mma a_full %.1f x_full %.1f | unpack raw_full %.1f a_empty %.1f wait_st %.1f total %.1f | xprod x_empty %.1f | mma total %.1f\n",
+            avg[0] / 1e3, avg[2] / 1e3, avg[3] / 1e3, avg[4] / 1e3, avg[5] / 1e3, avg[9] / 1e3, avg[10] / 1e3, avg[6] / 1e3, avg[8] / 1e3);
   } else if (getenv("PIPO_WS_DEBUG") && (atoi(getenv("PIPO_WS_DEBUG")) & 32)) {
     std::vector<uint64_t> ts(148 * 8);
     CK(cudaMemcpy(ts.data(), ctx->ws + (15ll << 20), ts.size() * 8, cudaMemcpyDeviceToHost));

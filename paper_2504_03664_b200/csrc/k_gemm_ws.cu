@@ -99,6 +99,27 @@ __device__ __forceinline__ bool elect_one() {
   return pred != 0;
 }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// polling wait with back-off, for warps that idle most of the time (the epilogue)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (true) {
+    asm volatile(
+        "{\n.reg .pred P1;\nmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(64);
+  }
+}
 
 // stream-K partition of U units over G CTAs (U * G < 2^32: checked by the launchers)
 __device__ __forceinline__ int64_t u_begin(int64_t c, int64_t U, int64_t G) {
@@ -569,7 +590,7 @@ __device__ __forceinline__ uint64_t clk() {
   return t;
 }
 
-template <int BN, int KBU, int NACC, int UW>
+template <int BN, int KBU, int NACC, int UW, bool FIN>
 __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
     gemm_tm_kernel(const __grid_constant__ CUtensorMap xmap, LinearArgs a, int n_rt, int m_tiles, int G, int dbg) {
   using C = TmCfg<BN, KBU, NACC, UW>;
@@ -628,6 +649,7 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
   if (tid == 0) gstamp(10);
   uint64_t* wt = (dbg & 32) ? reinterpret_cast<uint64_t*>(a.ws + (15ll << 20)) + blockIdx.x * 16 : nullptr;
   uint64_t w_acc[2] = {0, 0};
+  uint64_t w_st = 0;   // debug: unpack warps' tcgen05.wait::st cycles
   const uint64_t t_begin = clk();
 #define TWAIT(slot, bar, par)                          \
   do {                                                 \
@@ -780,42 +802,36 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
           tmem_st32(a_base + sa * C::A_COLS + k * 64 + t * 32 + lane_off, o);
         }
         if (u + 1 < u1) load_unit(iu + 1, cw, s2);   // registers are free once the stores are issued
+        const uint64_t tst_ = wt ? clk() : 0;
         asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        if (wt) w_st += clk() - tst_;
         ws::tc_before();
         __syncwarp();
         if (lane == 0) ws::mbar_arrive(&a_full[sa]);
       }
     }
   } else {
-    // ---------------- epilogue ----------------
+    // ---------------- epilogue: every segment but the last ----------------
+    // (a segment = this CTA's maximal run of units inside one output tile).  The first
+    // segment of a range that starts inside a tile is a stream-K CONTRIBUTOR: its partial
+    // goes to the workspace early, released by a flag.  The last segment is drained below
+    // by all unpack + epilogue warps together.
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     int seg = 0;
     int64_t u = u0;
-    const int64_t first_tile_mine = u0 / n_ku;
     while (u < u1) {
       const int64_t tile = u / n_ku;
       const int64_t seg_end = min(u1, (tile + 1) * n_ku);
+      if (seg_end == u1 && FIN) break;                     // the last segment: below
       const bool full = (u == tile * n_ku) && (seg_end == (tile + 1) * n_ku);
       const int pr = (int)(tile % n_pairs), mt = (int)(tile / n_pairs);
       const int m0 = mt * BN;
       const int ntile = (2 * pr + 1 < n_rt) ? 2 : 1;
       const int ab = seg % NACC;
-      {
-        uint32_t done = 0;
-        const uint32_t addr = smem_u32(&acc_full[ab]), par = (seg / NACC) & 1;
-        while (true) {
-          asm volatile(
-              "{\n.reg .pred P1;\nmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
-              : "=r"(done)
-              : "r"(addr), "r"(par)
-              : "memory");
-          if (done) break;
-          __nanosleep(128);
-        }
-      }
+      ws::mbar_wait_sleep(&acc_full[ab], (uint32_t)((seg / NACC) & 1));
       ws::tc_after();
-      const int slot = 2 * (int)blockIdx.x + (tile == first_tile_mine ? 0 : 1);
+      const int slot = 2 * (int)blockIdx.x + ((FIN || u == u0) ? 0 : 1);
       float* part = a.ws + (int64_t)slot * (2 * BN * 128);
       for (int tt = 0; tt < ntile; ++tt) {
         const uint32_t t_row = tmem + ab * (2 * BN) + tt * BN + ((uint32_t)(quarter * 32) << 16);
@@ -834,10 +850,86 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
       ws::tc_before();
       __syncwarp();
       if (lane == 0) ws::mbar_arrive(&acc_empty[ab]);
+      if (FIN && !full) {   // contributor (only the first segment can be one): release the partial
+        __threadfence();
+        ws::named_bar(2, 128);
+        if (warp == C::E0 && lane == 0) ws::st_release_u32(a.flags + blockIdx.x, 1u);
+      }
       u = seg_end;
       ++seg;
     }
     if (warp == C::E0 && lane == 0) gstamp(12);
+  }
+  if (FIN && warp >= 2 && warp < C::XW && u0 < u1) {
+    // ---------------- the last segment: all unpack + epilogue warps ----------------
+    //  full        -> fused epilogue
+    //  contributor -> partial + release flag (a range inside one tile)
+    //  finisher    -> the CTA owning the tile's first unit: waits the flags of the CTAs
+    //                 that cover the rest of the tile (their partials were written early,
+    //                 in their first segment), adds them in k order — the order of the
+    //                 separate reduce (0 + own + next + ...), so the result is bit-identical
+    //                 — and runs the fused epilogue.  No second kernel.
+    constexpr int NGRP = (C::UWW + 4) / 4;                  // warps per lane quarter
+    const int quarter = warp & 3, grp = (warp - 2) >> 2;    // grp 0..NGRP-1
+    const int row = quarter * 32 + lane;
+    const int64_t tile = (u1 - 1) / n_ku, ts0 = tile * n_ku, te = ts0 + n_ku;
+    const int seg = (int)(tile - u0 / n_ku);
+    const int ab = seg % NACC;
+    const bool contributor = u0 > ts0;
+    const bool finisher = !contributor && u1 < te;
+    const int pr = (int)(tile % n_pairs), mt = (int)(tile / n_pairs);
+    const int m0 = mt * BN;
+    const int ntile = (2 * pr + 1 < n_rt) ? 2 : 1;
+    int c_last = (int)blockIdx.x;
+    if (finisher)
+      while (c_last + 1 < G && ws::u_begin(c_last + 1, U, G) < te) ++c_last;
+    ws::mbar_wait_sleep(&acc_full[ab], (uint32_t)((seg / NACC) & 1));
+    ws::tc_after();
+    if (finisher) {
+      if (warp == 2 && lane == 0)
+        for (int cc = (int)blockIdx.x + 1; cc <= c_last; ++cc)
+          while (ws::ld_acquire_u32(a.flags + cc) == 0) __nanosleep(32);
+      ws::named_bar(1, NGRP * 128);
+    }
+    float* part = a.ws + (int64_t)(2 * (int)blockIdx.x) * (2 * BN * 128);
+    for (int ch = grp; ch < ntile * (BN / 16); ch += NGRP) {
+      const int tt = ch / (BN / 16), c0 = (ch % (BN / 16)) * 16;
+      const int n = (2 * pr + tt) * 128 + row;
+      float v[16];
+      ws::tmem_ld16(tmem + ab * (2 * BN) + tt * BN + c0 + ((uint32_t)(quarter * 32) << 16), v);
+      if (contributor) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) __stcg(part + (tt * BN + c0 + j) * 128 + row, v[j]);
+        continue;
+      }
+      // k order (own, bid+1, bid+2, ...), two contributors' loads in flight at a time
+      int cc = (int)blockIdx.x + 1;
+      for (; cc <= c_last; cc += 2) {
+        const bool two = cc + 1 <= c_last;
+        const float* pa = a.ws + (int64_t)(2 * cc) * (2 * BN * 128) + (tt * BN + c0) * 128 + row;
+        const float* pb = pa + (two ? 2 * (2 * BN * 128) : 0);
+        float xa[16], xb[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) xa[j] = __ldcg(pa + j * 128);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) xb[j] = two ? __ldcg(pb + j * 128) : 0.f;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] += xa[j];
+        if (two)
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] += xb[j];
+      }
+      epi_store16(a.epi, m0 + c0, n, v);
+    }
+    if (contributor) {
+      __threadfence();
+      ws::named_bar(1, NGRP * 128);
+      if (warp == 2 && lane == 0) ws::st_release_u32(a.flags + blockIdx.x, 1u);
+    } else if (finisher) {
+      ws::named_bar(1, NGRP * 128);   // every partial read before the flags are re-armed
+      if (warp == 2 && lane == 0)
+        for (int cc = (int)blockIdx.x + 1; cc <= c_last; ++cc) a.flags[cc] = 0u;
+    }
   }
   if (wt && lane == 0) {
     // slots: 0/1 raw producer, 2/3 MMA (a_full, x_full), 4/5 unpack warp 2 (raw_full, a_empty),
@@ -845,6 +937,7 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
     const int role = warp == 0 ? 0 : warp == 1 ? 1 : warp == 2 ? 2 : warp == C::XW ? 3 : -1;
     if (role >= 0) { wt[2 * role] = w_acc[0]; wt[2 * role + 1] = w_acc[1]; }
     if (warp == 1) wt[8] = clk() - t_begin;
+    if (warp == 2) { wt[9] = w_st; wt[10] = clk() - t_begin; }
   }
 #undef TWAIT
   __syncwarp();
@@ -912,23 +1005,40 @@ static int run_ws(const LinearArgs& a, cudaStream_t st) {
 
 
 template <int BN, int KBU, int NACC = 2, int UW = 8>
-static int run_tm(const LinearArgs& a, cudaStream_t st) {
+static int run_tm(const LinearArgs& a_in, cudaStream_t st) {
   using C = TmCfg<BN, KBU, NACC, UW>;
-  ensure_max_smem(gemm_tm_kernel<BN, KBU, NACC, UW>, C::SMEM);
+  LinearArgs a = a_in;
   const int n_rt = (a.N + 127) / 128, m_tiles = (a.M + BN - 1) / BN, n_kb = a.K / 64;
   const int n_pairs = (n_rt + 1) / 2, n_ku = n_kb / KBU;
   const int64_t U = (int64_t)n_pairs * m_tiles * n_ku;
   const int G = (int)std::max<int64_t>(1, std::min<int64_t>(a.num_sms, U / (8 / KBU)));
+  // In-kernel fixup when a split tile spans at most ~3.5 CTAs (units per CTA >= 2/7 of a
+  // tile's units): its finisher then adds one to three partials.  Wider spans (long-K
+  // matrices: c5 out-proj / FC2, c6 QKV / FC2) keep the separate reduce, which spreads the
+  // sums over the whole GPU instead of one finisher CTA per tile (measured on B200,
+  // profiles/r02/tm_fin/).
+  static const int dbg = getenv("PIPO_WS_DEBUG") ? atoi(getenv("PIPO_WS_DEBUG")) : 0;
+  const bool fin = (int64_t)n_ku * G * 2 <= 7 * U && !(dbg & 512);   // debug 512: always the separate reduce
+  if (fin) ensure_max_smem(gemm_tm_kernel<BN, KBU, NACC, UW, true>, C::SMEM);
+  else ensure_max_smem(gemm_tm_kernel<BN, KBU, NACC, UW, false>, C::SMEM);
   if ((int64_t)2 * G * 2 * BN * 128 > a.ws_floats || U * G >= (1ll << 32)) return -1;
+  // fixup flags: the top 512 split-K counters (zero at rest; the finisher re-arms them)
+  if (fin && (a.n_counters < 1024 || G > 512)) return -1;
+  a.flags = reinterpret_cast<uint32_t*>(a.counters + a.n_counters - 512);
   CUtensorMap map;
   if (!make_xmap(&map, a.x, a.M, a.K, BN)) return -1;
-  static const int dbg = getenv("PIPO_WS_DEBUG") ? atoi(getenv("PIPO_WS_DEBUG")) : 0;
-  // Stream-K fixup as a separate launch (ws_reduce2_kernel, PDL).  Three in-kernel
-  // alternatives were built and measured SLOWER on B200 (profiles/r02/tm_fixup/, DESIGN.md
-  // §6): the tile's first CTA finishing from TMEM, the last-arriving contributor summing all
-  // partials, and a tail phase where the sharing CTAs reduce their tiles together (+4-5 us
-  // on every c5 linear).
-  launch_pdl(gemm_tm_kernel<BN, KBU, NACC, UW>, dim3(G), dim3(C::THREADS), C::SMEM, st, map, a, n_rt, m_tiles, G, dbg);
+  if (fin) {
+    // Stream-K fixup inside the kernel: the CTA owning a split tile's first unit finishes
+    // it from TMEM with its neighbours' partials (written early, released by flags).  The
+    // finisher spins on other CTAs' flags, so every CTA must be able to become resident:
+    // G <= #SMs at one CTA per SM, and a contributor never waits on anything but its own
+    // pipeline.
+    launch_pdl(gemm_tm_kernel<BN, KBU, NACC, UW, true>, dim3(G), dim3(C::THREADS), C::SMEM, st, map, a, n_rt, m_tiles,
+               G, dbg);
+    return 1;
+  }
+  launch_pdl(gemm_tm_kernel<BN, KBU, NACC, UW, false>, dim3(G), dim3(C::THREADS), C::SMEM, st, map, a, n_rt, m_tiles,
+             G, dbg);
   if (dbg & 64) return 1;   // debug: main kernel only
   if (G > 1) {
     // (tile, 4 columns) x (2 weight tiles x 32 row quads)

@@ -44,6 +44,7 @@ struct LinearArgs {
   int64_t ws_floats = 0;
   int* counters = nullptr;    // split-K arrival counters (zeroed, self-resetting)
   int n_counters = 0;
+  uint32_t* flags = nullptr;  // in-kernel stream-K fixup flags (zero at rest, self-resetting)
   int num_sms = 148;
 };
 
