@@ -403,8 +403,8 @@ _CLASS_KERNELS = {"linear_decode": ("gemm_tm_kernel", "gemm_ws_kernel", "gemv_in
 
 def cupti_kernel_times(pl, tok_dev, steps, timed_steps, kst, profile: bool):
     """Kernel-only GPU time per unit of each class from a CUPTI trace (torch.profiler)
-    of `steps` extra decode steps run right after the timed region (a class's kernels
-    as the union of their intervals, e.g. a GEMM and its overlapping stream-K reduce).  Units and algorithmic bytes
+    of `steps` extra decode steps run right after the timed region (each kernel's time
+    exclusive of its stream predecessors, so PDL overlap is not counted twice).  Units and algorithmic bytes
     per unit come from the event-timed region (`timed_steps` steps).  Every rank runs
     the steps (the sharded variant has a collective); only `profile` ranks trace."""
     import torch
@@ -421,34 +421,33 @@ def cupti_kernel_times(pl, tok_dev, steps, timed_steps, kst, profile: bool):
             torch.cuda.synchronize()
     except Exception as e:  # noqa: BLE001  (profiler unavailable: report, do not fail the bench)
         return {"error": str(e)[:200]}
-    # per class, the UNION of its kernels' intervals: a GEMM and its stream-K reduce
-    # overlap under programmatic dependent launch, and summing their durations would count
-    # the overlap twice
-    iv = {c: [] for c in _CLASS_KERNELS}
+    # per kernel, its EXCLUSIVE time on its stream: the part of [start, end] after every
+    # earlier kernel of the same stream has ended.  Kernels are launched with programmatic
+    # dependent launch, so a kernel "starts" while its predecessor drains and waits in
+    # griddepcontrol.wait; its raw duration would count the predecessor's tail too (and a
+    # GEMM + its overlapping stream-K reduce would be counted twice).
+    by_stream = {}
     names = {}
     for e in prof.events():
-        if e.device_type != torch.autograd.DeviceType.CUDA:
-            continue
-        for c, pats in _CLASS_KERNELS.items():
-            if any(n in e.name for n in pats):
-                iv[c].append((e.time_range.start, e.time_range.end))
-                names.setdefault(c, set()).add(e.name.split("(")[0].split("<")[0])
-                break
-    tot = {}
-    for c, lst in iv.items():
-        t, cur_s, cur_e = 0.0, None, None
-        for a, b in sorted(lst):
-            if cur_e is None or a > cur_e:
-                if cur_e is not None:
-                    t += cur_e - cur_s
-                cur_s, cur_e = a, b
-            else:
-                cur_e = max(cur_e, b)
-        if cur_e is not None:
-            t += cur_e - cur_s
-        tot[c] = t * 1e-6
+        if e.device_type != torch.autograd.DeviceType.CUDA or e.name.startswith(("Memcpy", "Memset")):
+            continue   # kernels only: the copy engines' transfers overlap the kernels by design
+        sid = getattr(e, "device_resource_id", None)
+        by_stream.setdefault(sid if sid is not None else e.thread, []).append(e)
+    tot = {c: 0.0 for c in _CLASS_KERNELS}
+    for evs in by_stream.values():
+        run_end = None
+        for e in sorted(evs, key=lambda x: x.time_range.start):
+            a, b = e.time_range.start, e.time_range.end
+            excl = max(0.0, b - (a if run_end is None else max(a, run_end)))
+            run_end = b if run_end is None else max(run_end, b)
+            for c, pats in _CLASS_KERNELS.items():
+                if any(n in e.name for n in pats):
+                    tot[c] += excl * 1e-6
+                    names.setdefault(c, set()).add(e.name.split("(")[0].split("<")[0])
+                    break
     out = {"source": f"torch.profiler CUDA activity (CUPTI), {steps} untimed steps right after the timed region; "
-                     "per class the union of its kernels' intervals"}
+                     "per kernel its exclusive time on its stream (after every earlier kernel of the stream ended)",
+           "streams": len(by_stream)}
     for c, t in tot.items():
         k = kst.get(c)
         if not k or not k["units"] or t <= 0:
@@ -480,6 +479,13 @@ def roofline_of(cupti: dict | None, kernels: dict, kst: dict, steps: int, peaks:
     if not table:
         return None
     dom = max(table, key=lambda c: table[c]["ms_per_step"])
+
+    def frac_of(v):
+        tt = v["us_per_unit"] * 1e-6
+        th, tc_ = v["bytes_per_unit"] / (hbm * 1e9), v["flops_per_unit"] / (tc * 1e12)
+        return {"bound": "tensor" if tc_ > th else "hbm", "frac": max(th, tc_) / tt, "us_per_unit": v["us_per_unit"],
+                "ms_per_step": v["ms_per_step"]}
+    by_class = {c: frac_of(v) for c, v in table.items()}
     u = table[dom]
     t = u["us_per_unit"] * 1e-6
     t_hbm = u["bytes_per_unit"] / (hbm * 1e9)
@@ -494,7 +500,8 @@ def roofline_of(cupti: dict | None, kernels: dict, kst: dict, steps: int, peaks:
             "flops_per_unit": u["flops_per_unit"], "t_hbm_us": t_hbm * 1e6, "t_tensor_us": t_tc * 1e6,
             "frac_hbm": t_hbm / t, "frac_tensor": t_tc / t,
             "event_us_per_unit": (ev["ms_per_step"] * steps / ev["units"] * 1e3) if ev else None,
-            "peak_source": "MEASURED_PEAKS.json: hbm_gbs (copy) / bf16_tflops_sustained (fp16 dense = bf16 rate)"}
+            "peak_source": "MEASURED_PEAKS.json: hbm_gbs (copy) / bf16_tflops_sustained (fp16 dense = bf16 rate)",
+            "by_class": by_class}
 
 
 def ncu_traffic(cls, args):

@@ -107,6 +107,17 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
 __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// non-blocking phase test: issued early, its result consumed later, so the mbarrier round
+// trip overlaps other work
+__device__ __forceinline__ uint32_t mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n.reg .pred P1;\nmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
+      : "=r"(done)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return done;
+}
 // polling wait with back-off, for warps that idle most of the time (the epilogue)
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;
@@ -534,6 +545,11 @@ __global__ void __launch_bounds__(256) ws_reduce2_kernel(LinearArgs a, int n_rt,
 // (mbarrier waits, tcgen05.commit, producer bookkeeping) is amortised over 8*KBU MMAs.
 // NACC = 2 accumulator buffers (the epilogue of one tile overlaps the next tile's MMAs);
 // 8 unpack warps (warp -> tile x lane quarter, all KBU k-blocks), software-pipelined.
+// Per-unit mbarrier round trips are the kernel's hidden cost (~150-250 cycles each even on
+// a completed phase; clock64 trace in profiles/r02/tm_fin/trace/): the MMA issuer waits on
+// a_full only — one unpack warp (the "x gate") waits for the unit's x tile before its
+// a_full arrival — and the unpack warps test the next raw stage with a non-blocking
+// test_wait a unit's work before they need it.
 template <int BN, int KBU, int NACC = 2, int UW = 98>
 struct TmCfg {
   static constexpr int RAW_T = KBU * (int)kInt4BlockBytes;     // one tile's blocks (contiguous)
@@ -730,7 +746,7 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
       const uint32_t d = tmem + ab * (2 * BN);
       for (int64_t v = u; v < seg_end; ++v) {
         TWAIT(0, &a_full[sa], ph_a);
-        TWAIT(1, &x_full[sx], ph_x);
+        // x_full: implied by a_full (the x gate unpack warp waits for it before arriving)
         ws::tc_after();
         if (ws::elect_one()) {
           const uint32_t at = a_base + sa * C::A_COLS;
@@ -773,9 +789,9 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
       // barrier/latency chain overlaps the store completion
       uint4 cw[KBU][2];
       __half2 s2[KBU];
-      auto load_unit = [&](int64_t iu, uint4 (&c)[KBU][2], __half2 (&sc)[KBU]) {
+      auto load_unit = [&](int64_t iu, uint4 (&c)[KBU][2], __half2 (&sc)[KBU], uint32_t ready) {
         const int s = (int)(iu % C::NR);
-        TWAIT(0, &raw_full[s], (uint32_t)((iu / C::NR) & 1));
+        if (!ready) TWAIT(0, &raw_full[s], (uint32_t)((iu / C::NR) & 1));
 #pragma unroll
         for (int k = 0; k < KBU; ++k) {
           const uint8_t* rs = raw + s * C::RAW + t * C::RAW_T + k * kInt4BlockBytes;
@@ -786,10 +802,21 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
         __syncwarp();
         if (lane == 0) ws::mbar_arrive(&raw_empty[s]);
       };
-      if (u0 < u1) load_unit(0, cw, s2);
+      if (u0 < u1) load_unit(0, cw, s2, 0u);
+      // x gate: one unpack warp also waits for the unit's activation tile before its a_full
+      // arrival, so the MMA warp's single a_full wait covers both operands (one mbarrier
+      // round trip less on the MMA issuer's per-unit loop); its test is issued here and
+      // consumed ~a unit's unpack work later
+      const bool xgate = warp == 2;
       for (int64_t u = u0; u < u1; ++u) {
         const int64_t iu = u - u0;
         const int sa = (int)(iu % C::NA);
+        const int sxg = (int)(iu % C::NX);
+        const uint32_t pxg = (uint32_t)((iu / C::NX) & 1);
+        const uint32_t xok = xgate ? ws::mbar_test(&x_full[sxg], pxg) : 1u;
+        // the next unit's raw stage, tested now and loaded after this unit's TMEM stores
+        const uint32_t rok =
+            u + 1 < u1 ? ws::mbar_test(&raw_full[(iu + 1) % C::NR], (uint32_t)(((iu + 1) / C::NR) & 1)) : 0u;
         TWAIT(1, &a_empty[sa], (uint32_t)(((iu / C::NA) & 1) ^ 1));
         ws::tc_after();
 #pragma unroll
@@ -801,10 +828,11 @@ __global__ void __launch_bounds__(TmCfg<BN, KBU, NACC, UW>::THREADS, 1)
           for (int ch = 0; ch < 8; ++ch) dequant8(w[ch], s2[k], reinterpret_cast<__half2*>(o + ch * 4));
           tmem_st32(a_base + sa * C::A_COLS + k * 64 + t * 32 + lane_off, o);
         }
-        if (u + 1 < u1) load_unit(iu + 1, cw, s2);   // registers are free once the stores are issued
+        if (u + 1 < u1) load_unit(iu + 1, cw, s2, rok);   // registers are free once the stores are issued
         const uint64_t tst_ = wt ? clk() : 0;
         asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
         if (wt) w_st += clk() - tst_;
+        if (!xok) ws::mbar_wait(&x_full[sxg], pxg);
         ws::tc_before();
         __syncwarp();
         if (lane == 0) ws::mbar_arrive(&a_full[sa]);
