@@ -304,7 +304,8 @@ pipo_status pipo_bench_attention(pipo_ctx* ctx, int32_t b, int32_t L, int32_t d,
 
 /* Decode attention kernel: q [b][d] fp16 bits (pre-scaled), k/v [L][b][d] fp16
  * bits (position-major) -> o [b][d] fp32.  n_heads | d.  variant: 0 = production
- * kernel (one K/V row per warp), 1 = the lane-group variant (16-B row loads). */
+ * choice (the lane-group kernel up to 1536 (b, head) pairs, one K/V row per warp above),
+ * 1 = the lane-group kernel (16-B row loads), 3 = the one-row-per-warp kernel. */
 pipo_status pipo_attention_decode(pipo_ctx* ctx, const uint16_t* q, const uint16_t* k,
                                   const uint16_t* v, int32_t b, int32_t L, int32_t d,
                                   int32_t n_heads, int32_t variant, float* o);

@@ -970,11 +970,16 @@ int launch_attention_decode(const AttnArgs& a, cudaStream_t st) {
   // c6 attention 1.98 -> 1.33 ms/step, c7 0.435 -> 0.36; profiles/r01/gqa_tc); 3 forces the
   // one-row-per-warp kernel for a GQA group (test hook); 5 / 6 force the 4- / 2-warp
   // tensor-core GQA kernel (launch_attention_decode_gqa_mma)
+  // MHA default by the number of (b, head) pairs: the lane-group kernel for up to 1536
+  // pairs (c2 18.1 -> 13.4 us, c3 50.1 -> 46.8), one row per warp above (c5: 155 vs 173 us;
+  // profiles/r02/attn_sk/).  A stream-K variant (one resident wave over the flattened
+  // (b, head, position) space, split pairs merged by the last CTA) measured slower at c5
+  // (159 vs 155 us isolated, 170 vs 167 in the step) and was not kept.
   const int uc = a.use_cuda_cores;
-  const int var = uc == 1 ? 1 : uc == 3 ? 0 : G == 1 ? 0 : (uc == 5 || uc == 6) ? uc : 2;
+  const int pairs = a.b * a.n_heads / G;
+  const int var = uc == 1 ? 1 : uc == 3 ? 0 : G == 1 ? (pairs <= 1536 ? 1 : 0) : (uc == 5 || uc == 6) ? uc : 2;
   if (var >= 2) return launch_attention_decode_gqa_mma(a, G, var, st);
   const bool v2 = var == 1;
-  const int pairs = a.b * a.n_heads / G;
   // enough CTAs for ~8 waves of resident blocks (9 per SM): the block scheduler then
   // balances the tail to within ~1/8 of the kernel; splits merge in a second kernel
   // Split positions only when (b, head) pairs cannot fill the GPU: measured on B200

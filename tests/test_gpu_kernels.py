@@ -164,8 +164,9 @@ def test_linear_special_cases_exact(env, path):
 
 @pytest.mark.parametrize("b,L,d,H", [(1, 1, 128, 2), (2, 7, 256, 4), (3, 65, 256, 2), (4, 300, 512, 4),
                                      (2, 544, 1024, 8), (64, 40, 512, 8)])
-@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("variant", [0, 1, 3])
 def test_attention_decode_vs_oracle(env, b, L, d, H, variant):
+    """variant 0 = the launcher's choice, 1 = lane-group kernel, 3 = one row per warp."""
     pipo, pl = env
     rng = np.random.default_rng(b * 1000 + L)
     q = (rng.standard_normal((b, d)) * (d // H) ** -0.5).astype(np.float16)
