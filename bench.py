@@ -445,7 +445,7 @@ def cupti_kernel_times(pl, tok_dev, steps, timed_steps, kst, profile: bool):
                     tot[c] += excl * 1e-6
                     names.setdefault(c, set()).add(e.name.split("(")[0].split("<")[0])
                     break
-    out = {"source": f"torch.profiler CUDA activity (CUPTI), {steps} untimed steps right after the timed region; "
+    out = {"source": f"torch.profiler CUDA activity (CUPTI), {steps} untimed, uninstrumented steps right after the timed region; "
                      "per kernel its exclusive time on its stream (after every earlier kernel of the stream ended)",
            "streams": len(by_stream)}
     for c, t in tot.items():
@@ -694,9 +694,13 @@ def run_pipo(args):
 
     # CUPTI (torch.profiler) view of 3 extra steps: true per-kernel GPU durations with the
     # copy stream running — the roofline's timing
+    # (run uninstrumented: no timing events between the kernels, the production launch
+    # sequence with its programmatic-dependent-launch overlaps)
     cupti = None
     if not args.no_cupti:
+        pipo.pipo_set_flags(pl.ctx, 0)
         cupti = cupti_kernel_times(pl, tok_dev, 3, args.steps, kst, profile=(rank == 0))
+        pipo.pipo_set_flags(pl.ctx, flags)
 
     value = aggregate_throughput(b, world, args.steps, t_dev)
     ms = t_dev / args.steps * 1e3

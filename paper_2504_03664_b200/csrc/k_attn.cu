@@ -993,8 +993,12 @@ int launch_attention_decode(const AttnArgs& a, cudaStream_t st) {
   n_splits = (L + per - 1) / per;
   if (n_splits > 1 && (int64_t)a.b * a.n_heads * n_splits * (hd + 2) > a.ws_floats) return -1;
   dim3 grid(a.n_heads / G, a.b, n_splits);
+  // MHA decode attention is launched WITHOUT programmatic dependent launch (launch_k): as
+  // the QKV GEMM's early-launched dependent it measured 197 us per c5 layer in the step vs
+  // 161 us launched plainly (c5 device tier uninstrumented 3 740 -> 4 070 tok/s;
+  // profiles/r02/pdl_attn/).  The one-wave GQA kernel keeps PDL (same time either way).
   if (!v2) {   // one K/V row per warp: measured 0-5% ahead of v2 at c3-c5 (MHA)
-#define PIPO_DECODE(HDV, GV) launch_pdl_k(attn_decode_kernel<HDV, GV>, grid, dim3(128), 0, st, a, n_splits, per)
+#define PIPO_DECODE(HDV, GV) launch_k(attn_decode_kernel<HDV, GV>, grid, dim3(128), 0, st, a, n_splits, per)
     if (hd == 64) {
       if (G == 1) PIPO_DECODE(64, 1); else if (G == 2) PIPO_DECODE(64, 2); else if (G == 4) PIPO_DECODE(64, 4);
       else PIPO_DECODE(64, 8);
@@ -1004,7 +1008,7 @@ int launch_attention_decode(const AttnArgs& a, cudaStream_t st) {
     }
 #undef PIPO_DECODE
   } else {     // v2: lane groups with 16-B row loads
-#define PIPO_DECODE2(HDV, GV) launch_pdl_k(attn_decode_v2_kernel<HDV, GV>, grid, dim3(128), 0, st, a, n_splits, per)
+#define PIPO_DECODE2(HDV, GV) launch_k(attn_decode_v2_kernel<HDV, GV>, grid, dim3(128), 0, st, a, n_splits, per)
     if (hd == 64) {
       if (G == 1) PIPO_DECODE2(64, 1); else if (G == 2) PIPO_DECODE2(64, 2); else if (G == 4) PIPO_DECODE2(64, 4);
       else PIPO_DECODE2(64, 8);

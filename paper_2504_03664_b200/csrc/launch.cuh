@@ -36,6 +36,22 @@ static cudaError_t launch_pdl_k(void (*kern)(KArgs...), dim3 grid, dim3 block, s
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+// Plain launch (no PDL attribute) for multi-wave kernels that follow a one-wave GEMM: the
+// decode attention launched as the QKV GEMM's programmatic dependent measured 197 us per
+// c5 layer in the step against 161 us launched plainly (uninstrumented CUPTI, device
+// tier; profiles/r02/pdl_attn/); its pdl_wait() is then a no-op.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.numAttrs = 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // cudaFuncAttributeMaxDynamicSharedMemorySize applies to the CURRENT device: track it per
 // (device, kernel, size) so a second context on another GPU of the same process gets it
 // too; thread-safe (contexts may live on different host threads).
