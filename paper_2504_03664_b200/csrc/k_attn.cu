@@ -14,6 +14,7 @@
 // splits merge in fixed order in a second kernel (log-sum-exp weights).
 #include <float.h>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "launch.cuh"
@@ -80,14 +81,34 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnArgs a, int n_spli
 #pragma unroll
     for (int e = 0; e < E; ++e) acc[g][e] = 0.f;
   }
+  // raw K/V rows of the next 4-position group are loaded while the current group is
+  // computed (register double buffer of the undecoded halves): two groups in flight per warp
+  using Raw = typename std::conditional<E == 4, uint2, uint32_t>::type;
+  Raw kn[4], vn[4];
+  auto fetch = [&](int p0) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int p = max(lo, min(p0 + u, hi - 1));
+      kn[u] = *reinterpret_cast<const Raw*>(kbase + p * pstride);
+      vn[u] = *reinterpret_cast<const Raw*>(vbase + p * pstride);
+    }
+  };
+  auto decode = [&](const Raw& r, float* out) {
+    if constexpr (E == 2) {
+      const float2 v = __half22float2(*reinterpret_cast<const __half2*>(&r));
+      out[0] = v.x; out[1] = v.y;
+    } else {
+      const float2 x = __half22float2(*reinterpret_cast<const __half2*>(&r.x));
+      const float2 y = __half22float2(*reinterpret_cast<const __half2*>(&r.y));
+      out[0] = x.x; out[1] = x.y; out[2] = y.x; out[3] = y.y;
+    }
+  };
+  if (lo + 4 * warp < hi) fetch(lo + 4 * warp);
   for (int p0 = lo + 4 * warp; p0 < hi; p0 += 16) {
     float kr[4][E], vr[4][E], s[G][4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int p = min(p0 + u, hi - 1);
-      load_row<E>(kbase + p * pstride, kr[u]);
-      load_row<E>(vbase + p * pstride, vr[u]);
-    }
+    for (int u = 0; u < 4; ++u) { decode(kn[u], kr[u]); decode(vn[u], vr[u]); }
+    if (p0 + 16 < hi) fetch(p0 + 16);
 #pragma unroll
     for (int g = 0; g < G; ++g)
 #pragma unroll
