@@ -96,6 +96,22 @@ __global__ void __launch_bounds__(640, 1) ub_kernel(int test, int n, int p0, int
       o[2] = t2 - t0;
     }
     __syncwarp();
+  } else if (test == 9 && warp == 1) {   // MMA rate, 128 x p0 x 16 A in TMEM, p1 accumulators round-robin
+    if (elect_one()) {
+      const uint32_t id = idesc_f16(128, p0);
+      mma_ts(tmem, tmem + 256, db0, id, 0);
+      mma_commit(&bar[0]);
+      mbar_wait(&bar[0], 0);
+      uint64_t t0 = clk();
+      for (int i = 0; i < n; ++i) {
+        const uint64_t db = db0 + (uint64_t)(((i & 3) * 32) >> 4);
+        mma_ts(tmem + (i % p1) * 64, tmem + 256 + (i & 7) * 8, db, id, 1);
+      }
+      mma_commit(&bar[0]);
+      mbar_wait(&bar[0], 1);
+      o[1] = (clk() - t0) / n;   // completion
+    }
+    __syncwarp();
   } else if (test == 3 && warp == 1) {   // groups of p1 MMAs + commit + wait (serial latency per group)
     if (elect_one()) {
       const uint32_t id = idesc_f16(128, p0);
@@ -308,6 +324,11 @@ int main(int argc, char** argv) {
     run(b, 2, 256, N, 1, 1);
   }
   run("MMA TS 128x64x16 x256, 148 CTAs", 2, 256, 64, 0, 148);
+  for (int na : {1, 2, 3, 4}) {
+    char b[64];
+    snprintf(b, 64, "MMA TS 128x64x16 x512, %d acc round-robin", na);
+    run(b, 9, 512, 64, na, 1);
+  }
   for (int g : {4, 8, 16, 32}) {
     char b[64];
     snprintf(b, 64, "group of %d MMAs N64 + commit + wait (cyc)", g);
