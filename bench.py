@@ -401,6 +401,34 @@ _CLASS_KERNELS = {"linear_decode": ("gemm_tm_kernel", "gemm_ws_kernel", "gemv_in
                   "lm_head": ("gemm_kernel", "lm_head")}
 
 
+def exclusive_class_times(events, classes):
+    """Kernel time per class from (stream, start_us, end_us, name) device events: each
+    kernel counts only the part of [start, end] after every earlier kernel of its stream
+    has ended.  Kernels are launched with programmatic dependent launch, so a kernel
+    "starts" while its predecessor drains (its CTAs wait in griddepcontrol.wait); raw
+    durations would count that overlap twice (a GEMM + its overlapping stream-K reduce).
+    Memcpy/memset events are skipped: the copy engines overlap the kernels by design.
+    Returns ({class: seconds}, {class: set(kernel names)}, number of streams)."""
+    by_stream = {}
+    for sid, a, b, name in events:
+        if name.startswith(("Memcpy", "Memset")):
+            continue
+        by_stream.setdefault(sid, []).append((a, b, name))
+    tot = {c: 0.0 for c in classes}
+    names = {}
+    for evs in by_stream.values():
+        run_end = None
+        for a, b, name in sorted(evs):
+            excl = max(0.0, b - (a if run_end is None else max(a, run_end)))
+            run_end = b if run_end is None else max(run_end, b)
+            for c, pats in classes.items():
+                if any(n in name for n in pats):
+                    tot[c] += excl * 1e-6
+                    names.setdefault(c, set()).add(name.split("(")[0].split("<")[0])
+                    break
+    return tot, names, len(by_stream)
+
+
 def cupti_kernel_times(pl, tok_dev, steps, timed_steps, kst, profile: bool):
     """Kernel-only GPU time per unit of each class from a CUPTI trace (torch.profiler)
     of `steps` extra decode steps run right after the timed region (each kernel's time
@@ -421,33 +449,13 @@ def cupti_kernel_times(pl, tok_dev, steps, timed_steps, kst, profile: bool):
             torch.cuda.synchronize()
     except Exception as e:  # noqa: BLE001  (profiler unavailable: report, do not fail the bench)
         return {"error": str(e)[:200]}
-    # per kernel, its EXCLUSIVE time on its stream: the part of [start, end] after every
-    # earlier kernel of the same stream has ended.  Kernels are launched with programmatic
-    # dependent launch, so a kernel "starts" while its predecessor drains and waits in
-    # griddepcontrol.wait; its raw duration would count the predecessor's tail too (and a
-    # GEMM + its overlapping stream-K reduce would be counted twice).
-    by_stream = {}
-    names = {}
-    for e in prof.events():
-        if e.device_type != torch.autograd.DeviceType.CUDA or e.name.startswith(("Memcpy", "Memset")):
-            continue   # kernels only: the copy engines' transfers overlap the kernels by design
-        sid = getattr(e, "device_resource_id", None)
-        by_stream.setdefault(sid if sid is not None else e.thread, []).append(e)
-    tot = {c: 0.0 for c in _CLASS_KERNELS}
-    for evs in by_stream.values():
-        run_end = None
-        for e in sorted(evs, key=lambda x: x.time_range.start):
-            a, b = e.time_range.start, e.time_range.end
-            excl = max(0.0, b - (a if run_end is None else max(a, run_end)))
-            run_end = b if run_end is None else max(run_end, b)
-            for c, pats in _CLASS_KERNELS.items():
-                if any(n in e.name for n in pats):
-                    tot[c] += excl * 1e-6
-                    names.setdefault(c, set()).add(e.name.split("(")[0].split("<")[0])
-                    break
+    evs = [(getattr(e, "device_resource_id", None) if getattr(e, "device_resource_id", None) is not None else e.thread,
+            e.time_range.start, e.time_range.end, e.name)
+           for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+    tot, names, n_streams = exclusive_class_times(evs, _CLASS_KERNELS)
     out = {"source": f"torch.profiler CUDA activity (CUPTI), {steps} untimed, uninstrumented steps right after the timed region; "
                      "per kernel its exclusive time on its stream (after every earlier kernel of the stream ended)",
-           "streams": len(by_stream)}
+           "streams": n_streams}
     for c, t in tot.items():
         k = kst.get(c)
         if not k or not k["units"] or t <= 0:
