@@ -81,16 +81,13 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnArgs a, int n_spli
 #pragma unroll
     for (int e = 0; e < E; ++e) acc[g][e] = 0.f;
   }
-  // raw K/V rows of the next 4-position group are loaded while the current group is
-  // computed (register double buffer of the undecoded halves): two groups in flight per warp
   using Raw = typename std::conditional<E == 4, uint2, uint32_t>::type;
-  Raw kn[4], vn[4];
-  auto fetch = [&](int p0) {
+  auto fetch = [&](Raw (&kk)[4], Raw (&vv)[4], int p0) {
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int p = max(lo, min(p0 + u, hi - 1));
-      kn[u] = *reinterpret_cast<const Raw*>(kbase + p * pstride);
-      vn[u] = *reinterpret_cast<const Raw*>(vbase + p * pstride);
+      kk[u] = *reinterpret_cast<const Raw*>(kbase + p * pstride);
+      vv[u] = *reinterpret_cast<const Raw*>(vbase + p * pstride);
     }
   };
   auto decode = [&](const Raw& r, float* out) {
@@ -103,12 +100,11 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnArgs a, int n_spli
       out[0] = x.x; out[1] = x.y; out[2] = y.x; out[3] = y.y;
     }
   };
-  if (lo + 4 * warp < hi) fetch(lo + 4 * warp);
-  for (int p0 = lo + 4 * warp; p0 < hi; p0 += 16) {
+  // one 4-position group: scores, online softmax, P.V (the group's raw rows in kk / vv)
+  auto step = [&](const Raw (&kk)[4], const Raw (&vv)[4], int p0) {
     float kr[4][E], vr[4][E], s[G][4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) { decode(kn[u], kr[u]); decode(vn[u], vr[u]); }
-    if (p0 + 16 < hi) fetch(p0 + 16);
+    for (int u = 0; u < 4; ++u) { decode(kk[u], kr[u]); decode(vv[u], vr[u]); }
 #pragma unroll
     for (int g = 0; g < G; ++g)
 #pragma unroll
@@ -145,6 +141,17 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnArgs a, int n_spli
       }
       m_run[g] = mx;
     }
+  };
+  // raw K/V rows of the next 4-position group are loaded while the current group is
+  // computed (register double buffer of the undecoded halves; a third buffer measured
+  // 15 % slower at c5: 89 registers, 5 CTAs/SM; profiles/r02/attn_prefetch/)
+  Raw kn[4], vn[4], kc_[4], vc_[4];
+  if (lo + 4 * warp < hi) fetch(kn, vn, lo + 4 * warp);
+  for (int p0 = lo + 4 * warp; p0 < hi; p0 += 16) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { kc_[u] = kn[u]; vc_[u] = vn[u]; }
+    if (p0 + 16 < hi) fetch(kn, vn, p0 + 16);
+    step(kc_, vc_, p0);
   }
 #pragma unroll
   for (int g = 0; g < G; ++g) {
