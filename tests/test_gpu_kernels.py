@@ -86,13 +86,15 @@ def test_linear_vs_oracle(env, M, N, K, wfmt):
 
 @pytest.mark.parametrize("M,N,K", [(64, 512, 2048), (40, 200, 1024), (33, 384, 320), (64, 2304, 7168),
                                    (16, 1024, 8192), (64, 384, 4160), (1, 1664, 4096), (8, 7168, 28672),
-                                   (64, 5376, 7168), (31, 896, 1088), (64, 12800, 2048), (48, 9984, 1536)])
+                                   (64, 5376, 7168), (31, 896, 1088), (64, 12800, 2048), (48, 9984, 1536),
+                                   (12, 4096, 1024), (24, 8192, 1024)])
 @pytest.mark.parametrize("path", ["tm", "pair"])
 def test_linear_tm_stream_k_deterministic(env, M, N, K, path):
     """The decode GEMMs (stream-K over CTAs / SM pairs; partials summed in k order by the
     reduce kernel or, for split tiles spanning <= ~3.5 CTAs, by the finishing CTA inside
     the kernel (tm: (40, 200, 1024), (31, 896, 1088), (64, 12800, 2048), (48, 9984, 1536)
-    take the in-kernel fixup with 2-4 contributors per tile), or by the finishing pair
+    take the in-kernel fixup with 2-4 contributors per tile, as do (12, 4096, 1024) and
+    (24, 8192, 1024) with the 16- and 32-token tiles), or by the finishing pair
     (pair)) within the bar
     and bit-reproducible run to run (the tier-invariance tests rely on it); K/64 odd
     (4160) takes the tm kernel's 1-k-block units; N not a multiple of 512 leaves the pair
