@@ -197,9 +197,7 @@ static int run_head(const LinearArgs& a, bool lm_head, cudaStream_t st) {
   const int G = std::min(a.num_sms, n_rt);
   if (lm_head) {
     ensure_max_smem(lm_head_stream_kernel<BN>, C::SMEM);
-    // plain launch: as the final LayerNorm's programmatic dependent the head measured
-    // 159.6 us in the c5 host-tier step, launched plainly 155.8 (profiles/r02/pdl_attn/)
-    launch_k(lm_head_stream_kernel<BN>, dim3(G), dim3(C::THREADS), C::SMEM, st, wmap, xmap, a, n_rt);
+    launch_pdl_k(lm_head_stream_kernel<BN>, dim3(G), dim3(C::THREADS), C::SMEM, st, wmap, xmap, a, n_rt);
   } else {
     ensure_max_smem(gemm_f16_stream_kernel<BN>, C::SMEM);
     launch_pdl_k(gemm_f16_stream_kernel<BN>, dim3(G), dim3(C::THREADS), C::SMEM, st, wmap, xmap, a, n_rt);
